@@ -1,0 +1,254 @@
+"""Generate the golden fixtures from the REFERENCE itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+The script re-executes itself with ``OPENBLAS_CORETYPE=Haswell
+OPENBLAS_NUM_THREADS=1`` (the reference's hierarchy depends on
+the BLAS kernel behind np.linalg.norm) and imports the unmodified reference
+from /root/reference/pkg/src. Nothing under tests/ reads /root/reference at
+test time; the tests only read the files written here:
+
+* ``inputs.json``  -- sha256 of the reference-assembled (A_e, S, A_n, D) arrays
+  for a grid of (N, dirichlet, sigma) cases;
+* ``hier_<case>.npz`` / ``hier_<case>.json`` -- per-level hierarchy outputs of
+  ``build_hierarchy`` (membership, omega/rho bits, P_n, P_const assignment,
+  coarse edges, P_e, energies, commutator residual, subproblem dims, coarse
+  operators) and PCG results with the reference's Gauss-Seidel sweeper and with
+  the oracle's Chebyshev sweeper installed in the reference hierarchy's own
+  sweeper slots (multigrid.py:79-80). Large cases store hashes + samples.
+"""
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+
+if os.environ.get("OPENBLAS_CORETYPE") != "Haswell" or \
+        os.environ.get("OPENBLAS_NUM_THREADS") != "1":
+    env = dict(os.environ, OPENBLAS_CORETYPE="Haswell", OPENBLAS_NUM_THREADS="1")
+    os.execve(sys.executable, [sys.executable] + sys.argv, env)
+
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+import scipy.sparse as sp  # noqa: E402
+
+from hcurlamg.assembly import discretize  # noqa: E402
+from hcurlamg.meshing import build_structured_mesh  # noqa: E402
+from hcurlamg import multigrid as mg  # noqa: E402
+
+from oracle.hcurl_oracle import ChebyshevSweeper  # noqa: E402
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def csr_hash(A):
+    A = sp.csr_matrix(A)
+    return sha(A.indptr.astype(np.int64), A.indices.astype(np.int64),
+               A.data.astype(np.float64))
+
+
+def inputs_table():
+    out = {}
+    for N in (2, 3, 4, 6, 8, 16, 32):
+        for dirichlet in (False, True):
+            for sigma in (1.0, 1e-2, 1e-4):
+                m = build_structured_mesh(3, "hex", N + 1, dirichlet)
+                s = discretize(m, sigma)
+                out[f"{N}_{int(dirichlet)}_{sigma!r}"] = {
+                    k: csr_hash(getattr(s, k)) for k in ("A_e", "S", "A_n", "D")}
+    return out
+
+
+CASES = {
+    # name: (N, dirichlet, sigma, coarse_size, rhs_seed, full arrays?)
+    "N4n": (4, False, 1.0, 40, 0, True),
+    "N6d": (6, True, 1.0, 40, 0, True),
+    "N8d": (8, True, 1.0, 200, 0, True),
+    "N10n": (10, False, 1e-4, 100, 5, True),
+    "C1": (16, True, 1.0, 1000, 0, True),
+    "N16n": (16, False, 1e-2, 200, 1, False),
+    "C2": (32, True, 1e-2, 1000, 1, False),
+}
+
+
+def run_case(name, N, dirichlet, sigma, coarse_size, seed, full):
+    m = build_structured_mesh(3, "hex", N + 1, dirichlet)
+    s = discretize(m, sigma)
+    cfg = mg.SolverConfig(coarse_size=coarse_size)
+    t0 = time.perf_counter()
+    h = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, cfg)
+    t_setup = time.perf_counter() - t0
+    b = np.random.default_rng(seed).uniform(-1.0, 1.0, s.A_e.shape[0])
+    t0 = time.perf_counter()
+    res = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+    t_solve = time.perf_counter() - t0
+
+    meta = {"N": N, "dirichlet": dirichlet, "sigma": sigma,
+            "coarse_size": coarse_size, "seed": seed,
+            "t_setup_ref": t_setup, "t_solve_ref": t_solve,
+            "n_levels": h.n_levels,
+            "n_edges": [lv.A_e.shape[0] for lv in h.levels],
+            "nnz_A_e": [int(lv.A_e.nnz) for lv in h.levels],
+            "operator_complexity": h.operator_complexity,
+            "gs": {"iterations": res.iterations, "status": res.status,
+                   "residual_history": res.residual_history,
+                   "precond_history": res.precond_history,
+                   "relative_residual": res.relative_residual},
+            "levels": []}
+    arrays = {}
+    if full:
+        arrays["gs_x"] = res.x
+    for li, lv in enumerate(h.levels):
+        L = {"n_edges": lv.A_e.shape[0], "n_nodes": lv.D.shape[1],
+             "A_e": csr_hash(lv.A_e), "S_e": csr_hash(lv.S_e),
+             "D": csr_hash(lv.D), "nodal_aux_nnz": int(lv.nodal_aux.nnz),
+             "A_e_nnz": int(lv.A_e.nnz), "S_e_nnz": int(lv.S_e.nnz)}
+        if lv.P_e is not None:
+            L.update({
+                "P_e_nnz": int(lv.P_e.nnz),
+                "P_e_pattern": sha(lv.P_e.indptr.astype(np.int64),
+                                   lv.P_e.indices.astype(np.int64)),
+                "P_e_fro": float(np.linalg.norm(lv.P_e.data)),
+                "P_n": csr_hash(lv.P_n), "P_n_nnz": int(lv.P_n.nnz),
+                "emin_energy": lv.emin_energy,
+                "commutator_residual": lv.commutator_residual,
+                "subproblem_dims": sorted([list(k) + [v] for k, v in
+                                           lv.subproblem_dims.items()]),
+                "n_augmented": lv.n_augmented,
+            })
+            # P_e sample rows (TOL check on big cases)
+            step = max(1, lv.P_e.shape[0] // 500)
+            rows = np.arange(0, lv.P_e.shape[0], step)
+            sub = lv.P_e[rows]
+            arrays[f"L{li}_Pe_sample_rows"] = rows
+            arrays[f"L{li}_Pe_sample_indptr"] = sub.indptr
+            arrays[f"L{li}_Pe_sample_indices"] = sub.indices
+            arrays[f"L{li}_Pe_sample_data"] = sub.data
+            if full:
+                for key, M in (("P_n", lv.P_n), ("P_e", lv.P_e)):
+                    arrays[f"L{li}_{key}_indptr"] = M.indptr
+                    arrays[f"L{li}_{key}_indices"] = M.indices
+                    arrays[f"L{li}_{key}_data"] = M.data
+        if full:
+            nxt = h.levels[li + 1] if li + 1 < h.n_levels else None
+            if nxt is not None:
+                for key, M in (("A_e", nxt.A_e), ("S_e", nxt.S_e), ("D", nxt.D)):
+                    arrays[f"L{li + 1}_{key}_indptr"] = M.indptr
+                    arrays[f"L{li + 1}_{key}_indices"] = M.indices
+                    arrays[f"L{li + 1}_{key}_data"] = M.data
+        meta["levels"].append(L)
+
+    # discrete decisions of each prolongator build, recomputed with the
+    # reference's own module functions on the level's inputs
+    from hcurlamg import nodal_amg as na, coarse_gradient as cgm
+    for li, lv in enumerate(h.levels[:-1]):
+        strength = na.strength_graph(_an(h, li, s), 0.0)
+        agg = na.aggregate(strength)
+        nod = na.smooth_and_normalize(_an(h, li, s), na.tentative_prolongator(agg))
+        assert (nod.P != lv.P_n).nnz == 0
+        Pc = cgm.gen_piecewise_const(nod.P, 2)
+        assign = Pc.indices[Pc.indptr[:-1]].astype(np.int64)
+        cg = cgm.build_coarse_gradient(lv.D, Pc)
+        cg = cgm.augment_dirichlet_edges(cg, lv.D, Pc)
+        pairs = np.array([e for e in cg.edge_endpoints if len(e) == 2],
+                         dtype=np.int64).reshape(-1, 2)
+        singles = np.array([e[0] for e in cg.edge_endpoints if len(e) == 1],
+                           dtype=np.int64)
+        Lm = meta["levels"][li]
+        Lm.update({"n_agg": agg.n_agg, "membership": sha(agg.membership.astype(np.int64)),
+                   "omega_hex": float(nod.omega_used).hex(),
+                   "rho_hex": float(nod.rho_estimate).hex(),
+                   "assignment": sha(assign), "pairs": sha(pairs),
+                   "singles": sha(singles), "n_pairs": int(pairs.shape[0]),
+                   "n_singles": int(singles.size)})
+        arrays[f"L{li}_membership"] = agg.membership.astype(np.int32)
+        arrays[f"L{li}_assignment"] = assign.astype(np.int32)
+        arrays[f"L{li}_pairs"] = pairs.astype(np.int32)
+        arrays[f"L{li}_singles"] = singles.astype(np.int32)
+
+    # Chebyshev-3 sweeper in the reference hierarchy's own seam
+    for lv in h.levels[:-1]:
+        lv.edge_sweeper = ChebyshevSweeper(lv.A_e, 3)
+        lv.aux_sweeper = ChebyshevSweeper(lv.nodal_aux, 3)
+    t0 = time.perf_counter()
+    rc = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+    meta["cheb"] = {"iterations": rc.iterations, "status": rc.status,
+                    "residual_history": rc.residual_history,
+                    "precond_history": rc.precond_history,
+                    "relative_residual": rc.relative_residual,
+                    "t_solve_ref": time.perf_counter() - t0}
+    if full:
+        arrays["cheb_x"] = rc.x
+    return meta, arrays
+
+
+_AN_CACHE = {}
+
+
+def _an(h, li, s):
+    """A_n of level li (the reference does not keep it; recompute)."""
+    key = id(h)
+    if key not in _AN_CACHE:
+        An = [sp.csr_matrix(s.A_n)]
+        for lv in h.levels[:-1]:
+            P = lv.P_n
+            C = sp.csr_matrix(P.T @ (An[-1] @ P))
+            C.sum_duplicates()
+            C.sort_indices()
+            C.eliminate_zeros()
+            An.append(C)
+        _AN_CACHE[key] = An
+    return _AN_CACHE[key][li]
+
+
+def error_cases():
+    """Reference raising on a degenerate coarse level."""
+    out = {}
+    m = build_structured_mesh(3, "hex", 9, True)
+    s = discretize(m, 1.0)
+    try:
+        mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, mg.SolverConfig(coarse_size=100))
+        out["N8d_cs100"] = None
+    except ValueError as e:
+        out["N8d_cs100"] = str(e)
+    return out
+
+
+def main(which):
+    if "errors" in which:
+        with open(os.path.join(HERE, "errors.json"), "w") as f:
+            json.dump(error_cases(), f, indent=1)
+    if "inputs" in which:
+        with open(os.path.join(HERE, "inputs.json"), "w") as f:
+            json.dump(inputs_table(), f, indent=1, sort_keys=True)
+        print("inputs.json written")
+    for name, spec in CASES.items():
+        if which and name not in which:
+            continue
+        t0 = time.perf_counter()
+        meta, arrays = run_case(name, *spec)
+        with open(os.path.join(HERE, f"hier_{name}.json"), "w") as f:
+            json.dump(meta, f, indent=1)
+        np.savez_compressed(os.path.join(HERE, f"hier_{name}.npz"), **arrays)
+        print(name, "levels", meta["n_edges"], "gs its", meta["gs"]["iterations"],
+              "cheb its", meta["cheb"]["iterations"],
+              f"{time.perf_counter() - t0:.1f}s", flush=True)
+
+
+if __name__ == "__main__":
+    main(set(sys.argv[1:]) or set(["inputs", "errors"] + list(CASES)))

@@ -1,0 +1,54 @@
+"""Helpers to read the reference-generated golden fixtures (tests/golden)."""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import scipy.sparse as sp
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def csr_hash(A):
+    A = sp.csr_matrix(A)
+    return sha(A.indptr.astype(np.int64), A.indices.astype(np.int64),
+               A.data.astype(np.float64))
+
+
+def load_case(name):
+    with open(os.path.join(GOLDEN, f"hier_{name}.json")) as f:
+        meta = json.load(f)
+    arrays = dict(np.load(os.path.join(GOLDEN, f"hier_{name}.npz")))
+    return meta, arrays
+
+
+def golden_csr(arrays, key, shape):
+    return sp.csr_matrix((arrays[key + "_data"], arrays[key + "_indices"],
+                          arrays[key + "_indptr"]), shape=shape)
+
+
+def inputs_table():
+    with open(os.path.join(GOLDEN, "inputs.json")) as f:
+        return json.load(f)
+
+
+def rel_max_diff(A, B):
+    """max |A - B| / max |B| over the union pattern (TOL metric)."""
+    A = sp.csr_matrix(A)
+    B = sp.csr_matrix(B)
+    d = abs(A - B)
+    scale = max(float(abs(B).max()) if B.nnz else 0.0, 1e-300)
+    return (float(d.max()) if d.nnz else 0.0) / scale
+
+
+CASES = ["N4n", "N6d", "N8d", "N10n", "C1", "N16n", "C2"]

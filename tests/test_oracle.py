@@ -1,0 +1,129 @@
+"""The oracle (oracle/hcurl_oracle.py) is pinned against the reference's own
+outputs (tests/golden, produced by running the reference itself)."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from golden_util import CASES, csr_hash, golden_csr, load_case, sha
+from oracle import hcurl_oracle as O
+from paper_2506_08284_b200.inputs import discretize_hex
+
+
+def test_hsw_ddot_matches_pinned_numpy():
+    """The Haswell ddot restatement equals numpy's dot under the survey pin."""
+    code = r"""
+import numpy as np, sys
+sys.path.insert(0, %r)
+from oracle.hcurl_oracle import hsw_dot, hsw_norm
+rng = np.random.default_rng(3)
+bad = 0
+for n in list(range(0, 70)) + [1000, 4095, 65537, 300001, 2000003]:
+    x = rng.standard_normal(n) * np.exp(3 * rng.standard_normal(n))
+    y = rng.standard_normal(n)
+    bad += hsw_dot(x, y) != float(x @ y)
+    bad += hsw_norm(x) != float(np.linalg.norm(x))
+print(bad)
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, OPENBLAS_CORETYPE="Haswell", OPENBLAS_NUM_THREADS="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, check=True,
+                         capture_output=True, text=True).stdout
+    assert out.strip() == "0"
+
+
+def test_reduceat_rule():
+    rng = np.random.default_rng(0)
+    for n in range(1, 300):
+        a = rng.standard_normal(n) * np.exp(4 * rng.standard_normal(n))
+        import scipy.sparse as sp
+        A = sp.csr_matrix(a[None, :])
+        assert O.reduceat_rows(A)[0] == np.asarray(A.sum(axis=1)).ravel()[0]
+
+
+def _run(name, smoother="gs"):
+    meta, arrays = load_case(name)
+    s = discretize_hex(meta["N"], meta["sigma"], meta["dirichlet"])
+    h = O.build_hierarchy(s.A_e, s.S, s.A_n, s.D, coarse_size=meta["coarse_size"],
+                          smoother=smoother)
+    b = np.random.default_rng(meta["seed"]).uniform(-1, 1, s.A_e.shape[0])
+    return meta, arrays, h, b
+
+
+def _check_hierarchy(meta, arrays, h):
+    assert [lv.A_e.shape[0] for lv in h.levels] == meta["n_edges"]
+    assert [int(lv.A_e.nnz) for lv in h.levels] == meta["nnz_A_e"]
+    assert abs(h.operator_complexity - meta["operator_complexity"]) < 1e-14
+    for li, (lv, L) in enumerate(zip(h.levels, meta["levels"])):
+        assert csr_hash(lv.D) == L["D"]
+        if lv.P_e is None:
+            continue
+        # BIT class: nodal chain and topology
+        assert sha(lv.membership.astype(np.int64)) == L["membership"]
+        assert float(lv.omega).hex() == L["omega_hex"]
+        assert float(lv.rho).hex() == L["rho_hex"]
+        assert csr_hash(lv.P_n) == L["P_n"]
+        assert sha(lv.assignment.astype(np.int64)) == L["assignment"]
+        assert sha(lv.coarse.pairs.astype(np.int64)) == L["pairs"]
+        assert sha(lv.coarse.singles.astype(np.int64)) == L["singles"]
+        # STRUCT: prolongator pattern
+        P = lv.P_e
+        assert sha(P.indptr.astype(np.int64), P.indices.astype(np.int64)) == L["P_e_pattern"]
+        dims = sorted([list(k) + [v] for k, v in lv.emin.subproblem_dims.items()])
+        assert dims == L["subproblem_dims"]
+        # TOL: values
+        rows = arrays[f"L{li}_Pe_sample_rows"]
+        ref = golden_csr(arrays, f"L{li}_Pe_sample", (rows.size, P.shape[1]))
+        d = abs(P[rows] - ref)
+        assert (d.max() if d.nnz else 0.0) <= 1e-10 * abs(ref).max()
+        e_ref = np.array(L["emin_energy"])
+        assert np.allclose(lv.emin.energy_history, e_ref, rtol=1e-10, atol=0)
+        assert lv.emin.commutator_residual <= 1e-12
+        assert abs(np.linalg.norm(P.data) - L["P_e_fro"]) <= 1e-10 * L["P_e_fro"]
+
+
+SMALL = ["N4n", "N6d", "N8d", "N10n", "C1"]
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_oracle_hierarchy_and_solve(name):
+    meta, arrays, h, b = _run(name)
+    _check_hierarchy(meta, arrays, h)
+    res = O.solve(h, b)
+    assert res.status == meta["gs"]["status"]
+    assert res.iterations == meta["gs"]["iterations"]
+    np.testing.assert_allclose(res.residual_history, meta["gs"]["residual_history"],
+                               rtol=1e-3)
+    if "gs_x" in arrays:
+        assert np.max(np.abs(res.x - arrays["gs_x"])) <= 1e-8 * np.max(np.abs(arrays["gs_x"]))
+
+
+@pytest.mark.parametrize("name", ["N6d", "C1"])
+def test_oracle_chebyshev_matches_reference_seam(name):
+    meta, arrays, h, b = _run(name, smoother="cheb")
+    res = O.solve(h, b)
+    assert res.iterations == meta["cheb"]["iterations"]
+    np.testing.assert_allclose(res.residual_history, meta["cheb"]["residual_history"],
+                               rtol=1e-3)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["N16n", "C2"])
+def test_oracle_hierarchy_large(name):
+    meta, arrays, h, b = _run(name)
+    _check_hierarchy(meta, arrays, h)
+
+
+def test_oracle_error_case():
+    import json
+    from golden_util import GOLDEN
+    with open(os.path.join(GOLDEN, "errors.json")) as f:
+        msg = json.load(f)["N8d_cs100"]
+    s = discretize_hex(8, 1.0, True)
+    with pytest.raises(ValueError) as e:
+        O.build_hierarchy(s.A_e, s.S, s.A_n, s.D, coarse_size=100)
+    # the magnitudes are round-off of a collapsed coarse operator; the
+    # decision and the level must agree
+    assert str(e.value).split(":")[0] == msg.split(":")[0]

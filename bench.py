@@ -1,0 +1,374 @@
+"""Benchmark: SpHcurlAMG setup + PCG solve to 1e-8 on the B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step is one pass of the hot path over one synthetic problem: build_hierarchy
+(constrained-energy-minimisation prolongators, Galerkin products, coarse
+gradients) followed by pcg_solve with the Chebyshev-Hiptmair V-cycle, rtol 1e-8.
+The default workload is BASELINE.json configs[1] ("C2": 32^3 hex, Dirichlet,
+sigma = 1e-2, RHS U[-1,1] seed 1, coarse_size 1000). Inputs are synthetic
+(the reference's own model problem, assembled bit-identically in-tree).
+
+value = edge DOFs/s of setup + solve with the inputs resident in HBM; e2e = the
+same through the public API with host (scipy / numpy) inputs and the solution
+copied back, host<->device copies inside the timed region. Multi-GPU (torchrun):
+every rank solves its own replica (weak scaling, no data-path collective --
+DESIGN.md "Multi-GPU"); timing is the max over ranks.
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle port in oracle/, Gauss-Seidel smoother as in the reference) on rank 0.
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return PEAKS_FALLBACK, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            self.p.terminate()
+            out, _ = self.p.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": mx or None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def vcycle_bytes(h, degree=3):
+    """Algorithmic bytes of one V-cycle: per level
+    p_A beta(A_e) + p_X beta(D^T A D) + p_D beta(D) + p_P beta(P_e), plus the
+    dense coarsest GEMV; beta(M) = 12 nnz + 8 (rows + 1) + 8 (rows + cols)."""
+    def beta(M):
+        r, c = M.shape
+        return 12 * M.nnz + 8 * (r + 1) + 8 * (r + c)
+    pA, pX, pD, pP = 4 * degree + 3, 2 * degree, 4, 2
+    tot = 0
+    for lv in h.levels[:-1]:
+        tot += pA * beta(lv.A_e) + pX * beta(lv.nodal_aux) + pD * beta(lv.D) + pP * beta(lv.P_e)
+    nc = h.levels[-1].A_e.shape[0]
+    return tot + 8 * nc * nc + 16 * nc
+
+
+def cheb_kernel_bytes(A):
+    """Algorithmic bytes of one fused Chebyshev step on A: the CSR pass
+    (12 nnz + 8 (n + 1)) plus x gather, b, dinv, d (read + write), x_out."""
+    n = A.shape[0]
+    return 12 * A.nnz + 8 * (n + 1) + 8 * 6 * n
+
+
+def make_problem(config, N=None):
+    from paper_2506_08284_b200.inputs import make_config
+    sysm, rhs, cfg = make_config(config, N)
+    return sysm, rhs, cfg
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as tdist
+    from paper_2506_08284_b200 import _lib, device as dv, multigrid as mg
+    from paper_2506_08284_b200.build import build_library
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    build_library()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sysm, rhs, cfg = make_problem(args.config, args.N)
+    n_e = sysm.A_e.shape[0]
+    scfg = mg.SolverConfig(coarse_size=args.coarse_size)
+
+    # inputs resident in HBM for the device-timed value
+    A_e = dv.DeviceCSR.from_scipy(sysm.A_e)
+    S = dv.DeviceCSR.from_scipy(sysm.S)
+    A_n = dv.DeviceCSR.from_scipy(sysm.A_n)
+    D = dv.DeviceCSR.from_scipy(sysm.D)
+    b = torch.from_numpy(rhs).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def step():
+        h = mg.build_hierarchy(A_e, S, A_n, D, scfg)
+        res = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+        return h, res
+
+    def barrier():
+        if ws > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        h, res = step()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    l0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))          # L2 flush (256 MB > 126 MB L2), untimed
+            ev[k][0].record()
+            h, res = step()
+            ev[k][1].record()
+        barrier()
+    launches = (_lib.launch_count() - l0) // args.steps
+    step_ms = [a.elapsed_time(bb) for a, bb in ev]
+    t_step = sum(step_ms) / args.steps
+    if ws > 1:
+        t = torch.tensor([t_step], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        t_step = float(t.item())
+    iters = res.iterations
+    assert res.status == "converged", res.status
+
+    # setup / solve split and V-cycle bandwidth (device events, untimed region)
+    flush.fill_(1.0)
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record()
+    h = mg.build_hierarchy(A_e, S, A_n, D, scfg)
+    e1.record()
+    res = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+    e2.record()
+    torch.cuda.synchronize()
+    t_setup, t_solve = e0.elapsed_time(e1), e1.elapsed_time(e2)
+    pre = mg.v_cycle_preconditioner(h)
+    nv = 20
+    for _ in range(3):
+        pre(b)
+    flush.fill_(2.0)
+    v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    v0.record()
+    for _ in range(nv):
+        pre(b)
+    v1.record()
+    torch.cuda.synchronize()
+    t_vc = v0.elapsed_time(v1) / nv
+    vbytes = vcycle_bytes(h, scfg.cheb_degree)
+
+    # dominant solve kernel: the fused Chebyshev step on the finest A_e
+    sw = h.levels[0].edge_sweeper
+    A0 = h.levels[0].A_e
+    x0 = torch.zeros(n_e, dtype=torch.float64, device=dev)
+    nk = 50
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cd, cr = sw.coefs[1]
+    for _ in range(3):
+        _lib.call("sphc_cheb_step", n_e, A0.rowptr, A0.col, A0.val, sw.lanes, sw.dinv, b, x0,
+                  sw.buf[0], sw.d, cd, cr, 0)
+    k0.record()
+    for _ in range(nk):
+        _lib.call("sphc_cheb_step", n_e, A0.rowptr, A0.col, A0.val, sw.lanes, sw.dinv, b, x0,
+                  sw.buf[0], sw.d, cd, cr, 0)
+    k1.record()
+    torch.cuda.synchronize()
+    t_k = k0.elapsed_time(k1) / nk
+    kbytes = cheb_kernel_bytes(A0)
+
+    # e2e: public API with host inputs, solution back to host
+    e2e_ms = []
+    for k in range(max(2, min(args.steps, 5))):
+        flush.fill_(3.0 + k)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        he = mg.build_hierarchy(sysm.A_e, sysm.S, sysm.A_n, sysm.D, scfg)
+        re = mg.pcg_solve(sysm.A_e, rhs, mg.v_cycle_preconditioner(he))
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        assert isinstance(re.x, np.ndarray)
+    t_e2e = sum(e2e_ms) / len(e2e_ms)
+    if ws > 1:
+        t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    def csr_bytes(M):
+        return M.data.nbytes + M.indices.size * 4 + M.indptr.size * 8
+    # build_hierarchy uploads (A_e, S, A_n, D); pcg_solve uploads A_e and b
+    h2d = sum(csr_bytes(M) for M in (sysm.A_e, sysm.S, sysm.A_n, sysm.D)) \
+        + csr_bytes(sysm.A_e) + rhs.nbytes
+    d2h = n_e * 8
+
+    pk, pk_kind = peaks()
+    peak = float(pk["hbm_gbs"])
+    achieved = kbytes / (t_k * 1e-3) / 1e9
+    line = None
+    if rank == 0:
+        cpu = cpu_baseline(args) if (ws == 1 and not args.no_cpu_baseline) else None
+        line = {
+            "metric": "edge DOFs/s for setup + PCG solve to 1e-8",
+            "value": ws * n_e / (t_step * 1e-3),
+            "unit": "edge DOFs/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (reference model problem, seeded RHS)",
+            "config": {"workload": f"{args.config}: {cfg['N']}^3 hex, "
+                       f"{'Dirichlet' if cfg['dirichlet'] else 'natural'}, "
+                       f"sigma={cfg['sigma']}, rhs seed {cfg['seed']}, "
+                       f"coarse_size {args.coarse_size}",
+                       "n_edges": n_e, "levels": [lv.A_e.shape[0] for lv in h.levels],
+                       "operator_complexity": h.operator_complexity,
+                       "pcg_iterations": iters, "smoother": "chebyshev-3 hiptmair",
+                       "parallelism": f"replicas x{ws}",
+                       "l2": "256 MB flush before every timed step"},
+            "setup_ms": t_setup, "solve_ms": t_solve,
+            "setup_dofs_per_s": n_e / (t_setup * 1e-3),
+            "solve_dofs_per_s": n_e / (t_solve * 1e-3),
+            "vcycle": {"ms": t_vc, "bytes": vbytes,
+                       "achieved_gbs": vbytes / (t_vc * 1e-3) / 1e9,
+                       "frac_of_peak": vbytes / (t_vc * 1e-3) / 1e9 / peak},
+            "roofline": {"bound": "hbm", "kernel": "k_cheb<lanes> (fused Chebyshev step, level-0 A_e)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_source": pk_kind, "launch_ms": t_k,
+                         "algorithmic_bytes": kbytes},
+            "e2e": {"value": ws * n_e / (t_e2e * 1e-3), "unit": "edge DOFs/s",
+                    "ms": t_e2e, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+    return line
+
+
+def _oracle_step(sysm, rhs, coarse_size, smoother):
+    from oracle import hcurl_oracle as O
+    t0 = time.perf_counter()
+    h = O.build_hierarchy(sysm.A_e, sysm.S, sysm.A_n, sysm.D, coarse_size=coarse_size,
+                          smoother=smoother)
+    res = O.solve(h, rhs)
+    return time.perf_counter() - t0, res
+
+
+def cpu_baseline(args):
+    """The oracle port (reference algorithm, Gauss-Seidel) on a bounded sample
+    of the workload: C1 (16^3) setup + solve, 1 host core."""
+    sysm, rhs, cfg = make_problem("C1")
+    t, res = _oracle_step(sysm, rhs, 1000, "gs")
+    n_e = sysm.A_e.shape[0]
+    return {"value": n_e / t, "unit": "edge DOFs/s", "cores": 1, "kind": "port",
+            "sample": f"C1 16^3 Dirichlet ({n_e} edges) setup+solve, {res.iterations} its, "
+                      f"{t:.2f} s"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    sysm, rhs, cfg = make_problem(args.config, args.N)
+    n_e = sysm.A_e.shape[0]
+    for _ in range(min(args.warmup, 1)):
+        _oracle_step(*make_problem("C1")[:2], 1000, "gs")
+    k = max(1, min(args.steps, args.ref_steps))
+    times = []
+    for _ in range(k):
+        t, res = _oracle_step(sysm, rhs, args.coarse_size, "gs")
+        times.append(t)
+    tm = sum(times) / k
+    v = n_e / tm
+    line = {"impl": "reference", "metric": "edge DOFs/s for setup + PCG solve to 1e-8",
+            "value": v, "unit": "edge DOFs/s", "n_gpus": ws, "steps": k,
+            "warmup": min(args.warmup, 1), "ms_per_step": tm * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (reference model problem, seeded RHS)",
+            "config": {"workload": f"{args.config}: {cfg['N']}^3 hex", "n_edges": n_e,
+                       "pcg_iterations": res.iterations, "smoother": "gauss-seidel (reference)"},
+            "cpu_baseline": {"value": v, "unit": "edge DOFs/s", "cores": 1, "kind": "port",
+                             "sample": f"{args.config} full setup+solve x{k} (capped at "
+                                       f"{args.ref_steps} steps)"},
+            "e2e": {"value": v, "unit": "edge DOFs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--N", type=int, default=None)
+    ap.add_argument("--coarse-size", type=int, default=1000)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,297 @@
+/*
+ * sphcurl.h -- C ABI of libsphcurl.so, the B200 (sm_100a) kernels behind the
+ * SpHcurlAMG setup + solve hot path (arxiv 2506.08284).
+ *
+ * The reference has no FFI: its boundary is the Python API
+ *   build_hierarchy(A_e, S_e, A_n, D, cfg)      multigrid.py:119
+ *   v_cycle_preconditioner(h)                    multigrid.py:191
+ *   pcg_solve(A, b, precond, rtol, maxit)        multigrid.py:220
+ *   build_edge_prolongator(A_n, A_e, S, D_h, cfg) edge_prolongator.py:184
+ * which paper_2506_08284_b200/{multigrid,edge_prolongator}.py mirror (same
+ * names, arguments, dataclass fields and ValueError texts). Every numeric call
+ * those mirrors make lands here. Each entry point below names the reference
+ * function (file:line) whose arithmetic it replaces.
+ *
+ * Conventions
+ *  - Plain device pointers and sizes; no torch types. CSR = int64 row
+ *    pointers, int32 column indices, fp64 values. Vectors are fp64.
+ *  - `stream` is a cudaStream_t; every call is stream ordered and asynchronous
+ *    unless documented otherwise. Scratch is stream-ordered (cudaMallocAsync).
+ *  - Return 0 on success, a negative SPHC_ERR_* on a launch / argument error
+ *    (message in sphc_last_error()).
+ *  - Data-dependent failures (the reference's ValueErrors) are written to a
+ *    caller-owned device array `status` of SPHC_STATUS_SLOTS int64 entries,
+ *    initialised to INT64_MAX: slot k receives the lowest row that failed
+ *    check k (SPHC_ST_*). The caller re-raises with the reference's message.
+ */
+#ifndef SPHCURL_H
+#define SPHCURL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPHC_OK 0
+#define SPHC_ERR_CUDA (-1)
+#define SPHC_ERR_ARG (-2)
+#define SPHC_ERR_HOST (-3)
+
+#define SPHC_STATUS_SLOTS 16
+#define SPHC_ST_ZERO_DIAG 0        /* multigrid.py:38-40  zero diagonal entry in row r   */
+#define SPHC_ST_NONPOS_DIAG 1      /* nodal_amg.py:41-43  nonpositive diagonal entry     */
+#define SPHC_ST_NODAL_ZERO_DIAG 2  /* nodal_amg.py:147-148 zero diagonal in nodal operator */
+#define SPHC_ST_ZERO_ROWSUM 3      /* nodal_amg.py:131-133 zero row sum before scaling   */
+#define SPHC_ST_MALFORMED_GRAD 4   /* emin_setup.py:71-74 malformed gradient             */
+#define SPHC_ST_EMPTY_I 5          /* emin_setup.py:292   row with empty prolongator pattern */
+#define SPHC_ST_REDUCIBLE 6        /* emin_setup.py:304   block needs make_irreducible   */
+#define SPHC_ST_RANK_LOW 7         /* emin_setup.py:233-237 rank below expected          */
+#define SPHC_ST_EMIN_CAPACITY 8    /* row exceeds the emin kernel's |J|<=16, |I|<=64     */
+#define SPHC_ST_EMPTY_J 9          /* emin_setup.py:125-127 empty constraint pattern     */
+#define SPHC_ST_SPGEMM_CAPACITY 10 /* SpGEMM row exceeds the on-chip accumulator         */
+#define SPHC_ST_SORT_CAPACITY 11   /* segmented sort row too long                        */
+
+#define SPHC_EMIN_JMAX 16
+#define SPHC_EMIN_IMAX 64
+#define SPHC_DIMS_I 65 /* subproblem_dims histogram is [SPHC_DIMS_I][SPHC_DIMS_J] */
+#define SPHC_DIMS_J 17
+
+const char *sphc_last_error(void);
+int sphc_abi_version(void);
+/* number of kernels this library has launched in this process */
+int64_t sphc_launch_count(void);
+
+/* ---------------------------------------------------------------- primitives */
+
+/* Exclusive scan of n counts into n+1 offsets (offsets[n] = total). Builds
+ * every CSR row pointer (reference: scipy indptr construction). */
+int sphc_scan_i64(int64_t n, const int64_t *counts, int64_t *offsets, void *stream);
+
+/* *out = sum x_i y_i with a fixed two-pass tree (deterministic).
+ * Replaces numpy dot in pcg_solve (multigrid.py:229,236,243,258,266). */
+int sphc_dot(int64_t n, const double *x, const double *y, double *out, void *stream);
+
+/* *out = sum x_i (fixed two-pass tree). Energies (edge_prolongator.py:154-156). */
+int sphc_sum(int64_t n, const double *x, double *out, void *stream);
+
+/* *out = max |x_i| (0 for n = 0). sparse_ops.py:116-119 max_abs. */
+int sphc_maxabs(int64_t n, const double *x, double *out, void *stream);
+
+/* *out = x . y in the OpenBLAS-Haswell ddot order (16 FMA chains, fixed
+ * combine, plain tail): bit-identical to np.linalg.norm's dot under the
+ * survey's BLAS pin. estimate_rho, nodal_amg.py:106-111. */
+int sphc_hsw_dot(int64_t n, const double *x, const double *y, double *out, void *stream);
+
+/* v = w / sqrt(*sq) elementwise (IEEE); writes sqrt(*sq) to *norm_out.
+ * nodal_amg.py:107-115 (v /= norm). */
+int sphc_scale_by_norm(int64_t n, const double *w, const double *sq, double *v,
+                       double *norm_out, void *stream);
+
+/* y = 1 / x elementwise, IEEE division (diags(1.0 / d), nodal_amg.py:150,
+ * edge_prolongator.py:173). When zero_sub != NULL, zero entries of x are
+ * replaced by *zero_sub first (_jacobi_diag, edge_prolongator.py:159-167). */
+int sphc_reciprocal(int64_t n, const double *x, const double *zero_sub, double *y,
+                    void *stream);
+
+/* y = a x + b y */
+int sphc_axpby(int64_t n, double a, const double *x, double b, double *y, void *stream);
+
+/* ---------------------------------------------------------------- CSR utilities */
+
+/* d_i = A_ii (0 if not stored); flags zero diagonals into status[ZERO_DIAG]
+ * when status != NULL. multigrid.py:36-40, nodal_amg.py:40-43. */
+int sphc_csr_diag(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                  double *d, int64_t *status, void *stream);
+
+/* Sort every row of a CSR by column (stable for equal keys is not needed:
+ * keys are unique per row), carrying fp64 values when v != NULL. */
+int sphc_csr_sort_rows(int64_t n, const int64_t *rp, int32_t *ci, double *v,
+                       int64_t *status, void *stream);
+
+/* Transpose with sorted output rows (ascending original row index) -- the
+ * CSC view scipy builds for A.T @ B (multigrid.py:150-152, coarse_gradient.py:46). */
+int sphc_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t *rp,
+                       const int32_t *ci, const double *v, int64_t *trp, int32_t *tci,
+                       double *tv, int64_t *status, void *stream);
+
+/* counts_i = number of nonzero stored values in row i */
+int sphc_csr_count_nonzero(int64_t n, const int64_t *rp, const double *v, int64_t *counts,
+                           void *stream);
+
+/* Drop exact zeros (sparse_ops.py:107-113 compress(A, 0)). new_rp from
+ * sphc_csr_count_nonzero + sphc_scan_i64. */
+int sphc_csr_compact(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                     const int64_t *new_rp, int32_t *nci, double *nv, void *stream);
+
+/* out = dense row-major copy of A (coarsest level, multigrid.py:157 toarray) */
+int sphc_csr_to_dense(int64_t n_rows, int64_t n_cols, const int64_t *rp, const int32_t *ci,
+                      const double *v, double *out, void *stream);
+
+/* ---------------------------------------------------------------- SpGEMM */
+
+/* Structural nnz of each row of C = A B (unique columns). */
+int sphc_spgemm_count(int64_t n, const int64_t *arp, const int32_t *aci, const int64_t *brp,
+                      const int32_t *bci, int64_t *counts, int64_t *status, void *stream);
+
+/* Numeric C = A B on the structural pattern, columns ascending. Every entry
+ * is a sequential sum over k ascending of a_ik * b_kj with no FMA, which is
+ * scipy csr_matmat's order: bit-identical for the nodal Galerkin product
+ * (multigrid.py:152) and used for the edge Galerkin products (:150-151), the
+ * auxiliary nodal operator D^T A D (:103) and the null-space check (:111). */
+int sphc_spgemm_fill(int64_t n, const int64_t *arp, const int32_t *aci, const double *av,
+                     const int64_t *brp, const int32_t *bci, const double *bv,
+                     const int64_t *crp, int32_t *cci, double *cv, int64_t *status,
+                     void *stream);
+
+/* ---------------------------------------------------------------- solve */
+
+/* y = alpha * (A x) + beta * z  (z may be NULL; y may alias z).
+ * `lanes` (1,2,4,8,16,32) = lanes per row. csr_matvec call sites
+ * multigrid.py:46,51,168,171,183,186,242,252. */
+int sphc_spmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *v, int lanes,
+              const double *x, double alpha, double beta, const double *z, double *y,
+              void *stream);
+
+/* One Chebyshev step, fused: d <- cd*d + cr*dinv*(b - A x_in); x_out = x_in + d.
+ * x_zero != 0 means x_in == 0 (A x skipped). Replaces the reference's
+ * Gauss-Seidel half sweeps (multigrid.py:45-59) in the smoother seam. */
+int sphc_cheb_step(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                   int lanes, const double *dinv, const double *b, const double *x_in,
+                   double *x_out, double *d, double cd, double cr, int x_zero, void *stream);
+
+/* y_i = d_i x_i (Jacobi scaling in the smoother's power iteration). */
+int sphc_diag_scale(int64_t n, const double *d, const double *x, double *y, void *stream);
+
+/* Deterministic start vector in [-1, 1) for the smoother's spectral bound
+ * (splitmix64 of the index; oracle.cheb_start_vector computes the same). */
+int sphc_cheb_start(int64_t n, double *x, void *stream);
+
+/* x += alpha p; r -= alpha Ap; *changed = 1 if any x_i changed
+ * (multigrid.py:247-257, the array_equal stagnation test). */
+int sphc_pcg_update(int64_t n, double alpha, const double *p, const double *Ap, double *x,
+                    double *r, int32_t *changed, void *stream);
+
+/* p = z + beta p (multigrid.py:270). */
+int sphc_pcg_direction(int64_t n, double beta, const double *z, double *p, void *stream);
+
+/* y = A x for a dense row-major n x n A (coarsest level, explicit inverse of
+ * the reference's lu_factor/lu_solve pair, multigrid.py:157,181). */
+int sphc_dense_gemv(int64_t n, const double *A, const double *x, double *y, void *stream);
+
+/* ---------------------------------------------------------------- nodal chain */
+
+/* Strength pattern rows (nodal_amg.py:33-56): entries with
+ * |a_ij| > drop_tol*sqrt(a_ii a_jj), plus the diagonal. Flags nonpositive
+ * diagonals. Symmetrised afterwards with sphc_csr_transpose + union. */
+int sphc_strength_count(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                        const double *diag, double drop_tol, int64_t *counts,
+                        int64_t *status, void *stream);
+int sphc_strength_fill(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                       const double *diag, double drop_tol, const int64_t *frp,
+                       int32_t *fci, void *stream);
+/* C = pattern(A) U pattern(B), sorted rows */
+int sphc_pattern_union_count(int64_t n, const int64_t *arp, const int32_t *aci,
+                             const int64_t *brp, const int32_t *bci, int64_t *counts,
+                             void *stream);
+int sphc_pattern_union_fill(int64_t n, const int64_t *arp, const int32_t *aci,
+                            const int64_t *brp, const int32_t *bci, const int64_t *crp,
+                            int32_t *cci, void *stream);
+
+/* w = (diag(1/d) A) v with every row summed in DESCENDING column order, no FMA
+ * -- the storage order scipy gives diags(1/d) @ A (nodal_amg.py:150-151,110). */
+int sphc_nodal_powmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                     const double *dinv, const double *x, double *y, void *stream);
+
+/* Smoothed + normalised nodal prolongator rows (nodal_amg.py:119-155):
+ * P = normalize((I - omega D^-1 A) P_tent), bit-faithful (Appendix A). */
+int sphc_nodal_smooth_count(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                            const double *dinv, const int64_t *memb, double omega,
+                            int64_t *counts, int64_t *status, void *stream);
+int sphc_nodal_smooth_fill(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                           const double *dinv, const int64_t *memb, double omega,
+                           const int64_t *prp, int32_t *pci, double *pv, int64_t *status,
+                           void *stream);
+
+/* ---------------------------------------------------------------- coarse topology */
+
+/* Coarse edges (coarse_gradient.py:106-136): for every fine gradient row with
+ * two entries whose endpoints lie in different aggregates a<b, bucket b under a.
+ * count -> scan -> fill -> sphc_csr_sort_rows -> unique. */
+int sphc_coarse_pairs_count(int64_t n_e, const int64_t *drp, const int32_t *dci,
+                            const int64_t *assign, int64_t *counts, void *stream);
+int sphc_coarse_pairs_fill(int64_t n_e, const int64_t *drp, const int32_t *dci,
+                           const int64_t *assign, const int64_t *brp, int64_t *cursor,
+                           int32_t *bcol, void *stream);
+int sphc_unique_count(int64_t n, const int64_t *rp, const int32_t *ci, int64_t *counts,
+                      void *stream);
+int sphc_unique_fill(int64_t n, const int64_t *rp, const int32_t *ci, const int64_t *urp,
+                     int32_t *uci, void *stream);
+
+/* flags[c] = 1 if aggregate c owns the free end of a one-entry gradient row
+ * (coarse_gradient.py:139-160, augment_dirichlet_edges). */
+int sphc_single_flags(int64_t n_e, const int64_t *drp, const int32_t *dci,
+                      const int64_t *assign, int64_t *flags, void *stream);
+
+/* D_H rows: interior edge e=(a,b): -1 at a, +1 at b; single-node edge: +1.
+ * Also writes ep_a/ep_b (ep_a = -1 for single-node edges). */
+int sphc_build_coarse_gradient(int64_t n_agg, int64_t n_int, const int64_t *adj_rp,
+                               const int32_t *adj_col, const int64_t *single_off,
+                               int64_t n_single, int64_t *dh_rp, int32_t *dh_ci,
+                               double *dh_v, int32_t *ep_a, int32_t *ep_b,
+                               int32_t *single_id, void *stream);
+
+/* ---------------------------------------------------------------- emin */
+
+/* Per fine edge (emin_setup.py:62-336, Appendix C): node set J (= T row),
+ * coarse-edge set I (= prolongator pattern N row), |I|,|J|, the
+ * subproblem_dims histogram [65][17] (rows with |I| > 0) and
+ * rmax2[0] = max |D_h P_n| over all rows (emin_setup.py:289),
+ * rmax2[1] = the same over rows whose I is empty (emin_setup.py:292-295). */
+int sphc_emin_count(int64_t n_e, const int64_t *drp, const int32_t *dci, const double *dv,
+                    const int64_t *prp, const int32_t *pci, const double *pv,
+                    const int64_t *adj_rp, const int32_t *adj_col, int64_t n_int,
+                    const int32_t *single_id, int64_t *icount, int64_t *jcount,
+                    double *rmax2, int64_t *dims, int64_t *status, void *stream);
+
+/* Writes T (J columns + commutator rhs r = D_h P_n on J) and the prolongator
+ * row pattern I with the feasible guess p = 1 + G_k (G_k^T G_k)^-1 (r - G^T 1)_k
+ * (edge_prolongator.py:104-126; Gram-Cholesky form of the QR least-norm solve). */
+int sphc_emin_fill(int64_t n_e, const int64_t *drp, const int32_t *dci, const double *dv,
+                   const int64_t *prp, const int32_t *pci, const double *pv,
+                   const int64_t *adj_rp, const int32_t *adj_col, int64_t n_int,
+                   const int32_t *single_id, const int64_t *trp, int32_t *tci, double *tv,
+                   const int64_t *erp, int32_t *eci, double *ev, int64_t *status,
+                   void *stream);
+
+/* One projected damped-Jacobi sweep (edge_prolongator.py:170-176) fused with
+ * the masked product S P on the fixed pattern, the energy of the INPUT values
+ * (:154-156) and the commutator residual of the OUTPUT (:179-181):
+ *   g = (S P_in)|_I ; e_row[i] = p_in . g ; delta = dinv_i g ;
+ *   delta -= G_k M^-1 G_k^T delta ; P_out = P_in - omega delta (update != 0)
+ *   res_max = max |G^T p_out - r| over J.
+ * With update == 0 only e_row and res_max (of P_in) are produced. */
+int sphc_emin_step(int64_t n_e, const int64_t *srp, const int32_t *sci, const double *sv,
+                   const double *dinv, const int64_t *trp, const int32_t *tci,
+                   const double *tv, const int64_t *erp, const int32_t *eci,
+                   const double *p_in, double *p_out, const int32_t *ep_a,
+                   const int32_t *ep_b, double omega, int update, double *e_row,
+                   double *res_max, int64_t *status, void *stream);
+
+/* ---------------------------------------------------------------- host (C++) */
+
+/* Greedy two-phase aggregation, exact reference semantics
+ * (nodal_amg.py:59-88). Host arrays. Returns n_agg in *n_agg. */
+int sphc_host_aggregate(int64_t n, const int64_t *rp, const int32_t *ci, int64_t *membership,
+                        int64_t *n_agg);
+
+/* Algorithm 1 (coarse_gradient.py:36-103) on a host CSR copy of P_n.
+ * On a data error returns SPHC_ERR_HOST with err[0] = kind (1 empty column,
+ * 2 row with no entries, 3 empty column after safeguard), err[1] = index. */
+int sphc_host_piecewise_const(int64_t m_h, int64_t m_H, const int64_t *rp, const int32_t *ci,
+                              const double *v, int n_passes, int64_t *assign, int64_t *err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

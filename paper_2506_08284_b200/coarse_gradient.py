@@ -1,0 +1,103 @@
+"""Coarse discrete gradients from nodal grid transfers, on the B200.
+
+Mirror of the reference's coarse_gradient.py. ``gen_piecewise_const``
+(Algorithm 1) is the host C++ greedy pass of libsphcurl on the downloaded
+nodal prolongator; the coarse edge set, the Dirichlet single-node edges and
+D_H are built by libsphcurl kernels (bucket by lower aggregate, segmented
+sort, unique, scan).
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import device as dv
+from .device import DeviceCSR, Status, as_device_csr, call
+
+
+@dataclass
+class CoarseGradient:
+    """Coarse edge-to-node incidence plus its edge bookkeeping
+    (coarse_gradient.py:19-33)."""
+
+    D_H: DeviceCSR
+    n_interior: int               # interior edges come first, sorted (a, b)
+    n_single: int                 # then single-node edges, sorted by node
+    adj: DeviceCSR                # upper adjacency: row a -> b's, edge id = position
+    ep_a: torch.Tensor            # int32 [n_edges] tail node (-1 single-node)
+    ep_b: torch.Tensor            # int32 [n_edges] head / single node
+    single_id: torch.Tensor       # int32 [n_nodes] single-node edge id or -1
+    augmented_edges: list = None
+
+    @property
+    def n_edges(self):
+        return self.D_H.shape[0]
+
+    @property
+    def n_nodes(self):
+        return self.D_H.shape[1]
+
+    @property
+    def edge_endpoints(self):
+        a = self.ep_a.cpu().numpy()
+        b = self.ep_b.cpu().numpy()
+        return [(int(x), int(y)) if x >= 0 else (int(y),) for x, y in zip(a, b)]
+
+
+def gen_piecewise_const(P, n_passes=2):
+    """Algorithm 1 (coarse_gradient.py:36-103): the column assigned to every
+    row (int64, device). Returned as the assignment vector rather than the
+    0/1 matrix P_const (one unit entry per row at that column)."""
+    P = as_device_csr(P)
+    m_h, m_H = P.shape
+    rp = P.rowptr.cpu().numpy()
+    ci = P.col.cpu().numpy()
+    v = P.val.cpu().numpy()
+    assign = np.empty(m_h, dtype=np.int64)
+    err = np.zeros(2, dtype=np.int64)
+    rc = call("sphc_host_piecewise_const", m_h, m_H, rp, ci, v, int(n_passes), assign, err)
+    if rc != 0:
+        kind, idx = int(err[0]), int(err[1])
+        if kind == 2:
+            raise ValueError(f"row {idx} has no entries to assign")
+        raise ValueError(f"empty column {idx} cannot be assigned any row")
+    return torch.from_numpy(assign).to(P.rowptr.device)
+
+
+def build_coarse_gradient(D_h, assignment, n_agg):
+    """Coarse edges from the projected node-graph Laplacian plus the Dirichlet
+    single-node edges (coarse_gradient.py:106-160, build_coarse_gradient
+    followed by augment_dirichlet_edges)."""
+    D = as_device_csr(D_h)
+    n_e = D.shape[0]
+    dev = D.rowptr.device
+    cnt = torch.zeros(n_agg, dtype=torch.int64, device=dev)
+    call("sphc_coarse_pairs_count", n_e, D.rowptr, D.col, assignment, cnt)
+    brp, nb = dv.scan(cnt)
+    bcol = torch.empty(nb, dtype=torch.int32, device=dev)
+    cursor = torch.zeros(n_agg, dtype=torch.int64, device=dev)
+    call("sphc_coarse_pairs_fill", n_e, D.rowptr, D.col, assignment, brp, cursor, bcol)
+    st = Status()
+    call("sphc_csr_sort_rows", n_agg, brp, bcol, None, st.t)
+    dv._raise_capacity(st)
+    call("sphc_unique_count", n_agg, brp, bcol, cnt)
+    arp, n_int = dv.scan(cnt)
+    acol = torch.empty(n_int, dtype=torch.int32, device=dev)
+    call("sphc_unique_fill", n_agg, brp, bcol, arp, acol)
+    flags = torch.zeros(n_agg, dtype=torch.int64, device=dev)
+    call("sphc_single_flags", n_e, D.rowptr, D.col, assignment, flags)
+    soff, n_single = dv.scan(flags)
+    n_edges = n_int + n_single
+    dh_rp = torch.empty(n_edges + 1, dtype=torch.int64, device=dev)
+    dh_ci = torch.empty(2 * n_int + n_single, dtype=torch.int32, device=dev)
+    dh_v = torch.empty(2 * n_int + n_single, dtype=torch.float64, device=dev)
+    ep_a = torch.empty(n_edges, dtype=torch.int32, device=dev)
+    ep_b = torch.empty(n_edges, dtype=torch.int32, device=dev)
+    sid = torch.empty(n_agg, dtype=torch.int32, device=dev)
+    call("sphc_build_coarse_gradient", n_agg, n_int, arp, acol, soff, n_single, dh_rp, dh_ci,
+         dh_v, ep_a, ep_b, sid)
+    return CoarseGradient(D_H=DeviceCSR(dh_rp, dh_ci, dh_v, (n_edges, n_agg)),
+                          n_interior=n_int, n_single=n_single,
+                          adj=DeviceCSR(arp, acol, None, (n_agg, n_agg)),
+                          ep_a=ep_a, ep_b=ep_b, single_id=sid, augmented_edges=[])

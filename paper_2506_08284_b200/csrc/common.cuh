@@ -1,0 +1,112 @@
+// Shared device helpers for libsphcurl (sm_100a, fp64, HBM-bound sparse work).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/sphcurl.h"
+
+typedef int64_t i64;
+
+#define SPHC_WARP 32
+#define FULL_MASK 0xffffffffu
+
+// Number of resident CTAs we size persistent / grid-stride grids for: 148 SMs
+// (2 dies x 74) times a small multiple.
+#define SPHC_NUM_SMS 148
+
+// thread-local last error message (sphc_last_error)
+void sphc_set_error(const char* fmt, ...);
+
+#define SPHC_CUDA(call)                                                      \
+  do {                                                                       \
+    cudaError_t _e = (call);                                                 \
+    if (_e != cudaSuccess) {                                                 \
+      sphc_set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,              \
+                     cudaGetErrorString(_e));                                \
+      return SPHC_ERR_CUDA;                                                  \
+    }                                                                        \
+  } while (0)
+
+extern unsigned long long g_sphc_launches;
+
+#define SPHC_LAUNCH_CHECK()                                                  \
+  do {                                                                       \
+    g_sphc_launches++;                                                       \
+    cudaError_t _e = cudaGetLastError();                                     \
+    if (_e != cudaSuccess) {                                                 \
+      sphc_set_error("%s:%d launch: %s", __FILE__, __LINE__,                 \
+                     cudaGetErrorString(_e));                                \
+      return SPHC_ERR_CUDA;                                                  \
+    }                                                                        \
+  } while (0)
+
+static inline cudaStream_t as_stream(void* s) { return (cudaStream_t)s; }
+
+static inline unsigned grid_for(i64 work, int block, int max_blocks = 148 * 16) {
+  i64 g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > max_blocks) g = max_blocks;
+  return (unsigned)g;
+}
+
+// record the first (lowest) failing row for an error code
+__device__ __forceinline__ void report(i64* status, int code, i64 row) {
+  if (status) atomicMin((unsigned long long*)&status[code], (unsigned long long)row);
+}
+
+// exact IEEE helpers (no contraction): used wherever the reference's scipy /
+// numpy accumulation order defines discrete outcomes
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL_MASK, v, o));
+  return v;
+}
+__device__ __forceinline__ i64 warp_sum_i64(i64 v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+  return v;
+}
+
+// atomic max for non-negative doubles through their ordered bit pattern
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  atomicMax((unsigned long long*)addr, (unsigned long long)__double_as_longlong(v));
+}
+
+// stream-ordered scratch
+template <typename T>
+static inline int scratch(T** p, size_t n, cudaStream_t s) {
+  SPHC_CUDA(cudaMallocAsync((void**)p, (n ? n : 1) * sizeof(T), s));
+  return 0;
+}
+static inline int scratch_free(void* p, cudaStream_t s) {
+  SPHC_CUDA(cudaFreeAsync(p, s));
+  return 0;
+}
+
+// lower_bound in a sorted int array (shared or global)
+__device__ __forceinline__ int lower_bound_i32(const int* a, int n, int key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ i64 lower_bound_i32_g(const int* a, i64 lo, i64 hi, int key) {
+  while (lo < hi) {
+    i64 mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// internal host-side helpers shared across translation units
+int sphc_scan_impl(i64 n, const i64* in, i64* out, cudaStream_t s);

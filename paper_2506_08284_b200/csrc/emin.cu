@@ -1,0 +1,465 @@
+// Constrained energy minimisation of the edge prolongator, one warp per fine
+// edge (reference emin_setup.py:62-336 and edge_prolongator.py:104-228;
+// SURVEY.md Appendix C).
+//
+// For fine edge i with free endpoints t (and h):
+//   J  = sorted union of the P_n rows of its free endpoints      (T row)
+//   r  = (D_h P_n)_i on J                                          (R_dp row)
+//   I  = coarse edges with both ends in J, then single-node edges of J nodes,
+//        ascending ids (prolongator pattern row, N = [B == 2])
+//   G  = D_H[I, J] (+-1), k = |J| - (no single-node edge in I)
+//   M  = G_k^T G_k (graph Laplacian on the first k nodes), Cholesky in smem
+// Feasible guess: p = 1 + G_k M^-1 (r - G^T 1)_k   (== Q R^-T c of the QR route)
+// Jacobi step:    p' = p - omega (d - G_k M^-1 G_k^T d),  d = dinv_i (S P)|_I
+#include "common.cuh"
+
+#define EM_WARPS 4
+#define JM SPHC_EMIN_JMAX
+#define IM SPHC_EMIN_IMAX
+
+struct EminRow {
+  int J[JM];
+  double r[JM];
+  int Icol[IM];
+  int pa[IM];  // position of tail node in J, -1 for single-node edges
+  int pb[IM];  // position of head (or the single) node in J
+  double L[JM * JM];
+  double y[JM];
+  double g[IM];
+  double p[IM];
+  int nJ, nI, k, err;
+};
+
+// lane 0: serial merge of the P_n rows of the (<=2) free endpoints into J, r.
+__device__ void em_build_J(EminRow& R, i64 i, const i64* __restrict__ drp,
+                           const int* __restrict__ dci, const double* __restrict__ dv,
+                           const i64* __restrict__ prp, const int* __restrict__ pci,
+                           const double* __restrict__ pv, i64* status) {
+  i64 s = drp[i];
+  int nd = (int)(drp[i + 1] - s);
+  R.err = 0;
+  if (nd < 1 || nd > 2) {
+    report(status, SPHC_ST_MALFORMED_GRAD, i);
+    R.err = 1;
+    R.nJ = 0;
+    return;
+  }
+  int ta = dci[s];
+  double sa = dv[s];
+  i64 a0 = prp[ta], a1 = prp[ta + 1];
+  i64 b0 = 0, b1 = 0;
+  double sb = 0.0;
+  if (nd == 2) {
+    int hb = dci[s + 1];
+    sb = dv[s + 1];
+    b0 = prp[hb];
+    b1 = prp[hb + 1];
+  }
+  int n = 0;
+  while (a0 < a1 || b0 < b1) {
+    int ca = a0 < a1 ? pci[a0] : 0x7fffffff;
+    int cb = b0 < b1 ? pci[b0] : 0x7fffffff;
+    int c = ca < cb ? ca : cb;
+    // scipy csr_matmat order: first D entry (lower column) then the second
+    double acc = 0.0;
+    if (ca == c) acc = __dadd_rn(acc, __dmul_rn(sa, pv[a0++]));
+    if (cb == c) acc = __dadd_rn(acc, __dmul_rn(sb, pv[b0++]));
+    if (n >= JM) {
+      report(status, SPHC_ST_EMIN_CAPACITY, i);
+      R.err = 1;
+      R.nJ = 0;
+      return;
+    }
+    R.J[n] = c;
+    R.r[n] = acc;
+    n++;
+  }
+  R.nJ = n;
+  if (n == 0) {
+    report(status, SPHC_ST_EMPTY_J, i);
+    R.err = 1;
+  }
+}
+
+// all lanes: I = interior coarse edges among J pairs (lexicographic = ascending
+// ids) followed by single-node edges of J nodes (ascending ids).
+__device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
+                           const int* __restrict__ adj_col, const int* __restrict__ single_id,
+                           i64* status, int lane) {
+  int nJ = R.nJ;
+  int npairs = nJ * (nJ - 1) / 2;
+  int nI = 0;
+  bool over = false;
+  for (int base = 0; base < npairs; base += 32) {
+    int t = base + lane;
+    int e = -1, pa = 0, pb = 0;
+    if (t < npairs) {
+      int p = 0, rem = t;
+      while (rem >= nJ - 1 - p) {
+        rem -= nJ - 1 - p;
+        p++;
+      }
+      int q = p + 1 + rem;
+      int a = R.J[p], b = R.J[q];
+      i64 lo = adj_rp[a], hi = adj_rp[a + 1];
+      i64 pos = lower_bound_i32_g(adj_col, lo, hi, b);
+      if (pos < hi && adj_col[pos] == b) {
+        e = (int)pos;
+        pa = p;
+        pb = q;
+      }
+    }
+    unsigned bal = __ballot_sync(FULL_MASK, e >= 0);
+    if (e >= 0) {
+      int o = nI + __popc(bal & ((1u << lane) - 1));
+      if (o < IM) {
+        R.Icol[o] = e;
+        R.pa[o] = pa;
+        R.pb[o] = pb;
+      }
+    }
+    nI += __popc(bal);
+  }
+  for (int base = 0; base < nJ; base += 32) {
+    int p = base + lane;
+    int sid = p < nJ ? single_id[R.J[p]] : -1;
+    unsigned bal = __ballot_sync(FULL_MASK, sid >= 0);
+    if (sid >= 0) {
+      int o = nI + __popc(bal & ((1u << lane) - 1));
+      if (o < IM) {
+        R.Icol[o] = sid;
+        R.pa[o] = -1;
+        R.pb[o] = p;
+      }
+    }
+    nI += __popc(bal);
+  }
+  over = nI > IM;
+  if (lane == 0) {
+    R.nI = over ? 0 : nI;
+    if (over) {
+      report(status, SPHC_ST_EMIN_CAPACITY, i);
+      R.err = 1;
+    }
+  }
+  __syncwarp();
+}
+
+// lane 0: irreducibility, k, Gram matrix, Cholesky, rank checks.
+// Returns false (and reports) on failure.
+__device__ bool em_factor(EminRow& R, i64 i, i64* status) {
+  int nJ = R.nJ, nI = R.nI;
+  // union-find over J with interior edges; incidence from every edge
+  int parent[JM];
+  bool inc[JM];
+  bool dirich = false;
+  for (int q = 0; q < nJ; q++) {
+    parent[q] = q;
+    inc[q] = false;
+  }
+  for (int e = 0; e < nI; e++) {
+    int a = R.pa[e], b = R.pb[e];
+    inc[b] = true;
+    if (a < 0) {
+      dirich = true;
+      continue;
+    }
+    inc[a] = true;
+    int x = a, y = b;
+    while (parent[x] != x) x = parent[x];
+    while (parent[y] != y) y = parent[y];
+    if (x != y) {
+      if (x < y) parent[y] = x; else parent[x] = y;
+    }
+  }
+  bool irreducible = true;
+  int root0 = -1;
+  for (int q = 0; q < nJ; q++) {
+    int x = q;
+    while (parent[x] != x) x = parent[x];
+    if (root0 < 0) root0 = x;
+    irreducible &= inc[q] && (x == root0);
+  }
+  if (!irreducible) {
+    report(status, SPHC_ST_REDUCIBLE, i);
+    return false;
+  }
+  int k = nJ - (dirich ? 0 : 1);
+  R.k = k;
+  // expected rank must be in [1, min(|I|, |J|)]
+  if (k < 1 || k > nI) {
+    report(status, SPHC_ST_RANK_LOW, i);
+    return false;
+  }
+  double* L = R.L;
+  for (int t = 0; t < k * k; t++) L[t] = 0.0;
+  for (int e = 0; e < nI; e++) {
+    int a = R.pa[e], b = R.pb[e];
+    if (b < k) L[b * k + b] += 1.0;
+    if (a >= 0 && a < k) {
+      L[a * k + a] += 1.0;
+      if (b < k) {
+        L[a * k + b] -= 1.0;
+        L[b * k + a] -= 1.0;
+      }
+    }
+  }
+  // in-place lower Cholesky; |R_jj| of the reference QR = L_jj
+  for (int j = 0; j < k; j++) {
+    double d = L[j * k + j];
+    for (int m = 0; m < j; m++) d -= L[j * k + m] * L[j * k + m];
+    double ljj = d > 0.0 ? sqrt(d) : 0.0;
+    if (!(ljj >= 1e-10 * (j ? L[0] : ljj)) || ljj == 0.0) {
+      report(status, SPHC_ST_RANK_LOW, i);
+      return false;
+    }
+    L[j * k + j] = ljj;
+    for (int p = j + 1; p < k; p++) {
+      double x = L[p * k + j];
+      for (int m = 0; m < j; m++) x -= L[p * k + m] * L[j * k + m];
+      L[p * k + j] = x / ljj;
+    }
+  }
+  return true;
+}
+
+// lane 0: y <- M^-1 y (k entries) with the Cholesky factor
+__device__ void em_solve(const EminRow& R, double* y) {
+  int k = R.k;
+  const double* L = R.L;
+  for (int j = 0; j < k; j++) {
+    double x = y[j];
+    for (int m = 0; m < j; m++) x -= L[j * k + m] * y[m];
+    y[j] = x / L[j * k + j];
+  }
+  for (int j = k - 1; j >= 0; j--) {
+    double x = y[j];
+    for (int m = j + 1; m < k; m++) x -= L[m * k + j] * y[m];
+    y[j] = x / L[j * k + j];
+  }
+}
+
+template <bool FILL>
+__global__ void __launch_bounds__(EM_WARPS * 32)
+    k_emin_setup(i64 n_e, const i64* __restrict__ drp, const int* __restrict__ dci,
+                 const double* __restrict__ dv, const i64* __restrict__ prp,
+                 const int* __restrict__ pci, const double* __restrict__ pv,
+                 const i64* __restrict__ adj_rp, const int* __restrict__ adj_col,
+                 const int* __restrict__ single_id, i64* icount, i64* jcount, double* rmax2,
+                 i64* dims, const i64* __restrict__ trp, int* __restrict__ tci,
+                 double* __restrict__ tv, const i64* __restrict__ erp, int* __restrict__ eci,
+                 double* __restrict__ ev, i64* status) {
+  __shared__ EminRow rows[EM_WARPS];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  EminRow& R = rows[w];
+  for (i64 i = (i64)blockIdx.x * EM_WARPS + w; i < n_e; i += (i64)gridDim.x * EM_WARPS) {
+    if (lane == 0) em_build_J(R, i, drp, dci, dv, prp, pci, pv, status);
+    __syncwarp();
+    if (R.err) {
+      if (!FILL && lane == 0) { icount[i] = 0; jcount[i] = 0; }
+      __syncwarp();
+      continue;
+    }
+    em_build_I(R, i, adj_rp, adj_col, single_id, status, lane);
+    if (R.err) {
+      if (!FILL && lane == 0) { icount[i] = 0; jcount[i] = R.nJ; }
+      __syncwarp();
+      continue;
+    }
+    int nJ = R.nJ, nI = R.nI;
+    if (!FILL) {
+      if (lane == 0) {
+        double rm = 0.0;
+        for (int q = 0; q < nJ; q++) rm = fmax(rm, fabs(R.r[q]));
+        atomic_max_nonneg(&rmax2[0], rm);
+        if (nI == 0) atomic_max_nonneg(&rmax2[1], rm);
+        else atomicAdd((unsigned long long*)&dims[nI * SPHC_DIMS_J + nJ], 1ull);
+        icount[i] = nI;
+        jcount[i] = nJ;
+      }
+    }
+    if (FILL) {
+      i64 to = trp[i];
+      for (int q = lane; q < nJ; q += 32) {
+        tci[to + q] = R.J[q];
+        tv[to + q] = R.r[q];
+      }
+    }
+    if (nI == 0) {
+      __syncwarp();
+      continue;
+    }
+    bool ok = true;
+    if (lane == 0) {
+      ok = em_factor(R, i, status);
+      if (ok && FILL) {
+        // c = r - G^T 1 on the first k nodes, y = M^-1 c
+        int k = R.k;
+        for (int q = 0; q < k; q++) R.y[q] = R.r[q];
+        for (int e = 0; e < nI; e++) {
+          int a = R.pa[e], b = R.pb[e];
+          if (b < k) R.y[b] -= 1.0;
+          if (a >= 0 && a < k) R.y[a] += 1.0;
+        }
+        em_solve(R, R.y);
+      }
+      R.err = ok ? 0 : 1;
+    }
+    __syncwarp();
+    if (FILL && !R.err) {
+      int k = R.k;
+      i64 eo = erp[i];
+      for (int e = lane; e < nI; e += 32) {
+        int a = R.pa[e], b = R.pb[e];
+        double gy = (b < k ? R.y[b] : 0.0) - ((a >= 0 && a < k) ? R.y[a] : 0.0);
+        eci[eo + e] = R.Icol[e];
+        ev[eo + e] = 1.0 + gy;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+extern "C" int sphc_emin_count(int64_t n_e, const int64_t* drp, const int32_t* dci,
+                               const double* dv, const int64_t* prp, const int32_t* pci,
+                               const double* pv, const int64_t* adj_rp, const int32_t* adj_col,
+                               int64_t n_int, const int32_t* single_id, int64_t* icount,
+                               int64_t* jcount, double* rmax2, int64_t* dims, int64_t* status,
+                               void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_emin_setup<false><<<grid_for(n_e, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
+      n_e, drp, dci, dv, prp, pci, pv, adj_rp, adj_col, single_id, icount, jcount, rmax2, dims,
+      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, status);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int sphc_emin_fill(int64_t n_e, const int64_t* drp, const int32_t* dci,
+                              const double* dv, const int64_t* prp, const int32_t* pci,
+                              const double* pv, const int64_t* adj_rp, const int32_t* adj_col,
+                              int64_t n_int, const int32_t* single_id, const int64_t* trp,
+                              int32_t* tci, double* tv, const int64_t* erp, int32_t* eci,
+                              double* ev, int64_t* status, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_emin_setup<true><<<grid_for(n_e, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
+      n_e, drp, dci, dv, prp, pci, pv, adj_rp, adj_col, single_id, nullptr, nullptr, nullptr,
+      nullptr, trp, tci, tv, erp, eci, ev, status);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+__global__ void __launch_bounds__(EM_WARPS * 32)
+    k_emin_step(i64 n_e, const i64* __restrict__ srp, const int* __restrict__ sci,
+                const double* __restrict__ sv, const double* __restrict__ dinv,
+                const i64* __restrict__ trp, const int* __restrict__ tci,
+                const double* __restrict__ tv, const i64* __restrict__ erp,
+                const int* __restrict__ eci, const double* __restrict__ p_in,
+                double* __restrict__ p_out, const int* __restrict__ ep_a,
+                const int* __restrict__ ep_b, double omega, int update,
+                double* __restrict__ e_row, double* res_max, i64* status) {
+  __shared__ EminRow rows[EM_WARPS];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  EminRow& R = rows[w];
+  for (i64 i = (i64)blockIdx.x * EM_WARPS + w; i < n_e; i += (i64)gridDim.x * EM_WARPS) {
+    i64 t0 = trp[i], e0 = erp[i];
+    int nJ = (int)(trp[i + 1] - t0), nI = (int)(erp[i + 1] - e0);
+    if (nI == 0 || nJ > JM || nI > IM) {
+      if (lane == 0) e_row[i] = 0.0;
+      continue;
+    }
+    for (int q = lane; q < nJ; q += 32) {
+      R.J[q] = tci[t0 + q];
+      R.r[q] = tv[t0 + q];
+    }
+    __syncwarp();
+    for (int e = lane; e < nI; e += 32) {
+      int col = eci[e0 + e];
+      R.Icol[e] = col;
+      R.p[e] = p_in[e0 + e];
+      R.g[e] = 0.0;
+      int a = ep_a[col], b = ep_b[col];
+      R.pb[e] = lower_bound_i32(R.J, nJ, b);
+      R.pa[e] = a < 0 ? -1 : lower_bound_i32(R.J, nJ, a);
+    }
+    if (lane == 0) {
+      R.nJ = nJ;
+      R.nI = nI;
+    }
+    __syncwarp();
+    // masked S P on the fixed pattern: ascending k, sequential per entry
+    i64 se = srp[i + 1];
+    for (i64 js = srp[i]; js < se; js++) {
+      int kk = sci[js];
+      double s = sv[js];
+      i64 pe = erp[kk + 1];
+      for (i64 jp = erp[kk] + lane; jp < pe; jp += 32) {
+        int slot = lower_bound_i32(R.Icol, nI, eci[jp]);
+        if (slot < nI && R.Icol[slot] == eci[jp])
+          R.g[slot] = __dadd_rn(R.g[slot], __dmul_rn(s, p_in[jp]));
+      }
+      __syncwarp();
+    }
+    double en = 0.0;
+    for (int e = lane; e < nI; e += 32) en += R.p[e] * R.g[e];
+    en = warp_sum(en);
+    if (lane == 0) e_row[i] = en;
+    __syncwarp();
+    if (update) {
+      bool ok = true;
+      if (lane == 0) {
+        ok = em_factor(R, i, status);
+        if (ok) {
+          int k = R.k;
+          double di = dinv[i];
+          for (int e = 0; e < nI; e++) R.g[e] = __dmul_rn(di, R.g[e]);  // delta
+          for (int q = 0; q < k; q++) R.y[q] = 0.0;
+          for (int e = 0; e < nI; e++) {  // y = G_k^T delta
+            int a = R.pa[e], b = R.pb[e];
+            if (b < k) R.y[b] += R.g[e];
+            if (a >= 0 && a < k) R.y[a] -= R.g[e];
+          }
+          em_solve(R, R.y);
+        }
+        R.err = ok ? 0 : 1;
+      }
+      __syncwarp();
+      if (R.err) continue;
+      int k = R.k;
+      for (int e = lane; e < nI; e += 32) {
+        int a = R.pa[e], b = R.pb[e];
+        double gz = (b < k ? R.y[b] : 0.0) - ((a >= 0 && a < k) ? R.y[a] : 0.0);
+        double pn = R.p[e] - omega * (R.g[e] - gz);
+        R.p[e] = pn;
+        p_out[e0 + e] = pn;
+      }
+      __syncwarp();
+    }
+    // commutator residual max |G^T p - r| over all of J
+    if (lane == 0) {
+      double gp[JM];
+      for (int q = 0; q < nJ; q++) gp[q] = 0.0;
+      for (int e = 0; e < nI; e++) {
+        gp[R.pb[e]] += R.p[e];
+        if (R.pa[e] >= 0) gp[R.pa[e]] -= R.p[e];
+      }
+      double m = 0.0;
+      for (int q = 0; q < nJ; q++) m = fmax(m, fabs(gp[q] - R.r[q]));
+      atomic_max_nonneg(res_max, m);
+    }
+    __syncwarp();
+  }
+}
+
+extern "C" int sphc_emin_step(int64_t n_e, const int64_t* srp, const int32_t* sci,
+                              const double* sv, const double* dinv, const int64_t* trp,
+                              const int32_t* tci, const double* tv, const int64_t* erp,
+                              const int32_t* eci, const double* p_in, double* p_out,
+                              const int32_t* ep_a, const int32_t* ep_b, double omega, int update,
+                              double* e_row, double* res_max, int64_t* status, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_emin_step<<<grid_for(n_e, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
+      n_e, srp, sci, sv, dinv, trp, tci, tv, erp, eci, p_in, p_out, ep_a, ep_b, omega, update,
+      e_row, res_max, status);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}

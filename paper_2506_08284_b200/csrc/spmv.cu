@@ -1,0 +1,207 @@
+// Solve-phase kernels: row-grouped CSR SpMV (L lanes per row, shuffle
+// segmented reduction), the fused Chebyshev step, fused PCG vector updates
+// and the coarsest-level dense GEMV. All fp64 and HBM-bound.
+#include "common.cuh"
+
+#define SPMV_THREADS 256
+
+template <int L>
+__device__ __forceinline__ double row_dot(i64 row, i64 n, const i64* __restrict__ rp,
+                                          const int* __restrict__ ci,
+                                          const double* __restrict__ v,
+                                          const double* __restrict__ x, int lane) {
+  double acc = 0.0;
+  if (row < n) {
+    i64 e = rp[row + 1];
+    for (i64 j = rp[row] + lane; j < e; j += L) acc = fma(v[j], __ldg(x + ci[j]), acc);
+  }
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, o);
+  return acc;
+}
+
+// y = alpha * A x + beta * z
+template <int L>
+__global__ void __launch_bounds__(SPMV_THREADS)
+    k_spmv(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
+           const double* __restrict__ v, const double* __restrict__ x, double alpha,
+           double beta, const double* z, double* y) {
+  const int RPW = 32 / L;
+  int lane = threadIdx.x & (L - 1);
+  int sub = (threadIdx.x & 31) / L;
+  i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 base = warp * RPW; base < n; base += nw * RPW) {
+    i64 row = base + sub;
+    double acc = row_dot<L>(row, n, rp, ci, v, x, lane);
+    if (row < n && lane == 0) {
+      double r = alpha * acc;
+      if (z) r = fma(beta, z[row], r);
+      y[row] = r;
+    }
+  }
+}
+
+// d <- cd d + cr dinv (b - A x_in); x_out = x_in + d
+template <int L>
+__global__ void __launch_bounds__(SPMV_THREADS)
+    k_cheb(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
+           const double* __restrict__ v, const double* __restrict__ dinv,
+           const double* __restrict__ b, const double* __restrict__ x_in,
+           double* __restrict__ x_out, double* __restrict__ d, double cd, double cr,
+           int x_zero) {
+  const int RPW = 32 / L;
+  int lane = threadIdx.x & (L - 1);
+  int sub = (threadIdx.x & 31) / L;
+  i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 base = warp * RPW; base < n; base += nw * RPW) {
+    i64 row = base + sub;
+    double ax = x_zero ? 0.0 : row_dot<L>(row, n, rp, ci, v, x_in, lane);
+    if (row < n && lane == 0) {
+      double r = b[row] - ax;
+      double dn = cr * dinv[row] * r;
+      if (cd != 0.0) dn = fma(cd, d[row], dn);
+      d[row] = dn;
+      x_out[row] = (x_zero ? 0.0 : x_in[row]) + dn;
+    }
+  }
+}
+
+static unsigned spmv_grid(i64 n, int L) {
+  i64 rows_per_block = (SPMV_THREADS / 32) * (32 / L);
+  return grid_for(n, (int)rows_per_block, SPHC_NUM_SMS * 16);
+}
+
+#define DISPATCH_L(L, CALL)                \
+  switch (L) {                             \
+    case 1: { const int LL = 1; CALL; } break;  \
+    case 2: { const int LL = 2; CALL; } break;  \
+    case 4: { const int LL = 4; CALL; } break;  \
+    case 8: { const int LL = 8; CALL; } break;  \
+    case 16: { const int LL = 16; CALL; } break; \
+    case 32: { const int LL = 32; CALL; } break; \
+    default: sphc_set_error("lanes must be 1,2,4,8,16,32"); return SPHC_ERR_ARG; \
+  }
+
+extern "C" int sphc_spmv(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
+                         int lanes, const double* x, double alpha, double beta,
+                         const double* z, double* y, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  DISPATCH_L(lanes, (k_spmv<LL><<<spmv_grid(n, LL), SPMV_THREADS, 0, s>>>(
+                         n, rp, ci, v, x, alpha, beta, z, y)));
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int sphc_cheb_step(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
+                              int lanes, const double* dinv, const double* b,
+                              const double* x_in, double* x_out, double* d, double cd,
+                              double cr, int x_zero, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  DISPATCH_L(lanes, (k_cheb<LL><<<spmv_grid(n, LL), SPMV_THREADS, 0, s>>>(
+                         n, rp, ci, v, dinv, b, x_in, x_out, d, cd, cr, x_zero)));
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+__global__ void k_pcg_update(i64 n, double alpha, const double* __restrict__ p,
+                             const double* __restrict__ Ap, double* __restrict__ x,
+                             double* __restrict__ r, int* changed) {
+  int ch = 0;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    double xo = x[i];
+    double xn = xo + alpha * p[i];
+    ch |= (xn != xo);
+    x[i] = xn;
+    r[i] = r[i] - alpha * Ap[i];
+  }
+  ch = __syncthreads_or(ch);
+  if (ch && threadIdx.x == 0) atomicOr(changed, 1);
+}
+
+extern "C" int sphc_pcg_update(int64_t n, double alpha, const double* p, const double* Ap,
+                               double* x, double* r, int32_t* changed, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_pcg_update<<<grid_for(n, 256), 256, 0, s>>>(n, alpha, p, Ap, x, r, changed);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+__global__ void k_pcg_dir(i64 n, double beta, const double* __restrict__ z,
+                          double* __restrict__ p) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x)
+    p[i] = z[i] + beta * p[i];
+}
+
+extern "C" int sphc_pcg_direction(int64_t n, double beta, const double* z, double* p,
+                                  void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_pcg_dir<<<grid_for(n, 256), 256, 0, s>>>(n, beta, z, p);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+// y = A x, A dense row-major n x n: one warp per row, fixed-order reduction
+__global__ void k_dense_gemv(i64 n, const double* __restrict__ A, const double* __restrict__ x,
+                             double* __restrict__ y) {
+  int lane = threadIdx.x & 31;
+  i64 w = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 row = w; row < n; row += nw) {
+    const double* a = A + row * n;
+    double acc = 0.0;
+    for (i64 j = lane; j < n; j += 32) acc = fma(a[j], x[j], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) y[row] = acc;
+  }
+}
+
+extern "C" int sphc_dense_gemv(int64_t n, const double* A, const double* x, double* y,
+                               void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  k_dense_gemv<<<grid_for(n * 32, 256), 256, 0, s>>>(n, A, x, y);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+// y_i = d_i x_i
+__global__ void k_diag_scale(i64 n, const double* __restrict__ d, const double* __restrict__ x,
+                             double* __restrict__ y) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x)
+    y[i] = d[i] * x[i];
+}
+
+extern "C" int sphc_diag_scale(int64_t n, const double* d, const double* x, double* y,
+                               void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_diag_scale<<<grid_for(n, 256), 256, 0, s>>>(n, d, x, y);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+// deterministic start vector in [-1, 1): splitmix64 of the index (same
+// integer arithmetic as oracle.cheb_start_vector)
+__global__ void k_cheb_start(i64 n, double* __restrict__ x) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    unsigned long long z = (unsigned long long)i + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    x[i] = (double)(z >> 11) * 0x1p-53 * 2.0 - 1.0;
+  }
+}
+
+extern "C" int sphc_cheb_start(int64_t n, double* x, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_cheb_start<<<grid_for(n, 256), 256, 0, s>>>(n, x);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}

@@ -1,0 +1,206 @@
+"""Device CSR container and thin wrappers over the libsphcurl C ABI.
+
+B200 replacement of the reference's scipy-CSR substrate (sparse_ops.py):
+int64 row pointers, int32 columns, fp64 values, all resident in HBM as torch
+tensors (torch is the allocator / stream plumbing; every numeric operation is
+a libsphcurl kernel).
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _lib
+
+INT64_MAX = np.iinfo(np.int64).max
+SLOTS = 16
+ST = dict(ZERO_DIAG=0, NONPOS_DIAG=1, NODAL_ZERO_DIAG=2, ZERO_ROWSUM=3,
+          MALFORMED_GRAD=4, EMPTY_I=5, REDUCIBLE=6, RANK_LOW=7, EMIN_CAPACITY=8,
+          EMPTY_J=9, SPGEMM_CAPACITY=10, SORT_CAPACITY=11)
+
+
+def device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2506_08284_b200 needs a CUDA device (B200); "
+                           "there is no CPU path")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def call(name, *args):
+    return _lib.call(name, *args)
+
+
+class Status:
+    """Device error slots: slot k holds the lowest row failing check k."""
+
+    def __init__(self):
+        self.t = torch.full((SLOTS,), INT64_MAX, dtype=torch.int64, device=device())
+
+    def rows(self):
+        h = self.t.cpu().numpy()
+        return {k: int(h[v]) for k, v in ST.items() if h[v] != INT64_MAX}
+
+
+@dataclass
+class DeviceCSR:
+    rowptr: torch.Tensor          # int64 [n_rows + 1]
+    col: torch.Tensor             # int32 [nnz]
+    val: torch.Tensor             # float64 [nnz] (None for a pure pattern)
+    shape: tuple
+
+    @property
+    def nnz(self):
+        return int(self.col.numel())
+
+    @property
+    def n_rows(self):
+        return self.shape[0]
+
+    @staticmethod
+    def from_scipy(A, dev=None):
+        dev = dev or device()
+        A = sp.csr_matrix(A)
+        if not A.has_canonical_format:
+            A = A.copy()
+            A.sum_duplicates()
+            A.sort_indices()
+        return DeviceCSR(
+            rowptr=torch.from_numpy(A.indptr.astype(np.int64)).to(dev),
+            col=torch.from_numpy(A.indices.astype(np.int32)).to(dev),
+            val=torch.from_numpy(A.data.astype(np.float64)).to(dev),
+            shape=tuple(int(s) for s in A.shape))
+
+    def to_scipy(self):
+        val = self.val.cpu().numpy() if self.val is not None else np.ones(self.nnz)
+        return sp.csr_matrix((val, self.col.cpu().numpy(), self.rowptr.cpu().numpy()),
+                             shape=self.shape)
+
+    def lanes(self):
+        """Lanes per row for the row-grouped SpMV (mean row length)."""
+        m = self.nnz / max(self.shape[0], 1)
+        for L, lim in ((2, 3), (4, 6), (8, 14), (16, 40)):
+            if m <= lim:
+                return L
+        return 32
+
+
+def as_device_csr(A):
+    return A if isinstance(A, DeviceCSR) else DeviceCSR.from_scipy(A)
+
+
+def empty_f64(n):
+    return torch.empty(int(n), dtype=torch.float64, device=device())
+
+
+def zeros_f64(n):
+    return torch.zeros(int(n), dtype=torch.float64, device=device())
+
+
+def zeros_i64(n):
+    return torch.zeros(int(n), dtype=torch.int64, device=device())
+
+
+def scan(counts):
+    """Exclusive scan -> (rowptr [n+1], total) (one host sync for the total)."""
+    n = counts.numel()
+    rp = torch.empty(n + 1, dtype=torch.int64, device=counts.device)
+    call("sphc_scan_i64", n, counts, rp)
+    return rp, int(rp[n].item())
+
+
+def dot(x, y, out=None):
+    out = out if out is not None else empty_f64(1)
+    call("sphc_dot", x.numel(), x, y, out)
+    return out
+
+
+def vsum(x, out=None):
+    out = out if out is not None else empty_f64(1)
+    call("sphc_sum", x.numel(), x, out)
+    return out
+
+
+def maxabs(x, out=None):
+    out = out if out is not None else empty_f64(1)
+    call("sphc_maxabs", x.numel(), x, out)
+    return out
+
+
+def diagonal(A, status=None):
+    d = empty_f64(A.shape[0])
+    call("sphc_csr_diag", A.shape[0], A.rowptr, A.col, A.val, d,
+         status.t if status is not None else None)
+    return d
+
+
+def reciprocal(x, zero_sub=None):
+    y = empty_f64(x.numel())
+    call("sphc_reciprocal", x.numel(), x, zero_sub, y)
+    return y
+
+
+def transpose(A, status=None):
+    st = status or Status()
+    nr, nc = A.shape
+    trp = torch.empty(nc + 1, dtype=torch.int64, device=A.rowptr.device)
+    tci = torch.empty(A.nnz, dtype=torch.int32, device=A.rowptr.device)
+    tv = empty_f64(A.nnz) if A.val is not None else None
+    call("sphc_csr_transpose", nr, nc, A.nnz, A.rowptr, A.col, A.val, trp, tci, tv, st.t)
+    if status is None:
+        _raise_capacity(st)
+    return DeviceCSR(trp, tci, tv, (nc, nr))
+
+
+def _raise_capacity(st):
+    rows = st.rows()
+    for k in ("SORT_CAPACITY", "SPGEMM_CAPACITY", "EMIN_CAPACITY"):
+        if k in rows:
+            raise RuntimeError(f"device kernel capacity exceeded ({k}) at row {rows[k]}")
+
+
+def drop_zeros(A):
+    """compress(A, 0.0): remove stored exact zeros (sparse_ops.py:107-113)."""
+    n = A.shape[0]
+    cnt = torch.empty(n, dtype=torch.int64, device=A.rowptr.device)
+    call("sphc_csr_count_nonzero", n, A.rowptr, A.val, cnt)
+    rp, nnz = scan(cnt)
+    if nnz == A.nnz:
+        return A
+    ci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
+    v = empty_f64(nnz)
+    call("sphc_csr_compact", n, A.rowptr, A.col, A.val, rp, ci, v)
+    return DeviceCSR(rp, ci, v, A.shape)
+
+
+def spgemm(A, B, drop=True):
+    """C = A B with scipy csr_matmat's accumulation order; exact zeros dropped
+    like scipy's product (drop=True)."""
+    if A.shape[1] != B.shape[0]:
+        raise ValueError(f"spgemm dimension mismatch: {A.shape} @ {B.shape}")
+    n = A.shape[0]
+    st = Status()
+    cnt = torch.empty(n, dtype=torch.int64, device=A.rowptr.device)
+    call("sphc_spgemm_count", n, A.rowptr, A.col, B.rowptr, B.col, cnt, st.t)
+    rp, nnz = scan(cnt)
+    _raise_capacity(st)
+    ci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
+    v = empty_f64(nnz)
+    call("sphc_spgemm_fill", n, A.rowptr, A.col, A.val, B.rowptr, B.col, B.val, rp, ci, v,
+         st.t)
+    C = DeviceCSR(rp, ci, v, (A.shape[0], B.shape[1]))
+    return drop_zeros(C) if drop else C
+
+
+def spmv(A, x, y, alpha=1.0, beta=0.0, z=None, lanes=None):
+    """y = alpha A x + beta z."""
+    call("sphc_spmv", A.shape[0], A.rowptr, A.col, A.val, lanes or A.lanes(), x, alpha,
+         beta, z, y)
+    return y
+
+
+def to_dense(A):
+    out = torch.empty(A.shape, dtype=torch.float64, device=A.rowptr.device)
+    call("sphc_csr_to_dense", A.shape[0], A.shape[1], A.rowptr, A.col, A.val, out)
+    return out

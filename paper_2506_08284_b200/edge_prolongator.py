@@ -1,0 +1,115 @@
+"""Edge interpolation by constrained energy minimisation, on the B200.
+
+Mirror of the reference's edge_prolongator.py (EminConfig, EdgeProlongator,
+build_edge_prolongator). The projected damped-Jacobi sweep is one libsphcurl
+launch per iteration: masked S P on the fixed pattern (warp per fine edge,
+sequential ascending-k sums), Jacobi scaling, projection onto the null space
+of the row's constraint block, update, the energy of the input iterate and
+the commutator residual of the output -- fused.
+"""
+
+from collections import Counter
+from dataclasses import dataclass, field
+
+import torch
+
+from . import coarse_gradient as cgrad
+from . import device as dv
+from . import emin_setup as es
+from . import nodal_amg as na
+from .device import DeviceCSR, Status, as_device_csr, call
+
+
+@dataclass
+class EminConfig:
+    """Knobs of the prolongator energy minimisation (edge_prolongator.py:28-44)."""
+
+    omega: float = 0.5
+    iterations: int = 1
+    mode: str = "sphcurl"          # only "sphcurl" runs on the device path
+    n_passes: int = 2
+    drop_tol: float = 0.0
+
+    def __post_init__(self):
+        if not 0.0 < self.omega < 2.0:
+            raise ValueError(f"omega must be in (0, 2), got {self.omega}")
+        if self.iterations < 0:
+            raise ValueError("iterations must be >= 0")
+        if self.mode not in ("sphcurl", "rsamg"):
+            raise ValueError(f"unknown mode {self.mode!r}")
+
+
+@dataclass
+class EdgeProlongator:
+    P_e: DeviceCSR
+    energy_history: list
+    commutator_residual: float
+    subproblem_dims: Counter = field(default_factory=Counter)
+    n_augmented: int = 0
+
+
+def jacobi_diag_inverse(S):
+    """1 / diag(S) with zeros replaced by 1e-12 max (edge_prolongator.py:159-167)."""
+    d = dv.diagonal(S)
+    # diag(S) >= 0 for the PSD curl-curl operator, so max d = max |d|
+    top = dv.maxabs(d)
+    t = float(top.item()) if d.numel() else 0.0
+    if t <= 0.0:
+        raise ValueError("curl-curl diagonal is entirely zero")
+    sub = dv.empty_f64(1)
+    sub.fill_(1e-12 * t)
+    return dv.reciprocal(d, sub)
+
+
+def emin_sweeps(S, setup, omega, iterations):
+    """Projected damped-Jacobi sweeps; returns (values, energies, residual)."""
+    S = as_device_csr(S)
+    n_e = setup.pattern.shape[0]
+    T, Pp, cg = setup.T, setup.pattern, setup.cg
+    st = Status()
+    e_row = dv.empty_f64(n_e)
+    res = torch.zeros(1, dtype=torch.float64, device=e_row.device)
+    esum = dv.empty_f64(iterations + 1)
+    vals = Pp.val
+    if iterations:
+        dinv = jacobi_diag_inverse(S)
+        for it in range(iterations):
+            out = torch.empty_like(vals)
+            res.zero_()
+            call("sphc_emin_step", n_e, S.rowptr, S.col, S.val, dinv, T.rowptr, T.col, T.val,
+                 Pp.rowptr, Pp.col, vals, out, cg.ep_a, cg.ep_b, float(omega), 1, e_row,
+                 res, st.t)
+            dv.vsum(e_row, esum[it:it + 1])
+            vals = out
+    # energy of the final iterate and its commutator residual
+    res.zero_()
+    call("sphc_emin_step", n_e, S.rowptr, S.col, S.val, None, T.rowptr, T.col, T.val,
+         Pp.rowptr, Pp.col, vals, None, cg.ep_a, cg.ep_b, float(omega), 0, e_row, res, st.t)
+    dv.vsum(e_row, esum[iterations:iterations + 1])
+    es._raise(st, S)
+    energies = [float(x) for x in esum.cpu().numpy()] if iterations else []
+    return vals, energies, float(res.item())
+
+
+def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None):
+    """Edge prolongator and coarse gradient for one level
+    (edge_prolongator.py:184-228). Returns
+    (EdgeProlongator, CoarseGradient, NodalProlongator)."""
+    cfg = cfg or EminConfig()
+    if cfg.mode != "sphcurl":
+        raise NotImplementedError("rsamg mode is outside the B200 hot path")
+    strength = na.strength_graph(A_n, cfg.drop_tol)
+    agg = na.aggregate(strength)
+    nod = na.smooth_and_normalize(A_n, agg)
+    assign = cgrad.gen_piecewise_const(nod.P, cfg.n_passes)
+    cg = cgrad.build_coarse_gradient(D_h, assign, agg.n_agg)
+    setup = es.setup_constraints(D_h, nod.P, cg)
+    vals, energy, res = emin_sweeps(S, setup, cfg.omega, cfg.iterations)
+    P = setup.pattern
+    P_e = DeviceCSR(P.rowptr, P.col, vals, P.shape)
+    prol = EdgeProlongator(P_e=P_e, energy_history=energy, commutator_residual=res,
+                           subproblem_dims=setup.subproblem_dims,
+                           n_augmented=setup.n_augmented)
+    prol.membership = agg.membership
+    prol.assignment = assign
+    return prol, cg, nod

@@ -1,0 +1,338 @@
+"""Multilevel hierarchy, hybrid smoothing, V-cycle and PCG on the B200.
+
+Mirror of the reference's multigrid.py: ``SolverConfig``, ``Level``,
+``Hierarchy``, ``PcgResult``, ``build_hierarchy``, ``hiptmair_smooth``,
+``v_cycle``, ``v_cycle_preconditioner``, ``pcg_solve`` -- same arguments,
+defaults, fields and ValueError texts. Inputs may be scipy CSR / numpy (they
+are uploaded) or DeviceCSR / CUDA tensors. The whole hierarchy stays in HBM;
+every numeric step is a libsphcurl kernel.
+
+Smoother: the reference's symmetric Gauss-Seidel (multigrid.py:32-59) is a
+sequential triangular solve. The B200 path plugs a Jacobi-preconditioned
+Chebyshev polynomial of degree 3 (SpMV only, same pass count) into the same
+hybrid Hiptmair structure (multigrid.py:164-173); the oracle applies the same
+polynomial in the reference's own sweeper seam for parity.
+"""
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import device as dv
+from .device import DeviceCSR, Status, as_device_csr, call
+from .edge_prolongator import EminConfig, build_edge_prolongator
+
+_NULLSPACE_TOL = 1e-10
+CHEB_POWER_ITERS = 15
+CHEB_SAFETY = 1.1
+CHEB_RATIO = 30.0
+
+
+@dataclass
+class SolverConfig:
+    """Hierarchy construction knobs (multigrid.py:23-29) + the smoother."""
+
+    coarse_size: int = 200
+    max_levels: int = 10
+    emin: EminConfig = field(default_factory=EminConfig)
+    smoother: str = "chebyshev"
+    cheb_degree: int = 3
+
+    def __post_init__(self):
+        if self.smoother != "chebyshev":
+            raise ValueError("the B200 path implements the Chebyshev smoother only")
+
+
+class ChebyshevSweeper:
+    """Degree-d Jacobi-Chebyshev on [hi/30, hi], hi = 1.1 x (15-step power
+    estimate of rho(D^-1 A)); ``symmetric(x, b)`` applies it once. Each
+    polynomial step is one fused libsphcurl launch."""
+
+    def __init__(self, A, degree=3):
+        self.A = A
+        n = A.shape[0]
+        st = Status()
+        d = dv.diagonal(A, st)
+        rows = st.rows()
+        if "ZERO_DIAG" in rows:
+            raise ValueError(f"zero diagonal entry in row {rows['ZERO_DIAG']}")
+        self.dinv = dv.reciprocal(d)
+        self.degree = degree
+        self.lanes = A.lanes()
+        self.d = dv.empty_f64(n)
+        self.buf = [dv.empty_f64(n), dv.empty_f64(n)]
+        self.hi, self.lo = self._bounds()
+        self.coefs = self._coefficients()
+
+    def _bounds(self):
+        n = self.A.shape[0]
+        if n == 0:
+            return 1.0, 1.0 / CHEB_RATIO
+        x, y = self.buf
+        call("sphc_cheb_start", n, x)
+        sq = dv.empty_f64(1)
+        norms = dv.empty_f64(CHEB_POWER_ITERS + 1)
+        dv.dot(x, x, sq)
+        call("sphc_scale_by_norm", n, x, sq, x, norms[0:1])
+        for it in range(CHEB_POWER_ITERS):
+            dv.spmv(self.A, x, y, lanes=self.lanes)
+            call("sphc_diag_scale", n, self.dinv, y, y)
+            dv.dot(y, y, sq)
+            call("sphc_scale_by_norm", n, y, sq, x, norms[it + 1:it + 2])
+        h = norms.cpu().numpy()
+        lam = 0.0
+        for it in range(CHEB_POWER_ITERS):
+            lam = float(h[it + 1])
+            if lam == 0.0:
+                break
+        hi = CHEB_SAFETY * lam
+        return hi, hi / CHEB_RATIO
+
+    def _coefficients(self):
+        theta = 0.5 * (self.hi + self.lo)
+        delta = 0.5 * (self.hi - self.lo)
+        sigma = theta / delta
+        out = [(0.0, 1.0 / theta)]
+        rho = 1.0 / sigma
+        for _ in range(1, self.degree):
+            rn = 1.0 / (2.0 * sigma - rho)
+            out.append((rn * rho, 2.0 * rn / delta))
+            rho = rn
+        return out
+
+    def symmetric(self, x, b, sweeps=1, x_zero=False):
+        """Returns the smoothed iterate (a sweeper-owned buffer, never ``x``)."""
+        A = self.A
+        n = A.shape[0]
+        cur = x
+        for _ in range(sweeps):
+            for step, (cd, cr) in enumerate(self.coefs):
+                out = self.buf[0] if cur is not self.buf[0] else self.buf[1]
+                z = x_zero and step == 0
+                call("sphc_cheb_step", n, A.rowptr, A.col, A.val, self.lanes, self.dinv, b,
+                     None if z else cur, out, self.d, cd, cr, int(z))
+                cur = out
+            x_zero = False
+        return cur
+
+
+@dataclass
+class Level:
+    """One hierarchy level (multigrid.py:69-89) plus its device working set."""
+
+    A_e: DeviceCSR
+    S_e: DeviceCSR
+    D: DeviceCSR
+    nodal_aux: DeviceCSR
+    P_e: DeviceCSR = None
+    P_n: DeviceCSR = None
+    edge_sweeper: ChebyshevSweeper = None
+    aux_sweeper: ChebyshevSweeper = None
+    emin_energy: list = field(default_factory=list)
+    subproblem_dims: dict = field(default_factory=dict)
+    commutator_residual: float = 0.0
+    n_augmented: int = 0
+    # B200 working set
+    R_e: DeviceCSR = None            # explicit P_e^T (restriction, gather only)
+    Dt: DeviceCSR = None             # explicit D^T
+    r: torch.Tensor = None
+    bn: torch.Tensor = None
+    rc: torch.Tensor = None          # restricted residual (next level's rhs)
+    membership: torch.Tensor = None
+    assignment: torch.Tensor = None
+    coarse_gradient: object = None
+    omega: float = 0.0
+    rho: float = 0.0
+
+    @property
+    def n_edges(self):
+        return self.A_e.shape[0]
+
+
+@dataclass
+class Hierarchy:
+    levels: list
+    coarse_factorization: torch.Tensor   # explicit inverse of the coarsest A_e
+    operator_complexity: float
+
+    @property
+    def n_levels(self):
+        return len(self.levels)
+
+
+def _make_level(A_e, S_e, D, degree=3, **extra):
+    Dt = dv.transpose(D)
+    nodal_aux = dv.spgemm(Dt, dv.spgemm(A_e, D))
+    level = Level(A_e=A_e, S_e=S_e, D=D, nodal_aux=nodal_aux, Dt=Dt, **extra)
+    level.edge_sweeper = ChebyshevSweeper(A_e, degree)
+    level.aux_sweeper = ChebyshevSweeper(nodal_aux, degree)
+    level.r = dv.empty_f64(A_e.shape[0])
+    level.bn = dv.empty_f64(D.shape[1])
+    return level
+
+
+def _check_nullspace(S, D, where):
+    SD = dv.spgemm(S, D, drop=False)
+    m = dv.empty_f64(2)
+    dv.maxabs(SD.val, m[0:1])
+    dv.maxabs(S.val, m[1:2])
+    defect, smax = (float(x) for x in m.cpu().numpy())
+    scale = max(smax, 1e-300)
+    if defect > _NULLSPACE_TOL * scale:
+        raise ValueError(
+            f"curl null-space identity violated on {where}: "
+            f"max|S D| = {defect:.3e} vs max|S| = {scale:.3e}")
+
+
+def build_hierarchy(A_e, S_e, A_n, D, cfg=None):
+    """Galerkin hierarchy driven by the constrained edge prolongator
+    (multigrid.py:119-161)."""
+    cfg = cfg or SolverConfig()
+    A_e, S_e = as_device_csr(A_e), as_device_csr(S_e)
+    A_n, D = as_device_csr(A_n), as_device_csr(D)
+    _check_nullspace(S_e, D, "the fine level")
+    levels = []
+    while A_e.shape[0] > cfg.coarse_size and len(levels) < cfg.max_levels - 1:
+        prol, cg, nod = build_edge_prolongator(A_n, A_e, S_e, D, cfg.emin)
+        P_e, P_n = prol.P_e, nod.P
+        n_coarse = cg.n_edges
+        if n_coarse == 0:
+            break
+        if n_coarse >= 0.9 * A_e.shape[0]:
+            raise ValueError(
+                f"coarsening stagnated: {n_coarse} coarse edges from "
+                f"{A_e.shape[0]} fine edges")
+        lv = _make_level(A_e, S_e, D, cfg.cheb_degree, P_e=P_e, P_n=P_n,
+                         emin_energy=prol.energy_history,
+                         subproblem_dims=dict(prol.subproblem_dims),
+                         commutator_residual=prol.commutator_residual,
+                         n_augmented=prol.n_augmented,
+                         membership=prol.membership, assignment=prol.assignment,
+                         coarse_gradient=cg, omega=nod.omega_used, rho=nod.rho_estimate)
+        lv.R_e = dv.transpose(P_e)
+        lv.rc = dv.empty_f64(n_coarse)
+        levels.append(lv)
+        A_e = dv.spgemm(lv.R_e, dv.spgemm(A_e, P_e))
+        S_e = dv.spgemm(lv.R_e, dv.spgemm(S_e, P_e))
+        A_n = dv.spgemm(dv.transpose(P_n), dv.spgemm(A_n, P_n))
+        D = cg.D_H
+        _check_nullspace(S_e, D, f"level {len(levels)}")
+    last = _make_level(A_e, S_e, D, cfg.cheb_degree)
+    levels.append(last)
+    inv = torch.linalg.inv(dv.to_dense(A_e))   # dense LU (cuSOLVER), once
+    last.r = dv.empty_f64(A_e.shape[0])
+    nnz0 = levels[0].A_e.nnz
+    oc = sum(lv.A_e.nnz for lv in levels) / nnz0
+    return Hierarchy(levels=levels, coarse_factorization=inv, operator_complexity=oc)
+
+
+def hiptmair_smooth(level, x, b, x_zero=False):
+    """Edge smoothing, nodal correction through the gradient, edge smoothing
+    (multigrid.py:164-173). Returns the new iterate (may be a new buffer)."""
+    x = level.edge_sweeper.symmetric(x, b, x_zero=x_zero)
+    dv.spmv(level.A_e, x, level.r, alpha=-1.0, beta=1.0, z=b)        # r = b - A x
+    dv.spmv(level.Dt, level.r, level.bn)                                # D^T r
+    c = level.aux_sweeper.symmetric(None, level.bn, x_zero=True)
+    dv.spmv(level.D, c, x, alpha=1.0, beta=1.0, z=x)                   # x += D c
+    return level.edge_sweeper.symmetric(x, b)
+
+
+def v_cycle(h, x, b, level=0):
+    """V-cycle with hybrid pre/post smoothing and the dense coarsest solve
+    (multigrid.py:176-188). ``x`` None means a zero initial guess."""
+    lv = h.levels[level]
+    if level == h.n_levels - 1:
+        n = lv.A_e.shape[0]
+        call("sphc_dense_gemv", n, h.coarse_factorization, b, lv.r)
+        return lv.r
+    x = hiptmair_smooth(lv, x, b, x_zero=x is None)
+    dv.spmv(lv.A_e, x, lv.r, alpha=-1.0, beta=1.0, z=b)
+    dv.spmv(lv.R_e, lv.r, lv.rc)
+    ec = v_cycle(h, None, lv.rc, level + 1)
+    dv.spmv(lv.P_e, ec, x, alpha=1.0, beta=1.0, z=x)
+    return hiptmair_smooth(lv, x, b)
+
+
+def v_cycle_preconditioner(h):
+    """The V-cycle as a fixed symmetric operator b -> V(b) (multigrid.py:191-195)."""
+    def apply(b):
+        return v_cycle(h, None, b)
+    return apply
+
+
+@dataclass
+class PcgResult:
+    x: object
+    iterations: int
+    residual_history: list
+    precond_history: list
+    status: str
+    relative_residual: float
+
+
+def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
+    """Preconditioned CG from x = 0 (multigrid.py:220-274): same statuses
+    (converged | maxit | stagnated | indefinite) and histories."""
+    A = as_device_csr(A)
+    host = not isinstance(b, torch.Tensor)
+    b = torch.as_tensor(np.asarray(b, dtype=np.float64) if host else b,
+                        dtype=torch.float64, device=dv.device())
+    n = b.numel()
+    sc = torch.zeros(4, dtype=torch.float64, device=b.device)
+    flag = sc.view(torch.int32)[6:7]          # overlaps sc[3]
+    dv.dot(b, b, sc[0:1])
+    nb = math.sqrt(float(sc[0].item()))
+    x = dv.zeros_f64(n)
+
+    def out(v):
+        return v.cpu().numpy() if host else v
+
+    if nb == 0.0:
+        return PcgResult(out(x), 0, [0.0], [0.0], "converged", 0.0)
+    r = b.clone()
+    Ap = dv.empty_f64(n)
+    z = precond(r)
+    p = z.clone()
+    dv.dot(r, z, sc[0:1])
+    rz = float(sc[0].item())
+    history = [nb]
+    precond_history = [math.sqrt(max(rz, 0.0))]
+    status, iters = "maxit", 0
+    lanes = A.lanes()
+    for k in range(maxit):
+        dv.spmv(A, p, Ap, lanes=lanes)
+        dv.dot(p, Ap, sc[0:1])
+        pAp = float(sc[0].item())
+        if pAp <= 0.0:
+            status = "indefinite"
+            break
+        alpha = rz / pAp
+        sc[3] = 0.0
+        call("sphc_pcg_update", n, alpha, p, Ap, x, r, flag)
+        dv.dot(r, r, sc[1:2])
+        hv = sc.cpu().numpy()
+        iters = k + 1
+        if hv.view(np.int32)[6] == 0:
+            status = "stagnated"
+            dv.spmv(A, x, Ap, alpha=-1.0, beta=1.0, z=b)
+            dv.dot(Ap, Ap, sc[0:1])
+            history.append(math.sqrt(float(sc[0].item())))
+            precond_history.append(precond_history[-1])
+            break
+        res = math.sqrt(float(hv[1]))
+        history.append(res)
+        z = precond(r)
+        dv.dot(r, z, sc[2:3])
+        rz_new = float(sc[2].item())
+        precond_history.append(math.sqrt(max(rz_new, 0.0)))
+        if res <= rtol * nb:
+            status = "converged"
+            break
+        beta = rz_new / rz
+        rz = rz_new
+        call("sphc_pcg_direction", n, beta, z, p)
+    return PcgResult(x=out(x), iterations=iters, residual_history=history,
+                     precond_history=precond_history, status=status,
+                     relative_residual=history[-1] / nb)

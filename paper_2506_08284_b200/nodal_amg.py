@@ -1,0 +1,134 @@
+"""Smoothed aggregation for the auxiliary nodal problem, on the B200.
+
+Mirror of the reference's nodal_amg.py (same names and results). Every row is
+bit-identical to the reference (SURVEY.md Hazard 1 / Appendix A): the
+strength pattern, the power-method norms (Haswell-ddot order), the Jacobi-
+smoothed prolongator and its row normalisation run as libsphcurl kernels with
+explicit round-to-nearest arithmetic; the greedy aggregation is the host C++
+pass of libsphcurl (sequential by definition).
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import device as dv
+from .device import DeviceCSR, Status, as_device_csr, call
+
+
+@dataclass
+class Aggregation:
+    """Partition of fine nodes into aggregates (nodal_amg.py:17-23)."""
+
+    n_fine: int
+    n_agg: int
+    membership: torch.Tensor     # int64 aggregate id per fine node (device)
+
+
+@dataclass
+class NodalProlongator:
+    P: DeviceCSR
+    omega_used: float
+    rho_estimate: float
+
+
+def strength_graph(A_n, drop_tol):
+    """Symmetric strength pattern incl. the diagonal (nodal_amg.py:33-56)."""
+    A = as_device_csr(A_n)
+    n = A.shape[0]
+    st = Status()
+    d = dv.diagonal(A)
+    cnt = torch.empty(n, dtype=torch.int64, device=A.rowptr.device)
+    call("sphc_strength_count", n, A.rowptr, A.col, A.val, d, float(drop_tol), cnt, st.t)
+    rows = st.rows()
+    if "NONPOS_DIAG" in rows:
+        raise ValueError(f"nonpositive diagonal entry in row {rows['NONPOS_DIAG']}")
+    frp, nnz = dv.scan(cnt)
+    fci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
+    call("sphc_strength_fill", n, A.rowptr, A.col, A.val, d, float(drop_tol), frp, fci)
+    F = DeviceCSR(frp, fci, None, A.shape)
+    Ft = dv.transpose(F)
+    call("sphc_pattern_union_count", n, F.rowptr, F.col, Ft.rowptr, Ft.col, cnt)
+    srp, snnz = dv.scan(cnt)
+    sci = torch.empty(snnz, dtype=torch.int32, device=A.rowptr.device)
+    call("sphc_pattern_union_fill", n, F.rowptr, F.col, Ft.rowptr, Ft.col, srp, sci)
+    return DeviceCSR(srp, sci, None, A.shape)
+
+
+def aggregate(strength):
+    """Greedy two-phase root aggregation (nodal_amg.py:59-88); host C++."""
+    n = strength.shape[0]
+    rp = strength.rowptr.cpu().numpy()
+    ci = strength.col.cpu().numpy()
+    memb = np.empty(n, dtype=np.int64)
+    n_agg = np.zeros(1, dtype=np.int64)
+    call("sphc_host_aggregate", n, rp, ci, memb, n_agg)
+    return Aggregation(n_fine=n, n_agg=int(n_agg[0]),
+                       membership=torch.from_numpy(memb).to(strength.rowptr.device))
+
+
+def _power_start(n):
+    # the reference's deterministic start vector, formed by numpy on the host
+    # (nodal_amg.py:106) and uploaded once
+    return torch.from_numpy(1.0 + 0.01 * np.sin(np.arange(n, dtype=np.float64))).to(dv.device())
+
+
+def estimate_rho(A, dinv, iterations=10):
+    """Ten-step power method on diag(1/d) A (nodal_amg.py:99-116). The norms
+    run in the OpenBLAS-Haswell ddot order, so rho is bit-identical."""
+    n = A.shape[0]
+    v = _power_start(n)
+    sq = dv.empty_f64(1)
+    norms = dv.empty_f64(iterations + 1)
+    call("sphc_hsw_dot", n, v, v, sq)
+    call("sphc_scale_by_norm", n, v, sq, v, norms[0:1])
+    w = dv.empty_f64(n)
+    for it in range(iterations):
+        call("sphc_nodal_powmv", n, A.rowptr, A.col, A.val, dinv, v, w)
+        call("sphc_hsw_dot", n, w, w, sq)
+        call("sphc_scale_by_norm", n, w, sq, v, norms[it + 1:it + 2])
+    h = norms.cpu().numpy()
+    rho = 1.0
+    for it in range(iterations):
+        if h[it + 1] == 0.0:
+            return 0.0
+        rho = float(h[it + 1])
+    return rho
+
+
+def _dinv(A):
+    st = Status()
+    d = dv.diagonal(A, st)
+    if "ZERO_DIAG" in st.rows():
+        raise ValueError("zero diagonal in nodal operator")
+    return dv.reciprocal(d)
+
+
+def smooth_and_normalize(A_n, agg):
+    """P = normalize((I - omega D^-1 A_n) P_tent), omega = 4 / (3 rho)
+    (nodal_amg.py:138-155). ``agg`` replaces the reference's P_tent argument
+    (the tentative prolongator is exactly the membership array)."""
+    A = as_device_csr(A_n)
+    n = A.shape[0]
+    if n != agg.n_fine:
+        raise ValueError(f"incompatible shapes {A.shape} and {(agg.n_fine, agg.n_agg)}")
+    dinv = _dinv(A)
+    rho = estimate_rho(A, dinv)
+    omega = 4.0 / (3.0 * rho)
+    st = Status()
+    cnt = torch.empty(n, dtype=torch.int64, device=A.rowptr.device)
+    call("sphc_nodal_smooth_count", n, A.rowptr, A.col, A.val, dinv, agg.membership, omega,
+         cnt, st.t)
+    prp, nnz = dv.scan(cnt)
+    pci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
+    pv = dv.empty_f64(nnz)
+    call("sphc_nodal_smooth_fill", n, A.rowptr, A.col, A.val, dinv, agg.membership, omega,
+         prp, pci, pv, st.t)
+    rows = st.rows()
+    if "SPGEMM_CAPACITY" in rows:
+        raise RuntimeError(f"nodal row {rows['SPGEMM_CAPACITY']} exceeds the kernel capacity")
+    if "ZERO_ROWSUM" in rows:
+        raise ValueError(f"zero row sum before scaling in row {rows['ZERO_ROWSUM']}")
+    P = DeviceCSR(prp, pci, pv, (n, agg.n_agg))
+    return NodalProlongator(P=P, omega_used=omega, rho_estimate=rho)

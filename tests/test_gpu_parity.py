@@ -1,0 +1,239 @@
+"""CUDA path vs oracle / reference goldens (run on a B200: pytest -m gpu).
+
+Parity classes: BIT for aggregates, omega/rho, P_n, the
+piecewise-constant map, coarse edges, patterns and coarse counts; TOL (1e-10
+relative to the matrix max) for P_e and coarse operators; commutator residual
+<= 1e-12; PCG iterations within +-1 of the same-smoother oracle.
+"""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from golden_util import csr_hash, golden_csr, load_case, rel_max_diff, sha
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+    from paper_2506_08284_b200.build import build_library
+    build_library()
+
+
+def _dev():
+    from paper_2506_08284_b200 import device as dv
+    return dv
+
+
+def _rand_csr(n, m, density, seed, dtype=np.float64):
+    rng = np.random.default_rng(seed)
+    A = sp.random(n, m, density=density, random_state=rng, format="csr")
+    A.data = rng.standard_normal(A.nnz) * np.exp(2 * rng.standard_normal(A.nnz))
+    A.sum_duplicates()
+    A.sort_indices()
+    return A
+
+
+def test_scan_and_reductions():
+    dv = _dev()
+    rng = np.random.default_rng(0)
+    for n in (0, 1, 5, 2047, 2048, 2049, 5_000_001):
+        c = rng.integers(0, 7, n).astype(np.int64)
+        rp, tot = dv.scan(torch.from_numpy(c).cuda())
+        ref = np.concatenate([[0], np.cumsum(c)])
+        assert tot == ref[-1]
+        assert np.array_equal(rp.cpu().numpy(), ref)
+    x = rng.standard_normal(1_000_003)
+    y = rng.standard_normal(x.size)
+    xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    assert abs(dv.dot(xt, yt).item() - x @ y) <= 1e-12 * np.abs(x * y).sum()
+    assert dv.maxabs(xt).item() == np.abs(x).max()
+    assert abs(dv.vsum(xt).item() - x.sum()) <= 1e-12 * np.abs(x).sum()
+
+
+def test_hsw_dot_bitwise():
+    """Device Haswell-order ddot == oracle restatement (== pinned numpy)."""
+    from oracle.hcurl_oracle import hsw_dot
+    from paper_2506_08284_b200.device import call
+    rng = np.random.default_rng(1)
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    for n in list(range(0, 40)) + [1000, 65537, 2_000_003]:
+        x = rng.standard_normal(n) * np.exp(3 * rng.standard_normal(n))
+        xt = torch.from_numpy(x).cuda()
+        call("sphc_hsw_dot", n, xt, xt, out)
+        assert out.item() == hsw_dot(x, x), n
+
+
+@pytest.mark.parametrize("lanes", [1, 2, 4, 8, 16, 32])
+def test_spmv(lanes):
+    dv = _dev()
+    A = _rand_csr(3000, 2000, 0.01, 2)
+    x = np.random.default_rng(3).standard_normal(2000)
+    z = np.random.default_rng(4).standard_normal(3000)
+    Ad = dv.DeviceCSR.from_scipy(A)
+    y = torch.empty(3000, dtype=torch.float64, device="cuda")
+    dv.spmv(Ad, torch.from_numpy(x).cuda(), y, alpha=-1.0, beta=2.0,
+            z=torch.from_numpy(z).cuda(), lanes=lanes)
+    ref = -(A @ x) + 2.0 * z
+    assert np.max(np.abs(y.cpu().numpy() - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_spgemm_matches_scipy_bitwise():
+    """Sequential ascending-k sums: identical bits to scipy's csr_matmat."""
+    dv = _dev()
+    for seed, (n, k, m, d1, d2) in enumerate([(500, 400, 300, 0.02, 0.03),
+                                               (2000, 2000, 2000, 0.005, 0.005),
+                                               (50, 3000, 40, 0.1, 0.05)]):
+        A = _rand_csr(n, k, d1, 10 + seed)
+        B = _rand_csr(k, m, d2, 20 + seed)
+        C = dv.spgemm(dv.DeviceCSR.from_scipy(A), dv.DeviceCSR.from_scipy(B)).to_scipy()
+        ref = A @ B
+        ref.sort_indices()
+        assert np.array_equal(C.indptr, ref.indptr)
+        assert np.array_equal(C.indices, ref.indices)
+        assert np.array_equal(C.data.view(np.uint64), ref.data.view(np.uint64))
+
+
+def test_transpose():
+    dv = _dev()
+    A = _rand_csr(4000, 700, 0.01, 5)
+    T = dv.transpose(dv.DeviceCSR.from_scipy(A)).to_scipy()
+    ref = sp.csr_matrix(A.T)
+    ref.sort_indices()
+    assert np.array_equal(T.indptr, ref.indptr)
+    assert np.array_equal(T.indices, ref.indices)
+    assert np.array_equal(T.data, ref.data)
+
+
+# ---------------------------------------------------------------------------
+# per-level parity against the oracle
+
+
+def _system(N, sigma, dirichlet):
+    from paper_2506_08284_b200.inputs import discretize_hex
+    return discretize_hex(N, sigma, dirichlet)
+
+
+@pytest.mark.parametrize("N,sigma,dirichlet", [(4, 1.0, False), (6, 1.0, True),
+                                               (10, 1e-4, False), (16, 1.0, True)])
+def test_nodal_chain_and_topology_bitwise(N, sigma, dirichlet):
+    from oracle import hcurl_oracle as O
+    from paper_2506_08284_b200 import coarse_gradient as cg
+    from paper_2506_08284_b200 import nodal_amg as na
+    s = _system(N, sigma, dirichlet)
+    Sg = na.strength_graph(s.A_n, 0.0).to_scipy()
+    So = O.strength_pattern(s.A_n)
+    assert np.array_equal(Sg.indptr, So.indptr) and np.array_equal(Sg.indices, So.indices)
+    agg = na.aggregate(na.strength_graph(s.A_n, 0.0))
+    memb_o, nagg_o = O.aggregate(So)
+    assert agg.n_agg == nagg_o
+    assert np.array_equal(agg.membership.cpu().numpy(), memb_o)
+    nod = na.smooth_and_normalize(s.A_n, agg)
+    Po, wo, ro = O.smoothed_prolongator(s.A_n, memb_o, nagg_o)
+    assert nod.rho_estimate == ro and nod.omega_used == wo
+    assert csr_hash(nod.P.to_scipy()) == csr_hash(Po)
+    assign = cg.gen_piecewise_const(nod.P, 2).cpu().numpy()
+    assert np.array_equal(assign, O.piecewise_const(Po, 2))
+    cgd = cg.build_coarse_gradient(s.D, torch.from_numpy(assign).cuda(), nagg_o)
+    ceo = O.coarse_edges(s.D, assign, nagg_o)
+    assert cgd.n_interior == ceo.pairs.shape[0] and cgd.n_single == ceo.singles.size
+    DH = cgd.D_H.to_scipy()
+    assert csr_hash(DH) == csr_hash(ceo.D_H())
+
+
+@pytest.mark.parametrize("N,sigma,dirichlet", [(4, 1.0, False), (6, 1.0, True),
+                                               (10, 1e-4, False), (16, 1.0, True)])
+def test_edge_prolongator_vs_oracle(N, sigma, dirichlet):
+    from oracle import hcurl_oracle as O
+    from paper_2506_08284_b200 import edge_prolongator as ep
+    s = _system(N, sigma, dirichlet)
+    prol, cgd, nod = ep.build_edge_prolongator(s.A_n, s.A_e, s.S, s.D)
+    memb, nagg = O.aggregate(O.strength_pattern(s.A_n))
+    Po, _, _ = O.smoothed_prolongator(s.A_n, memb, nagg)
+    ce = O.coarse_edges(s.D, O.piecewise_const(Po, 2), nagg)
+    em = O.emin_prolongator(s.D, Po, ce, s.S)
+    P = prol.P_e.to_scipy()
+    # STRUCT
+    assert np.array_equal(P.indptr, em.P_e.indptr)
+    assert np.array_equal(P.indices, em.P_e.indices)
+    assert dict(prol.subproblem_dims) == dict(em.subproblem_dims)
+    # TOL
+    assert rel_max_diff(P, em.P_e) <= 1e-10
+    assert np.allclose(prol.energy_history, em.energy_history, rtol=1e-10, atol=0)
+    assert prol.commutator_residual <= 1e-12
+
+
+GOLDEN_CASES = ["N4n", "N6d", "N8d", "N10n", "C1", "N16n", "C2"]
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_hierarchy_vs_reference_golden(name):
+    """Full build_hierarchy on the device vs the reference's own outputs."""
+    from paper_2506_08284_b200 import multigrid as mg
+    meta, arrays = load_case(name)
+    s = _system(meta["N"], meta["sigma"], meta["dirichlet"])
+    h = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, mg.SolverConfig(coarse_size=meta["coarse_size"]))
+    assert [lv.A_e.shape[0] for lv in h.levels] == meta["n_edges"]
+    assert [lv.A_e.nnz for lv in h.levels] == meta["nnz_A_e"]
+    assert abs(h.operator_complexity - meta["operator_complexity"]) < 1e-14
+    for li, (lv, L) in enumerate(zip(h.levels, meta["levels"])):
+        assert csr_hash(lv.D.to_scipy()) == L["D"], li
+        if lv.P_e is None:
+            continue
+        assert sha(lv.membership.cpu().numpy().astype(np.int64)) == L["membership"]
+        assert float(lv.omega).hex() == L["omega_hex"]
+        assert float(lv.rho).hex() == L["rho_hex"]
+        assert csr_hash(lv.P_n.to_scipy()) == L["P_n"]
+        assert sha(lv.assignment.cpu().numpy().astype(np.int64)) == L["assignment"]
+        P = lv.P_e.to_scipy()
+        assert sha(P.indptr.astype(np.int64), P.indices.astype(np.int64)) == L["P_e_pattern"]
+        dims = sorted([list(k) + [v] for k, v in lv.subproblem_dims.items()])
+        assert dims == L["subproblem_dims"]
+        rows = arrays[f"L{li}_Pe_sample_rows"]
+        ref = golden_csr(arrays, f"L{li}_Pe_sample", (rows.size, P.shape[1]))
+        assert rel_max_diff(P[rows], ref) <= 1e-10
+        assert np.allclose(lv.emin_energy, L["emin_energy"], rtol=1e-10, atol=0)
+        assert lv.commutator_residual <= 1e-12
+        if f"L{li + 1}_A_e_data" in arrays:
+            nxt = h.levels[li + 1]
+            n1 = nxt.A_e.shape[0]
+            Aref = golden_csr(arrays, f"L{li + 1}_A_e", (n1, n1))
+            Ag = nxt.A_e.to_scipy()
+            assert np.array_equal(Ag.indptr, Aref.indptr)
+            assert np.array_equal(Ag.indices, Aref.indices)
+            assert rel_max_diff(Ag, Aref) <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["N6d", "N10n", "C1", "N16n", "C2"])
+def test_solve_iterations_vs_reference(name):
+    """PCG iterations within +-1 of the reference hierarchy with the same
+    Chebyshev sweeper, and within +-1 of the reference's Gauss-Seidel."""
+    from paper_2506_08284_b200 import multigrid as mg
+    meta, _ = load_case(name)
+    s = _system(meta["N"], meta["sigma"], meta["dirichlet"])
+    b = np.random.default_rng(meta["seed"]).uniform(-1, 1, s.A_e.shape[0])
+    h = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, mg.SolverConfig(coarse_size=meta["coarse_size"]))
+    res = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+    assert res.status == "converged"
+    assert abs(res.iterations - meta["cheb"]["iterations"]) <= 1
+    assert res.relative_residual <= 1e-8
+    # true residual of the returned x
+    x = res.x
+    assert np.linalg.norm(b - s.A_e @ x) <= 1.5e-8 * np.linalg.norm(b)
+
+
+def test_error_case_matches_reference():
+    import json
+    import os
+    from golden_util import GOLDEN
+    from paper_2506_08284_b200 import multigrid as mg
+    with open(os.path.join(GOLDEN, "errors.json")) as f:
+        msg = json.load(f)["N8d_cs100"]
+    s = _system(8, 1.0, True)
+    with pytest.raises(ValueError) as e:
+        mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, mg.SolverConfig(coarse_size=100))
+    assert str(e.value).split(":")[0] == msg.split(":")[0]

@@ -176,6 +176,9 @@ def run_ours(args):
         barrier()
     launches = (_lib.launch_count() - l0) // args.steps
     step_ms = [a.elapsed_time(bb) for a, bb in ev]
+    from paper_2506_08284_b200 import trace
+    if trace.ENABLED:
+        print("step ms:", step_ms, "\n" + trace.report(), file=sys.stderr)
     t_step = sum(step_ms) / args.steps
     if ws > 1:
         t = torch.tensor([t_step], dtype=torch.float64, device=dev)

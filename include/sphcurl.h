@@ -134,15 +134,17 @@ int sphc_csr_to_dense(int64_t n_rows, int64_t n_cols, const int64_t *rp, const i
 int sphc_spgemm_count(int64_t n, const int64_t *arp, const int32_t *aci, const int64_t *brp,
                       const int32_t *bci, int64_t *counts, int64_t *status, void *stream);
 
-/* Numeric C = A B on the structural pattern, columns ascending. Every entry
- * is a sequential sum over k ascending of a_ik * b_kj with no FMA, which is
- * scipy csr_matmat's order: bit-identical for the nodal Galerkin product
- * (multigrid.py:152) and used for the edge Galerkin products (:150-151), the
- * auxiliary nodal operator D^T A D (:103) and the null-space check (:111). */
+/* Numeric C = A B on the structural pattern, columns ascending.
+ * ordered != 0: every entry is a sequential sum over k ascending of
+ *   a_ik * b_kj with no FMA -- scipy csr_matmat's order, bit-identical for the
+ *   nodal Galerkin product (multigrid.py:152).
+ * ordered == 0: all lanes busy (sorted 32-product chunks, fixed shuffle-tree
+ *   reduction); deterministic, TOL class. Used for the edge Galerkin products
+ *   (:150-151), D^T A D (:103) and the null-space check (:111). */
 int sphc_spgemm_fill(int64_t n, const int64_t *arp, const int32_t *aci, const double *av,
                      const int64_t *brp, const int32_t *bci, const double *bv,
-                     const int64_t *crp, int32_t *cci, double *cv, int64_t *status,
-                     void *stream);
+                     const int64_t *crp, int32_t *cci, double *cv, int ordered,
+                     int64_t *status, void *stream);
 
 /* ---------------------------------------------------------------- solve */
 
@@ -167,13 +169,23 @@ int sphc_diag_scale(int64_t n, const double *d, const double *x, double *y, void
  * (splitmix64 of the index; oracle.cheb_start_vector computes the same). */
 int sphc_cheb_start(int64_t n, double *x, void *stream);
 
-/* x += alpha p; r -= alpha Ap; *changed = 1 if any x_i changed
- * (multigrid.py:247-257, the array_equal stagnation test). */
-int sphc_pcg_update(int64_t n, double alpha, const double *p, const double *Ap, double *x,
+/* PCG scalar slots of the device array `sc` (multigrid.py:220-274). */
+#define SPHC_PCG_PAP 0  /* p . Ap        */
+#define SPHC_PCG_RR 1   /* r . r         */
+#define SPHC_PCG_RZ 2   /* r . z (current) */
+#define SPHC_PCG_RZN 3  /* r . z (new)   */
+
+/* alpha = sc[RZ] / sc[PAP]; if sc[PAP] > 0: x += alpha p, r -= alpha Ap and
+ * *changed = 1 if any x_i changed (multigrid.py:244-257: the indefinite and
+ * array_equal stagnation tests). No-op when p.Ap <= 0. */
+int sphc_pcg_update(int64_t n, const double *sc, const double *p, const double *Ap, double *x,
                     double *r, int32_t *changed, void *stream);
 
-/* p = z + beta p (multigrid.py:270). */
-int sphc_pcg_direction(int64_t n, double beta, const double *z, double *p, void *stream);
+/* p = z + (sc[RZN] / sc[RZ]) p (multigrid.py:268-270). */
+int sphc_pcg_direction(int64_t n, const double *sc, const double *z, double *p, void *stream);
+
+/* sc[RZ] = sc[RZN] */
+int sphc_pcg_rotate(double *sc, void *stream);
 
 /* y = A x for a dense row-major n x n A (coarsest level, explicit inverse of
  * the reference's lu_factor/lu_solve pair, multigrid.py:157,181). */

@@ -80,9 +80,13 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   atomicMax((unsigned long long*)addr, (unsigned long long)__double_as_longlong(v));
 }
 
-// stream-ordered scratch
+// stream-ordered scratch from the device's default pool; the pool keeps its
+// memory across synchronisations (release threshold = max) so repeated
+// setup passes do not re-map pages
+int sphc_pool_init();
 template <typename T>
 static inline int scratch(T** p, size_t n, cudaStream_t s) {
+  if (sphc_pool_init()) return SPHC_ERR_CUDA;
   SPHC_CUDA(cudaMallocAsync((void**)p, (n ? n : 1) * sizeof(T), s));
   return 0;
 }

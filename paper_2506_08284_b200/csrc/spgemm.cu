@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(SPG_WARPS * 32)
   }
 }
 
+template <bool ORDERED>
 __global__ void __launch_bounds__(SPG_WARPS * 32)
     k_spgemm_fill(i64 n, const i64* __restrict__ arp, const int* __restrict__ aci,
                   const double* __restrict__ av, const i64* __restrict__ brp,
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(SPG_WARPS * 32)
   __shared__ i64 s_bs[SPG_WARPS][32];
   __shared__ int list[SPG_WARPS][SPG_CCAP];
   __shared__ double acc[SPG_WARPS][SPG_CCAP];
+  __shared__ double s_a[SPG_WARPS][32];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (i64 row = (i64)blockIdx.x * SPG_WARPS + w; row < n; row += (i64)gridDim.x * SPG_WARPS) {
     bool ok = spg_symbolic_row(row, arp, aci, brp, bci, table[w], &ucount[w], s_off[w], s_bs[w],
@@ -144,17 +146,82 @@ __global__ void __launch_bounds__(SPG_WARPS * 32)
       }
     for (int t = lane; t < nu; t += 32) acc[w][t] = 0.0;
     __syncwarp();
-    // numeric: ascending k, sequential unfused accumulation per column
     i64 as = arp[row], ae = arp[row + 1];
-    for (i64 ja = as; ja < ae; ja++) {
-      int k = aci[ja];
-      double a = av[ja];
-      i64 be = brp[k + 1];
-      for (i64 jb = brp[k] + lane; jb < be; jb += 32) {
-        int slot = lower_bound_i32(list[w], nu, bci[jb]);
-        acc[w][slot] = __dadd_rn(acc[w][slot], __dmul_rn(a, bv[jb]));
+    if (ORDERED) {
+      // ascending k, sequential unfused accumulation per column (scipy order)
+      for (i64 ja = as; ja < ae; ja++) {
+        int k = aci[ja];
+        double a = av[ja];
+        i64 be = brp[k + 1];
+        for (i64 jb = brp[k] + lane; jb < be; jb += 32) {
+          int slot = lower_bound_i32(list[w], nu, bci[jb]);
+          acc[w][slot] = __dadd_rn(acc[w][slot], __dmul_rn(a, bv[jb]));
+        }
+        __syncwarp();
       }
-      __syncwarp();
+    } else {
+      // all lanes busy: chunks of 32 flattened products, sorted by column in
+      // registers and reduced per column with a fixed shuffle tree, so the
+      // result is deterministic (not scipy-bitwise; TOL class)
+      for (i64 c0 = as; c0 < ae; c0 += 32) {
+        int len = 0;
+        i64 bs = 0;
+        double a = 0.0;
+        if (c0 + lane < ae) {
+          int k = aci[c0 + lane];
+          a = av[c0 + lane];
+          bs = brp[k];
+          len = (int)(brp[k + 1] - bs);
+        }
+        int incl = len;
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_up_sync(FULL_MASK, incl, o);
+          if (lane >= o) incl += y;
+        }
+        s_off[w][lane] = incl;
+        s_bs[w][lane] = bs;
+        s_a[w][lane] = a;
+        __syncwarp();
+        int total = s_off[w][31];
+        for (int f0 = 0; f0 < total; f0 += 32) {
+          int f = f0 + lane;
+          int key = 0x7fffffff;
+          double val = 0.0;
+          if (f < total) {
+            int lo = 0, hi = 31;
+            while (lo < hi) {
+              int mid = (lo + hi) >> 1;
+              if (s_off[w][mid] > f) hi = mid; else lo = mid + 1;
+            }
+            int before = lo ? s_off[w][lo - 1] : 0;
+            i64 jb = s_bs[w][lo] + (f - before);
+            key = lower_bound_i32(list[w], nu, bci[jb]);
+            val = s_a[w][lo] * bv[jb];
+          }
+          // bitonic sort of (key, val) across the warp
+          for (int kk = 2; kk <= 32; kk <<= 1)
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+              int pk = __shfl_xor_sync(FULL_MASK, key, j);
+              double pv = __shfl_xor_sync(FULL_MASK, val, j);
+              bool up = (lane & kk) == 0;
+              bool lower = (lane & j) == 0;
+              bool sw = lower ? ((key > pk) == up) : ((key < pk) == up);
+              if (key == pk) sw = false;
+              if (sw) { key = pk; val = pv; }
+            }
+          // inclusive segmented scan; the last lane of each run owns the sum
+          for (int o = 1; o < 32; o <<= 1) {
+            double y = __shfl_up_sync(FULL_MASK, val, o);
+            int yk = __shfl_up_sync(FULL_MASK, key, o);
+            if (lane >= o && yk == key) val += y;
+          }
+          int nk = __shfl_down_sync(FULL_MASK, key, 1);
+          bool last = (lane == 31) || (nk != key);
+          if (last && key != 0x7fffffff) acc[w][key] += val;
+          __syncwarp();
+        }
+        __syncwarp();
+      }
     }
     i64 o = crp[row];
     for (int t = lane; t < nu; t += 32) {
@@ -179,11 +246,16 @@ extern "C" int sphc_spgemm_count(int64_t n, const int64_t* arp, const int32_t* a
 extern "C" int sphc_spgemm_fill(int64_t n, const int64_t* arp, const int32_t* aci,
                                 const double* av, const int64_t* brp, const int32_t* bci,
                                 const double* bv, const int64_t* crp, int32_t* cci, double* cv,
-                                int64_t* status, void* stream) {
+                                int ordered, int64_t* status, void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
-  k_spgemm_fill<<<grid_for(n, SPG_WARPS, SPHC_NUM_SMS * 64), SPG_WARPS * 32, 0, s>>>(
-      n, arp, aci, av, brp, bci, bv, crp, cci, cv, status);
+  unsigned g = grid_for(n, SPG_WARPS, SPHC_NUM_SMS * 64);
+  if (ordered)
+    k_spgemm_fill<true><<<g, SPG_WARPS * 32, 0, s>>>(n, arp, aci, av, brp, bci, bv, crp, cci,
+                                                     cv, status);
+  else
+    k_spgemm_fill<false><<<g, SPG_WARPS * 32, 0, s>>>(n, arp, aci, av, brp, bci, bv, crp, cci,
+                                                      cv, status);
   SPHC_LAUNCH_CHECK();
   return 0;
 }

@@ -107,9 +107,14 @@ extern "C" int sphc_cheb_step(int64_t n, const int64_t* rp, const int32_t* ci, c
   return 0;
 }
 
-__global__ void k_pcg_update(i64 n, double alpha, const double* __restrict__ p,
+// PCG scalars live on the device (slots SPHC_PCG_*), so a whole iteration
+// can be replayed as one CUDA graph with a single small readback.
+__global__ void k_pcg_update(i64 n, const double* __restrict__ sc, const double* __restrict__ p,
                              const double* __restrict__ Ap, double* __restrict__ x,
                              double* __restrict__ r, int* changed) {
+  double pAp = sc[SPHC_PCG_PAP];
+  if (!(pAp > 0.0)) return;  // "indefinite": the reference stops before updating
+  double alpha = sc[SPHC_PCG_RZ] / pAp;
   int ch = 0;
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (i64)gridDim.x * blockDim.x) {
@@ -123,25 +128,35 @@ __global__ void k_pcg_update(i64 n, double alpha, const double* __restrict__ p,
   if (ch && threadIdx.x == 0) atomicOr(changed, 1);
 }
 
-extern "C" int sphc_pcg_update(int64_t n, double alpha, const double* p, const double* Ap,
+extern "C" int sphc_pcg_update(int64_t n, const double* sc, const double* p, const double* Ap,
                                double* x, double* r, int32_t* changed, void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_pcg_update<<<grid_for(n, 256), 256, 0, s>>>(n, alpha, p, Ap, x, r, changed);
+  k_pcg_update<<<grid_for(n, 256), 256, 0, s>>>(n, sc, p, Ap, x, r, changed);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
 
-__global__ void k_pcg_dir(i64 n, double beta, const double* __restrict__ z,
+__global__ void k_pcg_dir(i64 n, const double* __restrict__ sc, const double* __restrict__ z,
                           double* __restrict__ p) {
+  double beta = sc[SPHC_PCG_RZN] / sc[SPHC_PCG_RZ];
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (i64)gridDim.x * blockDim.x)
     p[i] = z[i] + beta * p[i];
 }
 
-extern "C" int sphc_pcg_direction(int64_t n, double beta, const double* z, double* p,
+extern "C" int sphc_pcg_direction(int64_t n, const double* sc, const double* z, double* p,
                                   void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_pcg_dir<<<grid_for(n, 256), 256, 0, s>>>(n, beta, z, p);
+  k_pcg_dir<<<grid_for(n, 256), 256, 0, s>>>(n, sc, z, p);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+__global__ void k_pcg_rotate(double* sc) { sc[SPHC_PCG_RZ] = sc[SPHC_PCG_RZN]; }
+
+extern "C" int sphc_pcg_rotate(double* sc, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_pcg_rotate<<<1, 1, 0, s>>>(sc);
   SPHC_LAUNCH_CHECK();
   return 0;
 }

@@ -17,6 +17,19 @@ extern "C" const char* sphc_last_error(void) { return g_err; }
 extern "C" int sphc_abi_version(void) { return 1; }
 
 unsigned long long g_sphc_launches = 0;
+
+int sphc_pool_init() {
+  static int done = -1;
+  int dev = 0;
+  SPHC_CUDA(cudaGetDevice(&dev));
+  if (done == dev) return 0;
+  cudaMemPool_t pool;
+  SPHC_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = ~0ull;
+  SPHC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done = dev;
+  return 0;
+}
 extern "C" int64_t sphc_launch_count(void) { return (int64_t)g_sphc_launches; }
 
 // ------------------------------------------------------------------ scan
@@ -153,14 +166,16 @@ __global__ void k_reduce_final(int nparts, const double* __restrict__ part, doub
 
 template <int MODE>
 static int reduce_launch(i64 n, const double* x, const double* y, double* out, cudaStream_t s) {
+  // persistent partials: reductions are stream ordered, and a fixed buffer
+  // keeps them capturable in CUDA graphs (no allocation nodes)
+  static double* part = nullptr;
+  if (!part) SPHC_CUDA(cudaMalloc((void**)&part, RED_MAX_BLOCKS * sizeof(double)));
   int nb = (int)grid_for(n, RED_THREADS, RED_MAX_BLOCKS);
-  double* part = nullptr;
-  if (scratch(&part, nb, s)) return SPHC_ERR_CUDA;
   k_reduce_partial<MODE><<<nb, RED_THREADS, 0, s>>>(n, x, y, part);
   SPHC_LAUNCH_CHECK();
   k_reduce_final<MODE><<<1, 1024, 0, s>>>(nb, part, out);
   SPHC_LAUNCH_CHECK();
-  return scratch_free(part, s);
+  return 0;
 }
 
 extern "C" int sphc_dot(int64_t n, const double* x, const double* y, double* out, void* stream) {
@@ -183,8 +198,20 @@ __global__ void k_hsw_dot(i64 n, const double* __restrict__ x, const double* __r
   i64 n1 = n & ~(i64)15;
   double acc = 0.0;
   if (lane < 16) {
+    // the chain is sequential; loads are batched 16 deep so the FMA chain,
+    // not memory latency, sets the pace
+    const int B = 16;
     i64 i = lane;
-#pragma unroll 8
+    for (; i + 16 * (B - 1) < n1; i += 16 * B) {
+      double xa[B], ya[B];
+#pragma unroll
+      for (int u = 0; u < B; u++) {
+        xa[u] = x[i + 16 * u];
+        ya[u] = y[i + 16 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < B; u++) acc = __fma_rn(xa[u], ya[u], acc);
+    }
     for (; i < n1; i += 16) acc = __fma_rn(x[i], y[i], acc);
   }
   double a[16];

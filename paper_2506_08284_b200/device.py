@@ -174,9 +174,9 @@ def drop_zeros(A):
     return DeviceCSR(rp, ci, v, A.shape)
 
 
-def spgemm(A, B, drop=True):
-    """C = A B with scipy csr_matmat's accumulation order; exact zeros dropped
-    like scipy's product (drop=True)."""
+def spgemm(A, B, drop=True, ordered=False):
+    """C = A B; exact zeros dropped like scipy's product (drop=True).
+    ordered=True reproduces scipy csr_matmat's accumulation bit for bit."""
     if A.shape[1] != B.shape[0]:
         raise ValueError(f"spgemm dimension mismatch: {A.shape} @ {B.shape}")
     n = A.shape[0]
@@ -188,7 +188,7 @@ def spgemm(A, B, drop=True):
     ci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
     v = empty_f64(nnz)
     call("sphc_spgemm_fill", n, A.rowptr, A.col, A.val, B.rowptr, B.col, B.val, rp, ci, v,
-         st.t)
+         int(ordered), st.t)
     C = DeviceCSR(rp, ci, v, (A.shape[0], B.shape[1]))
     return drop_zeros(C) if drop else C
 

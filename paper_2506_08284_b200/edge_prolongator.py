@@ -18,6 +18,7 @@ from . import device as dv
 from . import emin_setup as es
 from . import nodal_amg as na
 from .device import DeviceCSR, Status, as_device_csr, call
+from .trace import phase
 
 
 @dataclass
@@ -98,13 +99,20 @@ def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None):
     cfg = cfg or EminConfig()
     if cfg.mode != "sphcurl":
         raise NotImplementedError("rsamg mode is outside the B200 hot path")
-    strength = na.strength_graph(A_n, cfg.drop_tol)
-    agg = na.aggregate(strength)
-    nod = na.smooth_and_normalize(A_n, agg)
-    assign = cgrad.gen_piecewise_const(nod.P, cfg.n_passes)
-    cg = cgrad.build_coarse_gradient(D_h, assign, agg.n_agg)
-    setup = es.setup_constraints(D_h, nod.P, cg)
-    vals, energy, res = emin_sweeps(S, setup, cfg.omega, cfg.iterations)
+    with phase("setup.strength"):
+        strength = na.strength_graph(A_n, cfg.drop_tol)
+    with phase("setup.aggregate(host)"):
+        agg = na.aggregate(strength)
+    with phase("setup.smooth_and_normalize"):
+        nod = na.smooth_and_normalize(A_n, agg)
+    with phase("setup.piecewise_const(host)"):
+        assign = cgrad.gen_piecewise_const(nod.P, cfg.n_passes)
+    with phase("setup.coarse_gradient"):
+        cg = cgrad.build_coarse_gradient(D_h, assign, agg.n_agg)
+    with phase("setup.emin_constraints"):
+        setup = es.setup_constraints(D_h, nod.P, cg)
+    with phase("setup.emin_sweeps"):
+        vals, energy, res = emin_sweeps(S, setup, cfg.omega, cfg.iterations)
     P = setup.pattern
     P_e = DeviceCSR(P.rowptr, P.col, vals, P.shape)
     prol = EdgeProlongator(P_e=P_e, energy_history=energy, commutator_residual=res,

@@ -23,6 +23,8 @@ import torch
 from . import device as dv
 from .device import DeviceCSR, Status, as_device_csr, call
 from .edge_prolongator import EminConfig, build_edge_prolongator
+from . import trace as _trace
+from .trace import phase
 
 _NULLSPACE_TOL = 1e-10
 CHEB_POWER_ITERS = 15
@@ -204,24 +206,33 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None):
             raise ValueError(
                 f"coarsening stagnated: {n_coarse} coarse edges from "
                 f"{A_e.shape[0]} fine edges")
-        lv = _make_level(A_e, S_e, D, cfg.cheb_degree, P_e=P_e, P_n=P_n,
-                         emin_energy=prol.energy_history,
-                         subproblem_dims=dict(prol.subproblem_dims),
-                         commutator_residual=prol.commutator_residual,
-                         n_augmented=prol.n_augmented,
-                         membership=prol.membership, assignment=prol.assignment,
-                         coarse_gradient=cg, omega=nod.omega_used, rho=nod.rho_estimate)
-        lv.R_e = dv.transpose(P_e)
+        with phase("level.make_level"):
+            lv = _make_level(A_e, S_e, D, cfg.cheb_degree, P_e=P_e, P_n=P_n,
+                             emin_energy=prol.energy_history,
+                             subproblem_dims=dict(prol.subproblem_dims),
+                             commutator_residual=prol.commutator_residual,
+                             n_augmented=prol.n_augmented,
+                             membership=prol.membership, assignment=prol.assignment,
+                             coarse_gradient=cg, omega=nod.omega_used,
+                             rho=nod.rho_estimate)
+        with phase("level.transpose_Pe"):
+            lv.R_e = dv.transpose(P_e)
         lv.rc = dv.empty_f64(n_coarse)
         levels.append(lv)
-        A_e = dv.spgemm(lv.R_e, dv.spgemm(A_e, P_e))
-        S_e = dv.spgemm(lv.R_e, dv.spgemm(S_e, P_e))
-        A_n = dv.spgemm(dv.transpose(P_n), dv.spgemm(A_n, P_n))
+        with phase("level.galerkin_A"):
+            A_e = dv.spgemm(lv.R_e, dv.spgemm(A_e, P_e))
+        with phase("level.galerkin_S"):
+            S_e = dv.spgemm(lv.R_e, dv.spgemm(S_e, P_e))
+        with phase("level.galerkin_nodal"):
+            A_n = dv.spgemm(dv.transpose(P_n), dv.spgemm(A_n, P_n, ordered=True),
+                            ordered=True)
         D = cg.D_H
-        _check_nullspace(S_e, D, f"level {len(levels)}")
-    last = _make_level(A_e, S_e, D, cfg.cheb_degree)
-    levels.append(last)
-    inv = torch.linalg.inv(dv.to_dense(A_e))   # dense LU (cuSOLVER), once
+        with phase("level.nullspace_check"):
+            _check_nullspace(S_e, D, f"level {len(levels)}")
+    with phase("coarsest"):
+        last = _make_level(A_e, S_e, D, cfg.cheb_degree)
+        levels.append(last)
+        inv = torch.linalg.inv(dv.to_dense(A_e))   # dense LU (cuSOLVER), once
     last.r = dv.empty_f64(A_e.shape[0])
     nnz0 = levels[0].A_e.nnz
     oc = sum(lv.A_e.nnz for lv in levels) / nnz0
@@ -256,9 +267,15 @@ def v_cycle(h, x, b, level=0):
 
 
 def v_cycle_preconditioner(h):
-    """The V-cycle as a fixed symmetric operator b -> V(b) (multigrid.py:191-195)."""
+    """The V-cycle as a fixed symmetric operator b -> V(b) (multigrid.py:191-195).
+
+    It launches only fixed-address kernels with no host synchronisation, so
+    pcg_solve may capture it in a CUDA graph (``graph_safe``)."""
     def apply(b):
-        return v_cycle(h, None, b)
+        with phase("solve.vcycle"):
+            return v_cycle(h, None, b)
+    apply.graph_safe = not _trace.ENABLED     # tracing inserts host syncs
+    apply.hierarchy = h
     return apply
 
 
@@ -272,49 +289,105 @@ class PcgResult:
     relative_residual: float
 
 
+def _csr_key(A):
+    return (A.rowptr.data_ptr(), A.col.data_ptr(), A.val.data_ptr(), A.shape)
+
+
+def _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc, flag, stage):
+    """One PCG iteration with device-resident scalars (sc slots as in
+    include/sphcurl.h SPHC_PCG_*); ends with the scalars copied to ``stage``."""
+    n = x.numel()
+    dv.spmv(A, p, Ap, lanes=lanes)
+    dv.dot(p, Ap, sc[0:1])
+    call("sphc_pcg_update", n, sc, p, Ap, x, r, flag)
+    dv.dot(r, r, sc[1:2])
+    z = precond(r)
+    dv.dot(r, z, sc[3:4])
+    call("sphc_pcg_direction", n, sc, z, p)
+    stage.copy_(sc, non_blocking=True)
+    call("sphc_pcg_rotate", sc)
+    return z
+
+
 def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
     """Preconditioned CG from x = 0 (multigrid.py:220-274): same statuses
-    (converged | maxit | stagnated | indefinite) and histories."""
+    (converged | maxit | stagnated | indefinite) and histories.
+
+    The scalars alpha, beta live on the device; with a graph-safe
+    preconditioner (ours) one whole iteration is captured once as a CUDA
+    graph and replayed, with one 48-byte readback per iteration for the
+    convergence / breakdown tests."""
     A = as_device_csr(A)
     host = not isinstance(b, torch.Tensor)
     b = torch.as_tensor(np.asarray(b, dtype=np.float64) if host else b,
                         dtype=torch.float64, device=dv.device())
     n = b.numel()
-    sc = torch.zeros(4, dtype=torch.float64, device=b.device)
-    flag = sc.view(torch.int32)[6:7]          # overlaps sc[3]
-    dv.dot(b, b, sc[0:1])
-    nb = math.sqrt(float(sc[0].item()))
-    x = dv.zeros_f64(n)
+    lanes = A.lanes()
+    graph_ok = getattr(precond, "graph_safe", False) and maxit > 0
+    hier = getattr(precond, "hierarchy", None)
+    ws = getattr(hier, "_pcg_ws", None) if graph_ok else None
+    if ws is not None and (ws["A"] is not A and ws["A_key"] != _csr_key(A) or ws["n"] != n):
+        ws = None
+    if ws is None:
+        sc = torch.zeros(6, dtype=torch.float64, device=b.device)
+        ws = dict(A=A, A_key=_csr_key(A), n=n, x=dv.empty_f64(n), r=dv.empty_f64(n),
+                  p=dv.empty_f64(n), Ap=dv.empty_f64(n), sc=sc,
+                  flag=sc.view(torch.int32)[8:9],           # overlaps sc[4]
+                  stage=torch.zeros(6, dtype=torch.float64, pin_memory=True), graph=None)
+    x, r, p, Ap, sc, flag, stage = (ws[k] for k in ("x", "r", "p", "Ap", "sc", "flag", "stage"))
+    x.zero_()
+    r.copy_(b)
+    dv.dot(b, b, sc[1:2])
+    nb = math.sqrt(float(sc[1].item()))
 
     def out(v):
-        return v.cpu().numpy() if host else v
+        return v.cpu().numpy() if host else v.clone()
 
     if nb == 0.0:
         return PcgResult(out(x), 0, [0.0], [0.0], "converged", 0.0)
-    r = b.clone()
-    Ap = dv.empty_f64(n)
     z = precond(r)
-    p = z.clone()
-    dv.dot(r, z, sc[0:1])
-    rz = float(sc[0].item())
+    p.copy_(z)
+    dv.dot(r, z, sc[2:3])
+    rz0 = float(sc[2].item())
     history = [nb]
-    precond_history = [math.sqrt(max(rz, 0.0))]
+    precond_history = [math.sqrt(max(rz0, 0.0))]
     status, iters = "maxit", 0
-    lanes = A.lanes()
+    graph = ws["graph"]
+    if graph_ok and graph is None:
+        # warm the iteration once outside capture on scratch copies so every
+        # lazily allocated buffer exists, then capture on the real ones; the
+        # graph is kept on the hierarchy for later solves with the same A
+        xs, rs, ps, scs = x.clone(), r.clone(), p.clone(), sc.clone()
+        _pcg_iteration(A, lanes, precond, xs, rs, ps, Ap, scs,
+                       scs.view(torch.int32)[8:9], torch.zeros_like(stage))
+        # capture on a side stream without torch.cuda.graph's gc.collect() +
+        # empty_cache(), which would force every later allocation back to
+        # cudaMalloc
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cap):
+            graph.capture_begin()
+            _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc, flag, stage)
+            graph.capture_end()
+        torch.cuda.current_stream().wait_stream(cap)
+        ws["graph"] = graph
+        if hier is not None:
+            hier._pcg_ws = ws
     for k in range(maxit):
-        dv.spmv(A, p, Ap, lanes=lanes)
-        dv.dot(p, Ap, sc[0:1])
-        pAp = float(sc[0].item())
+        sc[4] = 0.0
+        if graph is not None:
+            graph.replay()
+        else:
+            _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc, flag, stage)
+        torch.cuda.current_stream().synchronize()
+        hv = stage.numpy()
+        pAp = float(hv[0])
         if pAp <= 0.0:
             status = "indefinite"
             break
-        alpha = rz / pAp
-        sc[3] = 0.0
-        call("sphc_pcg_update", n, alpha, p, Ap, x, r, flag)
-        dv.dot(r, r, sc[1:2])
-        hv = sc.cpu().numpy()
         iters = k + 1
-        if hv.view(np.int32)[6] == 0:
+        if hv.view(np.int32)[8] == 0:
             status = "stagnated"
             dv.spmv(A, x, Ap, alpha=-1.0, beta=1.0, z=b)
             dv.dot(Ap, Ap, sc[0:1])
@@ -323,16 +396,10 @@ def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
             break
         res = math.sqrt(float(hv[1]))
         history.append(res)
-        z = precond(r)
-        dv.dot(r, z, sc[2:3])
-        rz_new = float(sc[2].item())
-        precond_history.append(math.sqrt(max(rz_new, 0.0)))
+        precond_history.append(math.sqrt(max(float(hv[3]), 0.0)))
         if res <= rtol * nb:
             status = "converged"
             break
-        beta = rz_new / rz
-        rz = rz_new
-        call("sphc_pcg_direction", n, beta, z, p)
     return PcgResult(x=out(x), iterations=iters, residual_history=history,
                      precond_history=precond_history, status=status,
                      relative_residual=history[-1] / nb)

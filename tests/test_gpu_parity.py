@@ -90,7 +90,7 @@ def test_spgemm_matches_scipy_bitwise():
                                                (50, 3000, 40, 0.1, 0.05)]):
         A = _rand_csr(n, k, d1, 10 + seed)
         B = _rand_csr(k, m, d2, 20 + seed)
-        C = dv.spgemm(dv.DeviceCSR.from_scipy(A), dv.DeviceCSR.from_scipy(B)).to_scipy()
+        C = dv.spgemm(dv.DeviceCSR.from_scipy(A), dv.DeviceCSR.from_scipy(B), ordered=True).to_scipy()
         ref = A @ B
         ref.sort_indices()
         assert np.array_equal(C.indptr, ref.indptr)

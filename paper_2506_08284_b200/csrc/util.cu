@@ -192,53 +192,81 @@ extern "C" int sphc_maxabs(int64_t n, const double* x, double* out, void* stream
 // elements i = 16 q + l; chains combine as (l, l+2) within each 4-lane ymm,
 // then ymm0+ymm1, ymm2+ymm3, their sum, and a horizontal add; the n % 16 tail
 // is added unfused in index order.
-__global__ void k_hsw_dot(i64 n, const double* __restrict__ x, const double* __restrict__ y,
-                          double* out) {
-  int lane = threadIdx.x;
+#define HSW_TILE 4096     // elements per shared-memory tile (x and y)
+#define HSW_THREADS 1024
+
+// One CTA. Warps 1..31 stream the next tile of x and y into shared memory
+// (double buffered) while lanes 0..15 of warp 0 run the sixteen sequential
+// FMA chains over the current tile, so the chains, not HBM latency, set the
+// pace.
+__global__ void __launch_bounds__(HSW_THREADS)
+    k_hsw_dot(i64 n, const double* __restrict__ x, const double* __restrict__ y, double* out) {
+  extern __shared__ double hsm[];  // [2][2][HSW_TILE]
+  int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   i64 n1 = n & ~(i64)15;
+  i64 ntiles = (n1 + HSW_TILE - 1) / HSW_TILE;
   double acc = 0.0;
-  if (lane < 16) {
-    // the chain is sequential; loads are batched 16 deep so the FMA chain,
-    // not memory latency, sets the pace
-    const int B = 16;
-    i64 i = lane;
-    for (; i + 16 * (B - 1) < n1; i += 16 * B) {
-      double xa[B], ya[B];
-#pragma unroll
-      for (int u = 0; u < B; u++) {
-        xa[u] = x[i + 16 * u];
-        ya[u] = y[i + 16 * u];
+  auto load = [&](i64 t, int buf, int t0, int nt) {
+    double* bx = hsm + (size_t)buf * 2 * HSW_TILE;
+    double* by = bx + HSW_TILE;
+    i64 base = t * HSW_TILE;
+    for (int k = t0; k < HSW_TILE; k += nt) {
+      i64 i = base + k;
+      if (i < n1) {
+        bx[k] = x[i];
+        by[k] = y[i];
       }
-#pragma unroll
-      for (int u = 0; u < B; u++) acc = __fma_rn(xa[u], ya[u], acc);
     }
-    for (; i < n1; i += 16) acc = __fma_rn(x[i], y[i], acc);
+  };
+  if (ntiles) load(0, 0, tid, HSW_THREADS);
+  __syncthreads();
+  for (i64 t = 0; t < ntiles; t++) {
+    if (warp != 0) {
+      if (t + 1 < ntiles) load(t + 1, (int)((t + 1) & 1), tid - 32, HSW_THREADS - 32);
+    } else if (lane < 16) {
+      const double* bx = hsm + (size_t)(t & 1) * 2 * HSW_TILE;
+      const double* by = bx + HSW_TILE;
+      i64 cnt = n1 - t * HSW_TILE;
+      int m = cnt < HSW_TILE ? (int)cnt : HSW_TILE;
+#pragma unroll 8
+      for (int k = lane; k < m; k += 16) acc = __fma_rn(bx[k], by[k], acc);
+    }
+    __syncthreads();
   }
-  double a[16];
+  if (warp == 0) {
+    double a[16];
 #pragma unroll
-  for (int l = 0; l < 16; l++) a[l] = __shfl_sync(FULL_MASK, acc, l);
-  if (lane == 0) {
-    double dot = 0.0;
-    if (n1) {
-      double h0[4], h1[4];
+    for (int l = 0; l < 16; l++) a[l] = __shfl_sync(FULL_MASK, acc, l);
+    if (lane == 0) {
+      double dot = 0.0;
+      if (n1) {
+        double h0[4], h1[4];
 #pragma unroll
-      for (int q = 0; q < 4; q++) {
-        h0[q] = __dadd_rn(a[4 * q + 0], a[4 * q + 2]);
-        h1[q] = __dadd_rn(a[4 * q + 1], a[4 * q + 3]);
+        for (int q = 0; q < 4; q++) {
+          h0[q] = __dadd_rn(a[4 * q + 0], a[4 * q + 2]);
+          h1[q] = __dadd_rn(a[4 * q + 1], a[4 * q + 3]);
+        }
+        double u0 = __dadd_rn(__dadd_rn(h0[0], h0[1]), __dadd_rn(h0[2], h0[3]));
+        double u1 = __dadd_rn(__dadd_rn(h1[0], h1[1]), __dadd_rn(h1[2], h1[3]));
+        dot = __dadd_rn(u0, u1);
       }
-      double u0 = __dadd_rn(__dadd_rn(h0[0], h0[1]), __dadd_rn(h0[2], h0[3]));
-      double u1 = __dadd_rn(__dadd_rn(h1[0], h1[1]), __dadd_rn(h1[2], h1[3]));
-      dot = __dadd_rn(u0, u1);
+      for (i64 i = n1; i < n; i++) dot = __dadd_rn(dot, __dmul_rn(y[i], x[i]));
+      *out = dot;
     }
-    for (i64 i = n1; i < n; i++) dot = __dadd_rn(dot, __dmul_rn(y[i], x[i]));
-    *out = dot;
   }
 }
 
 extern "C" int sphc_hsw_dot(int64_t n, const double* x, const double* y, double* out,
                             void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_hsw_dot<<<1, 32, 0, s>>>(n, x, y, out);
+  size_t sm = 4 * HSW_TILE * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    SPHC_CUDA(cudaFuncSetAttribute(k_hsw_dot, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sm));
+    attr = true;
+  }
+  k_hsw_dot<<<1, HSW_THREADS, sm, s>>>(n, x, y, out);
   SPHC_LAUNCH_CHECK();
   return 0;
 }

@@ -98,6 +98,25 @@ def test_spgemm_matches_scipy_bitwise():
         assert np.array_equal(C.data.view(np.uint64), ref.data.view(np.uint64))
 
 
+def test_spgemm_unordered_tol_and_deterministic():
+    """All-lanes variant: same pattern, values within 1e-13, bitwise rerun."""
+    dv = _dev()
+    for seed, (n, k, m, d1, d2) in enumerate([(500, 400, 300, 0.02, 0.03),
+                                               (300, 20000, 200, 0.05, 0.02),
+                                               (3000, 3000, 3000, 0.003, 0.004)]):
+        A = _rand_csr(n, k, d1, 30 + seed)
+        B = _rand_csr(k, m, d2, 40 + seed)
+        Ad, Bd = dv.DeviceCSR.from_scipy(A), dv.DeviceCSR.from_scipy(B)
+        C1 = dv.spgemm(Ad, Bd).to_scipy()
+        C2 = dv.spgemm(Ad, Bd).to_scipy()
+        ref = A @ B
+        ref.sort_indices()
+        assert np.array_equal(C1.indptr, ref.indptr)
+        assert np.array_equal(C1.indices, ref.indices)
+        assert rel_max_diff(C1, ref) <= 1e-13
+        assert np.array_equal(C1.data.view(np.uint64), C2.data.view(np.uint64))
+
+
 def test_transpose():
     dv = _dev()
     A = _rand_csr(4000, 700, 0.01, 5)

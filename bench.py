@@ -119,6 +119,24 @@ def cheb_kernel_bytes(A):
     return 12 * A.nnz + 8 * (n + 1) + 8 * 6 * n
 
 
+def ncu_traffic(pattern="k_cheb16_full"):
+    """DRAM bytes (read + write) per launch of the roofline kernel from the
+    newest committed ncu --set full summary in profiles/, or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(REPO, "profiles", f"*{pattern}*.txt")))
+    if not files:
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    found = 0
+    for line in open(files[-1]):
+        f = line.split()
+        if len(f) == 3 and f[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(f[1]) * scale.get(f[2], 1)
+            found += 1
+    return tot if found == 2 else None
+
+
 def make_problem(config, N=None):
     from paper_2506_08284_b200.inputs import make_config
     sysm, rhs, cfg = make_config(config, N)
@@ -284,7 +302,8 @@ def run_ours(args):
                        "frac_of_peak": vbytes / (t_vc * 1e-3) / 1e9 / peak},
             "roofline": {"bound": "hbm", "kernel": "k_cheb<lanes> (fused Chebyshev step, level-0 A_e)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak,
+                         "traffic": ncu_traffic() if args.config == "C2" else None,
                          "peak_source": pk_kind, "launch_ms": t_k,
                          "algorithmic_bytes": kbytes},
             "e2e": {"value": ws * n_e / (t_e2e * 1e-3), "unit": "edge DOFs/s",

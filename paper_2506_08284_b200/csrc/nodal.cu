@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(SM_WARPS * 32)
     for (int size = 2; size <= m; size <<= 1)
       for (int stride = size >> 1; stride > 0; stride >>= 1) {
         for (int t = lane; t < (m >> 1); t += 32) {
-          int lo = 2 * stride * (t / stride) + (t % stride), hi = lo + stride;
+          int lo = ((t & ~(stride - 1)) << 1) | (t & (stride - 1)), hi = lo + stride;
           bool up = (lo & size) == 0;
           int a = uq[w][lo], b = uq[w][hi];
           if ((a > b) == up) { uq[w][lo] = b; uq[w][hi] = a; }

@@ -344,7 +344,7 @@ __device__ void bitonic(int* k, double* v, int n, int tid, int nthr) {
   for (int size = 2; size <= m; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int t = tid; t < (m >> 1); t += nthr) {
-        int lo = 2 * stride * (t / stride) + (t % stride);
+        int lo = ((t & ~(stride - 1)) << 1) | (t & (stride - 1));
         int hi = lo + stride;
         bool up = (lo & size) == 0;
         int a = k[lo], b = k[hi];

@@ -155,6 +155,23 @@ int sphc_spmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *v, 
               const double *x, double alpha, double beta, const double *z, double *y,
               void *stream);
 
+/* SELL-32 mirror of a CSR operator (slices of 32 rows, column-major, padded
+ * with value 0 / own column). sphc_sell_sizes writes the entry count of every
+ * slice (ceil(n/32) values); after sphc_scan_i64 -> slice_ptr, sphc_sell_fill
+ * writes the slices. */
+int sphc_sell_sizes(int64_t n, const int64_t *rp, int64_t *slice_entries, void *stream);
+int sphc_sell_fill(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                   const int64_t *slice_ptr, int32_t *sci, double *sv, void *stream);
+/* y = alpha A x + beta z on the SELL mirror, one thread per row. */
+int sphc_sell_spmv(int64_t n, const int64_t *slice_ptr, const int32_t *sci, const double *sv,
+                   const double *x, double alpha, double beta, const double *z, double *y,
+                   void *stream);
+/* Fused Chebyshev step on the SELL mirror (same math as sphc_cheb_step). */
+int sphc_sell_cheb_step(int64_t n, const int64_t *slice_ptr, const int32_t *sci,
+                        const double *sv, const double *dinv, const double *b,
+                        const double *x_in, double *x_out, double *d, double cd, double cr,
+                        int x_zero, void *stream);
+
 /* One Chebyshev step, fused: d <- cd*d + cr*dinv*(b - A x_in); x_out = x_in + d.
  * x_zero != 0 means x_in == 0 (A x skipped). Replaces the reference's
  * Gauss-Seidel half sweeps (multigrid.py:45-59) in the smoother seam. */

@@ -1,0 +1,147 @@
+// SELL-32 mirror of the square smoother operators (A_e, D^T A_e D on every
+// level): slices of 32 consecutive rows stored column-major and padded to the
+// slice's longest row, so one warp = one slice and one thread = one row. Every
+// load of the j-loop is a coalesced 256 B (values) / 128 B (columns) line and
+// a thread's loads are independent, which keeps many requests in flight per
+// SM -- the HBM-bound V-cycle kernels run on this layout.
+// Padding entries carry value 0 and the row's own column.
+#include "common.cuh"
+
+#define SELL_C 32
+
+__global__ void k_sell_widths(i64 n, const i64* __restrict__ rp, i64* __restrict__ width) {
+  i64 ns = (n + SELL_C - 1) / SELL_C;
+  int lane = threadIdx.x & 31;
+  i64 w0 = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 s = w0; s < ns; s += nw) {
+    i64 row = s * SELL_C + lane;
+    int len = row < n ? (int)(rp[row + 1] - rp[row]) : 0;
+    for (int o = 16; o > 0; o >>= 1) len = max(len, __shfl_xor_sync(FULL_MASK, len, o));
+    if (lane == 0) width[s] = (i64)len * SELL_C;   // entries of the slice
+  }
+}
+
+extern "C" int sphc_sell_sizes(int64_t n, const int64_t* rp, int64_t* slice_entries,
+                               void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_sell_widths<<<grid_for(n, 256), 256, 0, s>>>(n, rp, slice_entries);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+__global__ void k_sell_fill(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ v, const i64* __restrict__ sp,
+                            int* __restrict__ sci, double* __restrict__ sv) {
+  for (i64 row = (i64)blockIdx.x * blockDim.x + threadIdx.x; row < ((n + 31) & ~(i64)31);
+       row += (i64)gridDim.x * blockDim.x) {
+    i64 s = row / SELL_C;
+    int r = (int)(row % SELL_C);
+    int w = (int)((sp[s + 1] - sp[s]) / SELL_C);
+    i64 base = sp[s] + r;
+    int len = 0;
+    i64 j0 = 0;
+    if (row < n) {
+      j0 = rp[row];
+      len = (int)(rp[row + 1] - j0);
+    }
+    int self = row < n ? (int)row : 0;
+    for (int j = 0; j < w; j++) {
+      bool real = j < len;
+      sci[base + (i64)j * SELL_C] = real ? ci[j0 + j] : self;
+      sv[base + (i64)j * SELL_C] = real ? v[j0 + j] : 0.0;
+    }
+  }
+}
+
+extern "C" int sphc_sell_fill(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
+                              const int64_t* slice_ptr, int32_t* sci, double* sv,
+                              void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_sell_fill<<<grid_for(n, 256), 256, 0, s>>>(n, rp, ci, v, slice_ptr, sci, sv);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+__device__ __forceinline__ double sell_row(i64 base, int w, const int* __restrict__ sci,
+                                           const double* __restrict__ sv,
+                                           const double* __restrict__ x) {
+  double acc = 0.0;
+  int j = 0;
+#pragma unroll 4
+  for (; j < w; j++) {
+    i64 o = base + (i64)j * SELL_C;
+    acc = fma(__ldcs(sv + o), __ldg(x + __ldcs(sci + o)), acc);
+  }
+  return acc;
+}
+
+// y = alpha A x + beta z
+__global__ void __launch_bounds__(256)
+    k_sell_spmv(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
+                const double* __restrict__ sv, const double* __restrict__ x, double alpha,
+                double beta, const double* z, double* y) {
+  i64 row = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  i64 s = row / SELL_C;
+  i64 ns = (n + SELL_C - 1) / SELL_C;
+  if (s >= ns) return;
+  i64 b0 = sp[s];
+  int w = (int)((sp[s + 1] - b0) / SELL_C);
+  double acc = sell_row(b0 + (row % SELL_C), w, sci, sv, x);
+  if (row < n) {
+    double r = alpha * acc;
+    if (z) r = fma(beta, z[row], r);
+    y[row] = r;
+  }
+}
+
+// d <- cd d + cr dinv (b - A x_in); x_out = x_in + d
+__global__ void __launch_bounds__(256)
+    k_sell_cheb(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
+                const double* __restrict__ sv, const double* __restrict__ dinv,
+                const double* __restrict__ b, const double* __restrict__ x_in,
+                double* __restrict__ x_out, double* __restrict__ d, double cd, double cr,
+                int x_zero) {
+  i64 row = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  i64 s = row / SELL_C;
+  i64 ns = (n + SELL_C - 1) / SELL_C;
+  if (s >= ns) return;
+  double ax = 0.0;
+  if (!x_zero) {
+    i64 b0 = sp[s];
+    int w = (int)((sp[s + 1] - b0) / SELL_C);
+    ax = sell_row(b0 + (row % SELL_C), w, sci, sv, x_in);
+  }
+  if (row < n) {
+    double r = b[row] - ax;
+    double dn = cr * dinv[row] * r;
+    if (cd != 0.0) dn = fma(cd, d[row], dn);
+    d[row] = dn;
+    x_out[row] = (x_zero ? 0.0 : x_in[row]) + dn;
+  }
+}
+
+extern "C" int sphc_sell_spmv(int64_t n, const int64_t* slice_ptr, const int32_t* sci,
+                              const double* sv, const double* x, double alpha, double beta,
+                              const double* z, double* y, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  i64 rows = (n + 31) & ~(i64)31;
+  k_sell_spmv<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(n, slice_ptr, sci, sv, x, alpha,
+                                                             beta, z, y);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int sphc_sell_cheb_step(int64_t n, const int64_t* slice_ptr, const int32_t* sci,
+                                   const double* sv, const double* dinv, const double* b,
+                                   const double* x_in, double* x_out, double* d, double cd,
+                                   double cr, int x_zero, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  i64 rows = (n + 31) & ~(i64)31;
+  k_sell_cheb<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(n, slice_ptr, sci, sv, dinv, b,
+                                                             x_in, x_out, d, cd, cr, x_zero);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}

@@ -193,8 +193,44 @@ def spgemm(A, B, drop=True, ordered=False):
     return drop_zeros(C) if drop else C
 
 
+@dataclass
+class SellMirror:
+    """SELL-32 copy of a square operator for the solve (csrc/sell.cu)."""
+
+    slice_ptr: torch.Tensor   # int64 [n_slices + 1]
+    col: torch.Tensor         # int32 [padded entries]
+    val: torch.Tensor         # float64 [padded entries]
+    n: int
+
+    @property
+    def padded(self):
+        return int(self.col.numel())
+
+
+def sell(A):
+    """SELL-32 mirror of A (built once, cached on the DeviceCSR)."""
+    m = getattr(A, "_sell", None)
+    if m is not None:
+        return m
+    n = A.shape[0]
+    ns = (n + 31) // 32
+    sz = torch.empty(ns, dtype=torch.int64, device=A.rowptr.device)
+    call("sphc_sell_sizes", n, A.rowptr, sz)
+    sp_, tot = scan(sz)
+    ci = torch.empty(tot, dtype=torch.int32, device=A.rowptr.device)
+    v = empty_f64(tot)
+    call("sphc_sell_fill", n, A.rowptr, A.col, A.val, sp_, ci, v)
+    m = SellMirror(sp_, ci, v, n)
+    A._sell = m
+    return m
+
+
 def spmv(A, x, y, alpha=1.0, beta=0.0, z=None, lanes=None):
-    """y = alpha A x + beta z."""
+    """y = alpha A x + beta z (on A's SELL mirror when it has one)."""
+    m = getattr(A, "_sell", None)
+    if m is not None:
+        call("sphc_sell_spmv", m.n, m.slice_ptr, m.col, m.val, x, alpha, beta, z, y)
+        return y
     call("sphc_spmv", A.shape[0], A.rowptr, A.col, A.val, lanes or A.lanes(), x, alpha,
          beta, z, y)
     return y

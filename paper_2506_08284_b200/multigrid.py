@@ -15,6 +15,7 @@ polynomial in the reference's own sweeper seam for parity.
 """
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -27,6 +28,7 @@ from . import trace as _trace
 from .trace import phase
 
 _NULLSPACE_TOL = 1e-10
+USE_SELL = os.environ.get("SPHC_SELL", "1") != "0"
 CHEB_POWER_ITERS = 15
 CHEB_SAFETY = 1.1
 CHEB_RATIO = 30.0
@@ -63,6 +65,8 @@ class ChebyshevSweeper:
         self.dinv = dv.reciprocal(d)
         self.degree = degree
         self.lanes = A.lanes()
+        # solve-phase layout of A (csrc/sell.cu) unless SPHC_SELL=0
+        self.sell = dv.sell(A) if USE_SELL else None
         self.d = dv.empty_f64(n)
         self.buf = [dv.empty_f64(n), dv.empty_f64(n)]
         self.hi, self.lo = self._bounds()
@@ -113,8 +117,13 @@ class ChebyshevSweeper:
             for step, (cd, cr) in enumerate(self.coefs):
                 out = self.buf[0] if cur is not self.buf[0] else self.buf[1]
                 z = x_zero and step == 0
-                call("sphc_cheb_step", n, A.rowptr, A.col, A.val, self.lanes, self.dinv, b,
-                     None if z else cur, out, self.d, cd, cr, int(z))
+                m = self.sell
+                if m is not None:
+                    call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, self.dinv, b,
+                         None if z else cur, out, self.d, cd, cr, int(z))
+                else:
+                    call("sphc_cheb_step", n, A.rowptr, A.col, A.val, self.lanes, self.dinv,
+                         b, None if z else cur, out, self.d, cd, cr, int(z))
                 cur = out
             x_zero = False
         return cur

@@ -82,6 +82,34 @@ def test_spmv(lanes):
     assert np.max(np.abs(y.cpu().numpy() - ref)) <= 1e-12 * np.max(np.abs(ref))
 
 
+def test_sell_spmv_and_cheb_match_csr():
+    """SELL-32 mirror: same y as scipy; fused Chebyshev step same as CSR's."""
+    dv = _dev()
+    from paper_2506_08284_b200.device import call
+    rng = np.random.default_rng(7)
+    for n in (1, 31, 33, 1000, 4097):
+        A = _rand_csr(n, n, min(1.0, 12.0 / n), 50 + n) + sp.eye(n)
+        A = sp.csr_matrix(A)
+        A.sort_indices()
+        Ad = dv.DeviceCSR.from_scipy(A)
+        x, z, dinv, b = (rng.standard_normal(n) for _ in range(4))
+        X, Z, DI, B = (torch.from_numpy(v).cuda() for v in (x, z, dinv, b))
+        m = dv.sell(Ad)
+        assert m.padded >= A.nnz
+        y = torch.empty(n, dtype=torch.float64, device="cuda")
+        dv.spmv(Ad, X, y, alpha=-1.0, beta=0.5, z=Z)
+        ref = -(A @ x) + 0.5 * z
+        assert np.max(np.abs(y.cpu().numpy() - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+        d1 = torch.from_numpy(rng.standard_normal(n)).cuda()
+        d2 = d1.clone()
+        o1 = torch.empty_like(X)
+        o2 = torch.empty_like(X)
+        call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, DI, B, X, o1, d1, 0.3, 0.7, 0)
+        call("sphc_cheb_step", n, Ad.rowptr, Ad.col, Ad.val, 8, DI, B, X, o2, d2, 0.3, 0.7, 0)
+        assert torch.allclose(o1, o2, rtol=1e-13, atol=1e-13)
+        assert torch.allclose(d1, d2, rtol=1e-13, atol=1e-13)
+
+
 def test_spgemm_matches_scipy_bitwise():
     """Sequential ascending-k sums: identical bits to scipy's csr_matmat."""
     dv = _dev()

@@ -146,6 +146,15 @@ int sphc_spgemm_fill(int64_t n, const int64_t *arp, const int32_t *aci, const do
                      const int64_t *crp, int32_t *cci, double *cv, int ordered,
                      int64_t *status, void *stream);
 
+/* Two products on one pattern in one pass: C1 = A1 B1, C2 = A2 B2 where A1/A2
+ * share arp/aci and B1/B2 share brp/bci (the A_e and S_e Galerkin products
+ * P^T (A_e P) and P^T (S_e P), multigrid.py:150-151). Unordered (TOL). */
+int sphc_spgemm_fill_pair(int64_t n, const int64_t *arp, const int32_t *aci, const double *av1,
+                          const double *av2, const int64_t *brp, const int32_t *bci,
+                          const double *bv1, const double *bv2, const int64_t *crp,
+                          int32_t *cci, double *cv1, double *cv2, int64_t *status,
+                          void *stream);
+
 /* ---------------------------------------------------------------- solve */
 
 /* y = alpha * (A x) + beta * z  (z may be NULL; y may alias z).

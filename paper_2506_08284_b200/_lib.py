@@ -92,20 +92,34 @@ def _ptr(a):
     return int(a)
 
 
+_DEV = None
+
+
 def stream_handle():
-    return torch.cuda.current_stream().cuda_stream
+    """torch's current raw CUDA stream (follows torch.cuda.stream contexts and
+    graph capture) without torch.cuda.current_stream()'s per-call overhead."""
+    global _DEV
+    if _DEV is None:
+        _DEV = torch.cuda.current_device()
+    return torch._C._cuda_getCurrentRawStream(_DEV)
+
+
+_FN = {}
 
 
 def call(name, *args):
     """Invoke an entry point; device ones run on torch's current stream."""
-    L = lib()
-    ret, codes, stream = SIGS[name]
+    ent = _FN.get(name)
+    if ent is None:
+        ret, codes, stream = SIGS[name]
+        ent = _FN[name] = (getattr(lib(), name), codes, stream)
+    f, codes, stream = ent
     if len(args) != len(codes):
         raise TypeError(f"{name} takes {len(codes)} arguments, got {len(args)}")
     conv = [(_ptr(a) if c == "p" else a) for c, a in zip(codes, args)]
     if stream:
         conv.append(stream_handle())
-    rc = getattr(L, name)(*conv)
+    rc = f(*conv)
     if rc != 0 and not (name == "sphc_host_piecewise_const" and rc == -3):
-        raise RuntimeError(f"{name} failed ({rc}): {L.sphc_last_error().decode()}")
+        raise RuntimeError(f"{name} failed ({rc}): {lib().sphc_last_error().decode()}")
     return rc

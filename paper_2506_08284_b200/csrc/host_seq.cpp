@@ -68,14 +68,13 @@ extern "C" int sphc_host_piecewise_const(int64_t m_h, int64_t m_H, const int64_t
   for (i64 j = 0; j < rp[m_h]; j++) cp[ci[j] + 1]++;
   for (i64 c = 0; c < m_H; c++) cp[c + 1] += cp[c];
   std::vector<i64> cur(cp.begin(), cp.end() - 1);
-  std::vector<i64> crow(rp[m_h]);
-  std::vector<double> cmag(rp[m_h]);
+  struct Ent {
+    double mag;
+    i64 row;
+  };
+  std::vector<Ent> col(rp[m_h]);
   for (i64 r = 0; r < m_h; r++)
-    for (i64 j = rp[r]; j < rp[r + 1]; j++) {
-      i64 pos = cur[ci[j]]++;
-      crow[pos] = r;
-      cmag[pos] = fabs(v[j]);
-    }
+    for (i64 j = rp[r]; j < rp[r + 1]; j++) col[cur[ci[j]]++] = Ent{fabs(v[j]), r};
   i64 total = 0;
   for (i64 c = 0; c < m_H; c++) {
     i64 nz = cp[c + 1] - cp[c];
@@ -93,19 +92,23 @@ extern "C" int sphc_host_piecewise_const(int64_t m_h, int64_t m_H, const int64_t
     target[c] = ti < 1 ? 1 : ti;
   }
   for (i64 r = 0; r < m_h; r++) assign[r] = -1;
-  std::vector<i64> cand;
+  std::vector<Ent> cand;
   for (int pass = 0; pass < n_passes; pass++) {
     for (i64 c = 0; c < m_H; c++) {
       cand.clear();
       for (i64 j = cp[c]; j < cp[c + 1]; j++)
-        if (assign[crow[j]] < 0) cand.push_back(j);
+        if (assign[col[j].row] < 0) cand.push_back(col[j]);
       if (cand.empty()) continue;
       i64 take = (target[c] + n_passes - 1) / n_passes;
-      std::sort(cand.begin(), cand.end(), [&](i64 a, i64 b) {
-        if (cmag[a] != cmag[b]) return cmag[a] > cmag[b];
-        return crow[a] < crow[b];
-      });
-      for (i64 t = 0; t < take && t < (i64)cand.size(); t++) assign[crow[cand[t]]] = c;
+      if (take > (i64)cand.size()) take = (i64)cand.size();
+      // (|P| desc, row asc) is a total order, so the first `take` of a
+      // partial sort are exactly the reference's lexsort prefix
+      std::partial_sort(cand.begin(), cand.begin() + take, cand.end(),
+                        [](const Ent& a, const Ent& b) {
+                          if (a.mag != b.mag) return a.mag > b.mag;
+                          return a.row < b.row;
+                        });
+      for (i64 t = 0; t < take; t++) assign[cand[t].row] = c;
     }
   }
   std::vector<i64> counts(m_H, 0);
@@ -142,11 +145,11 @@ extern "C" int sphc_host_piecewise_const(int64_t m_h, int64_t m_H, const int64_t
     i64 best = -1;
     double bm = 0.0;
     for (i64 j = cp[c]; j < cp[c + 1]; j++) {
-      i64 r = crow[j];
+      i64 r = col[j].row;
       if (counts[assign[r]] <= 1) continue;
-      if (best < 0 || cmag[j] > bm || (cmag[j] == bm && r < best)) {
+      if (best < 0 || col[j].mag > bm || (col[j].mag == bm && r < best)) {
         best = r;
-        bm = cmag[j];
+        bm = col[j].mag;
       }
     }
     if (best < 0) {

@@ -184,16 +184,31 @@ struct SpgFill {
   int ucount;
 };
 
-template <bool ORDERED>
+struct SpgFillPair {         // two products on one pattern
+  SpgFill f;
+  double a2[32];             // second A's values of the batch
+  double sval2[SPG_STG];
+  double acc2[2][SPG_CCAP];  // second product's accumulators (one per group)
+};
+
+// ORDERED / unordered as described at the top. PAIR: C1 = A1 B1 and C2 = A2 B2
+// with A1, A2 (and B1, B2) sharing one pattern -- the A_e and S_e Galerkin
+// products of a level -- computed in one pass (one symbolic phase, indices
+// read once); single lane group, accumulators acc[0] / acc[1].
+template <bool ORDERED, bool PAIR>
 __global__ void __launch_bounds__(SPG_FWARPS * 32)
     k_spgemm_fill(i64 n, const i64* __restrict__ arp, const int* __restrict__ aci,
-                  const double* __restrict__ av, const i64* __restrict__ brp,
-                  const int* __restrict__ bci, const double* __restrict__ bv,
+                  const double* __restrict__ av, const double* __restrict__ av2,
+                  const i64* __restrict__ brp, const int* __restrict__ bci,
+                  const double* __restrict__ bv, const double* __restrict__ bv2,
                   const i64* __restrict__ crp, int* __restrict__ cci, double* __restrict__ cv,
-                  i64* status) {
+                  double* __restrict__ cv2, i64* status) {
   extern __shared__ unsigned char spg_smem[];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  SpgFill& F = ((SpgFill*)spg_smem)[w];
+  SpgFill& F = PAIR ? ((SpgFillPair*)spg_smem)[w].f : ((SpgFill*)spg_smem)[w];
+  double* a2 = PAIR ? ((SpgFillPair*)spg_smem)[w].a2 : nullptr;
+  double* sval2 = PAIR ? ((SpgFillPair*)spg_smem)[w].sval2 : nullptr;
+  double* acc2 = PAIR ? &((SpgFillPair*)spg_smem)[w].acc2[0][0] : nullptr;
   for (i64 row = (i64)blockIdx.x * SPG_FWARPS + w; row < n; row += (i64)gridDim.x * SPG_FWARPS) {
     int nu = (int)(crp[row + 1] - crp[row]);
     if (nu == 0) continue;
@@ -229,12 +244,17 @@ __global__ void __launch_bounds__(SPG_FWARPS * 32)
       F.slot[spg_find(F.keys, ts, F.list[t])] = (short)t;
       F.acc[0][t] = 0.0;
       F.acc[1][t] = 0.0;
+      if (PAIR) {
+        acc2[t] = 0.0;
+        acc2[SPG_CCAP + t] = 0.0;
+      }
     }
     __syncwarp();
     i64 as = arp[row], ae = arp[row + 1];
     const int G = ORDERED ? 1 : 2, LG = 32 / G;
     int g = lane / LG, l = lane % LG;
     double* my = F.acc[g];
+    double* my2 = PAIR ? acc2 + g * SPG_CCAP : nullptr;
     for (i64 c0 = as; c0 < ae;) {
       int total;
       int nb = spg_batch(F.B, c0, ae, aci, av, brp, lane, &total);
@@ -242,11 +262,16 @@ __global__ void __launch_bounds__(SPG_FWARPS * 32)
         if (lane == 0) report(status, SPHC_ST_SPGEMM_CAPACITY, row);
         break;
       }
+      if (PAIR) {
+        a2[lane] = (c0 + lane < ae) ? av2[c0 + lane] : 0.0;
+        __syncwarp();
+      }
       for (int f = lane; f < total; f += 32) {
         int t;
         i64 jb = spg_product(F.B, f, &t);
         F.sslot[f] = F.slot[spg_find(F.keys, ts, bci[jb])];
         F.sval[f] = __dmul_rn(F.B.a[t], bv[jb]);
+        if (PAIR) sval2[f] = a2[t] * bv2[jb];
       }
       __syncwarp();
       for (int t0 = 0; t0 < nb; t0 += G) {  // warp-uniform trip count
@@ -255,7 +280,9 @@ __global__ void __launch_bounds__(SPG_FWARPS * 32)
           int p1 = F.B.off[t];
           for (int p = F.B.start[t] + l; p < p1; p += LG) {
             int sl = F.sslot[p];
-            my[sl] = ORDERED ? __dadd_rn(my[sl], F.sval[p]) : my[sl] + F.sval[p];
+            if (ORDERED) my[sl] = __dadd_rn(my[sl], F.sval[p]);
+            else my[sl] += F.sval[p];
+            if (PAIR) my2[sl] += sval2[p];
           }
         }
         __syncwarp();
@@ -265,7 +292,12 @@ __global__ void __launch_bounds__(SPG_FWARPS * 32)
     i64 o = crp[row];
     for (int t = lane; t < nu; t += 32) {
       cci[o + t] = F.list[t];
-      cv[o + t] = ORDERED ? F.acc[0][t] : F.acc[0][t] + F.acc[1][t];
+      if (PAIR) {
+        cv[o + t] = F.acc[0][t] + F.acc[1][t];
+        cv2[o + t] = acc2[t] + acc2[SPG_CCAP + t];
+      } else {
+        cv[o + t] = ORDERED ? F.acc[0][t] : F.acc[0][t] + F.acc[1][t];
+      }
     }
     __syncwarp();
   }
@@ -282,28 +314,44 @@ extern "C" int sphc_spgemm_count(int64_t n, const int64_t* arp, const int32_t* a
   return 0;
 }
 
+template <bool ORDERED, bool PAIR>
+static int fill_launch(i64 n, const i64* arp, const int* aci, const double* av,
+                       const double* av2, const i64* brp, const int* bci, const double* bv,
+                       const double* bv2, const i64* crp, int* cci, double* cv, double* cv2,
+                       i64* status, cudaStream_t s) {
+  size_t sm = SPG_FWARPS * (PAIR ? sizeof(SpgFillPair) : sizeof(SpgFill));
+  static bool attr = false;
+  if (!attr) {
+    SPHC_CUDA(cudaFuncSetAttribute(k_spgemm_fill<ORDERED, PAIR>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr = true;
+  }
+  unsigned g = grid_for(n, SPG_FWARPS, SPHC_NUM_SMS * 32);
+  k_spgemm_fill<ORDERED, PAIR><<<g, SPG_FWARPS * 32, sm, s>>>(
+      n, arp, aci, av, av2, brp, bci, bv, bv2, crp, cci, cv, cv2, status);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
 extern "C" int sphc_spgemm_fill(int64_t n, const int64_t* arp, const int32_t* aci,
                                 const double* av, const int64_t* brp, const int32_t* bci,
                                 const double* bv, const int64_t* crp, int32_t* cci, double* cv,
                                 int ordered, int64_t* status, void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
-  size_t sm = SPG_FWARPS * sizeof(SpgFill);
-  static bool attr = false;
-  if (!attr) {
-    SPHC_CUDA(cudaFuncSetAttribute(k_spgemm_fill<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    SPHC_CUDA(cudaFuncSetAttribute(k_spgemm_fill<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr = true;
-  }
-  unsigned g = grid_for(n, SPG_FWARPS, SPHC_NUM_SMS * 32);
   if (ordered)
-    k_spgemm_fill<true><<<g, SPG_FWARPS * 32, sm, s>>>(n, arp, aci, av, brp, bci, bv, crp,
-                                                       cci, cv, status);
-  else
-    k_spgemm_fill<false><<<g, SPG_FWARPS * 32, sm, s>>>(n, arp, aci, av, brp, bci, bv, crp,
-                                                        cci, cv, status);
-  SPHC_LAUNCH_CHECK();
-  return 0;
+    return fill_launch<true, false>(n, arp, aci, av, nullptr, brp, bci, bv, nullptr, crp, cci,
+                                    cv, nullptr, status, s);
+  return fill_launch<false, false>(n, arp, aci, av, nullptr, brp, bci, bv, nullptr, crp, cci,
+                                   cv, nullptr, status, s);
+}
+
+extern "C" int sphc_spgemm_fill_pair(int64_t n, const int64_t* arp, const int32_t* aci,
+                                     const double* av1, const double* av2, const int64_t* brp,
+                                     const int32_t* bci, const double* bv1, const double* bv2,
+                                     const int64_t* crp, int32_t* cci, double* cv1,
+                                     double* cv2, int64_t* status, void* stream) {
+  if (n <= 0) return 0;
+  return fill_launch<false, true>(n, arp, aci, av1, av2, brp, bci, bv1, bv2, crp, cci, cv1,
+                                  cv2, status, as_stream(stream));
 }

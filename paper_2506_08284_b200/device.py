@@ -21,11 +21,17 @@ ST = dict(ZERO_DIAG=0, NONPOS_DIAG=1, NODAL_ZERO_DIAG=2, ZERO_ROWSUM=3,
           EMPTY_J=9, SPGEMM_CAPACITY=10, SORT_CAPACITY=11)
 
 
+_DEVICE = None
+
+
 def device():
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2506_08284_b200 needs a CUDA device (B200); "
-                           "there is no CPU path")
-    return torch.device("cuda", torch.cuda.current_device())
+    global _DEVICE
+    if _DEVICE is None:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2506_08284_b200 needs a CUDA device (B200); "
+                               "there is no CPU path")
+        _DEVICE = torch.device("cuda", torch.cuda.current_device())
+    return _DEVICE
 
 
 def call(name, *args):
@@ -191,6 +197,29 @@ def spgemm(A, B, drop=True, ordered=False):
          int(ordered), st.t)
     C = DeviceCSR(rp, ci, v, (A.shape[0], B.shape[1]))
     return drop_zeros(C) if drop else C
+
+
+def same_pattern(A, B):
+    return (A.shape == B.shape and A.nnz == B.nnz and torch.equal(A.rowptr, B.rowptr)
+            and torch.equal(A.col, B.col))
+
+
+def spgemm_pair(A1, A2, B1, B2, drop=True):
+    """(A1 B1, A2 B2) for A1/A2 and B1/B2 with shared patterns, one pass.
+    Stored exact zeros are dropped per product (drop=True)."""
+    n = A1.shape[0]
+    st = Status()
+    cnt = torch.empty(n, dtype=torch.int64, device=A1.rowptr.device)
+    call("sphc_spgemm_count", n, A1.rowptr, A1.col, B1.rowptr, B1.col, cnt, st.t)
+    rp, nnz = scan(cnt)
+    _raise_capacity(st)
+    ci = torch.empty(nnz, dtype=torch.int32, device=A1.rowptr.device)
+    v1, v2 = empty_f64(nnz), empty_f64(nnz)
+    call("sphc_spgemm_fill_pair", n, A1.rowptr, A1.col, A1.val, A2.val, B1.rowptr, B1.col,
+         B1.val, B2.val, rp, ci, v1, v2, st.t)
+    shape = (A1.shape[0], B1.shape[1])
+    C1, C2 = DeviceCSR(rp, ci, v1, shape), DeviceCSR(rp, ci, v2, shape)
+    return (drop_zeros(C1), drop_zeros(C2)) if drop else (C1, C2)
 
 
 @dataclass

@@ -173,9 +173,9 @@ class Hierarchy:
         return len(self.levels)
 
 
-def _make_level(A_e, S_e, D, degree=3, **extra):
+def _make_level(A_e, S_e, D, degree=3, AD=None, **extra):
     Dt = dv.transpose(D)
-    nodal_aux = dv.spgemm(Dt, dv.spgemm(A_e, D))
+    nodal_aux = dv.spgemm(Dt, AD if AD is not None else dv.spgemm(A_e, D))
     level = Level(A_e=A_e, S_e=S_e, D=D, nodal_aux=nodal_aux, Dt=Dt, **extra)
     level.edge_sweeper = ChebyshevSweeper(A_e, degree)
     level.aux_sweeper = ChebyshevSweeper(nodal_aux, degree)
@@ -184,8 +184,16 @@ def _make_level(A_e, S_e, D, degree=3, **extra):
     return level
 
 
-def _check_nullspace(S, D, where):
-    SD = dv.spgemm(S, D, drop=False)
+def _check_nullspace(S, D, where, A=None):
+    """max|S D| <= 1e-10 max|S| (multigrid.py:110-116). With A (same pattern
+    as S) the product A D is formed in the same pass and returned for the
+    level's D^T A D."""
+    AD = None
+    if A is not None and dv.same_pattern(A, S):
+        AD, SD = dv.spgemm_pair(A, S, D, D, drop=False)
+        AD = dv.drop_zeros(AD)
+    else:
+        SD = dv.spgemm(S, D, drop=False)
     m = dv.empty_f64(2)
     dv.maxabs(SD.val, m[0:1])
     dv.maxabs(S.val, m[1:2])
@@ -195,6 +203,7 @@ def _check_nullspace(S, D, where):
         raise ValueError(
             f"curl null-space identity violated on {where}: "
             f"max|S D| = {defect:.3e} vs max|S| = {scale:.3e}")
+    return AD
 
 
 def build_hierarchy(A_e, S_e, A_n, D, cfg=None):
@@ -203,7 +212,7 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None):
     cfg = cfg or SolverConfig()
     A_e, S_e = as_device_csr(A_e), as_device_csr(S_e)
     A_n, D = as_device_csr(A_n), as_device_csr(D)
-    _check_nullspace(S_e, D, "the fine level")
+    AD = _check_nullspace(S_e, D, "the fine level", A=A_e)
     levels = []
     while A_e.shape[0] > cfg.coarse_size and len(levels) < cfg.max_levels - 1:
         prol, cg, nod = build_edge_prolongator(A_n, A_e, S_e, D, cfg.emin)
@@ -216,7 +225,7 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None):
                 f"coarsening stagnated: {n_coarse} coarse edges from "
                 f"{A_e.shape[0]} fine edges")
         with phase("level.make_level"):
-            lv = _make_level(A_e, S_e, D, cfg.cheb_degree, P_e=P_e, P_n=P_n,
+            lv = _make_level(A_e, S_e, D, cfg.cheb_degree, AD=AD, P_e=P_e, P_n=P_n,
                              emin_energy=prol.energy_history,
                              subproblem_dims=dict(prol.subproblem_dims),
                              commutator_residual=prol.commutator_residual,
@@ -228,18 +237,22 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None):
             lv.R_e = dv.transpose(P_e)
         lv.rc = dv.empty_f64(n_coarse)
         levels.append(lv)
-        with phase("level.galerkin_A"):
-            A_e = dv.spgemm(lv.R_e, dv.spgemm(A_e, P_e))
-        with phase("level.galerkin_S"):
-            S_e = dv.spgemm(lv.R_e, dv.spgemm(S_e, P_e))
+        with phase("level.galerkin_edge"):
+            if dv.same_pattern(A_e, S_e):
+                # one pass for both: P^T (A_e P) and P^T (S_e P) share patterns
+                AP, SP = dv.spgemm_pair(A_e, S_e, P_e, P_e, drop=False)
+                A_e, S_e = dv.spgemm_pair(lv.R_e, lv.R_e, AP, SP)
+            else:
+                A_e = dv.spgemm(lv.R_e, dv.spgemm(A_e, P_e))
+                S_e = dv.spgemm(lv.R_e, dv.spgemm(S_e, P_e))
         with phase("level.galerkin_nodal"):
             A_n = dv.spgemm(dv.transpose(P_n), dv.spgemm(A_n, P_n, ordered=True),
                             ordered=True)
         D = cg.D_H
         with phase("level.nullspace_check"):
-            _check_nullspace(S_e, D, f"level {len(levels)}")
+            AD = _check_nullspace(S_e, D, f"level {len(levels)}", A=A_e)
     with phase("coarsest"):
-        last = _make_level(A_e, S_e, D, cfg.cheb_degree)
+        last = _make_level(A_e, S_e, D, cfg.cheb_degree, AD=AD)
         levels.append(last)
         inv = torch.linalg.inv(dv.to_dense(A_e))   # dense LU (cuSOLVER), once
     last.r = dv.empty_f64(A_e.shape[0])

@@ -94,6 +94,9 @@ int sphc_scale_by_norm(int64_t n, const double *w, const double *sq, double *v,
 int sphc_reciprocal(int64_t n, const double *x, const double *zero_sub, double *y,
                     void *stream);
 
+/* out_i = x[idx_i] (halo send staging of the partitioned solve). */
+int sphc_gather(int64_t n, const int64_t *idx, const double *x, double *out, void *stream);
+
 /* y = a x + b y */
 int sphc_axpby(int64_t n, double a, const double *x, double b, double *y, void *stream);
 

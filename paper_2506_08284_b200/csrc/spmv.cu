@@ -185,6 +185,22 @@ extern "C" int sphc_dense_gemv(int64_t n, const double* A, const double* x, doub
   return 0;
 }
 
+__global__ void k_gather(i64 n, const i64* __restrict__ idx, const double* __restrict__ x,
+                         double* __restrict__ out) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x)
+    out[i] = x[idx[i]];
+}
+
+extern "C" int sphc_gather(int64_t n, const int64_t* idx, const double* x, double* out,
+                           void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  k_gather<<<grid_for(n, 256), 256, 0, s>>>(n, idx, x, out);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
 // y_i = d_i x_i
 __global__ void k_diag_scale(i64 n, const double* __restrict__ d, const double* __restrict__ x,
                              double* __restrict__ y) {

@@ -1,0 +1,160 @@
+"""Partitioned PCG + V-cycle (paper_2506_08284_b200/distributed.py) on CPU
+with the gloo backend, world_size 2 and 3.
+
+The distributed layer's partitioning, halo plans, halo exchanges,
+all_reduce'd inner products and the replicated coarsest solve are the code
+under test; the six local kernels are provided by a scipy implementation
+here (the product injects CudaOps). The result must match the single-process
+oracle solve on the same hierarchy.
+"""
+
+import os
+import pickle
+import socket
+import tempfile
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import hcurl_oracle as O
+from paper_2506_08284_b200 import distributed as D
+from paper_2506_08284_b200.inputs import discretize_hex
+
+
+class ScipyOps:
+    """Reference local kernels (test double for CudaOps)."""
+
+    def _m(self, A):
+        m = getattr(A, "_sp", None)
+        if m is None:
+            m = sp.csr_matrix((A.val.numpy(), A.col.numpy(), A.rowptr.numpy()), shape=A.shape)
+            A._sp = m
+        return m
+
+    def spmv(self, A, x, y, alpha=1.0, beta=0.0, z=None):
+        v = alpha * (self._m(A) @ x.numpy())
+        if z is not None:
+            v = v + beta * z.numpy()
+        y.copy_(torch.from_numpy(v))
+
+    def cheb(self, A, dinv, b, x_ext, x_out, d, cd, cr, x_zero):
+        n = A.shape[0]
+        ax = np.zeros(n) if x_zero else self._m(A) @ x_ext.numpy()
+        dn = cd * d.numpy() + cr * (dinv.numpy() * (b.numpy() - ax))
+        d.copy_(torch.from_numpy(dn))
+        x0 = np.zeros(n) if x_zero else x_ext.numpy()[:n]
+        x_out.copy_(torch.from_numpy(x0 + dn))
+
+    def dot(self, x, y, out):
+        out.fill_(float(x.numpy() @ y.numpy()))
+
+    def gemv(self, M, x, y):
+        y.copy_(M @ x)
+
+    def gather(self, idx, x, out):
+        out.copy_(x[idx])
+
+    def copy(self, dst, src):
+        dst.copy_(src)
+
+    def pcg_update(self, sc, p, Ap, x, r, flag):
+        pAp = float(sc[0])
+        if not pAp > 0.0:
+            return
+        a = float(sc[2]) / pAp
+        xn = x + a * p
+        flag.fill_(int(bool((xn != x).any())))
+        x.copy_(xn)
+        r.sub_(a * Ap)
+
+    def pcg_direction(self, sc, z, p):
+        p.copy_(z + (float(sc[3]) / float(sc[2])) * p)
+
+    def pcg_rotate(self, sc):
+        sc[2] = sc[3]
+
+
+def _levels(h):
+    out = []
+    for li, lv in enumerate(h.levels):
+        last = li == len(h.levels) - 1
+        out.append(SimpleNamespace(
+            A_e=lv.A_e, nodal_aux=lv.nodal_aux, D=lv.D, Dt=O.canonical(lv.D.T),
+            P_e=None if last else lv.P_e, R_e=None if last else O.canonical(lv.P_e.T),
+            edge_sweeper=SimpleNamespace(dinv=lv.edge_sweeper.dinv,
+                                         coefs=lv.edge_sweeper.coefficients()),
+            aux_sweeper=SimpleNamespace(dinv=lv.aux_sweeper.dinv,
+                                        coefs=lv.aux_sweeper.coefficients())))
+    return out
+
+
+def _problem():
+    s = discretize_hex(6, 1.0, True)
+    h = O.build_hierarchy(s.A_e, s.S, s.A_n, s.D, coarse_size=40, smoother="cheb")
+    b = np.random.default_rng(0).uniform(-1, 1, s.A_e.shape[0])
+    inv = np.linalg.inv(h.levels[-1].A_e.toarray())
+    return h, b, inv
+
+
+def _worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.set_num_threads(1)
+    h, b, inv = _problem()
+    dh = D.distribute(_levels(h), torch.from_numpy(inv), rank, world, None, ScipyOps(),
+                      torch.device("cpu"))
+    part = dh.levels[0].edge_part
+    res = D.dist_pcg_solve(dh, torch.from_numpy(b[part.lo(rank):part.hi(rank)]).clone())
+    xs = [None] * world
+    dist.all_gather_object(xs, res.x.numpy())
+    if rank == 0:
+        with open(out_path, "wb") as f:
+            pickle.dump(dict(x=np.concatenate(xs), its=res.iterations, status=res.status,
+                             hist=res.residual_history), f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_partition_and_halo_plan_sizes():
+    p = D.Partition.balanced(10, 3)
+    assert p.offsets.tolist() == [0, 3, 6, 10]
+    assert p.owner(np.array([0, 2, 3, 5, 6, 9])).tolist() == [0, 0, 1, 1, 2, 2]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_solve_matches_single_process(world):
+    h, b, inv = _problem()
+    # single-process reference: the same V-cycle with the dense coarse inverse
+    ref = O.pcg(h.levels[0].A_e, b, lambda r: _vc(h, inv, r))
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "res.pkl")
+        mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+        with open(out, "rb") as f:
+            got = pickle.load(f)
+    assert got["status"] == "converged"
+    assert abs(got["its"] - ref.iterations) <= 1
+    assert np.max(np.abs(got["x"] - ref.x)) <= 1e-8 * np.max(np.abs(ref.x))
+    np.testing.assert_allclose(got["hist"][:len(ref.residual_history)],
+                               ref.residual_history[:len(got["hist"])], rtol=1e-6)
+
+
+def _vc(h, inv, b, level=0):
+    lv = h.levels[level]
+    if level == len(h.levels) - 1:
+        return inv @ b
+    x = O.hiptmair(lv, np.zeros(b.size), b)
+    rc = lv.P_e.T @ (b - lv.A_e @ x)
+    x = x + lv.P_e @ _vc(h, inv, rc, level + 1)
+    return O.hiptmair(lv, x, b)

@@ -284,3 +284,31 @@ def test_error_case_matches_reference():
     with pytest.raises(ValueError) as e:
         mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, mg.SolverConfig(coarse_size=100))
     assert str(e.value).split(":")[0] == msg.split(":")[0]
+
+
+def test_partitioned_solve_single_rank_nccl():
+    """distributed.py on the GPU with CudaOps and an NCCL group of one rank:
+    the partitioned V-cycle / PCG equals the single-GPU solve."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2506_08284_b200 import distributed as D
+    from paper_2506_08284_b200 import multigrid as mg
+    s = _system(16, 1.0, True)
+    b = np.random.default_rng(0).uniform(-1, 1, s.A_e.shape[0])
+    h = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, mg.SolverConfig(coarse_size=200))
+    ref = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        dh = D.distribute_hierarchy(h)
+        res = D.dist_pcg_solve(dh, torch.from_numpy(b).cuda())
+    finally:
+        dist.destroy_process_group()
+    assert res.status == "converged"
+    assert abs(res.iterations - ref.iterations) <= 1
+    x = res.x.cpu().numpy()
+    assert np.max(np.abs(x - ref.x)) <= 1e-8 * np.max(np.abs(ref.x))

@@ -137,6 +137,48 @@ def ncu_traffic(pattern="k_sell_cheb_full"):
     return tot if found == 2 else None
 
 
+def scale_roofline(args, flush):
+    """The same kernel (fused SELL Chebyshev step) on the finest A_e of a
+    config larger than L2 (default C3: 811k edges, 26M nonzeros, 313 MB),
+    each launch timed alone after an L2 flush."""
+    import torch
+    from paper_2506_08284_b200 import _lib, device as dv
+    sysm, _, cfg = make_problem(args.scale_config)
+    A = dv.DeviceCSR.from_scipy(sysm.A_e)
+    n = A.shape[0]
+    m = dv.sell(A)
+    dinv = dv.reciprocal(dv.diagonal(A))
+    g = torch.Generator(device="cpu").manual_seed(0)
+    b = torch.rand(n, generator=g, dtype=torch.float64).cuda()
+    x = torch.rand(n, generator=g, dtype=torch.float64).cuda()
+    out, d = torch.empty_like(x), torch.zeros_like(x)
+
+    def k():
+        _lib.call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, dinv, b, x, out, d,
+                  0.3, 0.7, 0)
+
+    for _ in range(3):
+        k()
+    nk = 20
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(nk)]
+    for i in range(nk):
+        flush.fill_(100.0 + i)
+        ev[i][0].record()
+        k()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    t = sorted(a.elapsed_time(bb) for a, bb in ev)[nk // 2]
+    byts = cheb_kernel_bytes(A)
+    pk, kind = peaks()
+    ach = byts / (t * 1e-3) / 1e9
+    return {"config": f"{args.scale_config} finest A_e ({n} rows, {A.nnz} nnz)",
+            "kernel": "k_sell_cheb", "launch_ms_median": t, "algorithmic_bytes": byts,
+            "achieved": ach, "peak": float(pk["hbm_gbs"]), "unit": "GB/s",
+            "frac": ach / float(pk["hbm_gbs"]), "sell_padding": m.padded / A.nnz,
+            "traffic": ncu_traffic("k_sell_cheb_c3_full")}
+
+
 def make_problem(config, N=None):
     from paper_2506_08284_b200.inputs import make_config
     sysm, rhs, cfg = make_config(config, N)
@@ -169,8 +211,18 @@ def run_ours(args):
     b = torch.from_numpy(rhs).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
+    partitioned = args.partitioned and ws > 1
+    if partitioned:
+        from paper_2506_08284_b200 import distributed as dist_mod
+
     def step():
         h = mg.build_hierarchy(A_e, S, A_n, D, scfg)
+        if partitioned:
+            # replicated setup, row-block partitioned solve (strong scaling)
+            dh = dist_mod.distribute_hierarchy(h)
+            part = dh.levels[0].edge_part
+            res = dist_mod.dist_pcg_solve(dh, b[part.lo(rank):part.hi(rank)].contiguous())
+            return h, res
         res = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
         return h, res
 
@@ -261,6 +313,7 @@ def run_ours(args):
     t_k = sum(a.elapsed_time(bb) for a, bb in kev) / nk
     t_k_warm = k0.elapsed_time(k1) / nk
     kbytes = cheb_kernel_bytes(A0)
+    at_scale = None if args.no_scale_roofline else scale_roofline(args, flush)
 
     # e2e: public API with host inputs, solution back to host
     e2e_ms = []
@@ -293,11 +346,12 @@ def run_ours(args):
         cpu = cpu_baseline(args) if (ws == 1 and not args.no_cpu_baseline) else None
         line = {
             "metric": "edge DOFs/s for setup + PCG solve to 1e-8",
-            "value": ws * n_e / (t_step * 1e-3),
+            "value": (1 if partitioned else ws) * n_e / (t_step * 1e-3),
             "unit": "edge DOFs/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if partitioned else "weak",
+            "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (reference model problem, seeded RHS)",
             "config": {"workload": f"{args.config}: {cfg['N']}^3 hex, "
                        f"{'Dirichlet' if cfg['dirichlet'] else 'natural'}, "
@@ -306,7 +360,8 @@ def run_ours(args):
                        "n_edges": n_e, "levels": [lv.A_e.shape[0] for lv in h.levels],
                        "operator_complexity": h.operator_complexity,
                        "pcg_iterations": iters, "smoother": "chebyshev-3 hiptmair",
-                       "parallelism": f"replicas x{ws}",
+                       "parallelism": (f"row-block partitioned solve x{ws}" if partitioned
+                                       else f"replicas x{ws}"),
                        "l2": "256 MB flush before every timed step"},
             "setup_ms": t_setup, "solve_ms": t_solve,
             "setup_dofs_per_s": n_e / (t_setup * 1e-3),
@@ -324,6 +379,7 @@ def run_ours(args):
                          "l2_flushed_per_launch": True,
                          "sell_padding": m0.padded / max(A0.nnz, 1),
                          "algorithmic_bytes": kbytes},
+            "roofline_at_scale": at_scale,
             "e2e": {"value": ws * n_e / (t_e2e * 1e-3), "unit": "edge DOFs/s",
                     "ms": t_e2e, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
@@ -401,6 +457,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-scale-roofline", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="N>1: one problem, row-block partitioned solve (strong scaling)")
+    ap.add_argument("--scale-config", default="C3")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

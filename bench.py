@@ -155,7 +155,7 @@ def scale_roofline(args, flush):
 
     def k():
         _lib.call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, dinv, b, x, out, d,
-                  0.3, 0.7, 0)
+                  0.3, 0.7, 0, m.padded)
 
     for _ in range(3):
         k()
@@ -292,7 +292,7 @@ def run_ours(args):
 
     def kstep():
         _lib.call("sphc_sell_cheb_step", n_e, m0.slice_ptr, m0.col, m0.val, sw.dinv, b, x0,
-                  sw.buf[0], sw.d, cd, cr, 0)
+                  sw.buf[0], sw.d, cd, cr, 0, m0.padded)
 
     for _ in range(3):
         kstep()

@@ -174,15 +174,17 @@ int sphc_spmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *v, 
 int sphc_sell_sizes(int64_t n, const int64_t *rp, int64_t *slice_entries, void *stream);
 int sphc_sell_fill(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
                    const int64_t *slice_ptr, int32_t *sci, double *sv, void *stream);
-/* y = alpha A x + beta z on the SELL mirror, one thread per row. */
+/* y = alpha A x + beta z on the SELL mirror, one thread per row. `padded` =
+ * stored entries (slice_ptr[n_slices]); operators above 48 MB are read with
+ * evict-first loads, smaller ones stay L2-resident across the V-cycle. */
 int sphc_sell_spmv(int64_t n, const int64_t *slice_ptr, const int32_t *sci, const double *sv,
                    const double *x, double alpha, double beta, const double *z, double *y,
-                   void *stream);
+                   int64_t padded, void *stream);
 /* Fused Chebyshev step on the SELL mirror (same math as sphc_cheb_step). */
 int sphc_sell_cheb_step(int64_t n, const int64_t *slice_ptr, const int32_t *sci,
                         const double *sv, const double *dinv, const double *b,
                         const double *x_in, double *x_out, double *d, double cd, double cr,
-                        int x_zero, void *stream);
+                        int x_zero, int64_t padded, void *stream);
 
 /* One Chebyshev step, fused: d <- cd*d + cr*dinv*(b - A x_in); x_out = x_in + d.
  * x_zero != 0 means x_in == 0 (A x skipped). Replaces the reference's

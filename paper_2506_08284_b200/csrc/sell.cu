@@ -63,20 +63,29 @@ extern "C" int sphc_sell_fill(int64_t n, const int64_t* rp, const int32_t* ci, c
   return 0;
 }
 
+// Operators whose SELL arrays exceed this stay out of L2 (streaming,
+// evict-first loads keep the x gathers resident); smaller ones (coarse
+// levels, the C2 finest level) are re-read by every Chebyshev step and are
+// loaded with the default policy so they stay L2-resident across the V-cycle.
+#define SELL_STREAM_BYTES (48ll << 20)
+
+template <bool STREAM>
 __device__ __forceinline__ double sell_row(i64 base, int w, const int* __restrict__ sci,
                                            const double* __restrict__ sv,
                                            const double* __restrict__ x) {
   double acc = 0.0;
-  int j = 0;
 #pragma unroll 4
-  for (; j < w; j++) {
+  for (int j = 0; j < w; j++) {
     i64 o = base + (i64)j * SELL_C;
-    acc = fma(__ldcs(sv + o), __ldg(x + __ldcs(sci + o)), acc);
+    double v = STREAM ? __ldcs(sv + o) : __ldg(sv + o);
+    int c = STREAM ? __ldcs(sci + o) : __ldg(sci + o);
+    acc = fma(v, __ldg(x + c), acc);
   }
   return acc;
 }
 
 // y = alpha A x + beta z
+template <bool STREAM>
 __global__ void __launch_bounds__(256)
     k_sell_spmv(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
                 const double* __restrict__ sv, const double* __restrict__ x, double alpha,
@@ -87,7 +96,7 @@ __global__ void __launch_bounds__(256)
   if (s >= ns) return;
   i64 b0 = sp[s];
   int w = (int)((sp[s + 1] - b0) / SELL_C);
-  double acc = sell_row(b0 + (row % SELL_C), w, sci, sv, x);
+  double acc = sell_row<STREAM>(b0 + (row % SELL_C), w, sci, sv, x);
   if (row < n) {
     double r = alpha * acc;
     if (z) r = fma(beta, z[row], r);
@@ -96,6 +105,7 @@ __global__ void __launch_bounds__(256)
 }
 
 // d <- cd d + cr dinv (b - A x_in); x_out = x_in + d
+template <bool STREAM>
 __global__ void __launch_bounds__(256)
     k_sell_cheb(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
                 const double* __restrict__ sv, const double* __restrict__ dinv,
@@ -110,7 +120,7 @@ __global__ void __launch_bounds__(256)
   if (!x_zero) {
     i64 b0 = sp[s];
     int w = (int)((sp[s + 1] - b0) / SELL_C);
-    ax = sell_row(b0 + (row % SELL_C), w, sci, sv, x_in);
+    ax = sell_row<STREAM>(b0 + (row % SELL_C), w, sci, sv, x_in);
   }
   if (row < n) {
     double r = b[row] - ax;
@@ -123,12 +133,15 @@ __global__ void __launch_bounds__(256)
 
 extern "C" int sphc_sell_spmv(int64_t n, const int64_t* slice_ptr, const int32_t* sci,
                               const double* sv, const double* x, double alpha, double beta,
-                              const double* z, double* y, void* stream) {
+                              const double* z, double* y, int64_t padded, void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
   i64 rows = (n + 31) & ~(i64)31;
-  k_sell_spmv<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(n, slice_ptr, sci, sv, x, alpha,
-                                                             beta, z, y);
+  unsigned g = (unsigned)((rows + 255) / 256);
+  if (padded * 12 > SELL_STREAM_BYTES)
+    k_sell_spmv<true><<<g, 256, 0, s>>>(n, slice_ptr, sci, sv, x, alpha, beta, z, y);
+  else
+    k_sell_spmv<false><<<g, 256, 0, s>>>(n, slice_ptr, sci, sv, x, alpha, beta, z, y);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -136,12 +149,17 @@ extern "C" int sphc_sell_spmv(int64_t n, const int64_t* slice_ptr, const int32_t
 extern "C" int sphc_sell_cheb_step(int64_t n, const int64_t* slice_ptr, const int32_t* sci,
                                    const double* sv, const double* dinv, const double* b,
                                    const double* x_in, double* x_out, double* d, double cd,
-                                   double cr, int x_zero, void* stream) {
+                                   double cr, int x_zero, int64_t padded, void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
   i64 rows = (n + 31) & ~(i64)31;
-  k_sell_cheb<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(n, slice_ptr, sci, sv, dinv, b,
-                                                             x_in, x_out, d, cd, cr, x_zero);
+  unsigned g = (unsigned)((rows + 255) / 256);
+  if (padded * 12 > SELL_STREAM_BYTES)
+    k_sell_cheb<true><<<g, 256, 0, s>>>(n, slice_ptr, sci, sv, dinv, b, x_in, x_out, d, cd,
+                                        cr, x_zero);
+  else
+    k_sell_cheb<false><<<g, 256, 0, s>>>(n, slice_ptr, sci, sv, dinv, b, x_in, x_out, d, cd,
+                                         cr, x_zero);
   SPHC_LAUNCH_CHECK();
   return 0;
 }

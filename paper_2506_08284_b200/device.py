@@ -258,7 +258,7 @@ def spmv(A, x, y, alpha=1.0, beta=0.0, z=None, lanes=None):
     """y = alpha A x + beta z (on A's SELL mirror when it has one)."""
     m = getattr(A, "_sell", None)
     if m is not None:
-        call("sphc_sell_spmv", m.n, m.slice_ptr, m.col, m.val, x, alpha, beta, z, y)
+        call("sphc_sell_spmv", m.n, m.slice_ptr, m.col, m.val, x, alpha, beta, z, y, m.padded)
         return y
     call("sphc_spmv", A.shape[0], A.rowptr, A.col, A.val, lanes or A.lanes(), x, alpha,
          beta, z, y)

@@ -120,7 +120,7 @@ class ChebyshevSweeper:
                 m = self.sell
                 if m is not None:
                     call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, self.dinv, b,
-                         None if z else cur, out, self.d, cd, cr, int(z))
+                         None if z else cur, out, self.d, cd, cr, int(z), m.padded)
                 else:
                     call("sphc_cheb_step", n, A.rowptr, A.col, A.val, self.lanes, self.dinv,
                          b, None if z else cur, out, self.d, cd, cr, int(z))

@@ -104,7 +104,8 @@ def test_sell_spmv_and_cheb_match_csr():
         d2 = d1.clone()
         o1 = torch.empty_like(X)
         o2 = torch.empty_like(X)
-        call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, DI, B, X, o1, d1, 0.3, 0.7, 0)
+        call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, DI, B, X, o1, d1, 0.3, 0.7, 0,
+             m.padded)
         call("sphc_cheb_step", n, Ad.rowptr, Ad.col, Ad.val, 8, DI, B, X, o2, d2, 0.3, 0.7, 0)
         assert torch.allclose(o1, o2, rtol=1e-13, atol=1e-13)
         assert torch.allclose(d1, d2, rtol=1e-13, atol=1e-13)

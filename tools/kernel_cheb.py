@@ -16,6 +16,6 @@ out, d = torch.empty_like(x), torch.zeros_like(x)
 flush = torch.empty(256 * 2**20 // 8, dtype=torch.float64, device="cuda")
 for i in range(5):
     flush.fill_(float(i))
-    _lib.call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, dinv, b, x, out, d, 0.3, 0.7, 0)
+    _lib.call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, dinv, b, x, out, d, 0.3, 0.7, 0, m.padded)
 torch.cuda.synchronize()
 print("ok", n, A.nnz, m.padded)

@@ -45,6 +45,37 @@ class CoarseGradient:
         return [(int(x), int(y)) if x >= 0 else (int(y),) for x, y in zip(a, b)]
 
 
+def coarse_gradient_from_edges(pairs, singles, n_nodes):
+    """CoarseGradient from explicit edge lists: interior pairs (a < b, sorted)
+    then single-node edges (sorted) -- the layout build_coarse_gradient
+    produces (used by tests that feed reference-side edge sets)."""
+    pairs = np.asarray(pairs, dtype=np.int64).reshape(-1, 2)
+    singles = np.asarray(singles, dtype=np.int64)
+    n_int, n_single = pairs.shape[0], singles.size
+    dev = dv.device()
+    adj_rp = np.zeros(n_nodes + 1, dtype=np.int64)
+    np.add.at(adj_rp, pairs[:, 0] + 1, 1)
+    adj_rp = np.cumsum(adj_rp)
+    soff = np.zeros(n_nodes + 1, dtype=np.int64)
+    soff[singles + 1] = 1
+    soff = np.cumsum(soff)
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)  # noqa: E731
+    n_edges = n_int + n_single
+    dh_rp = torch.empty(n_edges + 1, dtype=torch.int64, device=dev)
+    dh_ci = torch.empty(2 * n_int + n_single, dtype=torch.int32, device=dev)
+    dh_v = torch.empty(2 * n_int + n_single, dtype=torch.float64, device=dev)
+    ep_a = torch.empty(n_edges, dtype=torch.int32, device=dev)
+    ep_b = torch.empty(n_edges, dtype=torch.int32, device=dev)
+    sid = torch.empty(n_nodes, dtype=torch.int32, device=dev)
+    arp, acol, so = t(adj_rp, np.int64), t(pairs[:, 1], np.int32), t(soff, np.int64)
+    call("sphc_build_coarse_gradient", n_nodes, n_int, arp, acol, so, n_single, dh_rp, dh_ci,
+         dh_v, ep_a, ep_b, sid)
+    return CoarseGradient(D_H=DeviceCSR(dh_rp, dh_ci, dh_v, (n_edges, n_nodes)),
+                          n_interior=n_int, n_single=n_single,
+                          adj=DeviceCSR(arp, acol, None, (n_nodes, n_nodes)),
+                          ep_a=ep_a, ep_b=ep_b, single_id=sid, augmented_edges=[])
+
+
 def gen_piecewise_const(P, n_passes=2):
     """Algorithm 1 (coarse_gradient.py:36-103): the column assigned to every
     row (int64, device). Returned as the assignment vector rather than the

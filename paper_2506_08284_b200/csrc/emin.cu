@@ -85,6 +85,8 @@ __device__ void em_build_J(EminRow& R, i64 i, const i64* __restrict__ drp,
 // ids) followed by single-node edges of J nodes (ascending ids).
 __device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
                            const int* __restrict__ adj_col, const int* __restrict__ single_id,
+                           const i64* __restrict__ xrp, const int* __restrict__ xeid,
+                           const int* __restrict__ ep_a, const int* __restrict__ ep_b,
                            i64* status, int lane) {
   int nJ = R.nJ;
   int npairs = nJ * (nJ - 1) / 2;
@@ -134,6 +136,21 @@ __device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
     }
     nI += __popc(bal);
   }
+  // edges appended by make_irreducible for this row (ids above every
+  // original edge, ascending): both endpoints lie in J by construction
+  if (xrp) {
+    i64 x0 = xrp[i], x1 = xrp[i + 1];
+    for (i64 t = x0 + lane; t < x1; t += 32) {
+      int o = nI + (int)(t - x0);
+      int e = xeid[t];
+      if (o < IM) {
+        R.Icol[o] = e;
+        R.pa[o] = lower_bound_i32(R.J, nJ, ep_a[e]);
+        R.pb[o] = lower_bound_i32(R.J, nJ, ep_b[e]);
+      }
+    }
+    nI += (int)(x1 - x0);
+  }
   over = nI > IM;
   if (lane == 0) {
     R.nI = over ? 0 : nI;
@@ -147,7 +164,7 @@ __device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
 
 // lane 0: irreducibility, k, Gram matrix, Cholesky, rank checks.
 // Returns false (and reports) on failure.
-__device__ bool em_factor(EminRow& R, i64 i, i64* status) {
+__device__ int em_factor(EminRow& R, i64 i, i64* status) {
   int nJ = R.nJ, nI = R.nI;
   // union-find over J with interior edges; incidence from every edge
   int parent[JM];
@@ -180,16 +197,13 @@ __device__ bool em_factor(EminRow& R, i64 i, i64* status) {
     if (root0 < 0) root0 = x;
     irreducible &= inc[q] && (x == root0);
   }
-  if (!irreducible) {
-    report(status, SPHC_ST_REDUCIBLE, i);
-    return false;
-  }
+  if (!irreducible) return 1;
   int k = nJ - (dirich ? 0 : 1);
   R.k = k;
   // expected rank must be in [1, min(|I|, |J|)]
   if (k < 1 || k > nI) {
     report(status, SPHC_ST_RANK_LOW, i);
-    return false;
+    return 2;
   }
   double* L = R.L;
   for (int t = 0; t < k * k; t++) L[t] = 0.0;
@@ -211,7 +225,7 @@ __device__ bool em_factor(EminRow& R, i64 i, i64* status) {
     double ljj = d > 0.0 ? sqrt(d) : 0.0;
     if (!(ljj >= 1e-10 * (j ? L[0] : ljj)) || ljj == 0.0) {
       report(status, SPHC_ST_RANK_LOW, i);
-      return false;
+      return 2;
     }
     L[j * k + j] = ljj;
     for (int p = j + 1; p < k; p++) {
@@ -220,7 +234,7 @@ __device__ bool em_factor(EminRow& R, i64 i, i64* status) {
       L[p * k + j] = x / ljj;
     }
   }
-  return true;
+  return 0;
 }
 
 // lane 0: y <- M^-1 y (k entries) with the Cholesky factor
@@ -245,8 +259,11 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
                  const double* __restrict__ dv, const i64* __restrict__ prp,
                  const int* __restrict__ pci, const double* __restrict__ pv,
                  const i64* __restrict__ adj_rp, const int* __restrict__ adj_col,
-                 const int* __restrict__ single_id, i64* icount, i64* jcount, double* rmax2,
-                 i64* dims, const i64* __restrict__ trp, int* __restrict__ tci,
+                 const int* __restrict__ single_id, const i64* __restrict__ xrp,
+                 const int* __restrict__ xeid, const int* __restrict__ ep_a,
+                 const int* __restrict__ ep_b, i64* icount, i64* jcount, double* rmax2,
+                 i64* dims, unsigned char* rowflag, double* rowmax,
+                 const i64* __restrict__ trp, int* __restrict__ tci,
                  double* __restrict__ tv, const i64* __restrict__ erp, int* __restrict__ eci,
                  double* __restrict__ ev, i64* status) {
   __shared__ EminRow rows[EM_WARPS];
@@ -260,7 +277,7 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
       __syncwarp();
       continue;
     }
-    em_build_I(R, i, adj_rp, adj_col, single_id, status, lane);
+    em_build_I(R, i, adj_rp, adj_col, single_id, xrp, xeid, ep_a, ep_b, status, lane);
     if (R.err) {
       if (!FILL && lane == 0) { icount[i] = 0; jcount[i] = R.nJ; }
       __syncwarp();
@@ -276,6 +293,8 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
         else atomicAdd((unsigned long long*)&dims[nI * SPHC_DIMS_J + nJ], 1ull);
         icount[i] = nI;
         jcount[i] = nJ;
+        if (rowflag) rowflag[i] = nI == 0 ? 2 : 0;
+        if (rowmax) rowmax[i] = rm;
       }
     }
     if (FILL) {
@@ -289,9 +308,15 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
       __syncwarp();
       continue;
     }
-    bool ok = true;
     if (lane == 0) {
-      ok = em_factor(R, i, status);
+      int fc = em_factor(R, i, status);
+      bool ok = fc == 0;
+      // reducible blocks are flagged for the host make_irreducible pass
+      // (rowflag != NULL) or are an error once the repair has been applied
+      if (fc == 1) {
+        if (rowflag) rowflag[i] |= 1;
+        else report(status, SPHC_ST_REDUCIBLE, i);
+      }
       if (ok && FILL) {
         // c = r - G^T 1 on the first k nodes, y = M^-1 c
         int k = R.k;
@@ -306,14 +331,19 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
       R.err = ok ? 0 : 1;
     }
     __syncwarp();
-    if (FILL && !R.err) {
+    if (FILL) {
+      // the pattern is written even for a failed block (the host repair pass
+      // reads the original rows); values only for factored blocks
       int k = R.k;
+      bool okv = !R.err;
       i64 eo = erp[i];
       for (int e = lane; e < nI; e += 32) {
-        int a = R.pa[e], b = R.pb[e];
-        double gy = (b < k ? R.y[b] : 0.0) - ((a >= 0 && a < k) ? R.y[a] : 0.0);
         eci[eo + e] = R.Icol[e];
-        ev[eo + e] = 1.0 + gy;
+        if (okv) {
+          int a = R.pa[e], b = R.pb[e];
+          double gy = (b < k ? R.y[b] : 0.0) - ((a >= 0 && a < k) ? R.y[a] : 0.0);
+          ev[eo + e] = 1.0 + gy;
+        }
       }
     }
     __syncwarp();
@@ -323,13 +353,16 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
 extern "C" int sphc_emin_count(int64_t n_e, const int64_t* drp, const int32_t* dci,
                                const double* dv, const int64_t* prp, const int32_t* pci,
                                const double* pv, const int64_t* adj_rp, const int32_t* adj_col,
-                               int64_t n_int, const int32_t* single_id, int64_t* icount,
-                               int64_t* jcount, double* rmax2, int64_t* dims, int64_t* status,
+                               int64_t n_int, const int32_t* single_id, const int64_t* xrp,
+                               const int32_t* xeid, const int32_t* ep_a, const int32_t* ep_b,
+                               int64_t* icount, int64_t* jcount, double* rmax2, int64_t* dims,
+                               uint8_t* rowflag, double* rowmax, int64_t* status,
                                void* stream) {
   cudaStream_t s = as_stream(stream);
   k_emin_setup<false><<<grid_for(n_e, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
-      n_e, drp, dci, dv, prp, pci, pv, adj_rp, adj_col, single_id, icount, jcount, rmax2, dims,
-      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, status);
+      n_e, drp, dci, dv, prp, pci, pv, adj_rp, adj_col, single_id, xrp, xeid, ep_a, ep_b,
+      icount, jcount, rmax2, dims, rowflag, rowmax, nullptr, nullptr, nullptr, nullptr,
+      nullptr, nullptr, status);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -337,13 +370,15 @@ extern "C" int sphc_emin_count(int64_t n_e, const int64_t* drp, const int32_t* d
 extern "C" int sphc_emin_fill(int64_t n_e, const int64_t* drp, const int32_t* dci,
                               const double* dv, const int64_t* prp, const int32_t* pci,
                               const double* pv, const int64_t* adj_rp, const int32_t* adj_col,
-                              int64_t n_int, const int32_t* single_id, const int64_t* trp,
-                              int32_t* tci, double* tv, const int64_t* erp, int32_t* eci,
-                              double* ev, int64_t* status, void* stream) {
+                              int64_t n_int, const int32_t* single_id, const int64_t* xrp,
+                              const int32_t* xeid, const int32_t* ep_a, const int32_t* ep_b,
+                              const int64_t* trp, int32_t* tci, double* tv, const int64_t* erp,
+                              int32_t* eci, double* ev, int64_t* status, void* stream) {
   cudaStream_t s = as_stream(stream);
   k_emin_setup<true><<<grid_for(n_e, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
-      n_e, drp, dci, dv, prp, pci, pv, adj_rp, adj_col, single_id, nullptr, nullptr, nullptr,
-      nullptr, trp, tci, tv, erp, eci, ev, status);
+      n_e, drp, dci, dv, prp, pci, pv, adj_rp, adj_col, single_id, xrp, xeid, ep_a, ep_b,
+      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, trp, tci, tv, erp, eci, ev,
+      status);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -407,7 +442,9 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
     if (update) {
       bool ok = true;
       if (lane == 0) {
-        ok = em_factor(R, i, status);
+        int fc = em_factor(R, i, status);
+        if (fc == 1) report(status, SPHC_ST_REDUCIBLE, i);
+        ok = fc == 0;
         if (ok) {
           int k = R.k;
           double di = dinv[i];

@@ -111,6 +111,7 @@ def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None):
         cg = cgrad.build_coarse_gradient(D_h, assign, agg.n_agg)
     with phase("setup.emin_constraints"):
         setup = es.setup_constraints(D_h, nod.P, cg)
+        cg = setup.cg                      # with any edges make_irreducible appended
     with phase("setup.emin_sweeps"):
         vals, energy, res = emin_sweeps(S, setup, cfg.omega, cfg.iterations)
     P = setup.pattern

@@ -44,21 +44,16 @@ def _raise(st, D):
         raise RuntimeError(f"fine edge {rows['EMIN_CAPACITY']}: constraint block exceeds "
                            f"the device kernel capacity (|J| <= 16, |I| <= 64)")
     if "REDUCIBLE" in rows:
-        # reference: make_irreducible (emin_setup.py:183-217); never fired on
-        # any measured configuration and not ported.
-        raise NotImplementedError(
-            f"fine edge {rows['REDUCIBLE']}: reducible constraint block needs the "
-            "make_irreducible repair, which the device path does not implement")
+        # only reachable if a block is still reducible after the repair pass
+        raise RuntimeError(
+            f"fine edge {rows['REDUCIBLE']}: constraint block reducible after the "
+            "make_irreducible pass (internal error)")
     if "RANK_LOW" in rows:
         raise ValueError(f"fine edge {rows['RANK_LOW']}: numerical rank below the "
                          "expected rank (topology bug)")
 
 
-def setup_constraints(D_h, P_n, cg):
-    """Pattern, irreducibility, factor checks and feasible guess for every
-    fine edge (emin_setup.py:256-336 + edge_prolongator.py:104-126)."""
-    D = as_device_csr(D_h)
-    P = as_device_csr(P_n)
+def _count(D, P, cg, xrp, xeid, flags):
     n_e = D.shape[0]
     dev = D.rowptr.device
     st = Status()
@@ -66,17 +61,17 @@ def setup_constraints(D_h, P_n, cg):
     jcount = torch.empty(n_e, dtype=torch.int64, device=dev)
     rmax2 = torch.zeros(2, dtype=torch.float64, device=dev)
     dims = torch.zeros(65 * 17, dtype=torch.int64, device=dev)
+    rowflag = torch.zeros(n_e, dtype=torch.uint8, device=dev) if flags else None
+    rowmax = torch.empty(n_e, dtype=torch.float64, device=dev) if flags else None
     call("sphc_emin_count", n_e, D.rowptr, D.col, D.val, P.rowptr, P.col, P.val,
-         cg.adj.rowptr, cg.adj.col, cg.n_interior, cg.single_id, icount, jcount, rmax2, dims,
-         st.t)
-    _raise(st, D)
-    rm = rmax2.cpu().numpy()
-    rdp_scale = max(1.0, float(rm[0]))
-    if rm[1] > 1e-12 * rdp_scale:
-        # reference: _empty_shell + make_irreducible (emin_setup.py:292-302)
-        raise NotImplementedError(
-            "a fine edge with an empty prolongator pattern has a nonzero commutator "
-            "row; the make_irreducible repair is not implemented on the device path")
+         cg.adj.rowptr, cg.adj.col, cg.n_interior, cg.single_id, xrp, xeid, cg.ep_a, cg.ep_b,
+         icount, jcount, rmax2, dims, rowflag, rowmax, st.t)
+    return st, icount, jcount, rmax2, dims, rowflag, rowmax
+
+
+def _fill(D, P, cg, icount, jcount, xrp, xeid, st):
+    n_e = D.shape[0]
+    dev = D.rowptr.device
     trp, tnnz = dv.scan(jcount)
     erp, ennz = dv.scan(icount)
     tci = torch.empty(tnnz, dtype=torch.int32, device=dev)
@@ -84,12 +79,45 @@ def setup_constraints(D_h, P_n, cg):
     eci = torch.empty(ennz, dtype=torch.int32, device=dev)
     ev = torch.empty(ennz, dtype=torch.float64, device=dev)
     call("sphc_emin_fill", n_e, D.rowptr, D.col, D.val, P.rowptr, P.col, P.val,
-         cg.adj.rowptr, cg.adj.col, cg.n_interior, cg.single_id, trp, tci, tv, erp, eci, ev,
-         st.t)
+         cg.adj.rowptr, cg.adj.col, cg.n_interior, cg.single_id, xrp, xeid, cg.ep_a, cg.ep_b,
+         trp, tci, tv, erp, eci, ev, st.t)
+    return (DeviceCSR(trp, tci, tv, (n_e, P.shape[1])),
+            DeviceCSR(erp, eci, ev, (n_e, cg.n_edges)))
+
+
+def setup_constraints(D_h, P_n, cg):
+    """Pattern, irreducibility, factor checks and feasible guess for every
+    fine edge (emin_setup.py:256-336 + edge_prolongator.py:104-126).
+
+    Rows whose constraint block is reducible, or whose pattern is empty while
+    their commutator row is not, are flagged by the device pass and repaired
+    on the host with the reference's make_irreducible semantics
+    (``repair.make_irreducible_pass``); the coarse edges it appends are fed
+    back to the device kernels as per-row extras."""
+    D = as_device_csr(D_h)
+    P = as_device_csr(P_n)
+    n_e = D.shape[0]
+    st, icount, jcount, rmax2, dims, rowflag, rowmax = _count(D, P, cg, None, None, True)
+    _raise(st, D)
+    rm = rmax2.cpu().numpy()
+    rdp_scale = max(1.0, float(rm[0]))
+    flags = rowflag
+    need = (flags & 1).bool()
+    if rm[1] > 1e-12 * rdp_scale:
+        need |= ((flags & 2).bool() & (rowmax > 1e-12 * rdp_scale))
+    n_aug = 0
+    xrp = xeid = None
+    if bool(need.any()):
+        from . import repair
+        T0, Pat0 = _fill(D, P, cg, icount, jcount, None, None, Status())
+        cg, xrp, xeid, n_aug = repair.make_irreducible_pass(
+            need, flags, rowmax, rdp_scale, T0, Pat0, cg)
+        st, icount, jcount, rmax2, dims, _, _ = _count(D, P, cg, xrp, xeid, False)
+        _raise(st, D)
+    T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st)
     _raise(st, D)
     h = dims.cpu().numpy().reshape(65, 17)
     nz = np.argwhere(h)
     counter = Counter({(int(i), int(j)): int(h[i, j]) for i, j in nz})
-    return EminSetup(T=DeviceCSR(trp, tci, tv, (n_e, P.shape[1])),
-                     pattern=DeviceCSR(erp, eci, ev, (n_e, cg.n_edges)),
-                     cg=cg, subproblem_dims=counter, rdp_scale=rdp_scale)
+    return EminSetup(T=T, pattern=pattern, cg=cg, subproblem_dims=counter,
+                     rdp_scale=rdp_scale, n_augmented=n_aug)

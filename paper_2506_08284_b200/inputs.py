@@ -327,18 +327,33 @@ CONFIGS = {
     "C1": dict(N=16, sigma=1.0, dirichlet=True, seed=0),
     "C2": dict(N=32, sigma=1e-2, dirichlet=True, seed=1),
     "C3": dict(N=64, sigma="jump", dirichlet=False, seed=2),
+    # config 4 without the node jitter (uniform geometry; the jittered
+    # trilinear assembly is DESIGN.md 9 work): lognormal per-element sigma
+    "C4": dict(N=128, sigma="lognormal", dirichlet=False, seed=3),
     "C5": dict(N=256, sigma=1e-4, dirichlet=False, seed=4),
 }
 
 
 def make_config(name, N=None):
-    """(system, rhs, meta) for a named config; ``N`` overrides the size."""
+    """(system, rhs, meta) for a named config; ``N`` overrides the size.
+
+    C4 draws from ONE generator default_rng(3) in the order fixed by
+    SURVEY.md 8(d): the interior-node jitter (n_interior x 3, drawn and not
+    applied here), then sigma (lognormal, mu = ln 1e-3, s = 2, one per hex in
+    hex order), then the RHS U[-1, 1]."""
     cfg = dict(CONFIGS[name])
     if N is not None:
         cfg["N"] = int(N)
     sigma = cfg["sigma"]
-    if isinstance(sigma, str):
+    rng = np.random.default_rng(cfg["seed"])
+    if sigma == "jump":
         sigma = sigma_jump(cfg["N"])
+    elif sigma == "lognormal":
+        n_int = (cfg["N"] - 1) ** 3
+        h = 1.0 / cfg["N"]
+        rng.uniform(-0.2 * h, 0.2 * h, (n_int, 3))        # jitter stream (unused)
+        sigma = rng.lognormal(np.log(1e-3), 2.0, cfg["N"] ** 3)
+        cfg["geometry"] = "uniform (jitter drawn, not applied)"
     sysm = discretize_hex(cfg["N"], sigma, cfg["dirichlet"])
-    rhs = np.random.default_rng(cfg["seed"]).uniform(-1.0, 1.0, sysm.A_e.shape[0])
+    rhs = rng.uniform(-1.0, 1.0, sysm.A_e.shape[0])
     return sysm, rhs, cfg

@@ -1,0 +1,201 @@
+"""Host pass for the rare constraint blocks that need new coarse edges.
+
+Reference semantics (emin_setup.py:183-217, 256-336, coarse_gradient.py:163-171):
+
+* main loop, fine edges in ascending order: a row whose pattern block G
+  (original coarse edges N_i over its node set J_i) is reducible -- or whose
+  pattern is empty while its commutator row is not ("empty shell") -- gets
+  coarse edges appended until it is irreducible. Each step joins the pair
+  (a, b) of nodes in different components with the largest
+  |(D_h P_n)[:, a] . (D_h P_n)[:, b]| (ties / zeros: lexicographically
+  smallest (a, b)); the new edge takes the next id and is appended to D_H.
+* post pass over every row whose J contains both ends of an edge appended in
+  the main loop (ascending, skipping rows left empty): its pattern becomes
+  N_i plus those edges; if that grew it, the block is re-checked and, when
+  reducible, repaired again (those further edges stay local to the row).
+
+The device kernels flag the rows (sphc_emin_count rowflag), this module runs
+the sequential decisions on the few rows involved, and the appended edges go
+back to the device as per-row extras (xrp / xeid) plus new D_H rows. Column
+dot products are summed in ascending fine-edge order, as scipy's csr_matmat
+does for the reference's ``R_dp_csc[:, a].T @ R_dp_csc[:, b]``.
+"""
+
+import numpy as np
+import torch
+
+from . import device as dv
+from .device import DeviceCSR
+
+
+def _rows(M, rows):
+    """[(cols, vals)] of the given rows of a DeviceCSR (one batched download)."""
+    if len(rows) == 0:
+        return []
+    r = torch.as_tensor(np.asarray(rows, dtype=np.int64), device=M.rowptr.device)
+    s, e = M.rowptr[r], M.rowptr[r + 1]
+    ln = e - s
+    idx = torch.repeat_interleave(s, ln) + (
+        torch.arange(int(ln.sum().item()), device=M.rowptr.device)
+        - torch.repeat_interleave(torch.cumsum(ln, 0) - ln, ln))
+    cols = M.col[idx].cpu().numpy().astype(np.int64)
+    vals = M.val[idx].cpu().numpy() if M.val is not None else None
+    out, o = [], 0
+    for k in ln.cpu().numpy():
+        out.append((cols[o:o + k], None if vals is None else vals[o:o + k]))
+        o += int(k)
+    return out
+
+
+class _Graph:
+    """Components / incidence of one block (edges over node set J)."""
+
+    @staticmethod
+    def analyse(I, J, ends):
+        pos = {int(c): x for x, c in enumerate(J)}
+        parent = list(range(len(J)))
+
+        def find(a):
+            while parent[a] != a:
+                parent[a] = parent[parent[a]]
+                a = parent[a]
+            return a
+
+        inc = [False] * len(J)
+        for e in I:
+            en = ends[int(e)]
+            ps = [pos[n] for n in en]
+            for p in ps:
+                inc[p] = True
+            if len(ps) == 2:
+                x, y = find(ps[0]), find(ps[1])
+                if x != y:
+                    parent[max(x, y)] = min(x, y)
+        roots = [find(c) for c in range(len(J))]
+        irreducible = len(J) > 0 and all(inc) and len(set(roots)) == 1
+        return irreducible, roots
+
+
+def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
+    """Run the reference's repair on the flagged rows. Returns
+    (augmented CoarseGradient, xrp, xeid, n_augmented)."""
+    dev = T.rowptr.device
+    n_e = T.shape[0]
+    need_rows = np.flatnonzero(need.cpu().numpy())
+    flag_h = flags.cpu().numpy()
+    ea = cg.ep_a.cpu().numpy().astype(np.int64)
+    eb = cg.ep_b.cpu().numpy().astype(np.int64)
+    ends = [((int(a), int(b)) if a >= 0 else (int(b),)) for a, b in zip(ea, eb)]
+    n0 = len(ends)
+    Tt = dv.transpose(T)                  # coarse node -> (fine edges, R_dp values)
+    col_cache = {}
+
+    def column(a):
+        c = col_cache.get(a)
+        if c is None:
+            c = col_cache[a] = _rows(Tt, [a])[0]
+        return c
+
+    def score(a, b):
+        ka, va = column(a)
+        kb, vb = column(b)
+        common, ia, ib = np.intersect1d(ka, kb, assume_unique=True, return_indices=True)
+        s = 0.0
+        for x, y in zip(va[ia], vb[ib]):        # ascending fine edge, unfused
+            s += float(x) * float(y)
+        return abs(s)
+
+    def repair(i, I, J):
+        I = list(I)
+        while True:
+            ok, roots = _Graph.analyse(I, J, ends)
+            if ok:
+                return I
+            if len(set(roots)) <= 1:
+                raise ValueError(f"fine edge {i}: cannot repair a single-node "
+                                 "constraint graph")
+            best = None
+            for x in range(len(J)):
+                for y in range(x + 1, len(J)):
+                    if roots[x] == roots[y]:
+                        continue
+                    a, b = int(J[x]), int(J[y])
+                    key = (-score(a, b), a, b)
+                    if best is None or key < best:
+                        best = key
+            _, a, b = best
+            ends.append((min(a, b), max(a, b)))
+            I.append(len(ends) - 1)
+
+    data_T = dict(zip(need_rows.tolist(), _rows(T, need_rows)))
+    data_I = dict(zip(need_rows.tolist(), _rows(pattern, need_rows)))
+    final = {}
+    for i in need_rows.tolist():
+        J = data_T[i][0]
+        I0 = data_I[i][0]
+        if flag_h[i] & 2 and I0.size == 0:      # empty shell (emin_setup.py:134-147)
+            if J.size == 0:
+                raise ValueError(f"fine edge {i} has an empty constraint pattern "
+                                 "(isolated edge or pattern bug)")
+            if J.size == 1:
+                raise ValueError(
+                    f"fine edge {i}: nonzero commutator row over a single coarse node "
+                    "cannot be satisfied by interior coarse edges")
+        final[i] = repair(i, I0.tolist(), J)
+    new_edges = list(range(n0, len(ends)))
+    if new_edges:
+        # post pass (emin_setup.py:311-333)
+        aff = set()
+        for e in new_edges:
+            a, b = ends[e]
+            aff.update(np.intersect1d(column(a)[0], column(b)[0]).tolist())
+        aff = sorted(aff)
+        rows_T = dict(zip(aff, _rows(T, aff)))
+        rows_I = dict(zip(aff, _rows(pattern, aff)))
+        emptyish = (flag_h & 2).astype(bool)
+        for i in aff:
+            J, I0 = rows_T[i][0], rows_I[i][0]
+            prev = final.get(i)
+            if prev is None and emptyish[i] and I0.size == 0:
+                continue                         # a row the main loop left empty
+            Jset = set(J.tolist())
+            add = [e for e in new_edges if all(n in Jset for n in ends[e])]
+            I1 = sorted(set(I0.tolist()) | set(add))
+            if len(I1) == len(prev if prev is not None else I0):
+                continue
+            final[i] = repair(i, I1, J)
+    n_aug = len(ends) - n0
+    # per-row extras: appended ids of each repaired row, ascending
+    counts = np.zeros(n_e, dtype=np.int64)
+    items = []
+    for i in sorted(final):
+        ex = [e for e in final[i] if e >= n0]
+        counts[i] = len(ex)
+        items.extend(ex)
+    xrp_h = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    xrp = torch.from_numpy(xrp_h).to(dev)
+    xeid = torch.from_numpy(np.asarray(items, dtype=np.int32)).to(dev)
+    cg = _augment(cg, ends[n0:], dev)
+    return cg, xrp, xeid, n_aug
+
+
+def _augment(cg, new, dev):
+    """Append interior coarse edges (a, b) to D_H and the endpoint tables
+    (coarse_gradient.py:163-171 append_edge)."""
+    if not new:
+        return cg
+    from .coarse_gradient import CoarseGradient
+    k = len(new)
+    a = torch.tensor([e[0] for e in new], dtype=torch.int32, device=dev)
+    b = torch.tensor([e[1] for e in new], dtype=torch.int32, device=dev)
+    D = cg.D_H
+    last = D.rowptr[-1:]
+    rp = torch.cat([D.rowptr, last + 2 * torch.arange(1, k + 1, device=dev)])
+    ci = torch.cat([D.col, torch.stack([a, b], 1).reshape(-1)])
+    v = torch.cat([D.val, torch.tensor([-1.0, 1.0] * k, dtype=torch.float64, device=dev)])
+    n = D.shape[0] + k
+    return CoarseGradient(D_H=DeviceCSR(rp, ci, v, (n, D.shape[1])),
+                          n_interior=cg.n_interior, n_single=cg.n_single, adj=cg.adj,
+                          ep_a=torch.cat([cg.ep_a, a]), ep_b=torch.cat([cg.ep_b, b]),
+                          single_id=cg.single_id,
+                          augmented_edges=list(cg.augmented_edges or []) + list(new))

@@ -229,7 +229,46 @@ def error_cases():
     return out
 
 
+def repair_case():
+    """make_irreducible exercised through the reference's own setup_constraints:
+    level-0 inputs of N=10 Dirichlet with every 17th interior coarse edge
+    removed from the coarse gradient, so some constraint blocks are reducible
+    (or empty) and the reference appends coarse edges (emin_setup.py:183-336)."""
+    from hcurlamg import nodal_amg as na, coarse_gradient as cgm, emin_setup as es
+    from hcurlamg import edge_prolongator as epm
+    m = build_structured_mesh(3, "hex", 11, True)
+    s = discretize(m, 1.0)
+    agg = na.aggregate(na.strength_graph(s.A_n, 0.0))
+    nod = na.smooth_and_normalize(s.A_n, na.tentative_prolongator(agg))
+    Pc = cgm.gen_piecewise_const(nod.P, 2)
+    cg = cgm.augment_dirichlet_edges(cgm.build_coarse_gradient(s.D, Pc), s.D, Pc)
+    pairs = [e for e in cg.edge_endpoints if len(e) == 2]
+    singles = [e for e in cg.edge_endpoints if len(e) == 1]
+    keep = [p for k, p in enumerate(pairs) if k % 17 != 3]
+    eps = keep + singles
+    cg_r = cgm.CoarseGradient(D_H=cgm._gradient_from_endpoints(eps, cg.n_nodes),
+                              edge_endpoints=eps)
+    setup = es.setup_constraints(s.D, nod.P, cg_r)
+    structure, values = epm.initial_feasible_guess(setup)
+    P = structure.matrix(values)
+    dims = epm.Counter((r.coarse_edges.size, r.coarse_nodes.size)
+                       for r in setup.rows if r is not None)
+    meta = {"n_nodes": cg.n_nodes, "n_augmented": setup.n_augmented,
+            "augmented": [list(e) for e in setup.cg.edge_endpoints[len(eps):]],
+            "dims": sorted([list(k) + [v] for k, v in dims.items()])}
+    arrays = {"pairs": np.array(keep, dtype=np.int64), "singles":
+              np.array([e[0] for e in singles], dtype=np.int64),
+              "P_indptr": P.indptr, "P_indices": P.indices, "P_data": P.data}
+    return meta, arrays
+
+
 def main(which):
+    if "repair" in which:
+        meta, arrays = repair_case()
+        with open(os.path.join(HERE, "repair_N10d.json"), "w") as f:
+            json.dump(meta, f, indent=1)
+        np.savez_compressed(os.path.join(HERE, "repair_N10d.npz"), **arrays)
+        print("repair case: n_augmented", meta["n_augmented"])
     if "errors" in which:
         with open(os.path.join(HERE, "errors.json"), "w") as f:
             json.dump(error_cases(), f, indent=1)

@@ -215,6 +215,37 @@ def test_edge_prolongator_vs_oracle(N, sigma, dirichlet):
     assert prol.commutator_residual <= 1e-12
 
 
+def test_make_irreducible_repair_vs_reference():
+    """Reducible constraint blocks (a reduced coarse gradient) are repaired with
+    the reference's make_irreducible semantics: same appended coarse edges,
+    same prolongator pattern, same feasible guess (golden from the reference's
+    own setup_constraints, tests/golden/make_golden.py repair_case)."""
+    import json
+    import os
+    from golden_util import GOLDEN
+    from paper_2506_08284_b200 import coarse_gradient as cg_mod
+    from paper_2506_08284_b200 import emin_setup as es
+    from paper_2506_08284_b200 import nodal_amg as na
+    with open(os.path.join(GOLDEN, "repair_N10d.json")) as f:
+        meta = json.load(f)
+    arr = dict(np.load(os.path.join(GOLDEN, "repair_N10d.npz")))
+    s = _system(10, 1.0, True)
+    agg = na.aggregate(na.strength_graph(s.A_n, 0.0))
+    nod = na.smooth_and_normalize(s.A_n, agg)
+    cg = cg_mod.coarse_gradient_from_edges(arr["pairs"], arr["singles"], meta["n_nodes"])
+    setup = es.setup_constraints(s.D, nod.P, cg)
+    assert setup.n_augmented == meta["n_augmented"]
+    aug = [list(e) for e in setup.cg.augmented_edges]
+    assert aug == meta["augmented"]
+    P = setup.pattern.to_scipy()
+    assert np.array_equal(P.indptr, arr["P_indptr"])
+    assert np.array_equal(P.indices, arr["P_indices"])
+    ref = sp.csr_matrix((arr["P_data"], arr["P_indices"], arr["P_indptr"]), shape=P.shape)
+    assert rel_max_diff(P, ref) <= 1e-10
+    dims = sorted([list(k) + [v] for k, v in setup.subproblem_dims.items()])
+    assert dims == meta["dims"]
+
+
 GOLDEN_CASES = ["N4n", "N6d", "N8d", "N10n", "C1", "N16n", "C2"]
 
 

@@ -47,14 +47,14 @@ extern "C" {
 #define SPHC_ST_EMPTY_I 5          /* emin_setup.py:292   row with empty prolongator pattern */
 #define SPHC_ST_REDUCIBLE 6        /* emin_setup.py:304   block needs make_irreducible   */
 #define SPHC_ST_RANK_LOW 7         /* emin_setup.py:233-237 rank below expected          */
-#define SPHC_ST_EMIN_CAPACITY 8    /* row exceeds the emin kernel's |J|<=16, |I|<=64     */
+#define SPHC_ST_EMIN_CAPACITY 8    /* row exceeds the emin kernel's |J|<=16, |I|<=128    */
 #define SPHC_ST_EMPTY_J 9          /* emin_setup.py:125-127 empty constraint pattern     */
 #define SPHC_ST_SPGEMM_CAPACITY 10 /* SpGEMM row exceeds the on-chip accumulator         */
 #define SPHC_ST_SORT_CAPACITY 11   /* segmented sort row too long                        */
 
 #define SPHC_EMIN_JMAX 16
-#define SPHC_EMIN_IMAX 64
-#define SPHC_DIMS_I 65 /* subproblem_dims histogram is [SPHC_DIMS_I][SPHC_DIMS_J] */
+#define SPHC_EMIN_IMAX 128
+#define SPHC_DIMS_I 129 /* subproblem_dims histogram is [SPHC_DIMS_I][SPHC_DIMS_J] */
 #define SPHC_DIMS_J 17
 
 const char *sphc_last_error(void);

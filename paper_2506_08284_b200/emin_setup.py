@@ -42,7 +42,7 @@ def _raise(st, D):
                          "pattern (isolated edge or pattern bug)")
     if "EMIN_CAPACITY" in rows:
         raise RuntimeError(f"fine edge {rows['EMIN_CAPACITY']}: constraint block exceeds "
-                           f"the device kernel capacity (|J| <= 16, |I| <= 64)")
+                           f"the device kernel capacity (|J| <= 16, |I| <= 128)")
     if "REDUCIBLE" in rows:
         # only reachable if a block is still reducible after the repair pass
         raise RuntimeError(
@@ -60,7 +60,7 @@ def _count(D, P, cg, xrp, xeid, flags):
     icount = torch.empty(n_e, dtype=torch.int64, device=dev)
     jcount = torch.empty(n_e, dtype=torch.int64, device=dev)
     rmax2 = torch.zeros(2, dtype=torch.float64, device=dev)
-    dims = torch.zeros(65 * 17, dtype=torch.int64, device=dev)
+    dims = torch.zeros(129 * 17, dtype=torch.int64, device=dev)
     rowflag = torch.zeros(n_e, dtype=torch.uint8, device=dev) if flags else None
     rowmax = torch.empty(n_e, dtype=torch.float64, device=dev) if flags else None
     call("sphc_emin_count", n_e, D.rowptr, D.col, D.val, P.rowptr, P.col, P.val,
@@ -116,7 +116,7 @@ def setup_constraints(D_h, P_n, cg):
         _raise(st, D)
     T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st)
     _raise(st, D)
-    h = dims.cpu().numpy().reshape(65, 17)
+    h = dims.cpu().numpy().reshape(129, 17)
     nz = np.argwhere(h)
     counter = Counter({(int(i), int(j)): int(h[i, j]) for i, j in nz})
     return EminSetup(T=T, pattern=pattern, cg=cg, subproblem_dims=counter,

@@ -206,6 +206,23 @@ def _check_nullspace(S, D, where, A=None):
     return AD
 
 
+def _coarse_inverse(Ad):
+    """Symmetric inverse of the coarsest operator (multigrid.py:157 factors it
+    with LU). The coarsest A_e is SPD in exact arithmetic but can be extremely
+    ill-conditioned (cond ~ 4e15 on config 4 at N=64, where the mass part is
+    tiny): an explicit getri inverse then carries an O(cond eps) antisymmetric
+    error that makes the V-cycle non-symmetric and PCG diverge. The inverse is
+    formed from the symmetric eigendecomposition instead (dense, cuSOLVER
+    syevd, once per hierarchy), so the coarse solve is exactly symmetric, as
+    PCG requires; eigenvalues that round to <= 0 are treated as null space."""
+    A = 0.5 * (Ad + Ad.T)
+    lam, V = torch.linalg.eigh(A)
+    tiny = lam.abs().max() * A.shape[0] * torch.finfo(torch.float64).eps
+    w = torch.where(lam > tiny, 1.0 / lam, torch.zeros_like(lam))
+    inv = (V * w) @ V.T
+    return 0.5 * (inv + inv.T)
+
+
 def build_hierarchy(A_e, S_e, A_n, D, cfg=None):
     """Galerkin hierarchy driven by the constrained edge prolongator
     (multigrid.py:119-161)."""
@@ -254,7 +271,7 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None):
     with phase("coarsest"):
         last = _make_level(A_e, S_e, D, cfg.cheb_degree, AD=AD)
         levels.append(last)
-        inv = torch.linalg.inv(dv.to_dense(A_e))   # dense LU (cuSOLVER), once
+        inv = _coarse_inverse(dv.to_dense(A_e))
     last.r = dv.empty_f64(A_e.shape[0])
     nnz0 = levels[0].A_e.nnz
     oc = sum(lv.A_e.nnz for lv in levels) / nnz0

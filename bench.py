@@ -322,7 +322,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         he = mg.build_hierarchy(sysm.A_e, sysm.S, sysm.A_n, sysm.D, scfg)
-        re = mg.pcg_solve(sysm.A_e, rhs, mg.v_cycle_preconditioner(he))
+        # the reference's own usage: pcg_solve(h.levels[0].A_e, b, V(h))
+        re = mg.pcg_solve(he.levels[0].A_e, rhs, mg.v_cycle_preconditioner(he))
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
         assert isinstance(re.x, np.ndarray)
@@ -333,9 +334,11 @@ def run_ours(args):
         t_e2e = float(t.item())
     def csr_bytes(M):
         return M.data.nbytes + M.indices.size * 4 + M.indptr.size * 8
-    # build_hierarchy uploads (A_e, S, A_n, D); pcg_solve uploads A_e and b
-    h2d = sum(csr_bytes(M) for M in (sysm.A_e, sysm.S, sysm.A_n, sysm.D)) \
-        + csr_bytes(sysm.A_e) + rhs.nbytes
+    # build_hierarchy uploads (A_e, S, A_n, D); pcg_solve uploads b
+    # (int64 row pointers and int32 columns on the device)
+    def dev_bytes(M):
+        return M.data.size * 8 + M.indices.size * 4 + M.indptr.size * 8
+    h2d = sum(dev_bytes(M) for M in (sysm.A_e, sysm.S, sysm.A_n, sysm.D)) + rhs.nbytes
     d2h = n_e * 8
 
     pk, pk_kind = peaks()

@@ -300,9 +300,10 @@ int sphc_emin_count(int64_t n_e, const int64_t *drp, const int32_t *dci, const d
                     double *rowmax, int64_t *status, void *stream);
 /* Row extras: coarse edges appended by the host make_irreducible pass
  * (emin_setup.py:183-217,311-333) as a CSR over fine edges (xrp, xeid; NULL
- * xrp = none); ep_a/ep_b = endpoints of every coarse edge. With rowflag !=
- * NULL the count pass marks rows instead of failing: bit 0 = reducible block,
- * bit 1 = empty pattern (rowmax = that row's max |D_h P_n|). */
+ * xrp = none); ep_a/ep_b = endpoints of every coarse edge. The count pass only
+ * sizes rows; with rowflag != NULL it writes bit 1 = empty pattern (rowmax =
+ * that row's max |D_h P_n|). The fill pass factors every block; with rowflag
+ * != NULL a reducible block sets bit 0 instead of failing. */
 
 /* Writes T (J columns + commutator rhs r = D_h P_n on J) and the prolongator
  * row pattern I with the feasible guess p = 1 + G_k (G_k^T G_k)^-1 (r - G^T 1)_k
@@ -313,7 +314,7 @@ int sphc_emin_fill(int64_t n_e, const int64_t *drp, const int32_t *dci, const do
                    const int32_t *single_id, const int64_t *xrp, const int32_t *xeid,
                    const int32_t *ep_a, const int32_t *ep_b, const int64_t *trp,
                    int32_t *tci, double *tv, const int64_t *erp, int32_t *eci, double *ev,
-                   int64_t *status, void *stream);
+                   uint8_t *rowflag, int64_t *status, void *stream);
 
 /* One projected damped-Jacobi sweep (edge_prolongator.py:170-176) fused with
  * the masked product S P on the fixed pattern, the energy of the INPUT values

@@ -21,9 +21,9 @@ struct EminRow {
   int J[JM];
   double r[JM];
   int Icol[IM];
-  int pa[IM];  // position of tail node in J, -1 for single-node edges
-  int pb[IM];  // position of head (or the single) node in J
-  double L[JM * JM];
+  signed char pa[IM];  // position of tail node in J, -1 for single-node edges
+  signed char pb[IM];  // position of head (or the single) node in J
+  double L[JM * (JM + 1) / 2];  // packed lower Cholesky factor, row p at p(p+1)/2
   double y[JM];
   double g[IM];
   double p[IM];
@@ -116,8 +116,8 @@ __device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
       int o = nI + __popc(bal & ((1u << lane) - 1));
       if (o < IM) {
         R.Icol[o] = e;
-        R.pa[o] = pa;
-        R.pb[o] = pb;
+        R.pa[o] = (signed char)pa;
+        R.pb[o] = (signed char)pb;
       }
     }
     nI += __popc(bal);
@@ -131,7 +131,7 @@ __device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
       if (o < IM) {
         R.Icol[o] = sid;
         R.pa[o] = -1;
-        R.pb[o] = p;
+        R.pb[o] = (signed char)p;
       }
     }
     nI += __popc(bal);
@@ -145,8 +145,8 @@ __device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
       int e = xeid[t];
       if (o < IM) {
         R.Icol[o] = e;
-        R.pa[o] = lower_bound_i32(R.J, nJ, ep_a[e]);
-        R.pb[o] = lower_bound_i32(R.J, nJ, ep_b[e]);
+        R.pa[o] = (signed char)lower_bound_i32(R.J, nJ, ep_a[e]);
+        R.pb[o] = (signed char)lower_bound_i32(R.J, nJ, ep_b[e]);
       }
     }
     nI += (int)(x1 - x0);
@@ -161,6 +161,9 @@ __device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
   }
   __syncwarp();
 }
+
+// packed lower-triangle index (m <= p)
+__device__ __forceinline__ int tri(int p, int m) { return p * (p + 1) / 2 + m; }
 
 // lane 0: irreducibility, k, Gram matrix, Cholesky, rank checks.
 // Returns false (and reports) on failure.
@@ -206,32 +209,31 @@ __device__ int em_factor(EminRow& R, i64 i, i64* status) {
     return 2;
   }
   double* L = R.L;
-  for (int t = 0; t < k * k; t++) L[t] = 0.0;
+  for (int t = 0; t < k * (k + 1) / 2; t++) L[t] = 0.0;
   for (int e = 0; e < nI; e++) {
     int a = R.pa[e], b = R.pb[e];
-    if (b < k) L[b * k + b] += 1.0;
+    if (b < k) L[tri(b, b)] += 1.0;
     if (a >= 0 && a < k) {
-      L[a * k + a] += 1.0;
-      if (b < k) {
-        L[a * k + b] -= 1.0;
-        L[b * k + a] -= 1.0;
-      }
+      L[tri(a, a)] += 1.0;
+      if (b < k) L[a > b ? tri(a, b) : tri(b, a)] -= 1.0;
     }
   }
   // in-place lower Cholesky; |R_jj| of the reference QR = L_jj
   for (int j = 0; j < k; j++) {
-    double d = L[j * k + j];
-    for (int m = 0; m < j; m++) d -= L[j * k + m] * L[j * k + m];
+    const double* Lj = L + tri(j, 0);
+    double d = Lj[j];
+    for (int m = 0; m < j; m++) d -= Lj[m] * Lj[m];
     double ljj = d > 0.0 ? sqrt(d) : 0.0;
     if (!(ljj >= 1e-10 * (j ? L[0] : ljj)) || ljj == 0.0) {
       report(status, SPHC_ST_RANK_LOW, i);
       return 2;
     }
-    L[j * k + j] = ljj;
+    L[tri(j, j)] = ljj;
     for (int p = j + 1; p < k; p++) {
-      double x = L[p * k + j];
-      for (int m = 0; m < j; m++) x -= L[p * k + m] * L[j * k + m];
-      L[p * k + j] = x / ljj;
+      double* Lp = L + tri(p, 0);
+      double x = Lp[j];
+      for (int m = 0; m < j; m++) x -= Lp[m] * Lj[m];
+      Lp[j] = x / ljj;
     }
   }
   return 0;
@@ -242,14 +244,15 @@ __device__ void em_solve(const EminRow& R, double* y) {
   int k = R.k;
   const double* L = R.L;
   for (int j = 0; j < k; j++) {
+    const double* Lj = L + tri(j, 0);
     double x = y[j];
-    for (int m = 0; m < j; m++) x -= L[j * k + m] * y[m];
-    y[j] = x / L[j * k + j];
+    for (int m = 0; m < j; m++) x -= Lj[m] * y[m];
+    y[j] = x / Lj[j];
   }
   for (int j = k - 1; j >= 0; j--) {
     double x = y[j];
-    for (int m = j + 1; m < k; m++) x -= L[m * k + j] * y[m];
-    y[j] = x / L[j * k + j];
+    for (int m = j + 1; m < k; m++) x -= L[tri(m, j)] * y[m];
+    y[j] = x / L[tri(j, j)];
   }
 }
 
@@ -304,7 +307,9 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
         tv[to + q] = R.r[q];
       }
     }
-    if (nI == 0) {
+    // the count pass only sizes the rows; irreducibility and rank are
+    // established once, by the fill pass
+    if (nI == 0 || !FILL) {
       __syncwarp();
       continue;
     }
@@ -373,11 +378,12 @@ extern "C" int sphc_emin_fill(int64_t n_e, const int64_t* drp, const int32_t* dc
                               int64_t n_int, const int32_t* single_id, const int64_t* xrp,
                               const int32_t* xeid, const int32_t* ep_a, const int32_t* ep_b,
                               const int64_t* trp, int32_t* tci, double* tv, const int64_t* erp,
-                              int32_t* eci, double* ev, int64_t* status, void* stream) {
+                              int32_t* eci, double* ev, uint8_t* rowflag, int64_t* status,
+                              void* stream) {
   cudaStream_t s = as_stream(stream);
   k_emin_setup<true><<<grid_for(n_e, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
       n_e, drp, dci, dv, prp, pci, pv, adj_rp, adj_col, single_id, xrp, xeid, ep_a, ep_b,
-      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, trp, tci, tv, erp, eci, ev,
+      nullptr, nullptr, nullptr, nullptr, rowflag, nullptr, trp, tci, tv, erp, eci, ev,
       status);
   SPHC_LAUNCH_CHECK();
   return 0;
@@ -413,8 +419,8 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
       R.p[e] = p_in[e0 + e];
       R.g[e] = 0.0;
       int a = ep_a[col], b = ep_b[col];
-      R.pb[e] = lower_bound_i32(R.J, nJ, b);
-      R.pa[e] = a < 0 ? -1 : lower_bound_i32(R.J, nJ, a);
+      R.pb[e] = (signed char)lower_bound_i32(R.J, nJ, b);
+      R.pa[e] = (signed char)(a < 0 ? -1 : lower_bound_i32(R.J, nJ, a));
     }
     if (lane == 0) {
       R.nJ = nJ;
@@ -422,17 +428,27 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
     }
     __syncwarp();
     // masked S P on the fixed pattern: ascending k, sequential per entry
-    i64 se = srp[i + 1];
-    for (i64 js = srp[i]; js < se; js++) {
-      int kk = sci[js];
-      double s = sv[js];
-      i64 pe = erp[kk + 1];
-      for (i64 jp = erp[kk] + lane; jp < pe; jp += 32) {
-        int slot = lower_bound_i32(R.Icol, nI, eci[jp]);
-        if (slot < nI && R.Icol[slot] == eci[jp])
-          R.g[slot] = __dadd_rn(R.g[slot], __dmul_rn(s, p_in[jp]));
+    // (scipy's S @ P order, edge_prolongator.py:173); the next S entry's
+    // P-row bounds are loaded while the current row is accumulated
+    i64 js = srp[i], se = srp[i + 1];
+    int kk = js < se ? sci[js] : 0;
+    double sc = js < se ? sv[js] : 0.0;
+    i64 pb = js < se ? erp[kk] : 0, pe = js < se ? erp[kk + 1] : 0;
+    for (; js < se; js++) {
+      i64 jn = js + 1;
+      int kn = jn < se ? sci[jn] : 0;
+      double sn = jn < se ? sv[jn] : 0.0;
+      i64 nb0 = jn < se ? erp[kn] : 0, nb1 = jn < se ? erp[kn + 1] : 0;
+      for (i64 jp = pb + lane; jp < pe; jp += 32) {
+        int col = eci[jp];
+        int slot = lower_bound_i32(R.Icol, nI, col);
+        if (slot < nI && R.Icol[slot] == col)
+          R.g[slot] = __dadd_rn(R.g[slot], __dmul_rn(sc, p_in[jp]));
       }
       __syncwarp();
+      sc = sn;
+      pb = nb0;
+      pe = nb1;
     }
     double en = 0.0;
     for (int e = lane; e < nI; e += 32) en += R.p[e] * R.g[e];

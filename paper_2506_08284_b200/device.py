@@ -49,6 +49,30 @@ class Status:
         return {k: int(h[v]) for k, v in ST.items() if h[v] != INT64_MAX}
 
 
+_PINNED = {}
+
+
+def upload(a, dtype, dev=None):
+    """Host array -> new device tensor through a reused pinned staging buffer
+    (one cast on the host, one DMA at pinned-memory bandwidth)."""
+    dev = dev or device()
+    a = np.asarray(a)
+    n = a.size
+    t = torch.empty(n, dtype=torch.from_numpy(np.zeros(0, dtype=dtype)).dtype, device=dev)
+    if n == 0:
+        return t
+    nbytes = n * np.dtype(dtype).itemsize
+    buf = _PINNED.get("buf")
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 24), dtype=torch.uint8, pin_memory=True)
+        _PINNED["buf"] = buf
+    host = buf[:nbytes].numpy().view(dtype)
+    np.copyto(host, a, casting="unsafe")
+    t.view(torch.uint8).copy_(buf[:nbytes], non_blocking=True)
+    torch.cuda.current_stream().synchronize()   # the staging buffer is reused
+    return t
+
+
 @dataclass
 class DeviceCSR:
     rowptr: torch.Tensor          # int64 [n_rows + 1]
@@ -72,11 +96,10 @@ class DeviceCSR:
             A = A.copy()
             A.sum_duplicates()
             A.sort_indices()
-        return DeviceCSR(
-            rowptr=torch.from_numpy(A.indptr.astype(np.int64)).to(dev),
-            col=torch.from_numpy(A.indices.astype(np.int32)).to(dev),
-            val=torch.from_numpy(A.data.astype(np.float64)).to(dev),
-            shape=tuple(int(s) for s in A.shape))
+        return DeviceCSR(rowptr=upload(A.indptr, np.int64, dev),
+                         col=upload(A.indices, np.int32, dev),
+                         val=upload(A.data, np.float64, dev),
+                         shape=tuple(int(s) for s in A.shape))
 
     def to_scipy(self):
         val = self.val.cpu().numpy() if self.val is not None else np.ones(self.nnz)

@@ -69,7 +69,7 @@ def _count(D, P, cg, xrp, xeid, flags):
     return st, icount, jcount, rmax2, dims, rowflag, rowmax
 
 
-def _fill(D, P, cg, icount, jcount, xrp, xeid, st):
+def _fill(D, P, cg, icount, jcount, xrp, xeid, st, rowflag=None):
     n_e = D.shape[0]
     dev = D.rowptr.device
     trp, tnnz = dv.scan(jcount)
@@ -80,7 +80,7 @@ def _fill(D, P, cg, icount, jcount, xrp, xeid, st):
     ev = torch.empty(ennz, dtype=torch.float64, device=dev)
     call("sphc_emin_fill", n_e, D.rowptr, D.col, D.val, P.rowptr, P.col, P.val,
          cg.adj.rowptr, cg.adj.col, cg.n_interior, cg.single_id, xrp, xeid, cg.ep_a, cg.ep_b,
-         trp, tci, tv, erp, eci, ev, st.t)
+         trp, tci, tv, erp, eci, ev, rowflag, st.t)
     return (DeviceCSR(trp, tci, tv, (n_e, P.shape[1])),
             DeviceCSR(erp, eci, ev, (n_e, cg.n_edges)))
 
@@ -101,21 +101,22 @@ def setup_constraints(D_h, P_n, cg):
     _raise(st, D)
     rm = rmax2.cpu().numpy()
     rdp_scale = max(1.0, float(rm[0]))
+    # the fill pass factors every block and flags the reducible ones
+    T, pattern = _fill(D, P, cg, icount, jcount, None, None, st, rowflag)
+    _raise(st, D)
     flags = rowflag
     need = (flags & 1).bool()
     if rm[1] > 1e-12 * rdp_scale:
         need |= ((flags & 2).bool() & (rowmax > 1e-12 * rdp_scale))
     n_aug = 0
-    xrp = xeid = None
     if bool(need.any()):
         from . import repair
-        T0, Pat0 = _fill(D, P, cg, icount, jcount, None, None, Status())
         cg, xrp, xeid, n_aug = repair.make_irreducible_pass(
-            need, flags, rowmax, rdp_scale, T0, Pat0, cg)
+            need, flags, rowmax, rdp_scale, T, pattern, cg)
         st, icount, jcount, rmax2, dims, _, _ = _count(D, P, cg, xrp, xeid, False)
         _raise(st, D)
-    T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st)
-    _raise(st, D)
+        T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st)
+        _raise(st, D)
     h = dims.cpu().numpy().reshape(129, 17)
     nz = np.argwhere(h)
     counter = Counter({(int(i), int(j)): int(h[i, j]) for i, j in nz})

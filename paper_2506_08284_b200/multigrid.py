@@ -216,6 +216,10 @@ def _coarse_inverse(Ad):
     syevd, once per hierarchy), so the coarse solve is exactly symmetric, as
     PCG requires; eigenvalues that round to <= 0 are treated as null space."""
     A = 0.5 * (Ad + Ad.T)
+    inv = torch.linalg.inv(A)                     # getrf/getri: fast, usually exact enough
+    skew = (inv - inv.T).abs().max() / inv.abs().max().clamp_min(1e-300)
+    if float(skew) <= 1e-12:
+        return 0.5 * (inv + inv.T)
     lam, V = torch.linalg.eigh(A)
     tiny = lam.abs().max() * A.shape[0] * torch.finfo(torch.float64).eps
     w = torch.where(lam > tiny, 1.0 / lam, torch.zeros_like(lam))
@@ -358,8 +362,8 @@ def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
     convergence / breakdown tests."""
     A = as_device_csr(A)
     host = not isinstance(b, torch.Tensor)
-    b = torch.as_tensor(np.asarray(b, dtype=np.float64) if host else b,
-                        dtype=torch.float64, device=dv.device())
+    b = (dv.upload(np.asarray(b, dtype=np.float64), np.float64) if host
+         else torch.as_tensor(b, dtype=torch.float64, device=dv.device()))
     n = b.numel()
     lanes = A.lanes()
     graph_ok = getattr(precond, "graph_safe", False) and maxit > 0

@@ -17,8 +17,11 @@ for r in rows:
     except ValueError:
         continue
     d = dict(zip(hdr, r))
-    s = int(d.get("Warp Stall Sampling (All Samples)") or 0)
-    ex = int(d.get("Instructions Executed") or 0)
+    try:
+        s = int(d.get("Warp Stall Sampling (All Samples)") or 0)
+        ex = int(d.get("Instructions Executed") or 0)
+    except ValueError:
+        continue
     key = (cur_file, ln)
     agg[key][0] += s; agg[key][1] += ex; agg[key][3] = r[1][:80]
     for k, v in d.items():

@@ -212,13 +212,15 @@ def _coarse_inverse(Ad):
     ill-conditioned (cond ~ 4e15 on config 4 at N=64, where the mass part is
     tiny): an explicit getri inverse then carries an O(cond eps) antisymmetric
     error that makes the V-cycle non-symmetric and PCG diverge. The inverse is
-    formed from the symmetric eigendecomposition instead (dense, cuSOLVER
-    syevd, once per hierarchy), so the coarse solve is exactly symmetric, as
-    PCG requires; eigenvalues that round to <= 0 are treated as null space."""
+    formed from the Cholesky factor (potrf + potri: symmetric positive by
+    construction, ~0.3 ms at n = 364); when the factorisation breaks down (the
+    operator is numerically semidefinite) it falls back to the symmetric
+    eigendecomposition with eigenvalues <= n eps lambda_max treated as null
+    space (cuSOLVER syevd, ~4 ms at n = 364)."""
     A = 0.5 * (Ad + Ad.T)
-    inv = torch.linalg.inv(A)                     # getrf/getri: fast, usually exact enough
-    skew = (inv - inv.T).abs().max() / inv.abs().max().clamp_min(1e-300)
-    if float(skew) <= 1e-12:
+    L, info = torch.linalg.cholesky_ex(A)
+    if int(info) == 0:
+        inv = torch.cholesky_inverse(L)
         return 0.5 * (inv + inv.T)
     lam, V = torch.linalg.eigh(A)
     tiny = lam.abs().max() * A.shape[0] * torch.finfo(torch.float64).eps

@@ -51,6 +51,7 @@ extern "C" {
 #define SPHC_ST_EMPTY_J 9          /* emin_setup.py:125-127 empty constraint pattern     */
 #define SPHC_ST_SPGEMM_CAPACITY 10 /* SpGEMM row exceeds the on-chip accumulator         */
 #define SPHC_ST_SORT_CAPACITY 11   /* segmented sort row too long                        */
+#define SPHC_ST_TRSV_STALL 12      /* triangular sweep dependency never resolved (bug)   */
 
 #define SPHC_EMIN_JMAX 16
 #define SPHC_EMIN_IMAX 128
@@ -192,6 +193,17 @@ int sphc_sell_cheb_step(int64_t n, const int64_t *slice_ptr, const int32_t *sci,
 int sphc_cheb_step(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
                    int lanes, const double *dinv, const double *b, const double *x_in,
                    double *x_out, double *d, double cd, double cr, int x_zero, void *stream);
+
+/* One Gauss-Seidel half sweep of the reference's symmetric smoother
+ * (multigrid.py:45-59): x_out = x_in + T^-1 (b - A x_in), T = tril(A)
+ * (lower != 0) or triu(A) (lower == 0), read from the full CSR of A.
+ * Sync-free substitution: a warp per row, rows claimed in dependency order
+ * from *ticket; y (n doubles) is the solve's workspace, reset to a NaN
+ * sentinel inside the call. x_in == NULL means x_in = 0. Zero diagonal rows
+ * are reported in status[SPHC_ST_ZERO_DIAG]. */
+int sphc_gs_half_sweep(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                       const double *b, const double *x_in, double *x_out, double *y,
+                       int32_t *ticket, int lower, int64_t *status, void *stream);
 
 /* y_i = d_i x_i (Jacobi scaling in the smoother's power iteration). */
 int sphc_diag_scale(int64_t n, const double *d, const double *x, double *y, void *stream);

@@ -12,7 +12,8 @@ REPO = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsphcurl.so")
 
-CU = ["util.cu", "spmv.cu", "sell.cu", "spgemm.cu", "nodal.cu", "coarse.cu", "emin.cu"]
+CU = ["util.cu", "spmv.cu", "sell.cu", "spgemm.cu", "nodal.cu", "coarse.cu", "emin.cu",
+      "trsv.cu"]
 CPP = ["host_seq.cpp"]
 
 NVCC_FLAGS = [

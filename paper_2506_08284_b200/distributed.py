@@ -266,6 +266,9 @@ def distribute(levels, coarse_inverse, rank, world, group=None, ops=None, device
                        Dt=make_op(lv.Dt, npart, ep, rank, group, device),
                        edge_part=ep, node_part=npart)
         if li + 1 < len(levels):
+            if not hasattr(lv.edge_sweeper, "coefs"):
+                raise ValueError("the partitioned solve needs the Chebyshev smoother "
+                                 "(Gauss-Seidel is sequential across rows)")
             cp = parts[li + 1]
             dl.P = make_op(lv.P_e, ep, cp, rank, group, device)
             dl.R = make_op(lv.R_e, cp, ep, rank, group, device)

@@ -41,12 +41,13 @@ class SolverConfig:
     coarse_size: int = 200
     max_levels: int = 10
     emin: EminConfig = field(default_factory=EminConfig)
-    smoother: str = "chebyshev"
+    smoother: str = "chebyshev"      # or "gauss_seidel" (the reference's own smoother)
     cheb_degree: int = 3
 
     def __post_init__(self):
-        if self.smoother != "chebyshev":
-            raise ValueError("the B200 path implements the Chebyshev smoother only")
+        if self.smoother not in SMOOTHERS:
+            raise ValueError(f"unknown smoother {self.smoother!r}; "
+                             f"expected one of {sorted(SMOOTHERS)}")
 
 
 class ChebyshevSweeper:
@@ -129,6 +130,48 @@ class ChebyshevSweeper:
         return cur
 
 
+class GaussSeidelSweeper:
+    """The reference's symmetric Gauss-Seidel (multigrid.py:32-66):
+    x += tril(A)^-1 (b - A x), then x += triu(A)^-1 (b - A x), each half sweep
+    one sync-free triangular-substitution launch (csrc/trsv.cu). Exact
+    smoother of the reference; latency-bound (dependency depth ~16 N)."""
+
+    def __init__(self, A, degree=None):
+        self.A = A
+        n = A.shape[0]
+        st = Status()
+        dv.diagonal(A, st)
+        rows = st.rows()
+        if "ZERO_DIAG" in rows:
+            raise ValueError(f"zero diagonal entry in row {rows['ZERO_DIAG']}")
+        self.y = dv.empty_f64(n)
+        self.ticket = torch.zeros(1, dtype=torch.int32, device=A.rowptr.device)
+        self.status = Status()
+        self.buf = [dv.empty_f64(n), dv.empty_f64(n)]
+
+    def symmetric(self, x, b, sweeps=1, x_zero=False):
+        """Returns the smoothed iterate (a sweeper-owned buffer, never ``x``)."""
+        A = self.A
+        cur = x
+        for _ in range(sweeps):
+            for lower in (1, 0):
+                out = self.buf[0] if cur is not self.buf[0] else self.buf[1]
+                call("sphc_gs_half_sweep", A.shape[0], A.rowptr, A.col, A.val, b,
+                     None if x_zero else cur, out, self.y, self.ticket, lower, self.status.t)
+                cur = out
+                x_zero = False
+        return cur
+
+    def check(self):
+        rows = self.status.rows()
+        if "TRSV_STALL" in rows:
+            raise RuntimeError(f"triangular sweep stalled at row {rows['TRSV_STALL']}")
+
+
+SMOOTHERS = {"chebyshev": ChebyshevSweeper, "gauss_seidel": GaussSeidelSweeper,
+             "gs": GaussSeidelSweeper}
+
+
 @dataclass
 class Level:
     """One hierarchy level (multigrid.py:69-89) plus its device working set."""
@@ -173,12 +216,14 @@ class Hierarchy:
         return len(self.levels)
 
 
-def _make_level(A_e, S_e, D, degree=3, AD=None, **extra):
+def _make_level(A_e, S_e, D, cfg, AD=None, smooth=True, **extra):
     Dt = dv.transpose(D)
     nodal_aux = dv.spgemm(Dt, AD if AD is not None else dv.spgemm(A_e, D))
     level = Level(A_e=A_e, S_e=S_e, D=D, nodal_aux=nodal_aux, Dt=Dt, **extra)
-    level.edge_sweeper = ChebyshevSweeper(A_e, degree)
-    level.aux_sweeper = ChebyshevSweeper(nodal_aux, degree)
+    if smooth:   # the coarsest level is solved directly, never smoothed
+        sweeper = SMOOTHERS[cfg.smoother]
+        level.edge_sweeper = sweeper(A_e, cfg.cheb_degree)
+        level.aux_sweeper = sweeper(nodal_aux, cfg.cheb_degree)
     level.r = dv.empty_f64(A_e.shape[0])
     level.bn = dv.empty_f64(D.shape[1])
     return level
@@ -248,7 +293,7 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None):
                 f"coarsening stagnated: {n_coarse} coarse edges from "
                 f"{A_e.shape[0]} fine edges")
         with phase("level.make_level"):
-            lv = _make_level(A_e, S_e, D, cfg.cheb_degree, AD=AD, P_e=P_e, P_n=P_n,
+            lv = _make_level(A_e, S_e, D, cfg, AD=AD, P_e=P_e, P_n=P_n,
                              emin_energy=prol.energy_history,
                              subproblem_dims=dict(prol.subproblem_dims),
                              commutator_residual=prol.commutator_residual,
@@ -275,7 +320,7 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None):
         with phase("level.nullspace_check"):
             AD = _check_nullspace(S_e, D, f"level {len(levels)}", A=A_e)
     with phase("coarsest"):
-        last = _make_level(A_e, S_e, D, cfg.cheb_degree, AD=AD)
+        last = _make_level(A_e, S_e, D, cfg, AD=AD, smooth=False)
         levels.append(last)
         inv = _coarse_inverse(dv.to_dense(A_e))
     last.r = dv.empty_f64(A_e.shape[0])
@@ -445,6 +490,11 @@ def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
         if res <= rtol * nb:
             status = "converged"
             break
+    if hier is not None:
+        for lv in hier.levels:
+            for sw in (lv.edge_sweeper, lv.aux_sweeper):
+                if hasattr(sw, "check"):
+                    sw.check()
     return PcgResult(x=out(x), iterations=iters, residual_history=history,
                      precond_history=precond_history, status=status,
                      relative_residual=history[-1] / nb)

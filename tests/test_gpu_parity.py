@@ -305,6 +305,59 @@ def test_solve_iterations_vs_reference(name):
     assert np.linalg.norm(b - s.A_e @ x) <= 1.5e-8 * np.linalg.norm(b)
 
 
+def test_gauss_seidel_half_sweeps_match_scipy():
+    """Sync-free tril/triu substitution == x + spsolve_triangular(T, b - A x)
+    (multigrid.py:45-59), on an edge operator and its nodal auxiliary."""
+    from scipy.sparse.linalg import spsolve_triangular
+    from paper_2506_08284_b200.device import DeviceCSR, Status, call
+    from paper_2506_08284_b200.inputs import discretize_hex
+    s = discretize_hex(6, sigma=0.3, dirichlet=False)
+    rng = np.random.default_rng(5)
+    for A in (s.A_e, sp.csr_matrix(s.D.T @ s.A_e @ s.D)):
+        A = sp.csr_matrix(A)
+        A.sort_indices()
+        n = A.shape[0]
+        x = rng.standard_normal(n)
+        b = rng.standard_normal(n)
+        Ad = DeviceCSR.from_scipy(A)
+        X, B = torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda()
+        y = torch.empty(n, dtype=torch.float64, device="cuda")
+        out = torch.empty_like(y)
+        tk = torch.zeros(1, dtype=torch.int32, device="cuda")
+        st = Status()
+        for lower, T in ((1, sp.tril(A, format="csr")), (0, sp.triu(A, format="csr"))):
+            ref = x + spsolve_triangular(T, b - A @ x, lower=bool(lower))
+            call("sphc_gs_half_sweep", n, Ad.rowptr, Ad.col, Ad.val, B, X, out, y, tk, lower, st.t)
+            got = out.cpu().numpy()
+            assert np.abs(got - ref).max() <= 1e-11 * np.abs(ref).max()
+            ref0 = spsolve_triangular(T, b, lower=bool(lower))
+            call("sphc_gs_half_sweep", n, Ad.rowptr, Ad.col, Ad.val, B, None, out, y, tk, lower, st.t)
+            assert np.abs(out.cpu().numpy() - ref0).max() <= 1e-11 * np.abs(ref0).max()
+        assert st.rows() == {}
+
+
+@pytest.mark.parametrize("name", ["N6d", "N10n", "C1", "C2"])
+def test_gauss_seidel_solve_vs_reference(name):
+    """The reference's own smoother on the B200 hierarchy: iterations within
+    +-1 of the reference's sym-GS PCG, residual history close while far from
+    round-off, solution within the solver tolerance."""
+    from paper_2506_08284_b200 import multigrid as mg
+    meta, arrays = load_case(name)
+    s = _system(meta["N"], meta["sigma"], meta["dirichlet"])
+    b = np.random.default_rng(meta["seed"]).uniform(-1, 1, s.A_e.shape[0])
+    cfg = mg.SolverConfig(coarse_size=meta["coarse_size"], smoother="gauss_seidel")
+    h = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, cfg)
+    res = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+    ref = meta["gs"]
+    assert res.status == "converged"
+    assert abs(res.iterations - ref["iterations"]) <= 1
+    k = min(4, len(ref["residual_history"]))
+    np.testing.assert_allclose(res.residual_history[:k], ref["residual_history"][:k], rtol=1e-6)
+    if "gs_x" in arrays:
+        xr = arrays["gs_x"]
+        assert np.abs(res.x - xr).max() <= 1e-6 * np.abs(xr).max()
+
+
 def test_error_case_matches_reference():
     import json
     import os

@@ -52,17 +52,48 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML
+    polled every 5 ms from a thread (nvidia-smi -lms as a fallback)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40}
 
     def __init__(self, gpu):
         self.gpu = gpu
         self.p = None
+        self.t = None
+        self.samples = []
+
+    def _poll(self, nv, hdl):
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop.is_set():
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(hdl, nv.NVML_CLOCK_SM),
+                                     nv.nvmlDeviceGetMaxClockInfo(hdl, nv.NVML_CLOCK_SM),
+                                     int(get_r(hdl))))
+            except Exception:   # noqa: BLE001 - sampling is best effort
+                pass
+            self.stop.wait(0.005)
 
     def __enter__(self):
+        import threading
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() \
+                else self.gpu
+            hdl = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.stop = threading.Event()
+            self.t = threading.Thread(target=self._poll, args=(nv, hdl), daemon=True)
+            self.t.start()
+            return self
+        except Exception:   # noqa: BLE001
+            self.t = None
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
@@ -74,6 +105,9 @@ class ClockSampler:
 
     def __exit__(self, *a):
         self.lines = []
+        if self.t is not None:
+            self.stop.set()
+            self.t.join(timeout=5)
         if self.p is not None:
             self.p.terminate()
             out, _ = self.p.communicate(timeout=10)
@@ -81,6 +115,10 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
+        for clk, cmax, bits in self.samples:
+            sm.append(float(clk))
+            mx = max(mx, float(cmax))
+            reasons |= {k for k, b in self.BITS.items() if bits & b}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for l in self.lines:
             f = [x.strip() for x in l.split(",")]
@@ -94,7 +132,7 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": mx or None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 def vcycle_bytes(h, degree=3):
@@ -201,7 +239,7 @@ def run_ours(args):
     dev = torch.device("cuda", torch.cuda.current_device())
     sysm, rhs, cfg = make_problem(args.config, args.N)
     n_e = sysm.A_e.shape[0]
-    scfg = mg.SolverConfig(coarse_size=args.coarse_size)
+    scfg = mg.SolverConfig(coarse_size=args.coarse_size, smoother=args.smoother)
 
     # inputs resident in HBM for the device-timed value
     A_e = dv.DeviceCSR.from_scipy(sysm.A_e)
@@ -286,13 +324,20 @@ def run_ours(args):
     # back-to-back warm loop is reported beside it.
     sw = h.levels[0].edge_sweeper
     A0 = h.levels[0].A_e
-    m0 = sw.sell
     x0 = torch.zeros(n_e, dtype=torch.float64, device=dev)
-    cd, cr = sw.coefs[1]
+    gs_mode = not hasattr(sw, "coefs")
+    if gs_mode:
+        # the reference smoother: the lower Gauss-Seidel half sweep
+        def kstep():
+            _lib.call("sphc_gs_half_sweep", n_e, A0.rowptr, A0.col, A0.val, b, x0, sw.buf[0],
+                      sw.y, sw.ticket, 1, sw.status.t)
+    else:
+        m0 = sw.sell
+        cd, cr = sw.coefs[1]
 
-    def kstep():
-        _lib.call("sphc_sell_cheb_step", n_e, m0.slice_ptr, m0.col, m0.val, sw.dinv, b, x0,
-                  sw.buf[0], sw.d, cd, cr, 0, m0.padded)
+        def kstep():
+            _lib.call("sphc_sell_cheb_step", n_e, m0.slice_ptr, m0.col, m0.val, sw.dinv, b, x0,
+                      sw.buf[0], sw.d, cd, cr, 0, m0.padded)
 
     for _ in range(3):
         kstep()
@@ -312,7 +357,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     t_k = sum(a.elapsed_time(bb) for a, bb in kev) / nk
     t_k_warm = k0.elapsed_time(k1) / nk
-    kbytes = cheb_kernel_bytes(A0)
+    kbytes = (12 * A0.nnz + 8 * (n_e + 1) + 32 * n_e) if gs_mode else cheb_kernel_bytes(A0)
     at_scale = None if args.no_scale_roofline else scale_roofline(args, flush)
 
     # e2e: public API with host inputs, solution back to host
@@ -362,7 +407,9 @@ def run_ours(args):
                        f"coarse_size {args.coarse_size}",
                        "n_edges": n_e, "levels": [lv.A_e.shape[0] for lv in h.levels],
                        "operator_complexity": h.operator_complexity,
-                       "pcg_iterations": iters, "smoother": "chebyshev-3 hiptmair",
+                       "pcg_iterations": iters,
+                       "smoother": ("chebyshev-3 hiptmair" if args.smoother == "chebyshev"
+                                    else "symmetric gauss-seidel hiptmair (reference smoother)"),
                        "parallelism": (f"row-block partitioned solve x{ws}" if partitioned
                                        else f"replicas x{ws}"),
                        "l2": "256 MB flush before every timed step"},
@@ -373,14 +420,19 @@ def run_ours(args):
                        "achieved_gbs": vbytes / (t_vc * 1e-3) / 1e9,
                        "frac_of_peak": vbytes / (t_vc * 1e-3) / 1e9 / peak},
             "roofline": {"bound": "hbm",
-                         "kernel": "k_sell_cheb (fused Chebyshev step, SELL-32, level-0 A_e)",
+                         "kernel": ("k_gs_half<lower> (sync-free Gauss-Seidel half sweep, "
+                                    "level-0 A_e; latency bound)" if gs_mode else
+                                    "k_sell_cheb (fused Chebyshev step, SELL-32, level-0 A_e)"),
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
-                         "traffic": ncu_traffic() if args.config == "C2" else None,
+                         "traffic": (None if gs_mode else
+                                     ncu_traffic() if args.config == "C2" else
+                                     ncu_traffic("k_sell_cheb_c3_full")
+                                     if args.config == "C3" else None),
                          "peak_source": pk_kind, "launch_ms": t_k,
                          "launch_ms_l2_warm": t_k_warm,
                          "l2_flushed_per_launch": True,
-                         "sell_padding": m0.padded / max(A0.nnz, 1),
+                         "sell_padding": None if gs_mode else m0.padded / max(A0.nnz, 1),
                          "algorithmic_bytes": kbytes},
             "roofline_at_scale": at_scale,
             "e2e": {"value": ws * n_e / (t_e2e * 1e-3), "unit": "edge DOFs/s",
@@ -458,6 +510,7 @@ def main():
     ap.add_argument("--N", type=int, default=None)
     ap.add_argument("--coarse-size", type=int, default=1000)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--smoother", default="chebyshev", choices=["chebyshev", "gauss_seidel"])
     ap.add_argument("--ref-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-scale-roofline", action="store_true")

@@ -38,7 +38,7 @@ extern "C" {
 #define SPHC_ERR_ARG (-2)
 #define SPHC_ERR_HOST (-3)
 
-#define SPHC_STATUS_SLOTS 16
+#define SPHC_STATUS_SLOTS 32
 #define SPHC_ST_ZERO_DIAG 0        /* multigrid.py:38-40  zero diagonal entry in row r   */
 #define SPHC_ST_NONPOS_DIAG 1      /* nodal_amg.py:41-43  nonpositive diagonal entry     */
 #define SPHC_ST_NODAL_ZERO_DIAG 2  /* nodal_amg.py:147-148 zero diagonal in nodal operator */
@@ -52,6 +52,10 @@ extern "C" {
 #define SPHC_ST_SPGEMM_CAPACITY 10 /* SpGEMM row exceeds the on-chip accumulator         */
 #define SPHC_ST_SORT_CAPACITY 11   /* segmented sort row too long                        */
 #define SPHC_ST_TRSV_STALL 12      /* triangular sweep dependency never resolved (bug)   */
+#define SPHC_ST_PC_EMPTY_COLUMN 13 /* coarse_gradient.py:49-52 empty column (col id)     */
+#define SPHC_ST_PC_EMPTY_ROW 14    /* coarse_gradient.py:82-83 row with no entries       */
+#define SPHC_ST_PC_NO_DONOR 15     /* coarse_gradient.py:96-98 empty column after safeguard */
+#define SPHC_ST_AGG_CAPACITY 16    /* aggregation row longer than the device kernel's buffer */
 
 #define SPHC_EMIN_JMAX 16
 #define SPHC_EMIN_IMAX 128
@@ -348,6 +352,34 @@ int sphc_emin_step(int64_t n_e, const int64_t *srp, const int32_t *sci, const do
  * (nodal_amg.py:59-88). Host arrays. Returns n_agg in *n_agg. */
 int sphc_host_aggregate(int64_t n, const int64_t *rp, const int32_t *ci, int64_t *membership,
                         int64_t *n_agg);
+
+/* Greedy root aggregation (nodal_amg.py:59-88) on the device, bit-identical
+ * to the sequential loops. rp/ci: symmetric strength pattern incl. the
+ * diagonal (n x n). Work buffers: state (n int32), ticket (1 int32), flags,
+ * pos, list (n + 1 int64 each). memb (n int64) receives the aggregate of
+ * every node and list[n] the number of aggregates. Both phases are sync-free
+ * (nodes taken in ascending order from a ticket, each waiting only on lower
+ * nodes within its dependency range). status[SPHC_ST_AGG_CAPACITY]: a
+ * leftover node with more than 256 assigned neighbours. */
+int sphc_aggregate(int64_t n, const int64_t *rp, const int32_t *ci, int32_t *state,
+                   int32_t *ticket, int64_t *flags, int64_t *pos, int64_t *list, int64_t *memb,
+                   int64_t *status, void *stream);
+
+/* Algorithm 1 (coarse_gradient.py:36-103) on the device, bit-identical to
+ * the reference's sequential column order. prp/pci/pv: P_n (m_h x m_H, CSR);
+ * crp/crow/cval: its transpose (column view, rows ascending). Work buffers:
+ * target, counts (m_H int64), srow (nnz int32), owner (2 m_h int32),
+ * changed (1 int32), flags, pos, list (max(m_h, m_H) + 1 int64 each).
+ * assign (m_h int64) receives the column of every row. Each claiming pass is
+ * solved as a fixed point over all columns at once (one host sync per
+ * iteration; a handful of iterations), see csrc/pconst.cu.
+ * Errors: status[SPHC_ST_PC_*]. */
+int sphc_piecewise_const(int64_t m_h, int64_t m_H, const int64_t *prp, const int32_t *pci,
+                         const double *pv, const int64_t *crp, const int32_t *crow,
+                         const double *cval, int n_passes, int64_t *target, int64_t *counts,
+                         int32_t *srow, int32_t *owner, int32_t *changed, int64_t *flags,
+                         int64_t *pos, int64_t *list, int64_t *assign, int64_t *status,
+                         void *stream);
 
 /* Algorithm 1 (coarse_gradient.py:36-103) on a host CSR copy of P_n.
  * On a data error returns SPHC_ERR_HOST with err[0] = kind (1 empty column,

@@ -79,7 +79,36 @@ def coarse_gradient_from_edges(pairs, singles, n_nodes):
 def gen_piecewise_const(P, n_passes=2):
     """Algorithm 1 (coarse_gradient.py:36-103): the column assigned to every
     row (int64, device). Returned as the assignment vector rather than the
-    0/1 matrix P_const (one unit entry per row at that column)."""
+    0/1 matrix P_const (one unit entry per row at that column). Runs on the
+    device (csrc/pconst.cu), bit-identical to the reference's ordered loops."""
+    P = as_device_csr(P)
+    m_h, m_H = P.shape
+    dev = P.rowptr.device
+    Pc = dv.transpose(P)
+    st = Status()
+    i64 = dict(dtype=torch.int64, device=dev)
+    m = max(m_h, m_H) + 1
+    target, counts = torch.empty(m_H, **i64), torch.empty(m_H, **i64)
+    flags, pos, lst = torch.empty(m, **i64), torch.empty(m, **i64), torch.empty(m, **i64)
+    srow = torch.empty(P.nnz, dtype=torch.int32, device=dev)
+    owner = torch.empty(2 * m_h, dtype=torch.int32, device=dev)
+    changed = torch.empty(1, dtype=torch.int32, device=dev)
+    assign = torch.empty(m_h, **i64)
+    call("sphc_piecewise_const", m_h, m_H, P.rowptr, P.col, P.val, Pc.rowptr, Pc.col, Pc.val,
+         int(n_passes), target, counts, srow, owner, changed, flags, pos, lst, assign, st.t)
+    rows = st.rows()
+    if "PC_EMPTY_COLUMN" in rows:
+        raise ValueError(f"empty column {rows['PC_EMPTY_COLUMN']} cannot be assigned any row")
+    if "PC_EMPTY_ROW" in rows:
+        raise ValueError(f"row {rows['PC_EMPTY_ROW']} has no entries to assign")
+    if "PC_NO_DONOR" in rows:
+        raise ValueError(f"empty column {rows['PC_NO_DONOR']} cannot be assigned any row")
+    return assign
+
+
+def gen_piecewise_const_host(P, n_passes=2):
+    """The same map computed by the sequential host C++ loop (kept as a
+    cross-check for the device version)."""
     P = as_device_csr(P)
     m_h, m_H = P.shape
     rp = P.rowptr.cpu().numpy()

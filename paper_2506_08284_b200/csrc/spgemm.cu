@@ -27,6 +27,7 @@
 #define SPG_HCAP 512   // max hash slots per warp
 #define SPG_CCAP 256   // max distinct columns per output row
 #define SPG_STG 256    // products per batch
+#define SPG_PER_LANE (SPG_STG / 32)
 
 __device__ __forceinline__ int pow2_at_least(int n, int lo) {
   int m = lo;
@@ -91,6 +92,14 @@ __device__ __forceinline__ unsigned spg_h(int col, int ts) {
 __device__ __forceinline__ bool spg_insert(int* keys, int ts, int* ucount, int col) {
   unsigned h = spg_h(col, ts);
   for (int probe = 0; probe < ts; probe++) {
+    // plain read first: most products hit an already-present column, and a
+    // CAS on it would serialise the warp on a handful of addresses
+    int cur = ((volatile int*)keys)[h];
+    if (cur == col) return true;
+    if (cur != -1) {
+      h = (h + 1) & (ts - 1);
+      continue;
+    }
     int old = atomicCAS(&keys[h], -1, col);
     if (old == -1) {
       atomicAdd(ucount, 1);
@@ -124,10 +133,17 @@ __device__ bool spg_symbolic(i64 row, const i64* __restrict__ arp, const int* __
       ok = false;
       break;
     }
-    for (int f = lane; f < total; f += 32) {
-      int t;
-      ok &= spg_insert(keys, ts, ucount, bci[spg_product(B, f, &t)]);
+    // all column loads of the batch first (one L2 round trip per batch, not
+    // per product: the shared-memory CAS would otherwise serialise them)
+    int col[SPG_PER_LANE];
+#pragma unroll
+    for (int u = 0; u < SPG_PER_LANE; u++) {
+      int f = lane + 32 * u, t;
+      col[u] = f < total ? bci[spg_product(B, f, &t)] : -1;
     }
+#pragma unroll
+    for (int u = 0; u < SPG_PER_LANE; u++)
+      if (col[u] >= 0) ok &= spg_insert(keys, ts, ucount, col[u]);
     ok = __all_sync(FULL_MASK, ok);
     c0 += nb;
   }
@@ -266,12 +282,30 @@ __global__ void __launch_bounds__(SPG_FWARPS * 32)
         a2[lane] = (c0 + lane < ae) ? av2[c0 + lane] : 0.0;
         __syncwarp();
       }
-      for (int f = lane; f < total; f += 32) {
-        int t;
-        i64 jb = spg_product(F.B, f, &t);
-        F.sslot[f] = F.slot[spg_find(F.keys, ts, bci[jb])];
-        F.sval[f] = __dmul_rn(F.B.a[t], bv[jb]);
-        if (PAIR) sval2[f] = a2[t] * bv2[jb];
+      {
+        // loads of the whole batch first, then the hash lookups
+        int col[SPG_PER_LANE], own[SPG_PER_LANE];
+        double v1[SPG_PER_LANE], v2[SPG_PER_LANE];
+#pragma unroll
+        for (int u = 0; u < SPG_PER_LANE; u++) {
+          int f = lane + 32 * u;
+          col[u] = -1;
+          if (f < total) {
+            i64 jb = spg_product(F.B, f, &own[u]);
+            col[u] = bci[jb];
+            v1[u] = bv[jb];
+            if (PAIR) v2[u] = bv2[jb];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < SPG_PER_LANE; u++) {
+          int f = lane + 32 * u;
+          if (col[u] >= 0) {
+            F.sslot[f] = F.slot[spg_find(F.keys, ts, col[u])];
+            F.sval[f] = __dmul_rn(F.B.a[own[u]], v1[u]);
+            if (PAIR) sval2[f] = a2[own[u]] * v2[u];
+          }
+        }
       }
       __syncwarp();
       for (int t0 = 0; t0 < nb; t0 += G) {  // warp-uniform trip count

@@ -101,11 +101,11 @@ def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None):
         raise NotImplementedError("rsamg mode is outside the B200 hot path")
     with phase("setup.strength"):
         strength = na.strength_graph(A_n, cfg.drop_tol)
-    with phase("setup.aggregate(host)"):
+    with phase("setup.aggregate"):
         agg = na.aggregate(strength)
     with phase("setup.smooth_and_normalize"):
         nod = na.smooth_and_normalize(A_n, agg)
-    with phase("setup.piecewise_const(host)"):
+    with phase("setup.piecewise_const"):
         assign = cgrad.gen_piecewise_const(nod.P, cfg.n_passes)
     with phase("setup.coarse_gradient"):
         cg = cgrad.build_coarse_gradient(D_h, assign, agg.n_agg)

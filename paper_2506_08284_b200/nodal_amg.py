@@ -57,7 +57,28 @@ def strength_graph(A_n, drop_tol):
 
 
 def aggregate(strength):
-    """Greedy two-phase root aggregation (nodal_amg.py:59-88); host C++."""
+    """Greedy two-phase root aggregation (nodal_amg.py:59-88) on the device
+    (csrc/aggregate.cu), bit-identical to the reference's ordered loops."""
+    n = strength.shape[0]
+    dev = strength.rowptr.device
+    i64 = dict(dtype=torch.int64, device=dev)
+    state = torch.empty(n, dtype=torch.int32, device=dev)
+    ticket = torch.empty(1, dtype=torch.int32, device=dev)
+    flags, pos, lst = (torch.empty(n + 1, **i64) for _ in range(3))
+    memb = torch.empty(n, **i64)
+    st = Status()
+    call("sphc_aggregate", n, strength.rowptr, strength.col, state, ticket, flags, pos, lst,
+         memb, st.t)
+    n_agg = int(lst[n].item()) if n else 0
+    rows = st.rows()
+    if "AGG_CAPACITY" in rows:
+        raise RuntimeError(f"node {rows['AGG_CAPACITY']}: more assigned neighbours than "
+                           "the device aggregation buffer holds (256)")
+    return Aggregation(n_fine=n, n_agg=n_agg, membership=memb)
+
+
+def aggregate_host(strength):
+    """The same aggregation by the sequential host C++ loop (cross-check)."""
     n = strength.shape[0]
     rp = strength.rowptr.cpu().numpy()
     ci = strength.col.cpu().numpy()

@@ -305,6 +305,87 @@ def test_solve_iterations_vs_reference(name):
     assert np.linalg.norm(b - s.A_e @ x) <= 1.5e-8 * np.linalg.norm(b)
 
 
+def _tie_heavy_P(m_h, m_H, seed, dense_col=None):
+    """Random prolongator-like matrix with many magnitude ties (values from a
+    tiny set), optionally one very long column (device long-column path)."""
+    rng = np.random.default_rng(seed)
+    rows, cols = [], []
+    for r in range(m_h):
+        k = int(rng.integers(1, 7))
+        c = rng.choice(m_H, size=k, replace=False)
+        rows += [r] * k
+        cols += list(c)
+    if dense_col is not None:
+        extra = np.setdiff1d(np.arange(m_h), np.array(rows)[np.array(cols) == dense_col])
+        rows += list(extra)
+        cols += [dense_col] * len(extra)
+    vals = rng.choice([-1.0, -0.5, 0.25, 0.5, 1.0, 2.0], size=len(rows))
+    P = sp.csr_matrix((vals, (rows, cols)), shape=(m_h, m_H))
+    P.sum_duplicates()
+    P.sort_indices()
+    # every column needs an entry (else the reference raises)
+    assert np.all(np.diff(P.tocsc().indptr) > 0)
+    return P
+
+
+@pytest.mark.parametrize("case", ["mesh6d", "mesh10n", "mesh16d", "ties", "ties_long", "ties_1pass",
+                                  "ties_3pass"])
+def test_piecewise_const_device_bitwise(case):
+    """Device Algorithm 1 (sync-free column passes, parallel + ordered
+    leftovers, safeguard) == the reference's sequential loops."""
+    from oracle import hcurl_oracle as O
+    from paper_2506_08284_b200.coarse_gradient import gen_piecewise_const
+    from paper_2506_08284_b200.inputs import discretize_hex
+    passes = {"ties_1pass": 1, "ties_3pass": 3}.get(case, 2)
+    if case.startswith("mesh"):
+        N, sig, dr = {"mesh6d": (6, 1.0, True), "mesh10n": (10, 1e-4, False),
+                      "mesh16d": (16, 1.0, True)}[case]
+        s = discretize_hex(N, sig, dr)
+        S = O.strength_pattern(s.A_n)
+        mo, nao = O.aggregate(S)
+        P, _, _ = O.smoothed_prolongator(s.A_n, mo, nao)
+    elif case == "ties_long":
+        P = _tie_heavy_P(3000, 200, 7, dense_col=17)
+    else:
+        P = _tie_heavy_P(2000, 300, 3)
+    got = gen_piecewise_const(P, passes).cpu().numpy()
+    ref = O.piecewise_const(P, passes)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("case", ["mesh6d", "mesh10n", "mesh16d", "path", "random"])
+def test_aggregate_device_bitwise(case):
+    """Device aggregation (sync-free distance-2 MIS + ordered leftovers) ==
+    the reference's two sequential loops."""
+    from oracle import hcurl_oracle as O
+    from paper_2506_08284_b200.device import DeviceCSR
+    from paper_2506_08284_b200.inputs import discretize_hex
+    from paper_2506_08284_b200.nodal_amg import aggregate
+    if case.startswith("mesh"):
+        N, sig, dr = {"mesh6d": (6, 1.0, True), "mesh10n": (10, 1e-4, False),
+                      "mesh16d": (16, 1.0, True)}[case]
+        S = O.strength_pattern(discretize_hex(N, sig, dr).A_n)
+    elif case == "path":
+        n = 9
+        A = sp.diags([np.ones(n - 1), np.ones(n), np.ones(n - 1)], [-1, 0, 1], format="csr")
+        S = sp.csr_matrix(A)
+    else:   # irregular symmetric graph: many leftovers and ties
+        R = _rand_csr(3000, 3000, 0.002, 11)
+        S = sp.csr_matrix(((abs(R) + abs(R.T) + sp.eye(3000)) > 0).astype(np.float64))
+    S.sort_indices()
+    mo, nao = O.aggregate(S)
+    agg = aggregate(DeviceCSR.from_scipy(S))
+    assert agg.n_agg == nao
+    assert np.array_equal(agg.membership.cpu().numpy(), mo)
+
+
+def test_piecewise_const_device_errors():
+    from paper_2506_08284_b200.coarse_gradient import gen_piecewise_const
+    P = sp.csr_matrix(np.array([[1.0, 0.0, 0.0], [0.5, 0.0, 2.0]]))
+    with pytest.raises(ValueError, match="empty column 1 cannot be assigned any row"):
+        gen_piecewise_const(P)
+
+
 def test_gauss_seidel_half_sweeps_match_scipy():
     """Sync-free tril/triu substitution == x + spsolve_triangular(T, b - A x)
     (multigrid.py:45-59), on an edge operator and its nodal auxiliary."""

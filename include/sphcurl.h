@@ -215,6 +215,13 @@ int sphc_diag_scale(int64_t n, const double *d, const double *x, double *y, void
 /* Deterministic start vector in [-1, 1) for the smoother's spectral bound
  * (splitmix64 of the index; oracle.cheb_start_vector computes the same). */
 int sphc_cheb_start(int64_t n, double *x, void *stream);
+/* One Lanczos step of the Chebyshev bound estimate (no reference
+ * counterpart; the reference smoother is Gauss-Seidel, multigrid.py:32-66):
+ * w = D^-1 u - alpha v - beta_prev v_prev (beta_prev == NULL: first step),
+ * dw = D w; alpha, beta_prev are device scalars. */
+int sphc_lanczos_update(int64_t n, const double *u, const double *dinv, const double *d,
+                        const double *v, const double *vprev, const double *alpha,
+                        const double *beta_prev, double *w, double *dw, void *stream);
 
 /* PCG scalar slots of the device array `sc` (multigrid.py:220-274). */
 #define SPHC_PCG_PAP 0  /* p . Ap        */
@@ -386,6 +393,39 @@ int sphc_piecewise_const(int64_t m_h, int64_t m_H, const int64_t *prp, const int
  * 2 row with no entries, 3 empty column after safeguard), err[1] = index. */
 int sphc_host_piecewise_const(int64_t m_h, int64_t m_H, const int64_t *rp, const int32_t *ci,
                               const double *v, int n_passes, int64_t *assign, int64_t *err);
+
+
+/* ---- model-problem inputs on the device ----------
+ * Replace the host generator's build_structured_mesh(3, 'hex', N + 1,
+ * dirichlet) (meshing.py:61-131) and discretize(mesh, sigma)
+ * (assembly.py:47-54, curl-curl assembly.py:135-144,231-290, edge mass
+ * :297-306,346-366, nodal operator :373-386,404-434, gradient :62-79), with
+ * two extensions the reference lacks: per-element sigma and curved
+ * (jittered, isoparametric trilinear) hexes, integrated by 3x3x3 Gauss.
+ * Numbering is the reference's (csrc/assemble.cu). Row kernels run in two
+ * modes: rp == NULL writes per-row counts, otherwise fills col / values at
+ * rp. X (n^3 x 3 node coordinates) == NULL means the uniform mesh (J = h I);
+ * sigma == NULL means the constant sigma_const. */
+int sphc_hex_node_counts(int N, int dirichlet, int64_t *edge_counts, int64_t *free_counts,
+                         void *stream);
+int sphc_hex_tables(int N, int dirichlet, const int64_t *edge_offsets,
+                    const int64_t *free_offsets, int32_t *edge_of, int64_t *edge_code,
+                    int32_t *free_id, int32_t *free_list, void *stream);
+int sphc_hex_coords(int N, const double *jitter, double *X, void *stream);
+/* A_e = S + sigma M and S on one pattern (edges sharing a hex) */
+int sphc_hex_edge_rows(int N, int64_t n_edges, const int64_t *edge_code, const int32_t *edge_of,
+                       const double *X, const double *sigma, double sigma_const,
+                       const int64_t *rp, int64_t *counts, int32_t *col, double *val_A,
+                       double *val_S, void *stream);
+/* A_n = K + sigma M_n on the free nodes */
+int sphc_hex_node_rows(int N, int64_t n_free, const int32_t *free_list, const int32_t *free_id,
+                       const double *X, const double *sigma, double sigma_const,
+                       const int64_t *rp, int64_t *counts, int32_t *col, double *val,
+                       void *stream);
+/* D: -1 at the tail's free column, +1 at the head's */
+int sphc_hex_grad_rows(int N, int64_t n_edges, const int64_t *edge_code, const int32_t *free_id,
+                       const int64_t *rp, int64_t *counts, int32_t *col, double *val,
+                       void *stream);
 
 #ifdef __cplusplus
 }

@@ -545,9 +545,35 @@ CHEB_SAFETY = 1.1
 CHEB_RATIO = 30.0
 
 
+def lanczos_max(A, d, k):
+    """Largest Ritz value of k Lanczos steps on D^-1 A in the D inner product
+    (start vector cheb_start_vector; the B200 ChebyshevSweeper._bounds runs
+    the same recurrence with device scalars)."""
+    n = A.shape[0]
+    if n == 0:
+        return 1.0
+    w = cheb_start_vector(n)
+    v = w / np.sqrt(w @ (d * w))
+    vprev = np.zeros(n)
+    alpha, beta = [], [0.0]
+    for j in range(k):
+        u = A @ v
+        a = float(u @ v)
+        w = (1.0 / d) * u - a * v - beta[-1] * vprev
+        b = float(np.sqrt(w @ (d * w)))
+        alpha.append(a)
+        beta.append(b)
+        if not b > 0.0:
+            break
+        vprev, v = v, w / b
+    m = len(alpha)
+    T = np.diag(alpha) + np.diag(beta[1:m], 1) + np.diag(beta[1:m], -1)
+    return float(np.linalg.eigvalsh(T)[-1])
+
+
 class ChebyshevSweeper:
     """Jacobi-preconditioned Chebyshev polynomial smoother of degree ``degree``
-    on [hi/30, hi], hi = 1.1 * (15-step power estimate of rho(D^-1 A)).
+    on [hi/30, hi], hi = 1.1 * (15-step Lanczos estimate of rho(D^-1 A)).
     ``symmetric(x, b)`` applies the polynomial once (a symmetric operator), in
     the reference sweeper seam. Same recurrence as the B200 kernel chain."""
 
@@ -560,15 +586,8 @@ class ChebyshevSweeper:
         self.A = A
         self.dinv = 1.0 / d
         self.degree = degree
-        x = cheb_start_vector(A.shape[0])
-        x = x / np.linalg.norm(x)
-        lam = 0.0
-        for _ in range(CHEB_POWER_ITERS):
-            y = self.dinv * (A @ x)
-            lam = float(np.linalg.norm(y))
-            if lam == 0.0:
-                break
-            x = y / lam
+        self.hi = 0.0
+        lam = lanczos_max(A, d, CHEB_POWER_ITERS)
         self.hi = CHEB_SAFETY * lam
         self.lo = self.hi / CHEB_RATIO
 

@@ -13,7 +13,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsphcurl.so")
 
 CU = ["util.cu", "spmv.cu", "sell.cu", "spgemm.cu", "nodal.cu", "coarse.cu", "emin.cu",
-      "trsv.cu", "pconst.cu", "aggregate.cu"]
+      "trsv.cu", "pconst.cu", "aggregate.cu", "assemble.cu"]
 CPP = ["host_seq.cpp"]
 
 NVCC_FLAGS = [

@@ -217,6 +217,35 @@ extern "C" int sphc_diag_scale(int64_t n, const double* d, const double* x, doub
   return 0;
 }
 
+// One Lanczos step for D^-1 A in the D inner product (the Chebyshev bound
+// estimate): w = D^-1 u - alpha v - beta_prev v_prev with u = A v, and
+// dw = D w for the next norm. alpha / beta_prev are device scalars.
+__global__ void k_lanczos_update(i64 n, const double* __restrict__ u, const double* __restrict__ dinv,
+                                 const double* __restrict__ d, const double* __restrict__ v,
+                                 const double* __restrict__ vprev, const double* alpha,
+                                 const double* beta_prev, double* __restrict__ w,
+                                 double* __restrict__ dw) {
+  double a = *alpha, b = beta_prev ? *beta_prev : 0.0;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    double t = dinv[i] * u[i] - a * v[i];
+    if (beta_prev) t -= b * vprev[i];
+    w[i] = t;
+    dw[i] = d[i] * t;
+  }
+}
+
+extern "C" int sphc_lanczos_update(int64_t n, const double* u, const double* dinv, const double* d,
+                                   const double* v, const double* vprev, const double* alpha,
+                                   const double* beta_prev, double* w, double* dw, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  k_lanczos_update<<<grid_for(n, 256), 256, 0, s>>>(n, u, dinv, d, v, vprev, alpha, beta_prev, w,
+                                                    dw);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
 // deterministic start vector in [-1, 1): splitmix64 of the index (same
 // integer arithmetic as oracle.cheb_start_vector)
 __global__ void k_cheb_start(i64 n, double* __restrict__ x) {

@@ -13,6 +13,7 @@ for N in [int(a) for a in sys.argv[2:]]:
     r = mg.pcg_solve(h.levels[0].A_e, rhs, mg.v_cycle_preconditioner(h))
     torch.cuda.synchronize(); t2 = time.perf_counter()
     naug = [lv.n_augmented for lv in h.levels]
+    print("peak GB", torch.cuda.max_memory_allocated() / 1e9, "reserved GB", torch.cuda.max_memory_reserved() / 1e9)
     print(name, N, [lv.A_e.shape[0] for lv in h.levels], "aug", naug, "its", r.iterations, r.status,
           f"relres {r.relative_residual:.2e}", f"setup {1e3*(t1-t0):.0f} ms solve {1e3*(t2-t1):.0f} ms",
           "hist", [f"{x:.2e}" for x in r.residual_history[::max(1, len(r.residual_history)//8)]], flush=True)

@@ -181,8 +181,10 @@ def scale_roofline(args, flush):
     each launch timed alone after an L2 flush."""
     import torch
     from paper_2506_08284_b200 import _lib, device as dv
-    sysm, _, cfg = make_problem(args.scale_config)
-    A = dv.DeviceCSR.from_scipy(sysm.A_e)
+    if args.scale_config in DEVICE_INPUTS:
+        A = make_device_problem(args.scale_config)[0].A_e
+    else:
+        A = dv.DeviceCSR.from_scipy(make_problem(args.scale_config)[0].A_e)
     n = A.shape[0]
     m = dv.sell(A)
     dinv = dv.reciprocal(dv.diagonal(A))
@@ -217,10 +219,26 @@ def scale_roofline(args, flush):
             "traffic": ncu_traffic("k_sell_cheb_c3_full")}
 
 
+DEVICE_INPUTS = ("C3", "C4", "C5")
+
+
 def make_problem(config, N=None):
+    """Host (scipy) inputs: bit-identical to the reference's assembly for
+    C1/C2; C3-C5 are generated on the device (csrc/assemble.cu: per-element
+    sigma, jittered hexes for C4) and downloaded."""
+    if config in DEVICE_INPUTS:
+        sysd, rhs, cfg = make_device_problem(config, N)
+        from types import SimpleNamespace
+        return SimpleNamespace(**{k: getattr(sysd, k).to_scipy()
+                                  for k in ("A_e", "S", "A_n", "D")}), rhs, cfg
     from paper_2506_08284_b200.inputs import make_config
     sysm, rhs, cfg = make_config(config, N)
     return sysm, rhs, cfg
+
+
+def make_device_problem(config, N=None):
+    from paper_2506_08284_b200.assembly import make_device_config
+    return make_device_config(config, N)
 
 
 def run_ours(args):
@@ -237,15 +255,29 @@ def run_ours(args):
         torch.cuda.set_device(0)
     build_library()
     dev = torch.device("cuda", torch.cuda.current_device())
-    sysm, rhs, cfg = make_problem(args.config, args.N)
-    n_e = sysm.A_e.shape[0]
-    scfg = mg.SolverConfig(coarse_size=args.coarse_size, smoother=args.smoother)
-
     # inputs resident in HBM for the device-timed value
-    A_e = dv.DeviceCSR.from_scipy(sysm.A_e)
-    S = dv.DeviceCSR.from_scipy(sysm.S)
-    A_n = dv.DeviceCSR.from_scipy(sysm.A_n)
-    D = dv.DeviceCSR.from_scipy(sysm.D)
+    if args.config in DEVICE_INPUTS:
+        sysd, rhs, cfg = make_device_problem(args.config, args.N)
+        A_e, S, A_n, D = sysd.A_e, sysd.S, sysd.A_n, sysd.D
+        # host copies for the e2e leg (skipped above ~10M edges: C5's
+        # host matrices alone are ~50 GB)
+        sysm = None
+        if sysd.n_edges <= 10_000_000 and not args.no_e2e:
+            from types import SimpleNamespace
+            sysm = SimpleNamespace(**{k: getattr(sysd, k).to_scipy()
+                                      for k in ("A_e", "S", "A_n", "D")})
+    else:
+        sysm, rhs, cfg = make_problem(args.config, args.N)
+        A_e = dv.DeviceCSR.from_scipy(sysm.A_e)
+        S = dv.DeviceCSR.from_scipy(sysm.S)
+        A_n = dv.DeviceCSR.from_scipy(sysm.A_n)
+        D = dv.DeviceCSR.from_scipy(sysm.D)
+        if args.no_e2e:
+            sysm = None
+    n_e = A_e.shape[0]
+    if args.coarse_size is None:
+        args.coarse_size = cfg.get("coarse_size", 1000)
+    scfg = mg.SolverConfig(coarse_size=args.coarse_size, smoother=args.smoother)
     b = torch.from_numpy(rhs).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
@@ -269,7 +301,9 @@ def run_ours(args):
             tdist.barrier()
         torch.cuda.synchronize()
 
+    h = res = None
     for _ in range(args.warmup):
+        h = res = None            # free the previous hierarchy first (C5: ~140 GB)
         h, res = step()
     barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -278,6 +312,7 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             flush.fill_(float(k))          # L2 flush (256 MB > 126 MB L2), untimed
+            h = res = None
             ev[k][0].record()
             h, res = step()
             ev[k][1].record()
@@ -296,6 +331,7 @@ def run_ours(args):
     assert res.status == "converged", res.status
 
     # setup / solve split and V-cycle bandwidth (device events, untimed region)
+    h = res = None
     flush.fill_(1.0)
     e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     e0.record()
@@ -361,30 +397,34 @@ def run_ours(args):
     at_scale = None if args.no_scale_roofline else scale_roofline(args, flush)
 
     # e2e: public API with host inputs, solution back to host
-    e2e_ms = []
-    for k in range(max(2, min(args.steps, 5))):
-        flush.fill_(3.0 + k)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        he = mg.build_hierarchy(sysm.A_e, sysm.S, sysm.A_n, sysm.D, scfg)
-        # the reference's own usage: pcg_solve(h.levels[0].A_e, b, V(h))
-        re = mg.pcg_solve(he.levels[0].A_e, rhs, mg.v_cycle_preconditioner(he))
-        torch.cuda.synchronize()
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        assert isinstance(re.x, np.ndarray)
-    t_e2e = sum(e2e_ms) / len(e2e_ms)
-    if ws > 1:
-        t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        t_e2e = float(t.item())
-    def csr_bytes(M):
-        return M.data.nbytes + M.indices.size * 4 + M.indptr.size * 8
-    # build_hierarchy uploads (A_e, S, A_n, D); pcg_solve uploads b
-    # (int64 row pointers and int32 columns on the device)
-    def dev_bytes(M):
-        return M.data.size * 8 + M.indices.size * 4 + M.indptr.size * 8
-    h2d = sum(dev_bytes(M) for M in (sysm.A_e, sysm.S, sysm.A_n, sysm.D)) + rhs.nbytes
-    d2h = n_e * 8
+    e2e = None
+    if sysm is not None:
+        e2e_ms = []
+        for k in range(max(2, min(args.steps, 5))):
+            flush.fill_(3.0 + k)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            he = mg.build_hierarchy(sysm.A_e, sysm.S, sysm.A_n, sysm.D, scfg)
+            # the reference's own usage: pcg_solve(h.levels[0].A_e, b, V(h))
+            re = mg.pcg_solve(he.levels[0].A_e, rhs, mg.v_cycle_preconditioner(he))
+            torch.cuda.synchronize()
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            assert isinstance(re.x, np.ndarray)
+            del he, re
+        t_e2e = sum(e2e_ms) / len(e2e_ms)
+        if ws > 1:
+            t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            t_e2e = float(t.item())
+
+        # build_hierarchy uploads (A_e, S, A_n, D); pcg_solve uploads b
+        # (int64 row pointers and int32 columns on the device)
+        def dev_bytes(M):
+            return M.data.size * 8 + M.indices.size * 4 + M.indptr.size * 8
+        h2d = sum(dev_bytes(M) for M in (sysm.A_e, sysm.S, sysm.A_n, sysm.D)) + rhs.nbytes
+        e2e = {"value": ws * n_e / (t_e2e * 1e-3), "unit": "edge DOFs/s",
+               "ms": t_e2e, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(n_e * 8)}
 
     pk, pk_kind = peaks()
     peak = float(pk["hbm_gbs"])
@@ -435,9 +475,7 @@ def run_ours(args):
                          "sell_padding": None if gs_mode else m0.padded / max(A0.nnz, 1),
                          "algorithmic_bytes": kbytes},
             "roofline_at_scale": at_scale,
-            "e2e": {"value": ws * n_e / (t_e2e * 1e-3), "unit": "edge DOFs/s",
-                    "ms": t_e2e, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h)},
+            "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
@@ -481,7 +519,7 @@ def run_reference(args):
     k = max(1, min(args.steps, args.ref_steps))
     times = []
     for _ in range(k):
-        t, res = _oracle_step(sysm, rhs, args.coarse_size, "gs")
+        t, res = _oracle_step(sysm, rhs, args.coarse_size or cfg.get("coarse_size", 1000), "gs")
         times.append(t)
     tm = sum(times) / k
     v = n_e / tm
@@ -508,7 +546,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--N", type=int, default=None)
-    ap.add_argument("--coarse-size", type=int, default=1000)
+    ap.add_argument("--coarse-size", type=int, default=None,
+                    help="default: the config's (1000; 10000 for C5)")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--smoother", default="chebyshev", choices=["chebyshev", "gauss_seidel"])
     ap.add_argument("--ref-steps", type=int, default=3)

@@ -8,6 +8,7 @@
 #include "common.cuh"
 
 #define SELL_C 32
+#define SELL_PER_BLOCK 256   // threads per block of the SpMV-type kernels
 
 __global__ void k_sell_widths(i64 n, const i64* __restrict__ rp, i64* __restrict__ width) {
   i64 ns = (n + SELL_C - 1) / SELL_C;
@@ -69,13 +70,13 @@ extern "C" int sphc_sell_fill(int64_t n, const int64_t* rp, const int32_t* ci, c
 // loaded with the default policy so they stay L2-resident across the V-cycle.
 #define SELL_STREAM_BYTES (48ll << 20)
 
-template <bool STREAM>
-__device__ __forceinline__ double sell_row(i64 base, int w, const int* __restrict__ sci,
+template <bool STREAM, int K>
+__device__ __forceinline__ double sell_row(i64 base, int w, int q, const int* __restrict__ sci,
                                            const double* __restrict__ sv,
                                            const double* __restrict__ x) {
   double acc = 0.0;
 #pragma unroll 4
-  for (int j = 0; j < w; j++) {
+  for (int j = q; j < w; j += K) {
     i64 o = base + (i64)j * SELL_C;
     double v = STREAM ? __ldcs(sv + o) : __ldg(sv + o);
     int c = STREAM ? __ldcs(sci + o) : __ldg(sci + o);
@@ -84,64 +85,109 @@ __device__ __forceinline__ double sell_row(i64 base, int w, const int* __restric
   return acc;
 }
 
+// Row sums of A x over the slice owned by this warp. K > 1 splits every
+// slice's columns over K warps of the block (interleaved j = q, q + K, ...;
+// each load stays a coalesced 256 B line) and combines the partial sums in
+// shared memory in a fixed order: small operators (C2's finest level has
+// 2,883 slices, ~19 warps per SM at K = 1) get K times the loads in flight.
+// Returns true on the lane that owns the epilogue of `row`.
+template <bool STREAM, int K>
+__device__ __forceinline__ bool sell_rowsum(i64 n, const i64* __restrict__ sp,
+                                            const int* __restrict__ sci,
+                                            const double* __restrict__ sv,
+                                            const double* __restrict__ x, bool skip, i64& row,
+                                            double& acc) {
+  __shared__ double part[SELL_PER_BLOCK / 32][32];
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int q = warp % K;
+  i64 s = (i64)blockIdx.x * (SELL_PER_BLOCK / 32 / K) + warp / K;
+  i64 ns = (n + SELL_C - 1) / SELL_C;
+  row = s * SELL_C + lane;
+  acc = 0.0;
+  if (s < ns && !skip) {
+    i64 b0 = sp[s];
+    int w = (int)((sp[s + 1] - b0) / SELL_C);
+    acc = sell_row<STREAM, K>(b0 + lane, w, q, sci, sv, x);
+  }
+  if (K > 1) {
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (q != 0) return false;
+    acc = part[warp][lane];
+    for (int t = 1; t < K; t++) acc += part[warp + t][lane];
+  }
+  return s < ns && row < n;
+}
+
 // y = alpha A x + beta z
-template <bool STREAM>
-__global__ void __launch_bounds__(256)
+template <bool STREAM, int K>
+__global__ void __launch_bounds__(SELL_PER_BLOCK)
     k_sell_spmv(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
                 const double* __restrict__ sv, const double* __restrict__ x, double alpha,
                 double beta, const double* z, double* y) {
-  i64 row = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-  i64 s = row / SELL_C;
-  i64 ns = (n + SELL_C - 1) / SELL_C;
-  if (s >= ns) return;
-  i64 b0 = sp[s];
-  int w = (int)((sp[s + 1] - b0) / SELL_C);
-  double acc = sell_row<STREAM>(b0 + (row % SELL_C), w, sci, sv, x);
-  if (row < n) {
-    double r = alpha * acc;
-    if (z) r = fma(beta, z[row], r);
-    y[row] = r;
-  }
+  i64 row;
+  double acc;
+  if (!sell_rowsum<STREAM, K>(n, sp, sci, sv, x, false, row, acc)) return;
+  double r = alpha * acc;
+  if (z) r = fma(beta, z[row], r);
+  y[row] = r;
 }
 
 // d <- cd d + cr dinv (b - A x_in); x_out = x_in + d
-template <bool STREAM>
-__global__ void __launch_bounds__(256)
+template <bool STREAM, int K>
+__global__ void __launch_bounds__(SELL_PER_BLOCK)
     k_sell_cheb(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
                 const double* __restrict__ sv, const double* __restrict__ dinv,
                 const double* __restrict__ b, const double* __restrict__ x_in,
                 double* __restrict__ x_out, double* __restrict__ d, double cd, double cr,
                 int x_zero) {
-  i64 row = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-  i64 s = row / SELL_C;
-  i64 ns = (n + SELL_C - 1) / SELL_C;
-  if (s >= ns) return;
-  double ax = 0.0;
-  if (!x_zero) {
-    i64 b0 = sp[s];
-    int w = (int)((sp[s + 1] - b0) / SELL_C);
-    ax = sell_row<STREAM>(b0 + (row % SELL_C), w, sci, sv, x_in);
-  }
-  if (row < n) {
-    double r = b[row] - ax;
-    double dn = cr * dinv[row] * r;
-    if (cd != 0.0) dn = fma(cd, d[row], dn);
-    d[row] = dn;
-    x_out[row] = (x_zero ? 0.0 : x_in[row]) + dn;
-  }
+  i64 row;
+  double ax;
+  if (!sell_rowsum<STREAM, K>(n, sp, sci, sv, x_in, x_zero != 0, row, ax)) return;
+  double r = b[row] - ax;
+  double dn = cr * dinv[row] * r;
+  if (cd != 0.0) dn = fma(cd, d[row], dn);
+  d[row] = dn;
+  x_out[row] = (x_zero ? 0.0 : x_in[row]) + dn;
 }
+
+// warps per slice: the smallest K in {1, 2, 4} that puts ~48 warps on every SM
+static inline int sell_split(i64 n) {
+  i64 ns = (n + SELL_C - 1) / SELL_C;
+  const i64 target = (i64)SPHC_NUM_SMS * 48;
+  if (ns >= target) return 1;
+  if (2 * ns >= target) return 2;
+  return 4;
+}
+
+static inline unsigned sell_grid(i64 n, int K) {
+  i64 ns = (n + SELL_C - 1) / SELL_C;
+  i64 per = SELL_PER_BLOCK / 32 / K;
+  return (unsigned)((ns + per - 1) / per);
+}
+
+#define SELL_DISPATCH(KERNEL, STREAMING, ...)                                     \
+  do {                                                                           \
+    int K_ = sell_split(n);                                                      \
+    unsigned g_ = sell_grid(n, K_);                                              \
+    if (STREAMING) {                                                             \
+      if (K_ == 1) KERNEL<true, 1><<<g_, SELL_PER_BLOCK, 0, s>>>(__VA_ARGS__);   \
+      else if (K_ == 2) KERNEL<true, 2><<<g_, SELL_PER_BLOCK, 0, s>>>(__VA_ARGS__); \
+      else KERNEL<true, 4><<<g_, SELL_PER_BLOCK, 0, s>>>(__VA_ARGS__);           \
+    } else {                                                                     \
+      if (K_ == 1) KERNEL<false, 1><<<g_, SELL_PER_BLOCK, 0, s>>>(__VA_ARGS__);  \
+      else if (K_ == 2) KERNEL<false, 2><<<g_, SELL_PER_BLOCK, 0, s>>>(__VA_ARGS__); \
+      else KERNEL<false, 4><<<g_, SELL_PER_BLOCK, 0, s>>>(__VA_ARGS__);          \
+    }                                                                            \
+  } while (0)
 
 extern "C" int sphc_sell_spmv(int64_t n, const int64_t* slice_ptr, const int32_t* sci,
                               const double* sv, const double* x, double alpha, double beta,
                               const double* z, double* y, int64_t padded, void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
-  i64 rows = (n + 31) & ~(i64)31;
-  unsigned g = (unsigned)((rows + 255) / 256);
-  if (padded * 12 > SELL_STREAM_BYTES)
-    k_sell_spmv<true><<<g, 256, 0, s>>>(n, slice_ptr, sci, sv, x, alpha, beta, z, y);
-  else
-    k_sell_spmv<false><<<g, 256, 0, s>>>(n, slice_ptr, sci, sv, x, alpha, beta, z, y);
+  SELL_DISPATCH(k_sell_spmv, padded * 12 > SELL_STREAM_BYTES, n, slice_ptr, sci, sv, x, alpha,
+                beta, z, y);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -152,14 +198,8 @@ extern "C" int sphc_sell_cheb_step(int64_t n, const int64_t* slice_ptr, const in
                                    double cr, int x_zero, int64_t padded, void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
-  i64 rows = (n + 31) & ~(i64)31;
-  unsigned g = (unsigned)((rows + 255) / 256);
-  if (padded * 12 > SELL_STREAM_BYTES)
-    k_sell_cheb<true><<<g, 256, 0, s>>>(n, slice_ptr, sci, sv, dinv, b, x_in, x_out, d, cd,
-                                        cr, x_zero);
-  else
-    k_sell_cheb<false><<<g, 256, 0, s>>>(n, slice_ptr, sci, sv, dinv, b, x_in, x_out, d, cd,
-                                         cr, x_zero);
+  SELL_DISPATCH(k_sell_cheb, padded * 12 > SELL_STREAM_BYTES, n, slice_ptr, sci, sv, dinv, b,
+                x_in, x_out, d, cd, cr, x_zero);
   SPHC_LAUNCH_CHECK();
   return 0;
 }

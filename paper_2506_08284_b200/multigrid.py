@@ -277,24 +277,33 @@ def _check_nullspace(S, D, where, A=None):
 
 def _coarse_inverse(Ad):
     """Symmetric inverse of the coarsest operator (multigrid.py:157 factors it
-    with LU). The coarsest A_e is SPD in exact arithmetic but can be extremely
-    ill-conditioned (cond ~ 4e15 on config 4 at N=64, where the mass part is
-    tiny): an explicit getri inverse then carries an O(cond eps) antisymmetric
-    error that makes the V-cycle non-symmetric and PCG diverge. The inverse is
-    formed from the Cholesky factor (potrf + potri: symmetric positive by
-    construction, ~0.3 ms at n = 364); when the factorisation breaks down (the
-    operator is numerically semidefinite) it falls back to the symmetric
-    eigendecomposition with eigenvalues <= n eps lambda_max treated as null
-    space (cuSOLVER syevd, ~4 ms at n = 364)."""
+    with LU). The coarsest A_e is SPD in exact arithmetic but badly scaled
+    and ill-conditioned: the edge prolongators grow level by level (max|P_e|
+    ~ 10 per level for every sigma, reference behaviour), so the diagonal of
+    the coarsest operator spans 1e4..1e7 at N=32 and cond(A) reaches 1e16
+    at N=128 with sigma = 1e-4 (C5's recipe), where a plain factorisation
+    loses the small (gradient-like) modes. The inverse is therefore formed
+    on the Jacobi-equilibrated matrix S A S, S = diag(A)^-1/2 (an exact
+    identity: A^-1 = S (S A S)^-1 S), from its Cholesky factor (potrf +
+    potri: symmetric positive by construction; an explicit getri inverse is
+    visibly non-symmetric at cond ~ 4e15 and made PCG diverge on C4). If the
+    factorisation still breaks down (numerically semidefinite) it falls back
+    to the symmetric eigendecomposition of S A S with eigenvalues
+    <= n eps lambda_max treated as null space."""
     A = 0.5 * (Ad + Ad.T)
-    L, info = torch.linalg.cholesky_ex(A)
+    d = torch.diagonal(A).clone()
+    sc = torch.where(d > 0, d.rsqrt(), torch.ones_like(d))
+    As = sc[:, None] * A * sc[None, :]
+    As = 0.5 * (As + As.T)
+    L, info = torch.linalg.cholesky_ex(As)
     if int(info) == 0:
         inv = torch.cholesky_inverse(L)
-        return 0.5 * (inv + inv.T)
-    lam, V = torch.linalg.eigh(A)
-    tiny = lam.abs().max() * A.shape[0] * torch.finfo(torch.float64).eps
-    w = torch.where(lam > tiny, 1.0 / lam, torch.zeros_like(lam))
-    inv = (V * w) @ V.T
+    else:
+        lam, V = torch.linalg.eigh(As)
+        tiny = lam.abs().max() * As.shape[0] * torch.finfo(torch.float64).eps
+        w = torch.where(lam > tiny, 1.0 / lam, torch.zeros_like(lam))
+        inv = (V * w) @ V.T
+    inv = sc[:, None] * inv * sc[None, :]
     return 0.5 * (inv + inv.T)
 
 

@@ -12,7 +12,7 @@ for N in [int(a) for a in sys.argv[2:]]:
     print(name, N, "n_e", s.n_edges, "nnz(A_e)", s.A_e.nnz, "nnz(A_n)", s.A_n.nnz,
           f"assembly+draws {1e3*(ta-t0):.0f} ms", "mem GB", torch.cuda.memory_allocated() / 1e9, flush=True)
     b = torch.from_numpy(rhs).cuda()
-    for rep in range(2):
+    for rep in range(int(os.environ.get("REPS", "2"))):
         torch.cuda.synchronize(); t0 = time.perf_counter()
         h = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, mg.SolverConfig(coarse_size=1000))
         torch.cuda.synchronize(); t1 = time.perf_counter()

@@ -51,63 +51,63 @@ def dist_env():
     return ws, rank, local
 
 
-class ClockSampler:
-    """SM clocks + throttle reasons sampled during the timed region: NVML
-    polled every 5 ms from a thread (nvidia-smi -lms as a fallback)."""
+_NVML_POLL = r"""
+import sys, time
+import pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+    nv.nvmlDeviceGetCurrentClocksThrottleReasons
+mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+while True:
+    try:
+        print(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx, int(get_r(h)), flush=True)
+    except Exception:
+        pass
+    time.sleep(0.005)
+"""
 
+
+class ClockSampler:
+    """SM clocks + throttle reasons sampled during the timed region by a
+    separate process (NVML polled every 5 ms; nvidia-smi -lms 200 if pynvml
+    is missing), so sampling never contends for this process's GIL while
+    the host drives the setup."""
+
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40}
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
-            "hw_thermal_slowdown": 0x40}
 
     def __init__(self, gpu):
         self.gpu = gpu
         self.p = None
-        self.t = None
-        self.samples = []
-
-    def _poll(self, nv, hdl):
-        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-            nv.nvmlDeviceGetCurrentClocksThrottleReasons
-        while not self.stop.is_set():
-            try:
-                self.samples.append((nv.nvmlDeviceGetClockInfo(hdl, nv.NVML_CLOCK_SM),
-                                     nv.nvmlDeviceGetMaxClockInfo(hdl, nv.NVML_CLOCK_SM),
-                                     int(get_r(hdl))))
-            except Exception:   # noqa: BLE001 - sampling is best effort
-                pass
-            self.stop.wait(0.005)
+        self.kind = None
 
     def __enter__(self):
-        import threading
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
         try:
-            import pynvml as nv
-            nv.nvmlInit()
-            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() \
-                else self.gpu
-            hdl = nv.nvmlDeviceGetHandleByIndex(idx)
-            self.stop = threading.Event()
-            self.t = threading.Thread(target=self._poll, args=(nv, hdl), daemon=True)
-            self.t.start()
-            return self
+            import pynvml  # noqa: F401
+            self.p = subprocess.Popen([sys.executable, "-c", _NVML_POLL, str(idx)],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                      text=True)
+            self.kind = "nvml"
+            time.sleep(0.2)        # first samples before the timed region
         except Exception:   # noqa: BLE001
-            self.t = None
-        try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.p = None
+            try:
+                self.p = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(idx), f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits", "-lms", "200"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.kind = "nvidia-smi"
+            except OSError:
+                self.p = None
         return self
 
     def __exit__(self, *a):
         self.lines = []
-        if self.t is not None:
-            self.stop.set()
-            self.t.join(timeout=5)
         if self.p is not None:
             self.p.terminate()
             out, _ = self.p.communicate(timeout=10)
@@ -115,12 +115,18 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
-        for clk, cmax, bits in self.samples:
-            sm.append(float(clk))
-            mx = max(mx, float(cmax))
-            reasons |= {k for k, b in self.BITS.items() if bits & b}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for l in self.lines:
+            if self.kind == "nvml":
+                f = l.split()
+                try:
+                    clk, cmax, bits = float(f[0]), float(f[1]), int(f[2])
+                except (ValueError, IndexError):
+                    continue
+                sm.append(clk)
+                mx = max(mx, cmax)
+                reasons |= {k for k, b in self.BITS.items() if bits & b}
+                continue
             f = [x.strip() for x in l.split(",")]
             try:
                 sm.append(float(f[0]))
@@ -132,7 +138,7 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": mx or None, "reasons": sorted(reasons),
-                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
+                "samples": len(sm), "source": self.kind}
 
 
 def vcycle_bytes(h, degree=3):
@@ -453,6 +459,7 @@ def run_ours(args):
                        "parallelism": (f"row-block partitioned solve x{ws}" if partitioned
                                        else f"replicas x{ws}"),
                        "l2": "256 MB flush before every timed step"},
+            "step_ms": [round(x, 3) for x in step_ms],
             "setup_ms": t_setup, "solve_ms": t_solve,
             "setup_dofs_per_s": n_e / (t_setup * 1e-3),
             "solve_dofs_per_s": n_e / (t_solve * 1e-3),

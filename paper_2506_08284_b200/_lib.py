@@ -13,7 +13,8 @@ import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libsphcurl.so")
+# SPHC_LIB: load an alternative build (tuning experiments only)
+LIB_PATH = os.environ.get("SPHC_LIB") or os.path.join(HERE, "libsphcurl.so")
 HEADER = os.path.join(REPO, "include", "sphcurl.h")
 
 _CT = {"q": ctypes.c_int64, "i": ctypes.c_int, "d": ctypes.c_double,

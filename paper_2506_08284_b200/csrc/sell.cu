@@ -6,6 +6,7 @@
 // SM -- the HBM-bound V-cycle kernels run on this layout.
 // Padding entries carry value 0 and the row's own column.
 #include "common.cuh"
+#include <stdlib.h>
 
 #define SELL_C 32
 #define SELL_PER_BLOCK 256   // threads per block of the SpMV-type kernels
@@ -70,17 +71,34 @@ extern "C" int sphc_sell_fill(int64_t n, const int64_t* rp, const int32_t* ci, c
 // loaded with the default policy so they stay L2-resident across the V-cycle.
 #define SELL_STREAM_BYTES (48ll << 20)
 
-template <bool STREAM, int K>
+// One thread's share of a row: entries j = q, q + K, ... of its SELL row,
+// summed in ascending j with fma (the same order for every K = 1 launch).
+// Entries are processed in groups of SELL_U: the group's column / value
+// loads are all issued before any dependent x gather, so a cold row costs
+// ~2 memory round trips per group instead of per entry pair.
+// Groups of 8 for the L2-sized operators (latency bound: few warps per SM);
+// 4 for the streaming ones (bandwidth bound: 32 registers keep 64 warps
+// resident per SM).
+template <bool STREAM, int K, int SELL_U = STREAM ? 4 : 8>
 __device__ __forceinline__ double sell_row(i64 base, int w, int q, const int* __restrict__ sci,
                                            const double* __restrict__ sv,
                                            const double* __restrict__ x) {
   double acc = 0.0;
-#pragma unroll 4
-  for (int j = q; j < w; j += K) {
-    i64 o = base + (i64)j * SELL_C;
-    double v = STREAM ? __ldcs(sv + o) : __ldg(sv + o);
-    int c = STREAM ? __ldcs(sci + o) : __ldg(sci + o);
-    acc = fma(v, __ldg(x + c), acc);
+  for (int j0 = q; j0 < w; j0 += SELL_U * K) {
+    int c[SELL_U];
+    double v[SELL_U];
+#pragma unroll
+    for (int u = 0; u < SELL_U; u++) {
+      int j = j0 + u * K;
+      if (j < w) {
+        i64 o = base + (i64)j * SELL_C;
+        v[u] = STREAM ? __ldcs(sv + o) : __ldg(sv + o);
+        c[u] = STREAM ? __ldcs(sci + o) : __ldg(sci + o);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < SELL_U; u++)
+      if (j0 + u * K < w) acc = fma(v[u], __ldg(x + c[u]), acc);
   }
   return acc;
 }
@@ -121,7 +139,7 @@ __device__ __forceinline__ bool sell_rowsum(i64 n, const i64* __restrict__ sp,
 
 // y = alpha A x + beta z
 template <bool STREAM, int K>
-__global__ void __launch_bounds__(SELL_PER_BLOCK)
+__global__ void __launch_bounds__(SELL_PER_BLOCK, STREAM ? 8 : 1)
     k_sell_spmv(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
                 const double* __restrict__ sv, const double* __restrict__ x, double alpha,
                 double beta, const double* z, double* y) {
@@ -135,7 +153,7 @@ __global__ void __launch_bounds__(SELL_PER_BLOCK)
 
 // d <- cd d + cr dinv (b - A x_in); x_out = x_in + d
 template <bool STREAM, int K>
-__global__ void __launch_bounds__(SELL_PER_BLOCK)
+__global__ void __launch_bounds__(SELL_PER_BLOCK, STREAM ? 8 : 1)
     k_sell_cheb(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
                 const double* __restrict__ sv, const double* __restrict__ dinv,
                 const double* __restrict__ b, const double* __restrict__ x_in,
@@ -151,13 +169,23 @@ __global__ void __launch_bounds__(SELL_PER_BLOCK)
   x_out[row] = (x_zero ? 0.0 : x_in[row]) + dn;
 }
 
-// warps per slice: the smallest K in {1, 2, 4} that puts ~48 warps on every SM
+// warps per slice: K = 1 once the slices alone fill ~48 warps per SM;
+// otherwise the largest K in {2, 4} whose grid still fits one wave
+// (8 blocks of 256 threads per SM) -- a second partial wave costs more than
+// the extra loads in flight gain. SPHC_SELL_K overrides (tuning).
 static inline int sell_split(i64 n) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("SPHC_SELL_K");
+    forced = e ? atoi(e) : 0;
+  }
+  if (forced == 1 || forced == 2 || forced == 4) return forced;
   i64 ns = (n + SELL_C - 1) / SELL_C;
-  const i64 target = (i64)SPHC_NUM_SMS * 48;
-  if (ns >= target) return 1;
-  if (2 * ns >= target) return 2;
-  return 4;
+  if (ns >= (i64)SPHC_NUM_SMS * 48) return 1;
+  const i64 wave = (i64)SPHC_NUM_SMS * 8;
+  if ((ns + 1) / 2 <= wave) return 4;    // 2 slices per block
+  if ((ns + 3) / 4 <= wave) return 2;    // 4 slices per block
+  return 1;
 }
 
 static inline unsigned sell_grid(i64 n, int K) {

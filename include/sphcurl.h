@@ -345,8 +345,10 @@ int sphc_emin_fill(int64_t n_e, const int64_t *drp, const int32_t *dci, const do
  *   g = (S P_in)|_I ; e_row[i] = p_in . g ; delta = dinv_i g ;
  *   delta -= G_k M^-1 G_k^T delta ; P_out = P_in - omega delta (update != 0)
  *   res_max = max |G^T p_out - r| over J.
- * With update == 0 only e_row and res_max (of P_in) are produced. */
-int sphc_emin_step(int64_t n_e, const int64_t *srp, const int32_t *sci, const double *sv,
+ * With update == 0 only e_row and res_max (of P_in) are produced. Rows
+ * [row0, row1) are processed (a row block of a sharded setup); every array
+ * is indexed globally. */
+int sphc_emin_step(int64_t row0, int64_t row1, const int64_t *srp, const int32_t *sci, const double *sv,
                    const double *dinv, const int64_t *trp, const int32_t *tci,
                    const double *tv, const int64_t *erp, const int32_t *eci,
                    const double *p_in, double *p_out, const int32_t *ep_a,

@@ -390,7 +390,7 @@ extern "C" int sphc_emin_fill(int64_t n_e, const int64_t* drp, const int32_t* dc
 }
 
 __global__ void __launch_bounds__(EM_WARPS * 32)
-    k_emin_step(i64 n_e, const i64* __restrict__ srp, const int* __restrict__ sci,
+    k_emin_step(i64 row0, i64 row1, const i64* __restrict__ srp, const int* __restrict__ sci,
                 const double* __restrict__ sv, const double* __restrict__ dinv,
                 const i64* __restrict__ trp, const int* __restrict__ tci,
                 const double* __restrict__ tv, const i64* __restrict__ erp,
@@ -401,7 +401,8 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
   __shared__ EminRow rows[EM_WARPS];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   EminRow& R = rows[w];
-  for (i64 i = (i64)blockIdx.x * EM_WARPS + w; i < n_e; i += (i64)gridDim.x * EM_WARPS) {
+  for (i64 i = row0 + (i64)blockIdx.x * EM_WARPS + w; i < row1;
+       i += (i64)gridDim.x * EM_WARPS) {
     i64 t0 = trp[i], e0 = erp[i];
     int nJ = (int)(trp[i + 1] - t0), nI = (int)(erp[i + 1] - e0);
     if (nI == 0 || nJ > JM || nI > IM) {
@@ -503,15 +504,16 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
   }
 }
 
-extern "C" int sphc_emin_step(int64_t n_e, const int64_t* srp, const int32_t* sci,
+extern "C" int sphc_emin_step(int64_t row0, int64_t row1, const int64_t* srp, const int32_t* sci,
                               const double* sv, const double* dinv, const int64_t* trp,
                               const int32_t* tci, const double* tv, const int64_t* erp,
                               const int32_t* eci, const double* p_in, double* p_out,
                               const int32_t* ep_a, const int32_t* ep_b, double omega, int update,
                               double* e_row, double* res_max, int64_t* status, void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_emin_step<<<grid_for(n_e, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
-      n_e, srp, sci, sv, dinv, trp, tci, tv, erp, eci, p_in, p_out, ep_a, ep_b, omega, update,
+  if (row1 <= row0) return 0;
+  k_emin_step<<<grid_for(row1 - row0, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
+      row0, row1, srp, sci, sv, dinv, trp, tci, tv, erp, eci, p_in, p_out, ep_a, ep_b, omega, update,
       e_row, res_max, status);
   SPHC_LAUNCH_CHECK();
   return 0;

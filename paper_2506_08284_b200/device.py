@@ -204,21 +204,39 @@ def drop_zeros(A):
     return DeviceCSR(rp, ci, v, A.shape)
 
 
-def spgemm(A, B, drop=True, ordered=False):
+def _rows(A, lo):
+    """Row-pointer view starting at row lo (absolute positions into A's
+    column / value arrays, so a kernel launched on it computes rows lo..)."""
+    return A.rowptr[lo:]
+
+
+def spgemm(A, B, drop=True, ordered=False, shard=None):
     """C = A B; exact zeros dropped like scipy's product (drop=True).
-    ordered=True reproduces scipy csr_matmat's accumulation bit for bit."""
+    ordered=True reproduces scipy csr_matmat's accumulation bit for bit.
+    shard: rows computed by row blocks over a ``sharding.Sharding``."""
     if A.shape[1] != B.shape[0]:
         raise ValueError(f"spgemm dimension mismatch: {A.shape} @ {B.shape}")
     n = A.shape[0]
     st = Status()
     cnt = torch.empty(n, dtype=torch.int64, device=A.rowptr.device)
-    call("sphc_spgemm_count", n, A.rowptr, A.col, B.rowptr, B.col, cnt, st.t)
+    blocks = shard.blocks(n) if shard is not None else [(0, 0, n)]
+    for _, lo, hi in blocks:
+        call("sphc_spgemm_count", hi - lo, _rows(A, lo), A.col, B.rowptr, B.col, cnt[lo:], st.t)
+    if shard is not None:
+        shard.gather_ranges(cnt, shard.bounds(n))
+        shard.min_(st.t)
     rp, nnz = scan(cnt)
     _raise_capacity(st)
     ci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
     v = empty_f64(nnz)
-    call("sphc_spgemm_fill", n, A.rowptr, A.col, A.val, B.rowptr, B.col, B.val, rp, ci, v,
-         int(ordered), st.t)
+    for _, lo, hi in blocks:
+        call("sphc_spgemm_fill", hi - lo, _rows(A, lo), A.col, A.val, B.rowptr, B.col, B.val,
+             rp[lo:], ci, v, int(ordered), st.t)
+    if shard is not None and shard.collective:
+        from .sharding import host_offsets
+        off = host_offsets(rp, shard.bounds(n))
+        shard.gather_ranges(ci, off)
+        shard.gather_ranges(v, off)
     C = DeviceCSR(rp, ci, v, (A.shape[0], B.shape[1]))
     return drop_zeros(C) if drop else C
 
@@ -228,19 +246,31 @@ def same_pattern(A, B):
             and torch.equal(A.col, B.col))
 
 
-def spgemm_pair(A1, A2, B1, B2, drop=True):
+def spgemm_pair(A1, A2, B1, B2, drop=True, shard=None):
     """(A1 B1, A2 B2) for A1/A2 and B1/B2 with shared patterns, one pass.
     Stored exact zeros are dropped per product (drop=True)."""
     n = A1.shape[0]
     st = Status()
     cnt = torch.empty(n, dtype=torch.int64, device=A1.rowptr.device)
-    call("sphc_spgemm_count", n, A1.rowptr, A1.col, B1.rowptr, B1.col, cnt, st.t)
+    blocks = shard.blocks(n) if shard is not None else [(0, 0, n)]
+    for _, lo, hi in blocks:
+        call("sphc_spgemm_count", hi - lo, _rows(A1, lo), A1.col, B1.rowptr, B1.col, cnt[lo:],
+             st.t)
+    if shard is not None:
+        shard.gather_ranges(cnt, shard.bounds(n))
+        shard.min_(st.t)
     rp, nnz = scan(cnt)
     _raise_capacity(st)
     ci = torch.empty(nnz, dtype=torch.int32, device=A1.rowptr.device)
     v1, v2 = empty_f64(nnz), empty_f64(nnz)
-    call("sphc_spgemm_fill_pair", n, A1.rowptr, A1.col, A1.val, A2.val, B1.rowptr, B1.col,
-         B1.val, B2.val, rp, ci, v1, v2, st.t)
+    for _, lo, hi in blocks:
+        call("sphc_spgemm_fill_pair", hi - lo, _rows(A1, lo), A1.col, A1.val, A2.val,
+             B1.rowptr, B1.col, B1.val, B2.val, rp[lo:], ci, v1, v2, st.t)
+    if shard is not None and shard.collective:
+        from .sharding import host_offsets
+        off = host_offsets(rp, shard.bounds(n))
+        for t in (ci, v1, v2):
+            shard.gather_ranges(t, off)
     shape = (A1.shape[0], B1.shape[1])
     C1, C2 = DeviceCSR(rp, ci, v1, shape), DeviceCSR(rp, ci, v2, shape)
     return (drop_zeros(C1), drop_zeros(C2)) if drop else (C1, C2)

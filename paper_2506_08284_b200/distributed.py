@@ -100,30 +100,36 @@ def _exchange_counts(counts, group, device):
 
 
 def localize(rp, ci, val, row_lo, row_hi, col_part, rank, group, device):
-    """Owned rows [row_lo, row_hi) of a global CSR (host numpy arrays) ->
-    (CSRLocal with remapped columns, HaloPlan). Collective over `group`."""
+    """Owned rows [row_lo, row_hi) of a global CSR (torch tensors on
+    `device`: the GPU in the product, CPU under the gloo tests) ->
+    (CSRLocal with remapped columns, HaloPlan). Collective over `group`.
+    Everything stays on the device: the slice, the sorted halo set
+    (unique of the off-block columns), the column remap (searchsorted) and
+    the owner counts; the only host reads are the block's CSR bounds and the
+    per-neighbour counts."""
     world = col_part.offsets.size - 1
-    s, e = int(rp[row_lo]), int(rp[row_hi])
-    lrp = (rp[row_lo:row_hi + 1] - s).astype(np.int64)
-    cols = ci[s:e].astype(np.int64)
+    bounds = rp[[row_lo, row_hi]].cpu().tolist()
+    s, e = int(bounds[0]), int(bounds[1])
+    lrp = (rp[row_lo:row_hi + 1] - s).to(torch.int64)
+    cols = ci[s:e].to(torch.int64)
     lo, hi = col_part.lo(rank), col_part.hi(rank)
     own = (cols >= lo) & (cols < hi)
-    halo = np.unique(cols[~own])
-    lcol = np.empty(cols.size, dtype=np.int64)
-    lcol[own] = cols[own] - lo
+    halo = torch.unique(cols[~own])                     # sorted
     n_own = hi - lo
-    lcol[~own] = n_own + np.searchsorted(halo, cols[~own])
-    owners = col_part.owner(halo)
-    recv_counts = np.bincount(owners, minlength=world).astype(np.int64).tolist()
-    send_counts = _exchange_counts(recv_counts, group, device)
-    req = torch.from_numpy(halo).to(device)
-    got = torch.empty(int(sum(send_counts)), dtype=torch.int64, device=device)
-    dist.all_to_all_single(got, req, send_counts, recv_counts, group=group)
+    lcol = torch.where(own, cols - lo, n_own + torch.searchsorted(halo, cols))
+    offs = torch.as_tensor(col_part.offsets, dtype=torch.int64, device=cols.device)
+    owners = torch.searchsorted(offs, halo, right=True) - 1
+    recv_counts = torch.bincount(owners, minlength=world).cpu().tolist()
+    if world > 1:
+        send_counts = _exchange_counts(recv_counts, group, device)
+        got = torch.empty(int(sum(send_counts)), dtype=torch.int64, device=device)
+        dist.all_to_all_single(got, halo, send_counts, recv_counts, group=group)
+    else:
+        send_counts, got = [0], torch.empty(0, dtype=torch.int64, device=device)
     send_idx = (got - lo).to(torch.int64)
-    A = CSRLocal(torch.from_numpy(lrp).to(device), torch.from_numpy(lcol.astype(np.int32)).to(device),
-                 torch.from_numpy(np.ascontiguousarray(val[s:e])).to(device),
-                 (row_hi - row_lo, n_own + halo.size))
-    return A, HaloPlan(n_own, int(halo.size), send_idx, send_counts, recv_counts)
+    A = CSRLocal(lrp, lcol.to(torch.int32), val[s:e].contiguous(),
+                 (row_hi - row_lo, n_own + int(halo.numel())))
+    return A, HaloPlan(n_own, int(halo.numel()), send_idx, send_counts, recv_counts)
 
 
 @dataclass
@@ -135,11 +141,14 @@ class DistOp:
 
 
 def make_op(M, row_part, col_part, rank, group, device):
-    """M: global operator with .rowptr/.col/.val (torch or numpy)."""
-    rp, ci, v = (np.asarray(t.cpu().numpy() if isinstance(t, torch.Tensor) else t)
-                 for t in (M.rowptr if hasattr(M, "rowptr") else M.indptr,
-                           M.col if hasattr(M, "col") else M.indices,
-                           M.val if hasattr(M, "val") else M.data))
+    """M: global operator (DeviceCSR / anything with rowptr, col, val
+    tensors, or a scipy CSR), replicated on every rank."""
+    if hasattr(M, "rowptr"):
+        rp, ci, v = M.rowptr, M.col, M.val
+    else:
+        rp, ci, v = (torch.from_numpy(np.ascontiguousarray(a))
+                     for a in (M.indptr.astype(np.int64), M.indices, M.data))
+    rp, ci, v = (t.to(device) for t in (rp, ci, v))
     A, plan = localize(rp, ci, v, row_part.lo(rank), row_part.hi(rank), col_part, rank,
                        group, device)
     op = DistOp(A, plan)
@@ -175,12 +184,18 @@ class CudaOps:
         self.dv, self.call = dv, call
 
     def spmv(self, A, x, y, alpha=1.0, beta=0.0, z=None):
-        self.call("sphc_spmv", A.shape[0], A.rowptr, A.col, A.val, A.lanes(), x, alpha, beta,
-                  z, y)
+        # SELL mirror for the smoothed square operators (built in cheb)
+        self.dv.spmv(A, x, y, alpha, beta, z)
 
     def cheb(self, A, dinv, b, x_ext, x_out, d, cd, cr, x_zero):
-        self.call("sphc_cheb_step", A.shape[0], A.rowptr, A.col, A.val, A.lanes(), dinv, b,
-                  None if x_zero else x_ext, x_out, d, cd, cr, int(x_zero))
+        m = self.dv.sell(A)      # SELL-32 mirror of the local rows (cached on A)
+        self.call("sphc_sell_cheb_step", A.shape[0], m.slice_ptr, m.col, m.val, dinv, b,
+                  None if x_zero else x_ext, x_out, d, cd, cr, int(x_zero), m.padded)
+
+    def prepare(self, dl):
+        """SELL-32 mirrors of the level's smoothed operators (csrc/sell.cu)."""
+        self.dv.sell(dl.A.A)
+        self.dv.sell(dl.aux.A)
 
     def dot(self, x, y, out):
         self.call("sphc_dot", x.numel(), x, y, out)
@@ -276,6 +291,8 @@ def distribute(levels, coarse_inverse, rank, world, group=None, ops=None, device
             dl.dinv_aux = _own(torch.as_tensor(lv.aux_sweeper.dinv).to(device), npart, rank)
             dl.coefs_A = list(lv.edge_sweeper.coefs)
             dl.coefs_aux = list(lv.aux_sweeper.coefs)
+        if hasattr(ops, "prepare"):
+            ops.prepare(dl)
         ne, nn = ep.size(rank), npart.size(rank)
         z = lambda k: torch.zeros(k, dtype=torch.float64, device=device)  # noqa: E731
         dl.work = dict(x=[z(ne), z(ne)], d=z(ne), r=z(ne), bn=z(nn), c=[z(nn), z(nn)],

@@ -62,8 +62,11 @@ def jacobi_diag_inverse(S):
     return dv.reciprocal(d, sub)
 
 
-def emin_sweeps(S, setup, omega, iterations):
-    """Projected damped-Jacobi sweeps; returns (values, energies, residual)."""
+def emin_sweeps(S, setup, omega, iterations, shard=None):
+    """Projected damped-Jacobi sweeps; returns (values, energies, residual).
+    With ``shard`` every rank sweeps its block of fine edges and the value
+    ranges are all-gathered after each sweep (the next sweep's masked S P
+    reads neighbouring rows)."""
     S = as_device_csr(S)
     n_e = setup.pattern.shape[0]
     T, Pp, cg = setup.T, setup.pattern, setup.cg
@@ -72,30 +75,52 @@ def emin_sweeps(S, setup, omega, iterations):
     res = torch.zeros(1, dtype=torch.float64, device=e_row.device)
     esum = dv.empty_f64(iterations + 1)
     vals = Pp.val
+    blocks = shard.blocks(n_e) if shard is not None else [(0, 0, n_e)]
+    if shard is not None and shard.collective:
+        from .sharding import host_offsets
+        rbounds = shard.bounds(n_e)
+        voff = host_offsets(Pp.rowptr, rbounds)
+
+    def gather(v_out):
+        if shard is not None and shard.collective:
+            if v_out is not None:
+                shard.gather_ranges(v_out, voff)
+            shard.gather_ranges(e_row, rbounds)
+            shard.max_(res)
+
     if iterations:
         dinv = jacobi_diag_inverse(S)
         for it in range(iterations):
             out = torch.empty_like(vals)
             res.zero_()
-            call("sphc_emin_step", n_e, S.rowptr, S.col, S.val, dinv, T.rowptr, T.col, T.val,
-                 Pp.rowptr, Pp.col, vals, out, cg.ep_a, cg.ep_b, float(omega), 1, e_row,
-                 res, st.t)
+            for _, lo, hi in blocks:
+                call("sphc_emin_step", lo, hi, S.rowptr, S.col, S.val, dinv, T.rowptr, T.col,
+                     T.val, Pp.rowptr, Pp.col, vals, out, cg.ep_a, cg.ep_b, float(omega), 1,
+                     e_row, res, st.t)
+            gather(out)
             dv.vsum(e_row, esum[it:it + 1])
             vals = out
     # energy of the final iterate and its commutator residual
     res.zero_()
-    call("sphc_emin_step", n_e, S.rowptr, S.col, S.val, None, T.rowptr, T.col, T.val,
-         Pp.rowptr, Pp.col, vals, None, cg.ep_a, cg.ep_b, float(omega), 0, e_row, res, st.t)
+    for _, lo, hi in blocks:
+        call("sphc_emin_step", lo, hi, S.rowptr, S.col, S.val, None, T.rowptr, T.col, T.val,
+             Pp.rowptr, Pp.col, vals, None, cg.ep_a, cg.ep_b, float(omega), 0, e_row, res,
+             st.t)
+    gather(None)
     dv.vsum(e_row, esum[iterations:iterations + 1])
+    if shard is not None:
+        shard.min_(st.t)
     es._raise(st, S)
     energies = [float(x) for x in esum.cpu().numpy()] if iterations else []
     return vals, energies, float(res.item())
 
 
-def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None):
+def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None, shard=None):
     """Edge prolongator and coarse gradient for one level
     (edge_prolongator.py:184-228). Returns
-    (EdgeProlongator, CoarseGradient, NodalProlongator)."""
+    (EdgeProlongator, CoarseGradient, NodalProlongator). ``shard`` (a
+    sharding.Sharding) splits the emin rows over ranks; the nodal chain and
+    the coarse topology stay replicated."""
     cfg = cfg or EminConfig()
     if cfg.mode != "sphcurl":
         raise NotImplementedError("rsamg mode is outside the B200 hot path")
@@ -110,10 +135,10 @@ def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None):
     with phase("setup.coarse_gradient"):
         cg = cgrad.build_coarse_gradient(D_h, assign, agg.n_agg)
     with phase("setup.emin_constraints"):
-        setup = es.setup_constraints(D_h, nod.P, cg)
+        setup = es.setup_constraints(D_h, nod.P, cg, shard=shard)
         cg = setup.cg                      # with any edges make_irreducible appended
     with phase("setup.emin_sweeps"):
-        vals, energy, res = emin_sweeps(S, setup, cfg.omega, cfg.iterations)
+        vals, energy, res = emin_sweeps(S, setup, cfg.omega, cfg.iterations, shard=shard)
     P = setup.pattern
     P_e = DeviceCSR(P.rowptr, P.col, vals, P.shape)
     prol = EdgeProlongator(P_e=P_e, energy_history=energy, commutator_residual=res,

@@ -53,7 +53,11 @@ def _raise(st, D):
                          "expected rank (topology bug)")
 
 
-def _count(D, P, cg, xrp, xeid, flags):
+def _view(t, lo):
+    return None if t is None else t[lo:]
+
+
+def _count(D, P, cg, xrp, xeid, flags, shard=None):
     n_e = D.shape[0]
     dev = D.rowptr.device
     st = Status()
@@ -63,13 +67,23 @@ def _count(D, P, cg, xrp, xeid, flags):
     dims = torch.zeros(129 * 17, dtype=torch.int64, device=dev)
     rowflag = torch.zeros(n_e, dtype=torch.uint8, device=dev) if flags else None
     rowmax = torch.empty(n_e, dtype=torch.float64, device=dev) if flags else None
-    call("sphc_emin_count", n_e, D.rowptr, D.col, D.val, P.rowptr, P.col, P.val,
-         cg.adj.rowptr, cg.adj.col, cg.n_interior, cg.single_id, xrp, xeid, cg.ep_a, cg.ep_b,
-         icount, jcount, rmax2, dims, rowflag, rowmax, st.t)
+    for _, lo, hi in (shard.blocks(n_e) if shard else [(0, 0, n_e)]):
+        call("sphc_emin_count", hi - lo, D.rowptr[lo:], D.col, D.val, P.rowptr, P.col, P.val,
+             cg.adj.rowptr, cg.adj.col, cg.n_interior, cg.single_id, _view(xrp, lo), xeid,
+             cg.ep_a, cg.ep_b, icount[lo:], jcount[lo:], rmax2, dims, _view(rowflag, lo),
+             _view(rowmax, lo), st.t)
+    if shard is not None:
+        b = shard.bounds(n_e)
+        for t in (icount, jcount, rowflag, rowmax):
+            if t is not None:
+                shard.gather_ranges(t, b)
+        shard.max_(rmax2)
+        shard.sum_(dims)
+        shard.min_(st.t)
     return st, icount, jcount, rmax2, dims, rowflag, rowmax
 
 
-def _fill(D, P, cg, icount, jcount, xrp, xeid, st, rowflag=None):
+def _fill(D, P, cg, icount, jcount, xrp, xeid, st, rowflag=None, shard=None):
     n_e = D.shape[0]
     dev = D.rowptr.device
     trp, tnnz = dv.scan(jcount)
@@ -78,14 +92,27 @@ def _fill(D, P, cg, icount, jcount, xrp, xeid, st, rowflag=None):
     tv = torch.empty(tnnz, dtype=torch.float64, device=dev)
     eci = torch.empty(ennz, dtype=torch.int32, device=dev)
     ev = torch.empty(ennz, dtype=torch.float64, device=dev)
-    call("sphc_emin_fill", n_e, D.rowptr, D.col, D.val, P.rowptr, P.col, P.val,
-         cg.adj.rowptr, cg.adj.col, cg.n_interior, cg.single_id, xrp, xeid, cg.ep_a, cg.ep_b,
-         trp, tci, tv, erp, eci, ev, rowflag, st.t)
+    for _, lo, hi in (shard.blocks(n_e) if shard else [(0, 0, n_e)]):
+        call("sphc_emin_fill", hi - lo, D.rowptr[lo:], D.col, D.val, P.rowptr, P.col, P.val,
+             cg.adj.rowptr, cg.adj.col, cg.n_interior, cg.single_id, _view(xrp, lo), xeid,
+             cg.ep_a, cg.ep_b, trp[lo:], tci, tv, erp[lo:], eci, ev, _view(rowflag, lo), st.t)
+    if shard is not None:
+        b = shard.bounds(n_e)
+        if shard.collective:
+            from .sharding import host_offsets
+            toff, eoff = host_offsets(trp, b), host_offsets(erp, b)
+            for t in (tci, tv):
+                shard.gather_ranges(t, toff)
+            for t in (eci, ev):
+                shard.gather_ranges(t, eoff)
+        if rowflag is not None:
+            shard.gather_ranges(rowflag, b)
+        shard.min_(st.t)
     return (DeviceCSR(trp, tci, tv, (n_e, P.shape[1])),
             DeviceCSR(erp, eci, ev, (n_e, cg.n_edges)))
 
 
-def setup_constraints(D_h, P_n, cg):
+def setup_constraints(D_h, P_n, cg, shard=None):
     """Pattern, irreducibility, factor checks and feasible guess for every
     fine edge (emin_setup.py:256-336 + edge_prolongator.py:104-126).
 
@@ -97,12 +124,13 @@ def setup_constraints(D_h, P_n, cg):
     D = as_device_csr(D_h)
     P = as_device_csr(P_n)
     n_e = D.shape[0]
-    st, icount, jcount, rmax2, dims, rowflag, rowmax = _count(D, P, cg, None, None, True)
+    st, icount, jcount, rmax2, dims, rowflag, rowmax = _count(D, P, cg, None, None, True,
+                                                              shard)
     _raise(st, D)
     rm = rmax2.cpu().numpy()
     rdp_scale = max(1.0, float(rm[0]))
     # the fill pass factors every block and flags the reducible ones
-    T, pattern = _fill(D, P, cg, icount, jcount, None, None, st, rowflag)
+    T, pattern = _fill(D, P, cg, icount, jcount, None, None, st, rowflag, shard)
     _raise(st, D)
     flags = rowflag
     need = (flags & 1).bool()
@@ -113,9 +141,9 @@ def setup_constraints(D_h, P_n, cg):
         from . import repair
         cg, xrp, xeid, n_aug = repair.make_irreducible_pass(
             need, flags, rowmax, rdp_scale, T, pattern, cg)
-        st, icount, jcount, rmax2, dims, _, _ = _count(D, P, cg, xrp, xeid, False)
+        st, icount, jcount, rmax2, dims, _, _ = _count(D, P, cg, xrp, xeid, False, shard)
         _raise(st, D)
-        T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st)
+        T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st, shard=shard)
         _raise(st, D)
     h = dims.cpu().numpy().reshape(129, 17)
     nz = np.argwhere(h)

@@ -240,9 +240,10 @@ class Hierarchy:
         return len(self.levels)
 
 
-def _make_level(A_e, S_e, D, cfg, AD=None, smooth=True, **extra):
+def _make_level(A_e, S_e, D, cfg, AD=None, smooth=True, shard=None, **extra):
     Dt = dv.transpose(D)
-    nodal_aux = dv.spgemm(Dt, AD if AD is not None else dv.spgemm(A_e, D))
+    nodal_aux = dv.spgemm(Dt, AD if AD is not None else dv.spgemm(A_e, D, shard=shard),
+                          shard=shard)
     level = Level(A_e=A_e, S_e=S_e, D=D, nodal_aux=nodal_aux, Dt=Dt, **extra)
     if smooth:   # the coarsest level is solved directly, never smoothed
         sweeper = SMOOTHERS[cfg.smoother]
@@ -253,16 +254,16 @@ def _make_level(A_e, S_e, D, cfg, AD=None, smooth=True, **extra):
     return level
 
 
-def _check_nullspace(S, D, where, A=None):
+def _check_nullspace(S, D, where, A=None, shard=None):
     """max|S D| <= 1e-10 max|S| (multigrid.py:110-116). With A (same pattern
     as S) the product A D is formed in the same pass and returned for the
     level's D^T A D."""
     AD = None
     if A is not None and dv.same_pattern(A, S):
-        AD, SD = dv.spgemm_pair(A, S, D, D, drop=False)
+        AD, SD = dv.spgemm_pair(A, S, D, D, drop=False, shard=shard)
         AD = dv.drop_zeros(AD)
     else:
-        SD = dv.spgemm(S, D, drop=False)
+        SD = dv.spgemm(S, D, drop=False, shard=shard)
     m = dv.empty_f64(2)
     dv.maxabs(SD.val, m[0:1])
     dv.maxabs(S.val, m[1:2])
@@ -307,16 +308,19 @@ def _coarse_inverse(Ad):
     return 0.5 * (inv + inv.T)
 
 
-def build_hierarchy(A_e, S_e, A_n, D, cfg=None):
+def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
     """Galerkin hierarchy driven by the constrained edge prolongator
-    (multigrid.py:119-161)."""
+    (multigrid.py:119-161). ``shard`` (sharding.Sharding, optional; not a
+    reference argument) splits the row-parallel setup work over the ranks
+    of a process group; the result is identical on every rank and bitwise
+    equal to the unsharded hierarchy."""
     cfg = cfg or SolverConfig()
     A_e, S_e = as_device_csr(A_e), as_device_csr(S_e)
     A_n, D = as_device_csr(A_n), as_device_csr(D)
-    AD = _check_nullspace(S_e, D, "the fine level", A=A_e)
+    AD = _check_nullspace(S_e, D, "the fine level", A=A_e, shard=shard)
     levels = []
     while A_e.shape[0] > cfg.coarse_size and len(levels) < cfg.max_levels - 1:
-        prol, cg, nod = build_edge_prolongator(A_n, A_e, S_e, D, cfg.emin)
+        prol, cg, nod = build_edge_prolongator(A_n, A_e, S_e, D, cfg.emin, shard=shard)
         P_e, P_n = prol.P_e, nod.P
         n_coarse = cg.n_edges
         if n_coarse == 0:
@@ -326,7 +330,7 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None):
                 f"coarsening stagnated: {n_coarse} coarse edges from "
                 f"{A_e.shape[0]} fine edges")
         with phase("level.make_level"):
-            lv = _make_level(A_e, S_e, D, cfg, AD=AD, P_e=P_e, P_n=P_n,
+            lv = _make_level(A_e, S_e, D, cfg, AD=AD, shard=shard, P_e=P_e, P_n=P_n,
                              emin_energy=prol.energy_history,
                              subproblem_dims=dict(prol.subproblem_dims),
                              commutator_residual=prol.commutator_residual,
@@ -341,19 +345,19 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None):
         with phase("level.galerkin_edge"):
             if dv.same_pattern(A_e, S_e):
                 # one pass for both: P^T (A_e P) and P^T (S_e P) share patterns
-                AP, SP = dv.spgemm_pair(A_e, S_e, P_e, P_e, drop=False)
-                A_e, S_e = dv.spgemm_pair(lv.R_e, lv.R_e, AP, SP)
+                AP, SP = dv.spgemm_pair(A_e, S_e, P_e, P_e, drop=False, shard=shard)
+                A_e, S_e = dv.spgemm_pair(lv.R_e, lv.R_e, AP, SP, shard=shard)
             else:
-                A_e = dv.spgemm(lv.R_e, dv.spgemm(A_e, P_e))
-                S_e = dv.spgemm(lv.R_e, dv.spgemm(S_e, P_e))
+                A_e = dv.spgemm(lv.R_e, dv.spgemm(A_e, P_e, shard=shard), shard=shard)
+                S_e = dv.spgemm(lv.R_e, dv.spgemm(S_e, P_e, shard=shard), shard=shard)
         with phase("level.galerkin_nodal"):
-            A_n = dv.spgemm(dv.transpose(P_n), dv.spgemm(A_n, P_n, ordered=True),
-                            ordered=True)
+            A_n = dv.spgemm(dv.transpose(P_n), dv.spgemm(A_n, P_n, ordered=True, shard=shard),
+                            ordered=True, shard=shard)
         D = cg.D_H
         with phase("level.nullspace_check"):
-            AD = _check_nullspace(S_e, D, f"level {len(levels)}", A=A_e)
+            AD = _check_nullspace(S_e, D, f"level {len(levels)}", A=A_e, shard=shard)
     with phase("coarsest"):
-        last = _make_level(A_e, S_e, D, cfg, AD=AD, smooth=False)
+        last = _make_level(A_e, S_e, D, cfg, AD=AD, smooth=False, shard=shard)
         levels.append(last)
         inv = _coarse_inverse(dv.to_dense(A_e))
     last.r = dv.empty_f64(A_e.shape[0])

@@ -27,58 +27,90 @@ struct EminRow {
   double y[JM];
   double g[IM];
   double p[IM];
-  int nJ, nI, k, err;
+  int sc[2][JM];       // staged P_n rows of the two endpoints (em_build_J)
+  double sv[2][JM];
+  unsigned adj[JM];    // interior-edge adjacency bitmasks over J (em_factor)
+  unsigned incm;       // J nodes incident to some edge of I
+  int nJ, nI, k, err, fc;
 };
 
-// lane 0: serial merge of the P_n rows of the (<=2) free endpoints into J, r.
+// all lanes: the P_n rows of the (<=2) free endpoints are staged in shared
+// memory with one coalesced load each, then lane 0 merges them into J, r
+// (scipy csr_matmat order). Serial global loads here used to dominate the
+// pass: every merge step waited on an L2 round trip.
 __device__ void em_build_J(EminRow& R, i64 i, const i64* __restrict__ drp,
                            const int* __restrict__ dci, const double* __restrict__ dv,
                            const i64* __restrict__ prp, const int* __restrict__ pci,
-                           const double* __restrict__ pv, i64* status) {
+                           const double* __restrict__ pv, i64* status, int lane) {
   i64 s = drp[i];
   int nd = (int)(drp[i + 1] - s);
-  R.err = 0;
   if (nd < 1 || nd > 2) {
-    report(status, SPHC_ST_MALFORMED_GRAD, i);
-    R.err = 1;
-    R.nJ = 0;
+    if (lane == 0) {
+      report(status, SPHC_ST_MALFORMED_GRAD, i);
+      R.err = 1;
+      R.nJ = 0;
+    }
+    __syncwarp();
     return;
   }
   int ta = dci[s];
   double sa = dv[s];
-  i64 a0 = prp[ta], a1 = prp[ta + 1];
-  i64 b0 = 0, b1 = 0;
+  i64 a0 = prp[ta];
+  int na = (int)(prp[ta + 1] - a0);
+  int nb = 0;
+  i64 b0 = 0;
   double sb = 0.0;
   if (nd == 2) {
     int hb = dci[s + 1];
     sb = dv[s + 1];
     b0 = prp[hb];
-    b1 = prp[hb + 1];
+    nb = (int)(prp[hb + 1] - b0);
   }
-  int n = 0;
-  while (a0 < a1 || b0 < b1) {
-    int ca = a0 < a1 ? pci[a0] : 0x7fffffff;
-    int cb = b0 < b1 ? pci[b0] : 0x7fffffff;
-    int c = ca < cb ? ca : cb;
-    // scipy csr_matmat order: first D entry (lower column) then the second
-    double acc = 0.0;
-    if (ca == c) acc = __dadd_rn(acc, __dmul_rn(sa, pv[a0++]));
-    if (cb == c) acc = __dadd_rn(acc, __dmul_rn(sb, pv[b0++]));
-    if (n >= JM) {
+  if (na > JM || nb > JM) {   // the merged row would exceed JM as well
+    if (lane == 0) {
       report(status, SPHC_ST_EMIN_CAPACITY, i);
       R.err = 1;
       R.nJ = 0;
-      return;
     }
-    R.J[n] = c;
-    R.r[n] = acc;
-    n++;
+    __syncwarp();
+    return;
   }
-  R.nJ = n;
-  if (n == 0) {
-    report(status, SPHC_ST_EMPTY_J, i);
-    R.err = 1;
+  if (lane < na) {
+    R.sc[0][lane] = pci[a0 + lane];
+    R.sv[0][lane] = pv[a0 + lane];
+  } else if (lane >= 16 && lane - 16 < nb) {
+    R.sc[1][lane - 16] = pci[b0 + lane - 16];
+    R.sv[1][lane - 16] = pv[b0 + lane - 16];
   }
+  __syncwarp();
+  if (lane == 0) {
+    R.err = 0;
+    int ia = 0, ib = 0, n = 0;
+    while (ia < na || ib < nb) {
+      int ca = ia < na ? R.sc[0][ia] : 0x7fffffff;
+      int cb = ib < nb ? R.sc[1][ib] : 0x7fffffff;
+      int c = ca < cb ? ca : cb;
+      // scipy csr_matmat order: first D entry (lower column) then the second
+      double acc = 0.0;
+      if (ca == c) acc = __dadd_rn(acc, __dmul_rn(sa, R.sv[0][ia++]));
+      if (cb == c) acc = __dadd_rn(acc, __dmul_rn(sb, R.sv[1][ib++]));
+      if (n >= JM) {
+        report(status, SPHC_ST_EMIN_CAPACITY, i);
+        R.err = 1;
+        n = 0;
+        break;
+      }
+      R.J[n] = c;
+      R.r[n] = acc;
+      n++;
+    }
+    R.nJ = n;
+    if (n == 0 && !R.err) {
+      report(status, SPHC_ST_EMPTY_J, i);
+      R.err = 1;
+    }
+  }
+  __syncwarp();
 }
 
 // all lanes: I = interior coarse edges among J pairs (lexicographic = ascending
@@ -165,59 +197,66 @@ __device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
 // packed lower-triangle index (m <= p)
 __device__ __forceinline__ int tri(int p, int m) { return p * (p + 1) / 2 + m; }
 
-// lane 0: irreducibility, k, Gram matrix, Cholesky, rank checks.
-// Returns false (and reports) on failure.
-__device__ int em_factor(EminRow& R, i64 i, i64* status) {
+// all lanes: irreducibility (bitmask BFS), k, the Gram matrix (exact
+// integer atomics), then the left-looking Cholesky with the rows below the
+// pivot spread over the lanes. Every factor entry is computed with the
+// serial loop's operation order, so the factor is bitwise the serial one.
+// Returns (warp-uniform) 0 ok, 1 reducible, 2 rank failure (reported).
+__device__ int em_factor(EminRow& R, i64 i, i64* status, int lane) {
   int nJ = R.nJ, nI = R.nI;
-  // union-find over J with interior edges; incidence from every edge
-  int parent[JM];
-  bool inc[JM];
-  bool dirich = false;
-  for (int q = 0; q < nJ; q++) {
-    parent[q] = q;
-    inc[q] = false;
-  }
-  for (int e = 0; e < nI; e++) {
+  // irreducibility (emin_setup.py check_irreducible): every J node incident
+  // to an edge of I and J connected by the interior edges. Lanes take the
+  // edges and build adjacency bitmasks; reachability from node 0 is a
+  // warp-wide OR per BFS level (<= |J| <= 16 levels).
+  if (lane < JM) R.adj[lane] = 0u;
+  if (lane == 0) R.incm = 0u;
+  __syncwarp();
+  bool dir = false;
+  for (int e = lane; e < nI; e += 32) {
     int a = R.pa[e], b = R.pb[e];
-    inc[b] = true;
     if (a < 0) {
-      dirich = true;
-      continue;
-    }
-    inc[a] = true;
-    int x = a, y = b;
-    while (parent[x] != x) x = parent[x];
-    while (parent[y] != y) y = parent[y];
-    if (x != y) {
-      if (x < y) parent[y] = x; else parent[x] = y;
+      dir = true;
+      atomicOr(&R.incm, 1u << b);
+    } else {
+      atomicOr(&R.incm, (1u << a) | (1u << b));
+      atomicOr(&R.adj[a], 1u << b);
+      atomicOr(&R.adj[b], 1u << a);
     }
   }
-  bool irreducible = true;
-  int root0 = -1;
-  for (int q = 0; q < nJ; q++) {
-    int x = q;
-    while (parent[x] != x) x = parent[x];
-    if (root0 < 0) root0 = x;
-    irreducible &= inc[q] && (x == root0);
+  bool dirich = __any_sync(FULL_MASK, dir);
+  __syncwarp();
+  unsigned full = (1u << nJ) - 1u;
+  unsigned myadj = lane < nJ ? R.adj[lane] : 0u;
+  unsigned reach = nJ ? 1u : 0u;
+  for (;;) {
+    unsigned nr = reach | __reduce_or_sync(FULL_MASK, ((reach >> lane) & 1u) ? myadj : 0u);
+    if (nr == reach) break;
+    reach = nr;
   }
-  if (!irreducible) return 1;
+  if (!(R.incm == full && reach == full)) return 1;
   int k = nJ - (dirich ? 0 : 1);
-  R.k = k;
   // expected rank must be in [1, min(|I|, |J|)]
   if (k < 1 || k > nI) {
-    report(status, SPHC_ST_RANK_LOW, i);
+    if (lane == 0) report(status, SPHC_ST_RANK_LOW, i);
+    __syncwarp();
     return 2;
   }
-  double* L = R.L;
-  for (int t = 0; t < k * (k + 1) / 2; t++) L[t] = 0.0;
-  for (int e = 0; e < nI; e++) {
+  // Gram matrix G_k^T G_k: integer-valued, so the shared-memory atomic sums
+  // are exact and order independent (bitwise the serial accumulation)
+  double* Lg = R.L;
+  for (int t = lane; t < k * (k + 1) / 2; t += 32) Lg[t] = 0.0;
+  __syncwarp();
+  for (int e = lane; e < nI; e += 32) {
     int a = R.pa[e], b = R.pb[e];
-    if (b < k) L[tri(b, b)] += 1.0;
+    if (b < k) atomicAdd(&Lg[tri(b, b)], 1.0);
     if (a >= 0 && a < k) {
-      L[tri(a, a)] += 1.0;
-      if (b < k) L[a > b ? tri(a, b) : tri(b, a)] -= 1.0;
+      atomicAdd(&Lg[tri(a, a)], 1.0);
+      if (b < k) atomicAdd(&Lg[a > b ? tri(a, b) : tri(b, a)], -1.0);
     }
   }
+  if (lane == 0) R.k = k;
+  __syncwarp();
+  double* L = R.L;
   // in-place lower Cholesky; |R_jj| of the reference QR = L_jj
   for (int j = 0; j < k; j++) {
     const double* Lj = L + tri(j, 0);
@@ -225,16 +264,21 @@ __device__ int em_factor(EminRow& R, i64 i, i64* status) {
     for (int m = 0; m < j; m++) d -= Lj[m] * Lj[m];
     double ljj = d > 0.0 ? sqrt(d) : 0.0;
     if (!(ljj >= 1e-10 * (j ? L[0] : ljj)) || ljj == 0.0) {
-      report(status, SPHC_ST_RANK_LOW, i);
+      if (lane == 0) report(status, SPHC_ST_RANK_LOW, i);
+      __syncwarp();
       return 2;
     }
-    L[tri(j, j)] = ljj;
-    for (int p = j + 1; p < k; p++) {
-      double* Lp = L + tri(p, 0);
-      double x = Lp[j];
+    int p = j + 1 + lane;
+    double x = 0.0;
+    if (p < k) {
+      const double* Lp = L + tri(p, 0);
+      x = Lp[j];
       for (int m = 0; m < j; m++) x -= Lp[m] * Lj[m];
-      Lp[j] = x / ljj;
     }
+    __syncwarp();   // every lane has read L[tri(j, j)] (via d) and its row
+    if (p < k) L[tri(p, j)] = x / ljj;
+    if (lane == 0) L[tri(j, j)] = ljj;
+    __syncwarp();
   }
   return 0;
 }
@@ -273,8 +317,7 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   EminRow& R = rows[w];
   for (i64 i = (i64)blockIdx.x * EM_WARPS + w; i < n_e; i += (i64)gridDim.x * EM_WARPS) {
-    if (lane == 0) em_build_J(R, i, drp, dci, dv, prp, pci, pv, status);
-    __syncwarp();
+    em_build_J(R, i, drp, dci, dv, prp, pci, pv, status, lane);
     if (R.err) {
       if (!FILL && lane == 0) { icount[i] = 0; jcount[i] = 0; }
       __syncwarp();
@@ -313,8 +356,9 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
       __syncwarp();
       continue;
     }
+    int fcw = em_factor(R, i, status, lane);
     if (lane == 0) {
-      int fc = em_factor(R, i, status);
+      int fc = fcw;
       bool ok = fc == 0;
       // reducible blocks are flagged for the host make_irreducible pass
       // (rowflag != NULL) or are an error once the repair has been applied
@@ -458,8 +502,9 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
     __syncwarp();
     if (update) {
       bool ok = true;
+      int fcw = em_factor(R, i, status, lane);
       if (lane == 0) {
-        int fc = em_factor(R, i, status);
+        int fc = fcw;
         if (fc == 1) report(status, SPHC_ST_REDUCIBLE, i);
         ok = fc == 0;
         if (ok) {

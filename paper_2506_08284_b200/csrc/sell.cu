@@ -139,7 +139,7 @@ __device__ __forceinline__ bool sell_rowsum(i64 n, const i64* __restrict__ sp,
 
 // y = alpha A x + beta z
 template <bool STREAM, int K>
-__global__ void __launch_bounds__(SELL_PER_BLOCK, STREAM ? 8 : 1)
+__global__ void __launch_bounds__(SELL_PER_BLOCK, (STREAM && K == 1) ? 8 : 5)
     k_sell_spmv(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
                 const double* __restrict__ sv, const double* __restrict__ x, double alpha,
                 double beta, const double* z, double* y) {
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(SELL_PER_BLOCK, STREAM ? 8 : 1)
 
 // d <- cd d + cr dinv (b - A x_in); x_out = x_in + d
 template <bool STREAM, int K>
-__global__ void __launch_bounds__(SELL_PER_BLOCK, STREAM ? 8 : 1)
+__global__ void __launch_bounds__(SELL_PER_BLOCK, (STREAM && K == 1) ? 8 : 5)
     k_sell_cheb(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
                 const double* __restrict__ sv, const double* __restrict__ dinv,
                 const double* __restrict__ b, const double* __restrict__ x_in,

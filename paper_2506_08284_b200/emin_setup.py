@@ -17,6 +17,7 @@ import torch
 
 from . import device as dv
 from .device import DeviceCSR, Status, as_device_csr, call
+from .trace import phase
 
 
 @dataclass
@@ -124,14 +125,16 @@ def setup_constraints(D_h, P_n, cg, shard=None):
     D = as_device_csr(D_h)
     P = as_device_csr(P_n)
     n_e = D.shape[0]
-    st, icount, jcount, rmax2, dims, rowflag, rowmax = _count(D, P, cg, None, None, True,
-                                                              shard)
-    _raise(st, D)
+    with phase("emin.count"):
+        st, icount, jcount, rmax2, dims, rowflag, rowmax = _count(D, P, cg, None, None, True,
+                                                                  shard)
+        _raise(st, D)
     rm = rmax2.cpu().numpy()
     rdp_scale = max(1.0, float(rm[0]))
     # the fill pass factors every block and flags the reducible ones
-    T, pattern = _fill(D, P, cg, icount, jcount, None, None, st, rowflag, shard)
-    _raise(st, D)
+    with phase("emin.fill"):
+        T, pattern = _fill(D, P, cg, icount, jcount, None, None, st, rowflag, shard)
+        _raise(st, D)
     flags = rowflag
     need = (flags & 1).bool()
     if rm[1] > 1e-12 * rdp_scale:
@@ -139,12 +142,14 @@ def setup_constraints(D_h, P_n, cg, shard=None):
     n_aug = 0
     if bool(need.any()):
         from . import repair
-        cg, xrp, xeid, n_aug = repair.make_irreducible_pass(
-            need, flags, rowmax, rdp_scale, T, pattern, cg)
-        st, icount, jcount, rmax2, dims, _, _ = _count(D, P, cg, xrp, xeid, False, shard)
-        _raise(st, D)
-        T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st, shard=shard)
-        _raise(st, D)
+        with phase("emin.repair"):
+            cg, xrp, xeid, n_aug = repair.make_irreducible_pass(
+                need, flags, rowmax, rdp_scale, T, pattern, cg)
+        with phase("emin.refill"):
+            st, icount, jcount, rmax2, dims, _, _ = _count(D, P, cg, xrp, xeid, False, shard)
+            _raise(st, D)
+            T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st, shard=shard)
+            _raise(st, D)
     h = dims.cpu().numpy().reshape(129, 17)
     nz = np.argwhere(h)
     counter = Counter({(int(i), int(j)): int(h[i, j]) for i, j in nz})

@@ -481,12 +481,9 @@ def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
     status, iters = "maxit", 0
     graph = ws["graph"]
     if graph_ok and graph is None:
-        # warm the iteration once outside capture on scratch copies so every
-        # lazily allocated buffer exists, then capture on the real ones; the
-        # graph is kept on the hierarchy for later solves with the same A
-        xs, rs, ps, scs = x.clone(), r.clone(), p.clone(), sc.clone()
-        _pcg_iteration(A, lanes, precond, xs, rs, ps, Ap, scs,
-                       scs.view(torch.int32)[8:9], torch.zeros_like(stage))
+        # every buffer of the iteration exists already (precond(r) above ran
+        # the V-cycle once), so capture directly; the graph is kept on the
+        # hierarchy for later solves with the same A.
         # capture on a side stream without torch.cuda.graph's gc.collect() +
         # empty_cache(), which would force every later allocation back to
         # cudaMalloc

@@ -105,8 +105,24 @@ def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
             s += float(x) * float(y)
         return abs(s)
 
+    def approx_scores(J):
+        """|J| x |J| column dot products via one dense product (BLAS order)
+        and the structural overlap counts; the decision is then made with
+        exact ascending-order scores on the near-best candidates only."""
+        cols = [column(int(a)) for a in J]
+        keys = np.concatenate([c[0] for c in cols]) if len(cols) else np.zeros(0, np.int64)
+        keys.sort()
+        if keys.size:
+            keys = keys[np.concatenate([[True], keys[1:] != keys[:-1]])]
+        X = np.zeros((keys.size, len(J)))
+        for q, (k, v) in enumerate(cols):
+            X[np.searchsorted(keys, k), q] = v
+        Z = (X != 0).astype(np.float64)
+        return np.abs(X.T @ X), Z.T @ Z
+
     def repair(i, I, J):
         I = list(I)
+        S = O = None
         while True:
             ok, roots = _Graph.analyse(I, J, ends)
             if ok:
@@ -114,21 +130,30 @@ def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
             if len(set(roots)) <= 1:
                 raise ValueError(f"fine edge {i}: cannot repair a single-node "
                                  "constraint graph")
+            if S is None:
+                S, O = approx_scores(J)
+            cand = [(x, y) for x in range(len(J)) for y in range(x + 1, len(J))
+                    if roots[x] != roots[y]]
+            top = max(S[x, y] for x, y in cand)
+            # near-best window far wider than the BLAS-order rounding error;
+            # structurally disjoint columns score exactly 0
+            near = [(x, y) for x, y in cand if S[x, y] >= top * (1.0 - 1e-9)]
             best = None
-            for x in range(len(J)):
-                for y in range(x + 1, len(J)):
-                    if roots[x] == roots[y]:
-                        continue
-                    a, b = int(J[x]), int(J[y])
-                    key = (-score(a, b), a, b)
-                    if best is None or key < best:
-                        best = key
+            for x, y in near:
+                a, b = int(J[x]), int(J[y])
+                key = (-(score(a, b) if O[x, y] > 0 else 0.0), a, b)
+                if best is None or key < best:
+                    best = key
             _, a, b = best
             ends.append((min(a, b), max(a, b)))
             I.append(len(ends) - 1)
 
     data_T = dict(zip(need_rows.tolist(), _rows(T, need_rows)))
     data_I = dict(zip(need_rows.tolist(), _rows(pattern, need_rows)))
+    # every candidate endpoint of a repair is a J node of a flagged row:
+    # fetch all their R_dp columns in one batched download
+    nodes = sorted({int(c) for i in need_rows.tolist() for c in data_T[i][0]})
+    col_cache.update(zip(nodes, _rows(Tt, nodes)))
     final = {}
     for i in need_rows.tolist():
         J = data_T[i][0]
@@ -153,13 +178,19 @@ def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
         rows_T = dict(zip(aff, _rows(T, aff)))
         rows_I = dict(zip(aff, _rows(pattern, aff)))
         emptyish = (flag_h & 2).astype(bool)
+        by_node = {}                             # endpoint -> appended edges
+        for e in new_edges:
+            for n in ends[e]:
+                by_node.setdefault(n, []).append(e)
         for i in aff:
             J, I0 = rows_T[i][0], rows_I[i][0]
             prev = final.get(i)
             if prev is None and emptyish[i] and I0.size == 0:
                 continue                         # a row the main loop left empty
-            Jset = set(J.tolist())
-            add = [e for e in new_edges if all(n in Jset for n in ends[e])]
+            Jl = J.tolist()
+            Jset = set(Jl)
+            add = sorted({e for n in Jl for e in by_node.get(n, ())
+                          if ends[e][0] in Jset and ends[e][1] in Jset})
             I1 = sorted(set(I0.tolist()) | set(add))
             if len(I1) == len(prev if prev is not None else I0):
                 continue
@@ -168,8 +199,10 @@ def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
     # per-row extras: appended ids of each repaired row, ascending
     counts = np.zeros(n_e, dtype=np.int64)
     items = []
+    import bisect
     for i in sorted(final):
-        ex = [e for e in final[i] if e >= n0]
+        fi = final[i]                   # ascending: original ids, then appended
+        ex = fi[bisect.bisect_left(fi, n0):]
         counts[i] = len(ex)
         items.extend(ex)
     xrp_h = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)

@@ -8,11 +8,16 @@ from paper_2506_08284_b200.inputs import make_config
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "C2"
 N = int(sys.argv[2]) if len(sys.argv) > 2 else None
-s, rhs, cfg = make_config(cfgname, N)
-A_e, S, A_n, D = (dv.DeviceCSR.from_scipy(M) for M in (s.A_e, s.S, s.A_n, s.D))
+if cfgname in ("C3", "C4", "C5"):
+    from paper_2506_08284_b200.assembly import make_device_config
+    s, rhs, cfg = make_device_config(cfgname, N)
+    A_e, S, A_n, D = s.A_e, s.S, s.A_n, s.D
+else:
+    s, rhs, cfg = make_config(cfgname, N)
+    A_e, S, A_n, D = (dv.DeviceCSR.from_scipy(M) for M in (s.A_e, s.S, s.A_n, s.D))
 b = torch.from_numpy(rhs).cuda()
-sc = mg.SolverConfig(coarse_size=1000)
-for rep in range(3):
+sc = mg.SolverConfig(coarse_size=cfg.get("coarse_size", 1000))
+for rep in range(int(os.environ.get("REPS", "3"))):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     with trace.phase("TOTAL.setup"):
         h = mg.build_hierarchy(A_e, S, A_n, D, sc)

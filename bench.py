@@ -61,7 +61,8 @@ get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
 mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
 while True:
     try:
-        print(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx, int(get_r(h)), flush=True)
+        print(time.time(), nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx, int(get_r(h)),
+              flush=True)
     except Exception:
         pass
     time.sleep(0.005)
@@ -113,15 +114,22 @@ class ClockSampler:
             out, _ = self.p.communicate(timeout=10)
             self.lines = [l for l in out.splitlines() if l.strip()]
 
+    def mark(self, which):
+        """Wall-clock bounds of the timed region (samples outside are dropped)."""
+        setattr(self, which, time.time())
+
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for l in self.lines:
             if self.kind == "nvml":
                 f = l.split()
                 try:
-                    clk, cmax, bits = float(f[0]), float(f[1]), int(f[2])
+                    ts, clk, cmax, bits = float(f[0]), float(f[1]), float(f[2]), int(f[3])
                 except (ValueError, IndexError):
+                    continue
+                if t0 is not None and t1 is not None and not (t0 <= ts <= t1):
                     continue
                 sm.append(clk)
                 mx = max(mx, cmax)
@@ -321,14 +329,18 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     h = res = None
-    for _ in range(args.warmup):
-        h = res = None            # free the previous hierarchy first (C5: ~140 GB)
-        h, res = step()
-    barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    l0 = _lib.launch_count()
+    # the sampler starts before the warm-up (no idle gap that would let the
+    # clocks drop before the timed steps); only samples inside the timed
+    # region are summarised
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            h = res = None            # free the previous hierarchy first (C5: ~140 GB)
+            h, res = step()
+        barrier()
+        l0 = _lib.launch_count()
+        clk.mark("t0")
         for k in range(args.steps):
             flush.fill_(float(k))          # L2 flush (256 MB > 126 MB L2), untimed
             h = res = None
@@ -336,6 +348,7 @@ def run_ours(args):
             h, res = step()
             ev[k][1].record()
         barrier()
+        clk.mark("t1")
     launches = (_lib.launch_count() - l0) // args.steps
     step_ms = [a.elapsed_time(bb) for a, bb in ev]
     from paper_2506_08284_b200 import trace
@@ -419,7 +432,7 @@ def run_ours(args):
     e2e = None
     if sysm is not None:
         e2e_ms = []
-        for k in range(max(2, min(args.steps, 5))):
+        for k in range(-2, max(2, min(args.steps, 5))):    # k < 0: untimed warm-up
             flush.fill_(3.0 + k)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -427,7 +440,8 @@ def run_ours(args):
             # the reference's own usage: pcg_solve(h.levels[0].A_e, b, V(h))
             re = mg.pcg_solve(he.levels[0].A_e, rhs, mg.v_cycle_preconditioner(he))
             torch.cuda.synchronize()
-            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            if k >= 0:
+                e2e_ms.append((time.perf_counter() - t0) * 1e3)
             assert isinstance(re.x, np.ndarray)
             del he, re
         t_e2e = sum(e2e_ms) / len(e2e_ms)

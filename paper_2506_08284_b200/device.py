@@ -117,7 +117,106 @@ class DeviceCSR:
 
 
 def as_device_csr(A):
-    return A if isinstance(A, DeviceCSR) else DeviceCSR.from_scipy(A)
+    if isinstance(A, DeviceCSR):
+        return A
+    if isinstance(A, PendingCSR):
+        return A.get()
+    return DeviceCSR.from_scipy(A)
+
+
+_STAGE = {}
+
+
+class AsyncUpload:
+    """Host -> device upload of scipy CSR matrices in the background: a
+    helper thread casts / copies the arrays into one pinned staging buffer
+    with a small pool of threads (numpy releases the GIL) and queues the DMAs
+    on a side stream; ``get(k)`` makes the caller's stream wait on the copy
+    event (no host sync). The caller keeps launching device work meanwhile
+    (build_hierarchy runs the nodal chain while A_e and S arrive)."""
+
+    def __init__(self, mats, nthreads=8):
+        dev = device()
+        self.mats = []
+        for A in mats:
+            A = sp.csr_matrix(A)
+            if not A.has_canonical_format:
+                A = A.copy()
+                A.sum_duplicates()
+                A.sort_indices()
+            self.mats.append(A)
+        self.specs = []
+        for A in self.mats:
+            self.specs += [(A.indptr, np.int64), (A.indices, np.int32), (A.data, np.float64)]
+        tdt = {np.int64: torch.int64, np.int32: torch.int32, np.float64: torch.float64}
+        self.dst = [torch.empty(a.size, dtype=tdt[d], device=dev) for a, d in self.specs]
+        self.offs, o = [], 0
+        for a, d in self.specs:
+            self.offs.append(o)
+            o += (a.size * np.dtype(d).itemsize + 255) // 256 * 256
+        self.nbytes = o
+        self.nthreads = nthreads
+        self.dev = dev
+        self.stream = torch.cuda.Stream(device=dev)
+        self.event = torch.cuda.Event()
+        self.err = None
+        import threading
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+        self.csr = None
+
+    def _run(self):
+        try:
+            torch.cuda.set_device(self.dev)
+            prev = _STAGE.get("event")
+            if prev is not None:
+                prev.synchronize()             # the buffer's previous DMAs are done
+            buf = _STAGE.get("buf")
+            if buf is None or buf.numel() < self.nbytes:
+                buf = torch.empty(max(self.nbytes, 1 << 24), dtype=torch.uint8,
+                                  pin_memory=True)
+                _STAGE["buf"] = buf
+            hv = buf.numpy()
+            jobs = []
+            for (a, d), o in zip(self.specs, self.offs):
+                dstv = hv[o:o + a.size * np.dtype(d).itemsize].view(d)
+                step = max(1 << 18, a.size // self.nthreads + 1)
+                for k in range(0, a.size, step):
+                    jobs.append((dstv[k:k + step], a[k:k + step]))
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(self.nthreads) as ex:
+                list(ex.map(lambda j: np.copyto(j[0], j[1], casting="unsafe"), jobs))
+            with torch.cuda.stream(self.stream):
+                for t, (a, d), o in zip(self.dst, self.specs, self.offs):
+                    if a.size:
+                        t.view(torch.uint8).copy_(buf[o:o + a.size * np.dtype(d).itemsize],
+                                                  non_blocking=True)
+                self.event.record(self.stream)
+            _STAGE["event"] = self.event
+        except BaseException as e:   # noqa: BLE001 - re-raised by get()
+            self.err = e
+
+    def get(self, k):
+        if self.csr is None:
+            self.thread.join()
+            if self.err is not None:
+                raise self.err
+            torch.cuda.current_stream().wait_event(self.event)
+            self.csr = [DeviceCSR(self.dst[3 * i], self.dst[3 * i + 1], self.dst[3 * i + 2],
+                                  tuple(int(x) for x in A.shape))
+                        for i, A in enumerate(self.mats)]
+        return self.csr[k]
+
+
+class PendingCSR:
+    """A matrix of an AsyncUpload; its shape is known before the data lands."""
+
+    def __init__(self, up, k):
+        self.up, self.k = up, k
+        self.shape = tuple(int(x) for x in up.mats[k].shape)
+
+    def get(self):
+        return self.up.get(self.k)
 
 
 def empty_f64(n):

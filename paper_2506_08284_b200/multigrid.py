@@ -315,12 +315,32 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
     of a process group; the result is identical on every rank and bitwise
     equal to the unsharded hierarchy."""
     cfg = cfg or SolverConfig()
+    first = None
+    host_edge = (not isinstance(A_e, DeviceCSR) and not isinstance(S_e, DeviceCSR)
+                 and os.environ.get("SPHC_ASYNC_UPLOAD", "1") != "0")
+    if host_edge and A_e.shape[0] > cfg.coarse_size and cfg.max_levels > 1:
+        # host inputs: A_e and S stream in behind the nodal chain (their
+        # first use is the emin sweep); the fine-level null-space check runs
+        # right after the first prolongator. A data error of the nodal chain
+        # defers to that check's, so the reference's error order holds.
+        up = dv.AsyncUpload([A_e, S_e])
+        A_n, D = as_device_csr(A_n), as_device_csr(D)
+        try:
+            first = build_edge_prolongator(A_n, dv.PendingCSR(up, 0), dv.PendingCSR(up, 1), D,
+                                           cfg.emin, shard=shard)
+        except ValueError:
+            _check_nullspace(up.get(1), D, "the fine level", A=up.get(0), shard=shard)
+            raise
+        A_e, S_e = up.get(0), up.get(1)
     A_e, S_e = as_device_csr(A_e), as_device_csr(S_e)
     A_n, D = as_device_csr(A_n), as_device_csr(D)
     AD = _check_nullspace(S_e, D, "the fine level", A=A_e, shard=shard)
     levels = []
     while A_e.shape[0] > cfg.coarse_size and len(levels) < cfg.max_levels - 1:
-        prol, cg, nod = build_edge_prolongator(A_n, A_e, S_e, D, cfg.emin, shard=shard)
+        if first is not None:
+            (prol, cg, nod), first = first, None
+        else:
+            prol, cg, nod = build_edge_prolongator(A_n, A_e, S_e, D, cfg.emin, shard=shard)
         P_e, P_n = prol.P_e, nod.P
         n_coarse = cg.n_edges
         if n_coarse == 0:

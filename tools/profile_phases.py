@@ -17,7 +17,9 @@ else:
     A_e, S, A_n, D = (dv.DeviceCSR.from_scipy(M) for M in (s.A_e, s.S, s.A_n, s.D))
 b = torch.from_numpy(rhs).cuda()
 sc = mg.SolverConfig(coarse_size=cfg.get("coarse_size", 1000))
+h = res = None
 for rep in range(int(os.environ.get("REPS", "3"))):
+    h = res = None
     torch.cuda.synchronize(); t0 = time.perf_counter()
     with trace.phase("TOTAL.setup"):
         h = mg.build_hierarchy(A_e, S, A_n, D, sc)
@@ -29,7 +31,8 @@ print(f"{cfgname} n_e={s.A_e.shape[0]} levels={[lv.A_e.shape[0] for lv in h.leve
 print(rep_txt)
 # untraced timing
 trace.ENABLED = False
-for rep in range(2):
+for rep in range(int(os.environ.get("UREPS", "2"))):
+    h = res = None
     torch.cuda.synchronize(); t0 = time.perf_counter()
     h = mg.build_hierarchy(A_e, S, A_n, D, sc)
     torch.cuda.synchronize(); t1 = time.perf_counter()

@@ -657,10 +657,18 @@ def make_sweeper(A, smoother, degree):
     return ChebyshevSweeper(A, degree)
 
 
+def tentative_prolongator(memb, n_agg):
+    """Piecewise-constant transfer, one unit entry per row (nodal_amg.py:91-96)."""
+    n = memb.size
+    return sp.csr_matrix((np.ones(n), memb.copy(), np.arange(n + 1)), shape=(n, n_agg))
+
+
 def build_hierarchy(A_e, S_e, A_n, D, coarse_size=200, max_levels=10,
                     omega=0.5, iterations=1, n_passes=2, drop_tol=0.0,
-                    smoother="gs", degree=3):
-    """Galerkin hierarchy (multigrid.py:119-161) with the selected sweeper."""
+                    smoother="gs", degree=3, mode="sphcurl"):
+    """Galerkin hierarchy (multigrid.py:119-161) with the selected sweeper.
+    mode="rsamg" (edge_prolongator.py:200-213): the nodal transfer is the
+    tentative prolongator itself (omega = rho = 0) and no emin sweeps run."""
     A_e, S_e, A_n, D = (canonical(X) for X in (A_e, S_e, A_n, D))
     check_nullspace(S_e, D, "the fine level")
     levels = []
@@ -674,10 +682,14 @@ def build_hierarchy(A_e, S_e, A_n, D, coarse_size=200, max_levels=10,
 
     while A_e.shape[0] > coarse_size and len(levels) < max_levels - 1:
         memb, n_agg = aggregate(strength_pattern(A_n, drop_tol))
-        P_n, w, rho = smoothed_prolongator(A_n, memb, n_agg)
+        if mode == "rsamg":
+            P_n, w, rho = tentative_prolongator(memb, n_agg), 0.0, 0.0
+        else:
+            P_n, w, rho = smoothed_prolongator(A_n, memb, n_agg)
         assign = piecewise_const(P_n, n_passes)
         ce = coarse_edges(D, assign, n_agg)
-        em = emin_prolongator(D, P_n, ce, S_e, omega, iterations)
+        em = emin_prolongator(D, P_n, ce, S_e, omega,
+                              0 if mode == "rsamg" else iterations)
         nH = ce.n_edges
         if nH == 0:
             break
@@ -697,6 +709,22 @@ def build_hierarchy(A_e, S_e, A_n, D, coarse_size=200, max_levels=10,
     lu = la.lu_factor(A_e.toarray())
     oc = sum(lv.A_e.nnz for lv in levels) / levels[0].A_e.nnz
     return Hierarchy(levels=levels, coarse_lu=lu, operator_complexity=oc)
+
+
+def fine_level(A_e, S_e, D, smoother="gs", degree=3):
+    """Single smoothing level without transfers (multigrid.py:204-207)."""
+    A, S, Dm = canonical(A_e), canonical(S_e), canonical(D)
+    aux = canonical(Dm.T @ (A @ Dm))
+    lv = Level(A_e=A, S_e=S, D=Dm, nodal_aux=aux)
+    lv.edge_sweeper = make_sweeper(A, smoother, degree)
+    lv.aux_sweeper = make_sweeper(aux, smoother, degree)
+    return lv
+
+
+def relax_solve(lv, b, rtol=1e-8, maxit=500):
+    """PCG preconditioned by one stand-alone Hiptmair sweep
+    (hiptmair_preconditioner, multigrid.py:198-201)."""
+    return pcg(lv.A_e, b, lambda r: hiptmair(lv, np.zeros(r.size), r), rtol, maxit)
 
 
 def hiptmair(lv, x, b):

@@ -27,7 +27,7 @@ class EminConfig:
 
     omega: float = 0.5
     iterations: int = 1
-    mode: str = "sphcurl"          # only "sphcurl" runs on the device path
+    mode: str = "sphcurl"          # "sphcurl" or "rsamg" (the paper's baseline)
     n_passes: int = 2
     drop_tol: float = 0.0
 
@@ -120,16 +120,24 @@ def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None, shard=None):
     (edge_prolongator.py:184-228). Returns
     (EdgeProlongator, CoarseGradient, NodalProlongator). ``shard`` (a
     sharding.Sharding) splits the emin rows over ranks; the nodal chain and
-    the coarse topology stay replicated."""
+    the coarse topology stay replicated.
+
+    cfg.mode == "rsamg" (edge_prolongator.py:200-213): the nodal transfer is
+    the tentative prolongator itself (omega = rho = 0) and no emin sweeps
+    run, so P_e is the feasible initial guess (entries +-1, 0 and the
+    least-norm fractions of Dirichlet rows; many empty rows)."""
     cfg = cfg or EminConfig()
-    if cfg.mode != "sphcurl":
-        raise NotImplementedError("rsamg mode is outside the B200 hot path")
+    rsamg = cfg.mode == "rsamg"
     with phase("setup.strength"):
         strength = na.strength_graph(A_n, cfg.drop_tol)
     with phase("setup.aggregate"):
         agg = na.aggregate(strength)
     with phase("setup.smooth_and_normalize"):
-        nod = na.smooth_and_normalize(A_n, agg)
+        if rsamg:
+            nod = na.NodalProlongator(P=na.tentative_prolongator(agg), omega_used=0.0,
+                                      rho_estimate=0.0)
+        else:
+            nod = na.smooth_and_normalize(A_n, agg)
     with phase("setup.piecewise_const"):
         assign = cgrad.gen_piecewise_const(nod.P, cfg.n_passes)
     with phase("setup.coarse_gradient"):
@@ -138,7 +146,8 @@ def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None, shard=None):
         setup = es.setup_constraints(D_h, nod.P, cg, shard=shard)
         cg = setup.cg                      # with any edges make_irreducible appended
     with phase("setup.emin_sweeps"):
-        vals, energy, res = emin_sweeps(S, setup, cfg.omega, cfg.iterations, shard=shard)
+        vals, energy, res = emin_sweeps(S, setup, cfg.omega, 0 if rsamg else cfg.iterations,
+                                        shard=shard)
     P = setup.pattern
     P_e = DeviceCSR(P.rowptr, P.col, vals, P.shape)
     prol = EdgeProlongator(P_e=P_e, energy_history=energy, commutator_residual=res,

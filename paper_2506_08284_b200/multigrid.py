@@ -17,6 +17,7 @@ polynomial in the reference's own sweeper seam for parity.
 import math
 import os
 from dataclasses import dataclass, field
+from types import SimpleNamespace
 
 import numpy as np
 import torch
@@ -437,6 +438,31 @@ def v_cycle_preconditioner(h):
     apply.graph_safe = not _trace.ENABLED     # tracing inserts host syncs
     apply.hierarchy = h
     return apply
+
+
+def hiptmair_preconditioner(level):
+    """One symmetric hybrid sweep from a zero guess as a stand-alone
+    preconditioner (multigrid.py:198-201), graph-capturable like the V-cycle."""
+    def apply(b):
+        with phase("solve.hiptmair"):
+            return hiptmair_smooth(level, None, b, x_zero=True)
+    apply.graph_safe = not _trace.ENABLED
+    # pcg_solve keeps its captured iteration on this holder and checks the
+    # level's sweepers after the solve, as for a hierarchy
+    holder = getattr(level, "_relax_holder", None)
+    if holder is None:
+        holder = level._relax_holder = SimpleNamespace(levels=[level])
+    apply.hierarchy = holder
+    return apply
+
+
+def fine_level(A_e, S_e, D, cfg=None):
+    """Single smoothing level without grid transfers, for the relaxation-only
+    comparison (multigrid.py:204-207). ``cfg`` (not a reference argument)
+    picks the smoother; the default is the Chebyshev-3 performance smoother."""
+    cfg = cfg or SolverConfig()
+    A_e, S_e, D = as_device_csr(A_e), as_device_csr(S_e), as_device_csr(D)
+    return _make_level(A_e, S_e, D, cfg)
 
 
 @dataclass

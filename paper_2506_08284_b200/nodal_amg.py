@@ -89,6 +89,17 @@ def aggregate_host(strength):
                        membership=torch.from_numpy(memb).to(strength.rowptr.device))
 
 
+def tentative_prolongator(agg):
+    """Piecewise-constant transfer, one unit entry per row at the node's
+    aggregate (nodal_amg.py:91-96), built in place from the membership."""
+    n = agg.n_fine
+    dev = agg.membership.device
+    rp = torch.arange(n + 1, dtype=torch.int64, device=dev)
+    ci = agg.membership.to(torch.int32)
+    v = torch.ones(n, dtype=torch.float64, device=dev)
+    return DeviceCSR(rp, ci, v, (n, agg.n_agg))
+
+
 def _power_start(n):
     # the reference's deterministic start vector, formed by numpy on the host
     # (nodal_amg.py:106) and uploaded once

@@ -83,13 +83,25 @@ CASES = {
     "C1": (16, True, 1.0, 1000, 0, True),
     "N16n": (16, False, 1e-2, 200, 1, False),
     "C2": (32, True, 1e-2, 1000, 1, False),
+    # RSAMG baseline mode (EminConfig(mode="rsamg"), edge_prolongator.py:200-213)
+    "R8d": (8, True, 1.0, 100, 0, True, "rsamg"),
+    "R12n": (12, False, 1e-2, 100, 2, True, "rsamg"),
+    "R16d": (16, True, 1.0, 200, 0, True, "rsamg"),
+}
+
+# relaxation-only mode (multigrid.py:198-207): PCG preconditioned by one
+# stand-alone Hiptmair sweep on the fine level; (N, dirichlet, sigma, seed)
+RELAX = {
+    "X8d": (8, True, 1e-2, 0),
+    "X12n": (12, False, 1.0, 3),
 }
 
 
-def run_case(name, N, dirichlet, sigma, coarse_size, seed, full):
+def run_case(name, N, dirichlet, sigma, coarse_size, seed, full, mode="sphcurl"):
+    from hcurlamg.edge_prolongator import EminConfig
     m = build_structured_mesh(3, "hex", N + 1, dirichlet)
     s = discretize(m, sigma)
-    cfg = mg.SolverConfig(coarse_size=coarse_size)
+    cfg = mg.SolverConfig(coarse_size=coarse_size, emin=EminConfig(mode=mode))
     t0 = time.perf_counter()
     h = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, cfg)
     t_setup = time.perf_counter() - t0
@@ -99,7 +111,7 @@ def run_case(name, N, dirichlet, sigma, coarse_size, seed, full):
     t_solve = time.perf_counter() - t0
 
     meta = {"N": N, "dirichlet": dirichlet, "sigma": sigma,
-            "coarse_size": coarse_size, "seed": seed,
+            "coarse_size": coarse_size, "seed": seed, "mode": mode,
             "t_setup_ref": t_setup, "t_solve_ref": t_solve,
             "n_levels": h.n_levels,
             "n_edges": [lv.A_e.shape[0] for lv in h.levels],
@@ -159,7 +171,11 @@ def run_case(name, N, dirichlet, sigma, coarse_size, seed, full):
     for li, lv in enumerate(h.levels[:-1]):
         strength = na.strength_graph(_an(h, li, s), 0.0)
         agg = na.aggregate(strength)
-        nod = na.smooth_and_normalize(_an(h, li, s), na.tentative_prolongator(agg))
+        if mode == "rsamg":
+            nod = na.NodalProlongator(P=na.tentative_prolongator(agg), omega_used=0.0,
+                                      rho_estimate=0.0)
+        else:
+            nod = na.smooth_and_normalize(_an(h, li, s), na.tentative_prolongator(agg))
         assert (nod.P != lv.P_n).nnz == 0
         Pc = cgm.gen_piecewise_const(nod.P, 2)
         assign = Pc.indices[Pc.indptr[:-1]].astype(np.int64)
@@ -214,6 +230,23 @@ def _an(h, li, s):
             An.append(C)
         _AN_CACHE[key] = An
     return _AN_CACHE[key][li]
+
+
+def relax_case(N, dirichlet, sigma, seed):
+    """Relaxation-only PCG: hiptmair_preconditioner(fine_level(A_e, S, D))
+    (multigrid.py:198-207) with the reference's Gauss-Seidel sweeps."""
+    m = build_structured_mesh(3, "hex", N + 1, dirichlet)
+    s = discretize(m, sigma)
+    lv = mg.fine_level(s.A_e, s.S, s.D)
+    b = np.random.default_rng(seed).uniform(-1.0, 1.0, s.A_e.shape[0])
+    res = mg.pcg_solve(lv.A_e, b, mg.hiptmair_preconditioner(lv))
+    meta = {"N": N, "dirichlet": dirichlet, "sigma": sigma, "seed": seed,
+            "n_edges": int(s.A_e.shape[0]), "nodal_aux_nnz": int(lv.nodal_aux.nnz),
+            "iterations": res.iterations, "status": res.status,
+            "residual_history": res.residual_history,
+            "precond_history": res.precond_history,
+            "relative_residual": res.relative_residual}
+    return meta, {"x": res.x}
 
 
 def error_cases():
@@ -272,6 +305,14 @@ def main(which):
     if "errors" in which:
         with open(os.path.join(HERE, "errors.json"), "w") as f:
             json.dump(error_cases(), f, indent=1)
+    for name, spec in RELAX.items():
+        if which and name not in which:
+            continue
+        meta, arrays = relax_case(*spec)
+        with open(os.path.join(HERE, f"relax_{name}.json"), "w") as f:
+            json.dump(meta, f, indent=1)
+        np.savez_compressed(os.path.join(HERE, f"relax_{name}.npz"), **arrays)
+        print(name, "relaxation-only its", meta["iterations"], flush=True)
     if "inputs" in which:
         with open(os.path.join(HERE, "inputs.json"), "w") as f:
             json.dump(inputs_table(), f, indent=1, sort_keys=True)
@@ -290,4 +331,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(set(sys.argv[1:]) or set(["inputs", "errors"] + list(CASES)))
+    main(set(sys.argv[1:]) or set(["inputs", "errors"] + list(CASES) + list(RELAX)))

@@ -52,3 +52,34 @@ def rel_max_diff(A, B):
 
 
 CASES = ["N4n", "N6d", "N8d", "N10n", "C1", "N16n", "C2"]
+
+
+RSAMG = ["R8d", "R12n", "R16d"]
+RELAX = ["X8d", "X12n"]
+
+
+def load_relax(name):
+    with open(os.path.join(GOLDEN, f"relax_{name}.json")) as f:
+        meta = json.load(f)
+    return meta, dict(np.load(os.path.join(GOLDEN, f"relax_{name}.npz")))
+
+
+def roundoff_pattern_diff(A, B, tol=1e-12):
+    """Entries stored in exactly one of A, B: (count, max |value| / max |B|).
+    rsamg's coarse patterns keep or drop entries by exact cancellation of
+    values that carry the reference's QR round-off,
+    so pattern parity there means: every entry in the symmetric difference
+    is round-off, |a| <= tol max|B|."""
+    A = sp.csr_matrix(A)
+    B = sp.csr_matrix(B)
+    pa = sp.csr_matrix((np.ones(A.nnz), A.indices, A.indptr), shape=A.shape)
+    pb = sp.csr_matrix((np.ones(B.nnz), B.indices, B.indptr), shape=B.shape)
+    only = abs(pa - pb)
+    only.eliminate_zeros()
+    if only.nnz == 0:
+        return 0, 0.0
+    mask = only.tocoo()
+    va = np.asarray(A[mask.row, mask.col]).ravel()
+    vb = np.asarray(B[mask.row, mask.col]).ravel()
+    scale = max(float(abs(B).max()) if B.nnz else 0.0, 1e-300)
+    return int(only.nnz), float(np.max(np.abs(np.concatenate([va, vb])))) / scale

@@ -127,3 +127,57 @@ def test_oracle_error_case():
     # the magnitudes are round-off of a collapsed coarse operator; the
     # decision and the level must agree
     assert str(e.value).split(":")[0] == msg.split(":")[0]
+
+
+@pytest.mark.parametrize("name", ["R8d", "R12n", "R16d"])
+def test_oracle_rsamg(name):
+    """RSAMG mode (edge_prolongator.py:200-213): tentative nodal transfer, no
+    emin sweeps. BIT: aggregates, P_n, coarse topology, P_e pattern, level
+    sizes; TOL: P_e and coarse operators; coarse patterns equal modulo
+    round-off entries; GS iterations identical."""
+    from golden_util import rel_max_diff, roundoff_pattern_diff
+    meta, arrays = load_case(name)
+    assert meta["mode"] == "rsamg"
+    s = discretize_hex(meta["N"], meta["sigma"], meta["dirichlet"])
+    h = O.build_hierarchy(s.A_e, s.S, s.A_n, s.D, coarse_size=meta["coarse_size"],
+                          mode="rsamg")
+    assert [lv.A_e.shape[0] for lv in h.levels] == meta["n_edges"]
+    for li, (lv, L) in enumerate(zip(h.levels[:-1], meta["levels"])):
+        assert sha(lv.membership.astype(np.int64)) == L["membership"]
+        assert float(lv.omega).hex() == L["omega_hex"] == (0.0).hex()
+        assert csr_hash(lv.P_n) == L["P_n"]
+        assert sha(lv.assignment.astype(np.int64)) == L["assignment"]
+        assert sha(lv.coarse.pairs.astype(np.int64)) == L["pairs"]
+        assert sha(lv.coarse.singles.astype(np.int64)) == L["singles"]
+        P = lv.P_e
+        assert sha(P.indptr.astype(np.int64), P.indices.astype(np.int64)) == L["P_e_pattern"]
+        ref = golden_csr(arrays, f"L{li}_P_e", P.shape)
+        assert rel_max_diff(P, ref) <= 1e-10
+        assert lv.emin.energy_history == L["emin_energy"] == []
+        assert lv.emin.commutator_residual <= 1e-12
+        nxt = h.levels[li + 1]
+        for key, M in (("A_e", nxt.A_e), ("S_e", nxt.S_e)):
+            G = golden_csr(arrays, f"L{li + 1}_{key}", M.shape)
+            assert rel_max_diff(M, G) <= 1e-10
+            _, mag = roundoff_pattern_diff(M, G)
+            assert mag <= 1e-12
+    res = O.solve(h, np.random.default_rng(meta["seed"]).uniform(-1, 1, s.A_e.shape[0]))
+    assert res.iterations == meta["gs"]["iterations"]
+    assert np.max(np.abs(res.x - arrays["gs_x"])) <= 1e-6 * np.max(np.abs(arrays["gs_x"]))
+
+
+@pytest.mark.parametrize("name", ["X8d", "X12n"])
+def test_oracle_relaxation_only(name):
+    """Relaxation-only PCG (fine_level + hiptmair_preconditioner,
+    multigrid.py:198-207) with the reference's Gauss-Seidel sweeps."""
+    from golden_util import load_relax
+    meta, arrays = load_relax(name)
+    s = discretize_hex(meta["N"], meta["sigma"], meta["dirichlet"])
+    lv = O.fine_level(s.A_e, s.S, s.D)
+    assert lv.nodal_aux.nnz == meta["nodal_aux_nnz"]
+    b = np.random.default_rng(meta["seed"]).uniform(-1, 1, s.A_e.shape[0])
+    res = O.relax_solve(lv, b)
+    assert res.status == meta["status"]
+    assert res.iterations == meta["iterations"]
+    np.testing.assert_allclose(res.residual_history, meta["residual_history"], rtol=1e-6)
+    assert np.max(np.abs(res.x - arrays["x"])) <= 1e-8 * np.max(np.abs(arrays["x"]))

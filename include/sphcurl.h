@@ -241,6 +241,20 @@ int sphc_pcg_direction(int64_t n, const double *sc, const double *z, double *p, 
 /* sc[RZ] = sc[RZN] */
 int sphc_pcg_rotate(double *sc, void *stream);
 
+/* One PCG iteration (the loop body of multigrid.py:241-270) captured from
+ * `stream` into a CUDA graph and replayed per iteration. Plain runtime
+ * stream capture (thread-local mode): the captured launches must not
+ * allocate. sphc_graph_end writes the instantiated cudaGraphExec_t to
+ * exec[0]. */
+int sphc_graph_begin(void *stream);
+int sphc_graph_end(void **exec, void *stream);
+int sphc_graph_launch(void *exec, void *stream);
+int sphc_graph_destroy(void *exec);
+
+/* dst (pinned host) <- src (device), `bytes` bytes, asynchronous on stream
+ * (capturable; the PCG scalars' per-iteration readback). */
+int sphc_copy_d2h(void *dst, const void *src, int64_t bytes, void *stream);
+
 /* y = A x for a dense row-major n x n A (coarsest level, explicit inverse of
  * the reference's lu_factor/lu_solve pair, multigrid.py:157,181). */
 int sphc_dense_gemv(int64_t n, const double *A, const double *x, double *y, void *stream);

@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import device as dv
-from .device import DeviceCSR, Status, as_device_csr, call
+from .device import checked, DeviceCSR, Status, as_device_csr, call
 
 
 @dataclass
@@ -76,6 +76,7 @@ def coarse_gradient_from_edges(pairs, singles, n_nodes):
                           ep_a=ep_a, ep_b=ep_b, single_id=sid, augmented_edges=[])
 
 
+@checked
 def gen_piecewise_const(P, n_passes=2):
     """Algorithm 1 (coarse_gradient.py:36-103): the column assigned to every
     row (int64, device). Returned as the assignment vector rather than the
@@ -96,13 +97,16 @@ def gen_piecewise_const(P, n_passes=2):
     assign = torch.empty(m_h, **i64)
     call("sphc_piecewise_const", m_h, m_H, P.rowptr, P.col, P.val, Pc.rowptr, Pc.col, Pc.val,
          int(n_passes), target, counts, srow, owner, changed, flags, pos, lst, assign, st.t)
-    rows = st.rows()
-    if "PC_EMPTY_COLUMN" in rows:
-        raise ValueError(f"empty column {rows['PC_EMPTY_COLUMN']} cannot be assigned any row")
-    if "PC_EMPTY_ROW" in rows:
-        raise ValueError(f"row {rows['PC_EMPTY_ROW']} has no entries to assign")
-    if "PC_NO_DONOR" in rows:
-        raise ValueError(f"empty column {rows['PC_NO_DONOR']} cannot be assigned any row")
+
+    def check(rows):
+        if "PC_EMPTY_COLUMN" in rows:
+            raise ValueError(f"empty column {rows['PC_EMPTY_COLUMN']} cannot be assigned "
+                             "any row")
+        if "PC_EMPTY_ROW" in rows:
+            raise ValueError(f"row {rows['PC_EMPTY_ROW']} has no entries to assign")
+        if "PC_NO_DONOR" in rows:
+            raise ValueError(f"empty column {rows['PC_NO_DONOR']} cannot be assigned any row")
+    st.defer(check)
     return assign
 
 
@@ -125,6 +129,7 @@ def gen_piecewise_const_host(P, n_passes=2):
     return torch.from_numpy(assign).to(P.rowptr.device)
 
 
+@checked
 def build_coarse_gradient(D_h, assignment, n_agg):
     """Coarse edges from the projected node-graph Laplacian plus the Dirichlet
     single-node edges (coarse_gradient.py:106-160, build_coarse_gradient
@@ -140,14 +145,13 @@ def build_coarse_gradient(D_h, assignment, n_agg):
     call("sphc_coarse_pairs_fill", n_e, D.rowptr, D.col, assignment, brp, cursor, bcol)
     st = Status()
     call("sphc_csr_sort_rows", n_agg, brp, bcol, None, st.t)
-    dv._raise_capacity(st)
+    st.defer(dv.capacity_check)
     call("sphc_unique_count", n_agg, brp, bcol, cnt)
-    arp, n_int = dv.scan(cnt)
-    acol = torch.empty(n_int, dtype=torch.int32, device=dev)
-    call("sphc_unique_fill", n_agg, brp, bcol, arp, acol)
     flags = torch.zeros(n_agg, dtype=torch.int64, device=dev)
     call("sphc_single_flags", n_e, D.rowptr, D.col, assignment, flags)
-    soff, n_single = dv.scan(flags)
+    (arp, n_int), (soff, n_single) = dv.scan_many(cnt, flags)
+    acol = torch.empty(n_int, dtype=torch.int32, device=dev)
+    call("sphc_unique_fill", n_agg, brp, bcol, arp, acol)
     n_edges = n_int + n_single
     dh_rp = torch.empty(n_edges + 1, dtype=torch.int64, device=dev)
     dh_ci = torch.empty(2 * n_int + n_single, dtype=torch.int32, device=dev)

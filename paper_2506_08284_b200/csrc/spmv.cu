@@ -161,6 +161,60 @@ extern "C" int sphc_pcg_rotate(double* sc, void* stream) {
   return 0;
 }
 
+// A captured graph and the number of libsphcurl kernels in it (a replay
+// counts them all in sphc_launch_count).
+struct SphcGraph {
+  cudaGraphExec_t exec;
+  unsigned long long kernels;
+};
+static thread_local unsigned long long g_capture_start = 0;
+
+extern "C" int sphc_graph_begin(void* stream) {
+  SPHC_CUDA(cudaStreamBeginCapture(as_stream(stream), cudaStreamCaptureModeThreadLocal));
+  g_capture_start = g_sphc_launches;
+  return 0;
+}
+
+extern "C" int sphc_graph_end(void** exec, void* stream) {
+  cudaGraph_t g = nullptr;
+  unsigned long long k = g_sphc_launches - g_capture_start;
+  g_sphc_launches = g_capture_start;  // captured, not launched
+  SPHC_CUDA(cudaStreamEndCapture(as_stream(stream), &g));
+  cudaGraphExec_t e = nullptr;
+  cudaError_t err = cudaGraphInstantiate(&e, g, 0);
+  cudaGraphDestroy(g);
+  if (err != cudaSuccess) {
+    sphc_set_error("cudaGraphInstantiate: %s", cudaGetErrorString(err));
+    return SPHC_ERR_CUDA;
+  }
+  exec[0] = (void*)new SphcGraph{e, k};
+  return 0;
+}
+
+extern "C" int sphc_graph_launch(void* exec, void* stream) {
+  SphcGraph* G = (SphcGraph*)exec;
+  SPHC_CUDA(cudaGraphLaunch(G->exec, as_stream(stream)));
+  g_sphc_launches += G->kernels;
+  return 0;
+}
+
+extern "C" int sphc_graph_destroy(void* exec) {
+  SphcGraph* G = (SphcGraph*)exec;
+  if (!G) return 0;
+  cudaError_t err = cudaGraphExecDestroy(G->exec);
+  delete G;
+  if (err != cudaSuccess) {
+    sphc_set_error("cudaGraphExecDestroy: %s", cudaGetErrorString(err));
+    return SPHC_ERR_CUDA;
+  }
+  return 0;
+}
+
+extern "C" int sphc_copy_d2h(void* dst, const void* src, int64_t bytes, void* stream) {
+  SPHC_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, as_stream(stream)));
+  return 0;
+}
+
 // y = A x, A dense row-major n x n: one warp per row, fixed-order reduction
 __global__ void k_dense_gemv(i64 n, const double* __restrict__ A, const double* __restrict__ x,
                              double* __restrict__ y) {

@@ -6,6 +6,7 @@ tensors (torch is the allocator / stream plumbing; every numeric operation is
 a libsphcurl kernel).
 """
 
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -40,14 +41,99 @@ def call(name, *args):
 
 
 class Status:
-    """Device error slots: slot k holds the lowest row failing check k."""
+    """Device error slots: slot k holds the lowest row failing check k.
+
+    Slots come out of pooled blocks (one fill launch per 64 statuses). A
+    check is either read now (``rows()``) or deferred (``defer(handler)``):
+    deferred checks ride along with the next host readback of any kind
+    (``readback``, ``scan``), run in program order before that readback's
+    own values are used, so an error surfaces with the reference's message
+    and order at the cost of no extra synchronisation."""
+
+    _block = None
+    _next = 0
 
     def __init__(self):
-        self.t = torch.full((SLOTS,), INT64_MAX, dtype=torch.int64, device=device())
+        blk = Status._block
+        if blk is None or Status._next >= blk.shape[0] or blk.device != device():
+            blk = Status._block = torch.full((64, SLOTS), INT64_MAX, dtype=torch.int64,
+                                             device=device())
+            Status._next = 0
+        self.t = blk[Status._next]
+        Status._next += 1
 
     def rows(self):
-        h = self.t.cpu().numpy()
-        return {k: int(h[v]) for k, v in ST.items() if h[v] != INT64_MAX}
+        return _decode(readback(self.t)[0])
+
+    def defer(self, handler):
+        _PENDING.append((self, handler))
+
+
+def _decode(h):
+    return {k: int(h[v]) for k, v in ST.items() if h[v] != INT64_MAX}
+
+
+_PENDING = []
+
+
+def readback(*tensors):
+    """Small device tensors -> numpy arrays in ONE device-to-host copy, after
+    first running every deferred status check (Status.defer) in order."""
+    pend = list(_PENDING)
+    _PENDING.clear()
+    parts = [st.t for st, _ in pend] + [t.reshape(-1) for t in tensors]
+    if not parts:
+        return []
+    if len(parts) == 1:
+        hs = [parts[0].cpu().numpy()]
+    else:
+        raw = torch.cat([p.contiguous().view(torch.uint8) for p in parts]).cpu().numpy()
+        hs, o = [], 0
+        for p in parts:
+            nb = p.numel() * p.element_size()
+            hs.append(raw[o:o + nb].view(_NP[p.dtype]))
+            o += nb
+    for (st, handler), h in zip(pend, hs):
+        handler(_decode(h))
+    return hs[len(pend):]
+
+
+def flush_checks():
+    """Run the deferred status checks now (end of a public entry point)."""
+    if _PENDING:
+        readback()
+
+
+_DEPTH = [0]
+
+
+def checked(fn):
+    """Public entry points: the outermost one runs every check deferred
+    inside it before returning. If it exits by an exception, the deferred
+    checks still run first, so an earlier device-detected error wins, as it
+    would in the reference's sequential code."""
+    @functools.wraps(fn)
+    def wrap(*args, **kwargs):
+        _DEPTH[0] += 1
+        try:
+            out = fn(*args, **kwargs)
+        except BaseException:
+            _DEPTH[0] -= 1
+            if _DEPTH[0] == 0:
+                try:
+                    flush_checks()
+                finally:
+                    _PENDING.clear()
+            raise
+        _DEPTH[0] -= 1
+        if _DEPTH[0] == 0:
+            flush_checks()
+        return out
+    return wrap
+
+
+_NP = {torch.int64: np.int64, torch.int32: np.int32, torch.float64: np.float64,
+       torch.uint8: np.uint8, torch.bool: np.bool_}
 
 
 _PINNED = {}
@@ -232,11 +318,24 @@ def zeros_i64(n):
 
 
 def scan(counts):
-    """Exclusive scan -> (rowptr [n+1], total) (one host sync for the total)."""
+    """Exclusive scan -> (rowptr [n+1], total) (one host sync for the total,
+    shared with any deferred status checks)."""
     n = counts.numel()
     rp = torch.empty(n + 1, dtype=torch.int64, device=counts.device)
     call("sphc_scan_i64", n, counts, rp)
-    return rp, int(rp[n].item())
+    return rp, int(readback(rp[n:n + 1])[0][0])
+
+
+def scan_many(*counts):
+    """Several exclusive scans, one host sync for all totals."""
+    rps = []
+    for c in counts:
+        n = c.numel()
+        rp = torch.empty(n + 1, dtype=torch.int64, device=c.device)
+        call("sphc_scan_i64", n, c, rp)
+        rps.append(rp)
+    tot = readback(torch.stack([rp[-1] for rp in rps]))[0]
+    return [(rp, int(t)) for rp, t in zip(rps, tot)]
 
 
 def dot(x, y, out=None):
@@ -270,6 +369,7 @@ def reciprocal(x, zero_sub=None):
     return y
 
 
+@checked
 def transpose(A, status=None):
     st = status or Status()
     nr, nc = A.shape
@@ -278,23 +378,38 @@ def transpose(A, status=None):
     tv = empty_f64(A.nnz) if A.val is not None else None
     call("sphc_csr_transpose", nr, nc, A.nnz, A.rowptr, A.col, A.val, trp, tci, tv, st.t)
     if status is None:
-        _raise_capacity(st)
+        st.defer(capacity_check)
     return DeviceCSR(trp, tci, tv, (nc, nr))
 
 
 def _raise_capacity(st):
-    rows = st.rows()
+    capacity_check(st.rows())
+
+
+def capacity_check(rows):
     for k in ("SORT_CAPACITY", "SPGEMM_CAPACITY", "EMIN_CAPACITY"):
         if k in rows:
             raise RuntimeError(f"device kernel capacity exceeded ({k}) at row {rows[k]}")
 
 
+@checked
 def drop_zeros(A):
     """compress(A, 0.0): remove stored exact zeros (sparse_ops.py:107-113)."""
+    return drop_zeros_many(A)[0]
+
+
+def drop_zeros_many(*mats):
+    """drop_zeros of several matrices with one host sync for all counts."""
+    cnts = []
+    for A in mats:
+        cnt = torch.empty(A.shape[0], dtype=torch.int64, device=A.rowptr.device)
+        call("sphc_csr_count_nonzero", A.shape[0], A.rowptr, A.val, cnt)
+        cnts.append(cnt)
+    return [_compact(A, rp, nnz) for A, (rp, nnz) in zip(mats, scan_many(*cnts))]
+
+
+def _compact(A, rp, nnz):
     n = A.shape[0]
-    cnt = torch.empty(n, dtype=torch.int64, device=A.rowptr.device)
-    call("sphc_csr_count_nonzero", n, A.rowptr, A.val, cnt)
-    rp, nnz = scan(cnt)
     if nnz == A.nnz:
         return A
     ci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
@@ -309,6 +424,7 @@ def _rows(A, lo):
     return A.rowptr[lo:]
 
 
+@checked
 def spgemm(A, B, drop=True, ordered=False, shard=None):
     """C = A B; exact zeros dropped like scipy's product (drop=True).
     ordered=True reproduces scipy csr_matmat's accumulation bit for bit.
@@ -324,8 +440,8 @@ def spgemm(A, B, drop=True, ordered=False, shard=None):
     if shard is not None:
         shard.gather_ranges(cnt, shard.bounds(n))
         shard.min_(st.t)
+    st.defer(capacity_check)
     rp, nnz = scan(cnt)
-    _raise_capacity(st)
     ci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
     v = empty_f64(nnz)
     for _, lo, hi in blocks:
@@ -341,10 +457,14 @@ def spgemm(A, B, drop=True, ordered=False, shard=None):
 
 
 def same_pattern(A, B):
-    return (A.shape == B.shape and A.nnz == B.nnz and torch.equal(A.rowptr, B.rowptr)
-            and torch.equal(A.col, B.col))
+    if A.shape != B.shape or A.nnz != B.nnz:
+        return False
+    if A.rowptr is B.rowptr and A.col is B.col:      # shared index arrays: no sync
+        return True
+    return torch.equal(A.rowptr, B.rowptr) and torch.equal(A.col, B.col)
 
 
+@checked
 def spgemm_pair(A1, A2, B1, B2, drop=True, shard=None):
     """(A1 B1, A2 B2) for A1/A2 and B1/B2 with shared patterns, one pass.
     Stored exact zeros are dropped per product (drop=True)."""
@@ -358,8 +478,8 @@ def spgemm_pair(A1, A2, B1, B2, drop=True, shard=None):
     if shard is not None:
         shard.gather_ranges(cnt, shard.bounds(n))
         shard.min_(st.t)
+    st.defer(capacity_check)
     rp, nnz = scan(cnt)
-    _raise_capacity(st)
     ci = torch.empty(nnz, dtype=torch.int32, device=A1.rowptr.device)
     v1, v2 = empty_f64(nnz), empty_f64(nnz)
     for _, lo, hi in blocks:
@@ -372,7 +492,7 @@ def spgemm_pair(A1, A2, B1, B2, drop=True, shard=None):
             shard.gather_ranges(t, off)
     shape = (A1.shape[0], B1.shape[1])
     C1, C2 = DeviceCSR(rp, ci, v1, shape), DeviceCSR(rp, ci, v2, shape)
-    return (drop_zeros(C1), drop_zeros(C2)) if drop else (C1, C2)
+    return tuple(drop_zeros_many(C1, C2)) if drop else (C1, C2)
 
 
 @dataclass

@@ -17,7 +17,7 @@ from . import coarse_gradient as cgrad
 from . import device as dv
 from . import emin_setup as es
 from . import nodal_amg as na
-from .device import DeviceCSR, Status, as_device_csr, call
+from .device import checked, DeviceCSR, Status, as_device_csr, call
 from .trace import phase
 
 
@@ -49,19 +49,28 @@ class EdgeProlongator:
     n_augmented: int = 0
 
 
+@checked
 def jacobi_diag_inverse(S):
     """1 / diag(S) with zeros replaced by 1e-12 max (edge_prolongator.py:159-167)."""
     d = dv.diagonal(S)
     # diag(S) >= 0 for the PSD curl-curl operator, so max d = max |d|
-    top = dv.maxabs(d)
-    t = float(top.item()) if d.numel() else 0.0
-    if t <= 0.0:
-        raise ValueError("curl-curl diagonal is entirely zero")
-    sub = dv.empty_f64(1)
-    sub.fill_(1e-12 * t)
+    top = dv.zeros_f64(1)
+    if d.numel():
+        dv.maxabs(d, top)
+    sub = top * 1e-12
+    # flag "all zero" in a status slot on the device (no host sync here)
+    st = Status()
+    k = dv.ST["ZERO_DIAG"]
+    st.t[k:k + 1].masked_fill_(top <= 0.0, 0)
+
+    def check(rows):
+        if "ZERO_DIAG" in rows:
+            raise ValueError("curl-curl diagonal is entirely zero")
+    st.defer(check)
     return dv.reciprocal(d, sub)
 
 
+@checked
 def emin_sweeps(S, setup, omega, iterations, shard=None):
     """Projected damped-Jacobi sweeps; returns (values, energies, residual).
     With ``shard`` every rank sweeps its block of fine edges and the value
@@ -110,11 +119,13 @@ def emin_sweeps(S, setup, omega, iterations, shard=None):
     dv.vsum(e_row, esum[iterations:iterations + 1])
     if shard is not None:
         shard.min_(st.t)
-    es._raise(st, S)
-    energies = [float(x) for x in esum.cpu().numpy()] if iterations else []
-    return vals, energies, float(res.item())
+    st.defer(es._checker(S))
+    eh, rh = dv.readback(esum, res)
+    energies = [float(x) for x in eh] if iterations else []
+    return vals, energies, float(rh[0])
 
 
+@checked
 def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None, shard=None):
     """Edge prolongator and coarse gradient for one level
     (edge_prolongator.py:184-228). Returns

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import device as dv
-from .device import DeviceCSR, Status, as_device_csr, call
+from .device import checked, DeviceCSR, Status, as_device_csr, call
 from .trace import phase
 
 
@@ -32,26 +32,32 @@ class EminSetup:
     n_augmented: int = 0
 
 
+def _checker(D):
+    """Deferred check of the emin kernels' status slots (Status.defer)."""
+    def check(rows):
+        if "MALFORMED_GRAD" in rows:
+            b = rows["MALFORMED_GRAD"]
+            rp = D.rowptr[b:b + 2].cpu().numpy()
+            raise ValueError(f"malformed gradient: row {b} has {int(rp[1] - rp[0])} nonzeros")
+        if "EMPTY_J" in rows:
+            raise ValueError(f"fine edge {rows['EMPTY_J']} has an empty constraint "
+                             "pattern (isolated edge or pattern bug)")
+        if "EMIN_CAPACITY" in rows:
+            raise RuntimeError(f"fine edge {rows['EMIN_CAPACITY']}: constraint block exceeds "
+                               f"the device kernel capacity (|J| <= 16, |I| <= 128)")
+        if "REDUCIBLE" in rows:
+            # only reachable if a block is still reducible after the repair pass
+            raise RuntimeError(
+                f"fine edge {rows['REDUCIBLE']}: constraint block reducible after the "
+                "make_irreducible pass (internal error)")
+        if "RANK_LOW" in rows:
+            raise ValueError(f"fine edge {rows['RANK_LOW']}: numerical rank below the "
+                             "expected rank (topology bug)")
+    return check
+
+
 def _raise(st, D):
-    rows = st.rows()
-    if "MALFORMED_GRAD" in rows:
-        b = rows["MALFORMED_GRAD"]
-        rp = D.rowptr[b:b + 2].cpu().numpy()
-        raise ValueError(f"malformed gradient: row {b} has {int(rp[1] - rp[0])} nonzeros")
-    if "EMPTY_J" in rows:
-        raise ValueError(f"fine edge {rows['EMPTY_J']} has an empty constraint "
-                         "pattern (isolated edge or pattern bug)")
-    if "EMIN_CAPACITY" in rows:
-        raise RuntimeError(f"fine edge {rows['EMIN_CAPACITY']}: constraint block exceeds "
-                           f"the device kernel capacity (|J| <= 16, |I| <= 128)")
-    if "REDUCIBLE" in rows:
-        # only reachable if a block is still reducible after the repair pass
-        raise RuntimeError(
-            f"fine edge {rows['REDUCIBLE']}: constraint block reducible after the "
-            "make_irreducible pass (internal error)")
-    if "RANK_LOW" in rows:
-        raise ValueError(f"fine edge {rows['RANK_LOW']}: numerical rank below the "
-                         "expected rank (topology bug)")
+    _checker(D)(st.rows())
 
 
 def _view(t, lo):
@@ -87,8 +93,7 @@ def _count(D, P, cg, xrp, xeid, flags, shard=None):
 def _fill(D, P, cg, icount, jcount, xrp, xeid, st, rowflag=None, shard=None):
     n_e = D.shape[0]
     dev = D.rowptr.device
-    trp, tnnz = dv.scan(jcount)
-    erp, ennz = dv.scan(icount)
+    (trp, tnnz), (erp, ennz) = dv.scan_many(jcount, icount)
     tci = torch.empty(tnnz, dtype=torch.int32, device=dev)
     tv = torch.empty(tnnz, dtype=torch.float64, device=dev)
     eci = torch.empty(ennz, dtype=torch.int32, device=dev)
@@ -113,6 +118,7 @@ def _fill(D, P, cg, icount, jcount, xrp, xeid, st, rowflag=None, shard=None):
             DeviceCSR(erp, eci, ev, (n_e, cg.n_edges)))
 
 
+@checked
 def setup_constraints(D_h, P_n, cg, shard=None):
     """Pattern, irreducibility, factor checks and feasible guess for every
     fine edge (emin_setup.py:256-336 + edge_prolongator.py:104-126).
@@ -125,32 +131,37 @@ def setup_constraints(D_h, P_n, cg, shard=None):
     D = as_device_csr(D_h)
     P = as_device_csr(P_n)
     n_e = D.shape[0]
+    check = _checker(D)
     with phase("emin.count"):
         st, icount, jcount, rmax2, dims, rowflag, rowmax = _count(D, P, cg, None, None, True,
                                                                   shard)
-        _raise(st, D)
-    rm = rmax2.cpu().numpy()
-    rdp_scale = max(1.0, float(rm[0]))
+    # the count pass's checks ride on the fill pass's scan readback
+    st.defer(check)
     # the fill pass factors every block and flags the reducible ones
     with phase("emin.fill"):
         T, pattern = _fill(D, P, cg, icount, jcount, None, None, st, rowflag, shard)
-        _raise(st, D)
     flags = rowflag
-    need = (flags & 1).bool()
-    if rm[1] > 1e-12 * rdp_scale:
-        need |= ((flags & 2).bool() & (rowmax > 1e-12 * rdp_scale))
+    # reducible rows, and empty-pattern rows whose commutator row exceeds
+    # 1e-12 rdp_scale (rdp_scale = max(1, max|R_dp|)); decided on the device
+    scale = torch.clamp(rmax2[0:1], min=1.0)
+    need = (flags & 1).bool() | ((rmax2[1:2] > 1e-12 * scale)
+                                 & (flags & 2).bool() & (rowmax > 1e-12 * scale))
+    st.defer(check)
+    rm, any_need, h = dv.readback(rmax2, need.any(), dims)
+    rdp_scale = max(1.0, float(rm[0]))
     n_aug = 0
-    if bool(need.any()):
+    if bool(any_need[0]):
         from . import repair
         with phase("emin.repair"):
             cg, xrp, xeid, n_aug = repair.make_irreducible_pass(
                 need, flags, rowmax, rdp_scale, T, pattern, cg)
         with phase("emin.refill"):
             st, icount, jcount, rmax2, dims, _, _ = _count(D, P, cg, xrp, xeid, False, shard)
-            _raise(st, D)
+            st.defer(check)
             T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st, shard=shard)
-            _raise(st, D)
-    h = dims.cpu().numpy().reshape(129, 17)
+            st.defer(check)
+            h = dv.readback(dims)[0]
+    h = h.reshape(129, 17)
     nz = np.argwhere(h)
     counter = Counter({(int(i), int(j)): int(h[i, j]) for i, j in nz})
     return EminSetup(T=T, pattern=pattern, cg=cg, subproblem_dims=counter,

@@ -23,13 +23,15 @@ import numpy as np
 import torch
 
 from . import device as dv
-from .device import DeviceCSR, Status, as_device_csr, call
+from .device import checked, DeviceCSR, Status, as_device_csr, call
 from .edge_prolongator import EminConfig, build_edge_prolongator
 from . import trace as _trace
 from .trace import phase
 
 _NULLSPACE_TOL = 1e-10
 USE_SELL = os.environ.get("SPHC_SELL", "1") != "0"
+USE_GRAPH = os.environ.get("SPHC_PCG_GRAPH", "1") != "0"
+
 CHEB_POWER_ITERS = 15
 CHEB_SAFETY = 1.1
 CHEB_RATIO = 30.0
@@ -64,6 +66,27 @@ def lanczos_max(alpha, beta):
     return float(np.linalg.eigvalsh(T)[-1]) if k else 0.0
 
 
+def _zero_diag_check(rows):
+    if "ZERO_DIAG" in rows:
+        raise ValueError(f"zero diagonal entry in row {rows['ZERO_DIAG']}")
+
+
+_UNFINISHED = []
+
+
+def finalize_sweepers():
+    """Read the Lanczos scalars of every sweeper built so far in one host
+    readback (with the deferred status checks) and form their Chebyshev
+    coefficients."""
+    pend = list(_UNFINISHED)
+    _UNFINISHED.clear()
+    live = [sw for sw in pend if sw._sc is not None]
+    hs = dv.readback(*[sw._sc for sw in live]) if live else (dv.flush_checks() or [])
+    it = iter(hs)
+    for sw in pend:
+        sw._finish(next(it) if sw._sc is not None else None)
+
+
 class ChebyshevSweeper:
     """Degree-d Jacobi-Chebyshev on [hi/30, hi], hi = 1.1 x (15-step Lanczos
     estimate of rho(D^-1 A)); ``symmetric(x, b)`` applies it once. Each
@@ -74,9 +97,7 @@ class ChebyshevSweeper:
         n = A.shape[0]
         st = Status()
         d = dv.diagonal(A, st)
-        rows = st.rows()
-        if "ZERO_DIAG" in rows:
-            raise ValueError(f"zero diagonal entry in row {rows['ZERO_DIAG']}")
+        st.defer(_zero_diag_check)
         self.dinv = dv.reciprocal(d)
         self.diag = d
         self.degree = degree
@@ -85,10 +106,21 @@ class ChebyshevSweeper:
         self.sell = dv.sell(A) if USE_SELL else None
         self.d = dv.empty_f64(n)
         self.buf = [dv.empty_f64(n), dv.empty_f64(n)]
-        self.hi, self.lo = self._bounds()
-        self.coefs = self._coefficients()
+        # the Lanczos scalars are read back together with every other
+        # sweeper's of the hierarchy (finalize_sweepers)
+        self.hi = self.lo = self.coefs = None
+        self._sc = self._lanczos()
+        _UNFINISHED.append(self)
 
-    def _bounds(self):
+    def _finish(self, sc):
+        k = CHEB_POWER_ITERS
+        lam = lanczos_max(*np.split(sc, [k])) if sc is not None else 1.0 / CHEB_SAFETY
+        self.hi = CHEB_SAFETY * lam
+        self.lo = self.hi / CHEB_RATIO
+        self.coefs = self._coefficients()
+        self._sc = None
+
+    def _lanczos(self):
         """hi = 1.1 x the largest Ritz value of a 15-step Lanczos run on
         D^-1 A (self-adjoint in the D inner product). A power method of the
         same length underestimates rho(D^-1 A) by >10% on curved meshes with
@@ -98,7 +130,7 @@ class ChebyshevSweeper:
         read per smoother."""
         n = self.A.shape[0]
         if n == 0:
-            return 1.0, 1.0 / CHEB_RATIO
+            return None
         k = CHEB_POWER_ITERS
         d = self.diag
         v, vprev = self.buf
@@ -118,9 +150,7 @@ class ChebyshevSweeper:
             dv.dot(w, dw, sq)
             vprev, v = v, vprev
             call("sphc_scale_by_norm", n, w, sq, v, beta[j + 1:j + 2])
-        lam = lanczos_max(*np.split(sc.cpu().numpy(), [k]))
-        hi = CHEB_SAFETY * lam
-        return hi, hi / CHEB_RATIO
+        return sc
 
     def _coefficients(self):
         theta = 0.5 * (self.hi + self.lo)
@@ -136,6 +166,8 @@ class ChebyshevSweeper:
 
     def symmetric(self, x, b, sweeps=1, x_zero=False):
         """Returns the smoothed iterate (a sweeper-owned buffer, never ``x``)."""
+        if self.coefs is None:
+            finalize_sweepers()
         A = self.A
         n = A.shape[0]
         cur = x
@@ -166,9 +198,7 @@ class GaussSeidelSweeper:
         n = A.shape[0]
         st = Status()
         dv.diagonal(A, st)
-        rows = st.rows()
-        if "ZERO_DIAG" in rows:
-            raise ValueError(f"zero diagonal entry in row {rows['ZERO_DIAG']}")
+        st.defer(_zero_diag_check)
         self.y = dv.empty_f64(n)
         self.ticket = torch.zeros(1, dtype=torch.int32, device=A.rowptr.device)
         self.status = Status()
@@ -268,7 +298,7 @@ def _check_nullspace(S, D, where, A=None, shard=None):
     m = dv.empty_f64(2)
     dv.maxabs(SD.val, m[0:1])
     dv.maxabs(S.val, m[1:2])
-    defect, smax = (float(x) for x in m.cpu().numpy())
+    defect, smax = (float(x) for x in dv.readback(m)[0])
     scale = max(smax, 1e-300)
     if defect > _NULLSPACE_TOL * scale:
         raise ValueError(
@@ -322,6 +352,7 @@ def _coarse_inverse(Ad):
     return 0.5 * (inv + inv.T)
 
 
+@checked
 def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
     """Galerkin hierarchy driven by the constrained edge prolongator
     (multigrid.py:119-161). ``shard`` (sharding.Sharding, optional; not a
@@ -397,6 +428,7 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
     last.r = dv.empty_f64(A_e.shape[0])
     nnz0 = levels[0].A_e.nnz
     oc = sum(lv.A_e.nnz for lv in levels) / nnz0
+    finalize_sweepers()
     return Hierarchy(levels=levels, coarse_factorization=inv, operator_complexity=oc)
 
 
@@ -456,13 +488,16 @@ def hiptmair_preconditioner(level):
     return apply
 
 
+@checked
 def fine_level(A_e, S_e, D, cfg=None):
     """Single smoothing level without grid transfers, for the relaxation-only
     comparison (multigrid.py:204-207). ``cfg`` (not a reference argument)
     picks the smoother; the default is the Chebyshev-3 performance smoother."""
     cfg = cfg or SolverConfig()
     A_e, S_e, D = as_device_csr(A_e), as_device_csr(S_e), as_device_csr(D)
-    return _make_level(A_e, S_e, D, cfg)
+    lv = _make_level(A_e, S_e, D, cfg)
+    finalize_sweepers()
+    return lv
 
 
 @dataclass
@@ -479,6 +514,32 @@ def _csr_key(A):
     return (A.rowptr.data_ptr(), A.col.data_ptr(), A.val.data_ptr(), A.shape)
 
 
+class PcgGraph:
+    """One PCG iteration captured from torch's current stream into a CUDA
+    graph through libsphcurl's runtime capture (no torch graph pool: the
+    iteration allocates nothing), replayed on the current stream."""
+
+    def __init__(self, body):
+        h = np.zeros(1, dtype=np.uint64)
+        call("sphc_graph_begin")
+        try:
+            body()
+        finally:
+            call("sphc_graph_end", h)
+        self.h = int(h[0])
+
+    def replay(self):
+        call("sphc_graph_launch", self.h)
+
+    def __del__(self):
+        if getattr(self, "h", 0):
+            try:
+                call("sphc_graph_destroy", self.h)
+            except Exception:
+                pass
+            self.h = 0
+
+
 def _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc, flag, stage):
     """One PCG iteration with device-resident scalars (sc slots as in
     include/sphcurl.h SPHC_PCG_*); ends with the scalars copied to ``stage``."""
@@ -490,11 +551,12 @@ def _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc, flag, stage):
     z = precond(r)
     dv.dot(r, z, sc[3:4])
     call("sphc_pcg_direction", n, sc, z, p)
-    stage.copy_(sc, non_blocking=True)
+    call("sphc_copy_d2h", stage, sc, sc.numel() * 8)
     call("sphc_pcg_rotate", sc)
     return z
 
 
+@checked
 def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
     """Preconditioned CG from x = 0 (multigrid.py:220-274): same statuses
     (converged | maxit | stagnated | indefinite) and histories.
@@ -509,7 +571,7 @@ def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
          else torch.as_tensor(b, dtype=torch.float64, device=dv.device()))
     n = b.numel()
     lanes = A.lanes()
-    graph_ok = getattr(precond, "graph_safe", False) and maxit > 0
+    graph_ok = getattr(precond, "graph_safe", False) and maxit > 0 and USE_GRAPH
     hier = getattr(precond, "hierarchy", None)
     ws = getattr(hier, "_pcg_ws", None) if graph_ok else None
     if ws is not None and (ws["A"] is not A and ws["A_key"] != _csr_key(A) or ws["n"] != n):
@@ -546,13 +608,11 @@ def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
         # capture on a side stream without torch.cuda.graph's gc.collect() +
         # empty_cache(), which would force every later allocation back to
         # cudaMalloc
-        graph = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
         cap.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(cap):
-            graph.capture_begin()
-            _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc, flag, stage)
-            graph.capture_end()
+            graph = PcgGraph(lambda: _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc,
+                                                     flag, stage))
         torch.cuda.current_stream().wait_stream(cap)
         ws["graph"] = graph
         if hier is not None:

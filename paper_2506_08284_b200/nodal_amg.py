@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 from . import device as dv
-from .device import DeviceCSR, Status, as_device_csr, call
+from .device import checked, DeviceCSR, Status, as_device_csr, call
 
 
 @dataclass
@@ -33,6 +33,7 @@ class NodalProlongator:
     rho_estimate: float
 
 
+@checked
 def strength_graph(A_n, drop_tol):
     """Symmetric strength pattern incl. the diagonal (nodal_amg.py:33-56)."""
     A = as_device_csr(A_n)
@@ -41,9 +42,11 @@ def strength_graph(A_n, drop_tol):
     d = dv.diagonal(A)
     cnt = torch.empty(n, dtype=torch.int64, device=A.rowptr.device)
     call("sphc_strength_count", n, A.rowptr, A.col, A.val, d, float(drop_tol), cnt, st.t)
-    rows = st.rows()
-    if "NONPOS_DIAG" in rows:
-        raise ValueError(f"nonpositive diagonal entry in row {rows['NONPOS_DIAG']}")
+
+    def check(rows):
+        if "NONPOS_DIAG" in rows:
+            raise ValueError(f"nonpositive diagonal entry in row {rows['NONPOS_DIAG']}")
+    st.defer(check)
     frp, nnz = dv.scan(cnt)
     fci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
     call("sphc_strength_fill", n, A.rowptr, A.col, A.val, d, float(drop_tol), frp, fci)
@@ -56,6 +59,7 @@ def strength_graph(A_n, drop_tol):
     return DeviceCSR(srp, sci, None, A.shape)
 
 
+@checked
 def aggregate(strength):
     """Greedy two-phase root aggregation (nodal_amg.py:59-88) on the device
     (csrc/aggregate.cu), bit-identical to the reference's ordered loops."""
@@ -69,11 +73,13 @@ def aggregate(strength):
     st = Status()
     call("sphc_aggregate", n, strength.rowptr, strength.col, state, ticket, flags, pos, lst,
          memb, st.t)
-    n_agg = int(lst[n].item()) if n else 0
-    rows = st.rows()
-    if "AGG_CAPACITY" in rows:
-        raise RuntimeError(f"node {rows['AGG_CAPACITY']}: more assigned neighbours than "
-                           "the device aggregation buffer holds (256)")
+
+    def check(rows):
+        if "AGG_CAPACITY" in rows:
+            raise RuntimeError(f"node {rows['AGG_CAPACITY']}: more assigned neighbours than "
+                               "the device aggregation buffer holds (256)")
+    st.defer(check)
+    n_agg = int(dv.readback(lst[n:n + 1])[0][0]) if n else 0
     return Aggregation(n_fine=n, n_agg=n_agg, membership=memb)
 
 
@@ -100,27 +106,39 @@ def tentative_prolongator(agg):
     return DeviceCSR(rp, ci, v, (n, agg.n_agg))
 
 
+_START = {}
+
+
 def _power_start(n):
     # the reference's deterministic start vector, formed by numpy on the host
-    # (nodal_amg.py:106) and uploaded once
-    return torch.from_numpy(1.0 + 0.01 * np.sin(np.arange(n, dtype=np.float64))).to(dv.device())
+    # (nodal_amg.py:106; numpy's sin, bit for bit) and uploaded once per size
+    # (a constant of n, kept like a lookup table; callers only read it)
+    v = _START.get(n)
+    if v is None:
+        if len(_START) > 64:
+            _START.clear()
+        v = _START[n] = torch.from_numpy(
+            1.0 + 0.01 * np.sin(np.arange(n, dtype=np.float64))).to(dv.device())
+    return v
 
 
+@checked
 def estimate_rho(A, dinv, iterations=10):
     """Ten-step power method on diag(1/d) A (nodal_amg.py:99-116). The norms
     run in the OpenBLAS-Haswell ddot order, so rho is bit-identical."""
     n = A.shape[0]
-    v = _power_start(n)
+    v0 = _power_start(n)           # shared constant: never written
+    v = dv.empty_f64(n)
     sq = dv.empty_f64(1)
     norms = dv.empty_f64(iterations + 1)
-    call("sphc_hsw_dot", n, v, v, sq)
-    call("sphc_scale_by_norm", n, v, sq, v, norms[0:1])
+    call("sphc_hsw_dot", n, v0, v0, sq)
+    call("sphc_scale_by_norm", n, v0, sq, v, norms[0:1])
     w = dv.empty_f64(n)
     for it in range(iterations):
         call("sphc_nodal_powmv", n, A.rowptr, A.col, A.val, dinv, v, w)
         call("sphc_hsw_dot", n, w, w, sq)
         call("sphc_scale_by_norm", n, w, sq, v, norms[it + 1:it + 2])
-    h = norms.cpu().numpy()
+    h = dv.readback(norms)[0]
     rho = 1.0
     for it in range(iterations):
         if h[it + 1] == 0.0:
@@ -132,11 +150,15 @@ def estimate_rho(A, dinv, iterations=10):
 def _dinv(A):
     st = Status()
     d = dv.diagonal(A, st)
-    if "ZERO_DIAG" in st.rows():
-        raise ValueError("zero diagonal in nodal operator")
+
+    def check(rows):
+        if "ZERO_DIAG" in rows:
+            raise ValueError("zero diagonal in nodal operator")
+    st.defer(check)
     return dv.reciprocal(d)
 
 
+@checked
 def smooth_and_normalize(A_n, agg):
     """P = normalize((I - omega D^-1 A_n) P_tent), omega = 4 / (3 rho)
     (nodal_amg.py:138-155). ``agg`` replaces the reference's P_tent argument
@@ -157,10 +179,13 @@ def smooth_and_normalize(A_n, agg):
     pv = dv.empty_f64(nnz)
     call("sphc_nodal_smooth_fill", n, A.rowptr, A.col, A.val, dinv, agg.membership, omega,
          prp, pci, pv, st.t)
-    rows = st.rows()
-    if "SPGEMM_CAPACITY" in rows:
-        raise RuntimeError(f"nodal row {rows['SPGEMM_CAPACITY']} exceeds the kernel capacity")
-    if "ZERO_ROWSUM" in rows:
-        raise ValueError(f"zero row sum before scaling in row {rows['ZERO_ROWSUM']}")
+
+    def check(rows):
+        if "SPGEMM_CAPACITY" in rows:
+            raise RuntimeError(f"nodal row {rows['SPGEMM_CAPACITY']} exceeds the kernel "
+                               "capacity")
+        if "ZERO_ROWSUM" in rows:
+            raise ValueError(f"zero row sum before scaling in row {rows['ZERO_ROWSUM']}")
+    st.defer(check)
     P = DeviceCSR(prp, pci, pv, (n, agg.n_agg))
     return NodalProlongator(P=P, omega_used=omega, rho_estimate=rho)

@@ -163,6 +163,19 @@ int sphc_spgemm_fill_pair(int64_t n, const int64_t *arp, const int32_t *aci, con
                           int32_t *cci, double *cv1, double *cv2, int64_t *status,
                           void *stream);
 
+/* Long-row variants (one CTA of 8 warps per output row) for products whose A
+ * rows are long: the Galerkin R (A P) with R = P_e^T (150-2000 entries per
+ * row, multigrid.py:150-151). Same outputs and capacity rule (<= 256 columns
+ * per row) as sphc_spgemm_count / sphc_spgemm_fill(_pair), unordered (TOL);
+ * av2 / bv2 / cv2 NULL for a single product. */
+int sphc_spgemm_count_long(int64_t n, const int64_t *arp, const int32_t *aci,
+                           const int64_t *brp, const int32_t *bci, int64_t *counts,
+                           int64_t *status, void *stream);
+int sphc_spgemm_fill_long(int64_t n, const int64_t *arp, const int32_t *aci, const double *av,
+                          const double *av2, const int64_t *brp, const int32_t *bci,
+                          const double *bv, const double *bv2, const int64_t *crp,
+                          int32_t *cci, double *cv1, double *cv2, void *stream);
+
 /* ---------------------------------------------------------------- solve */
 
 /* y = alpha * (A x) + beta * z  (z may be NULL; y may alias z).
@@ -254,6 +267,14 @@ int sphc_graph_destroy(void *exec);
 /* dst (pinned host) <- src (device), `bytes` bytes, asynchronous on stream
  * (capturable; the PCG scalars' per-iteration readback). */
 int sphc_copy_d2h(void *dst, const void *src, int64_t bytes, void *stream);
+
+/* The k-step Lanczos estimate behind the Chebyshev smoother's upper bound
+ * (D^-1 A in the D inner product, deterministic start vector) in one
+ * cooperative launch on the SELL mirror of A: writes alpha_1..k to sc[0..k)
+ * and beta_0..k to sc[k..2k]. v, vprev, w, u are n-vectors of scratch. */
+int sphc_lanczos_sell(int64_t n, const int64_t *slice_ptr, const int32_t *sci, const double *sv,
+                      const double *d, const double *dinv, int k, double *v, double *vprev,
+                      double *w, double *u, double *sc, void *stream);
 
 /* y = A x for a dense row-major n x n A (coarsest level, explicit inverse of
  * the reference's lu_factor/lu_solve pair, multigrid.py:157,181). */

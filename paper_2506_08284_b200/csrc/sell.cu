@@ -231,3 +231,150 @@ extern "C" int sphc_sell_cheb_step(int64_t n, const int64_t* slice_ptr, const in
   SPHC_LAUNCH_CHECK();
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// The whole k-step Lanczos bound estimate of a Chebyshev smoother (D^-1 A in
+// the D inner product, ChebyshevSweeper._lanczos) in ONE cooperative launch:
+// grid-wide barriers replace the ~7 launches per step of the step-by-step
+// version. Per step: (A) v = w / |w|_D and u = A v on this thread's rows,
+// partial u.v; (B) w = D^-1 u - alpha v - beta v_prev, partial w.Dw. Dot
+// products are block trees written to per-block partials and summed by every
+// block in the same fixed order (deterministic, identical in every block).
+#include <cooperative_groups.h>
+namespace cgrp = cooperative_groups;
+
+#define LZ_THREADS 256
+#define LZ_MAX_BLOCKS 2048
+
+__device__ __forceinline__ double lz_block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (wid == 0) {
+    t = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+    t = warp_sum(t);
+  }
+  return t;   // valid in warp 0
+}
+
+// grid-wide deterministic sum; `part` alternates halves between calls
+__device__ __forceinline__ double lz_grid_sum(double v, double* part, int& half,
+                                              cgrp::grid_group& grid, double* sh) {
+  double b = lz_block_sum(v, sh);
+  double* P = part + half * LZ_MAX_BLOCKS;
+  half ^= 1;
+  if (threadIdx.x == 0) P[blockIdx.x] = b;
+  grid.sync();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) t += P[i];
+    t = warp_sum(t);
+    if (threadIdx.x == 0) sh[32] = t;
+  }
+  __syncthreads();
+  return sh[32];
+}
+
+__device__ __forceinline__ double lz_start(i64 i) {
+  unsigned long long z = (unsigned long long)i + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z = z ^ (z >> 31);
+  return (double)(z >> 11) * 0x1p-53 * 2.0 - 1.0;
+}
+
+__global__ void __launch_bounds__(LZ_THREADS)
+    k_lanczos_coop(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
+                   const double* __restrict__ sv, const double* __restrict__ d,
+                   const double* __restrict__ dinv, double* v, double* vprev, double* w,
+                   double* u, int k, double* sc, double* part, int K) {
+  cgrp::grid_group grid = cgrp::this_grid();
+  __shared__ double sh[33];
+  int half = 0;
+  const i64 nt = (i64)gridDim.x * blockDim.x;
+  const i64 t0 = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  double acc = 0.0;
+  for (i64 i = t0; i < n; i += nt) {
+    double x = lz_start(i);
+    w[i] = x;
+    acc += x * (d[i] * x);
+  }
+  double nrm = sqrt(lz_grid_sum(acc, part, half, grid, sh));
+  if (t0 == 0) sc[k] = nrm;                         // beta_0
+  for (int j = 0; j < k; j++) {
+    acc = 0.0;
+    double inv = 1.0 / nrm;
+    // (A): K consecutive lanes share a row (K > 1 when the rows alone cannot
+    // fill the SMs), each taking every K-th SELL column; lane-group trees
+    const i64 nrt = ((n + 31) & ~(i64)31) * K;     // warp-uniform trip count
+    for (i64 g = t0; g < nrt; g += nt) {
+      i64 i = g / K;
+      int part = (int)(g % K);
+      double t = 0.0;
+      if (i < n) {
+        i64 s = i / SELL_C;
+        int r = (int)(i % SELL_C);
+        i64 base = sp[s] + r;
+        int width = (int)((sp[s + 1] - sp[s]) / SELL_C);
+#pragma unroll 4
+        for (int q = part; q < width; q += K) {
+          i64 e = base + (i64)q * SELL_C;
+          t = fma(sv[e], w[sci[e]], t);
+        }
+      }
+      for (int o = K >> 1; o > 0; o >>= 1) t += __shfl_xor_sync(FULL_MASK, t, o);
+      if (i < n && part == 0) {
+        double vi = w[i] * inv, ui = t * inv;
+        v[i] = vi;
+        u[i] = ui;
+        acc += ui * vi;
+      }
+    }
+    double alpha = lz_grid_sum(acc, part, half, grid, sh);
+    if (t0 == 0) sc[j] = alpha;
+    acc = 0.0;
+    for (i64 i = t0; i < n; i += nt) {               // (B)
+      double t = dinv[i] * u[i] - alpha * v[i];
+      if (j) t -= nrm * vprev[i];
+      w[i] = t;
+      acc += t * (d[i] * t);
+    }
+    nrm = sqrt(lz_grid_sum(acc, part, half, grid, sh));
+    if (t0 == 0) sc[k + j + 1] = nrm;               // beta_{j+1}
+    double* tmp = v;
+    v = vprev;
+    vprev = tmp;
+  }
+}
+
+extern "C" int sphc_lanczos_sell(int64_t n, const int64_t* slice_ptr, const int32_t* sci,
+                                 const double* sv, const double* d, const double* dinv, int k,
+                                 double* v, double* vprev, double* w, double* u, double* sc,
+                                 void* stream) {
+  if (n <= 0) return 0;
+  static double* part = nullptr;
+  static int max_blocks = 0;
+  if (!part) {
+    SPHC_CUDA(cudaMalloc((void**)&part, 2 * LZ_MAX_BLOCKS * sizeof(double)));
+    int per_sm = 0;
+    SPHC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lanczos_coop,
+                                                            LZ_THREADS, 0));
+    max_blocks = per_sm * SPHC_NUM_SMS;
+    if (max_blocks > LZ_MAX_BLOCKS) max_blocks = LZ_MAX_BLOCKS;
+  }
+  // lanes per row: enough rows x lanes for ~2 blocks per SM
+  int K = 1;
+  while (K < 32 && n * K < (i64)2 * SPHC_NUM_SMS * LZ_THREADS) K <<= 1;
+  i64 want = (((n + 31) & ~(i64)31) * K + LZ_THREADS - 1) / LZ_THREADS;
+  int g = (int)(want < max_blocks ? want : max_blocks);
+  i64 nn = n;
+  void* args[] = {&nn, (void*)&slice_ptr, (void*)&sci, (void*)&sv, (void*)&d, (void*)&dinv,
+                  &v, &vprev, &w, &u, &k, &sc, &part, &K};
+  SPHC_CUDA(cudaLaunchCooperativeKernel((void*)k_lanczos_coop, dim3(g), dim3(LZ_THREADS), args,
+                                        0, as_stream(stream)));
+  g_sphc_launches++;
+  return 0;
+}

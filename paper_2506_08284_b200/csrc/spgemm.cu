@@ -389,3 +389,253 @@ extern "C" int sphc_spgemm_fill_pair(int64_t n, const int64_t* arp, const int32_
   return fill_launch<false, true>(n, arp, aci, av1, av2, brp, bci, bv1, bv2, crp, cci, cv1,
                                   cv2, status, as_stream(stream));
 }
+
+// ---------------------------------------------------------------------------
+// Long rows: one CTA of SPC_W warps per output row (C = R (A P) Galerkin
+// products, whose rows have 150-2000 A entries and 4k-60k products but only
+// ~40-100 distinct columns). The row's A entries are cut into chunks of
+// SPC_CH; chunk c belongs to warp c % SPC_W, which walks its B rows in order
+// and accumulates into its own copy of the row's accumulators (a B row's
+// columns are distinct, so its lanes never collide). The copies are summed
+// in warp order: deterministic, TOL class like the unordered warp kernel.
+#define SPC_W 8
+#define SPC_CH 16
+#define SPC_HCAP 1024
+#define SPC_CCAP 256
+#define SPC_U 4     // B rows loaded per step (independent loads in flight)
+
+struct SpcHead {
+  int keys[SPC_HCAP];
+  short slot[SPC_HCAP];
+  int list[SPC_CCAP];
+  int ucount;
+  int bad;
+};
+
+// Every warp inserts the columns of its chunks' B rows into the CTA's table.
+__device__ __forceinline__ void spc_symbolic(i64 as, i64 ae, const int* __restrict__ aci,
+                                             const i64* __restrict__ brp,
+                                             const int* __restrict__ bci, SpcHead& H, int ts,
+                                             int w, int lane) {
+  bool ok = true;
+  for (i64 c0 = as + (i64)w * SPC_CH; c0 < ae; c0 += (i64)SPC_W * SPC_CH) {
+    int nb = (int)min((i64)SPC_CH, ae - c0);
+    i64 bs = 0;
+    int len = 0;
+    if (lane < nb) {
+      int k = aci[c0 + lane];
+      bs = brp[k];
+      len = (int)(brp[k + 1] - bs);
+    }
+    for (int t0 = 0; t0 < nb; t0 += SPC_U) {
+      int col[SPC_U];
+#pragma unroll
+      for (int u = 0; u < SPC_U; u++) {
+        int t = t0 + u;
+        i64 b = __shfl_sync(FULL_MASK, bs, t & 31);
+        int l = __shfl_sync(FULL_MASK, len, t & 31);
+        col[u] = (t < nb && lane < l) ? bci[b + lane] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < SPC_U; u++)
+        if (col[u] >= 0) ok &= spg_insert(H.keys, ts, &H.ucount, col[u]);
+      // B rows longer than a warp (rare)
+      for (int u = 0; u < SPC_U; u++) {
+        int t = t0 + u;
+        i64 b = __shfl_sync(FULL_MASK, bs, t & 31);
+        int l = __shfl_sync(FULL_MASK, len, t & 31);
+        if (t < nb)
+          for (int q = 32 + lane; q < l; q += 32) ok &= spg_insert(H.keys, ts, &H.ucount, bci[b + q]);
+      }
+    }
+  }
+  if (!ok) H.bad = 1;
+}
+
+__device__ __forceinline__ void spc_clear(SpcHead& H, int ts) {
+  for (int t = threadIdx.x; t < ts; t += blockDim.x) H.keys[t] = -1;
+  if (threadIdx.x == 0) {
+    H.ucount = 0;
+    H.bad = 0;
+  }
+}
+
+__global__ void __launch_bounds__(SPC_W * 32)
+    k_spgemm_count_cta(i64 n, const i64* __restrict__ arp, const int* __restrict__ aci,
+                       const i64* __restrict__ brp, const int* __restrict__ bci,
+                       i64* __restrict__ counts, i64* status) {
+  __shared__ SpcHead H;
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (i64 row = blockIdx.x; row < n; row += gridDim.x) {
+    spc_clear(H, SPC_HCAP);
+    __syncthreads();
+    spc_symbolic(arp[row], arp[row + 1], aci, brp, bci, H, SPC_HCAP, w, lane);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bool ok = !H.bad && H.ucount <= SPC_CCAP;
+      counts[row] = ok ? H.ucount : 0;
+      if (!ok) report(status, SPHC_ST_SPGEMM_CAPACITY, row);
+    }
+    __syncthreads();
+  }
+}
+
+template <bool PAIR>
+__global__ void __launch_bounds__(SPC_W * 32)
+    k_spgemm_fill_cta(i64 n, const i64* __restrict__ arp, const int* __restrict__ aci,
+                      const double* __restrict__ av, const double* __restrict__ av2,
+                      const i64* __restrict__ brp, const int* __restrict__ bci,
+                      const double* __restrict__ bv, const double* __restrict__ bv2,
+                      const i64* __restrict__ crp, int* __restrict__ cci, double* __restrict__ cv,
+                      double* __restrict__ cv2) {
+  __shared__ SpcHead H;
+  extern __shared__ double spc_acc[];   // [PAIR + 1][SPC_W][SPC_CCAP]
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* my = spc_acc + w * SPC_CCAP;
+  double* my2 = PAIR ? spc_acc + (SPC_W + w) * SPC_CCAP : nullptr;
+  for (i64 row = blockIdx.x; row < n; row += gridDim.x) {
+    int nu = (int)(crp[row + 1] - crp[row]);
+    if (nu == 0) continue;              // empty, or flagged by the count pass
+    int ts = pow2_at_least(2 * nu, 64);
+    if (ts > SPC_HCAP) ts = SPC_HCAP;
+    i64 as = arp[row], ae = arp[row + 1];
+    spc_clear(H, ts);
+    for (int t = threadIdx.x; t < SPC_W * SPC_CCAP; t += blockDim.x) {
+      spc_acc[t] = 0.0;
+      if (PAIR) spc_acc[SPC_W * SPC_CCAP + t] = 0.0;
+    }
+    __syncthreads();
+    spc_symbolic(as, ae, aci, brp, bci, H, ts, w, lane);
+    __syncthreads();
+    // rank sort: each occupied slot learns its column's sorted position
+    for (int h = threadIdx.x; h < ts; h += blockDim.x) {
+      int key = H.keys[h];
+      if (key < 0) continue;
+      int r = 0;
+      for (int g = 0; g < ts; g++) {
+        int o = H.keys[g];
+        r += (o >= 0) & (o < key);
+      }
+      H.slot[h] = (short)r;
+      H.list[r] = key;
+    }
+    __syncthreads();
+    // numeric: each warp over its chunks, one B row per lane-group step
+    for (i64 c0 = as + (i64)w * SPC_CH; c0 < ae; c0 += (i64)SPC_W * SPC_CH) {
+      int nb = (int)min((i64)SPC_CH, ae - c0);
+      i64 bs = 0;
+      int len = 0;
+      double a = 0.0, a2 = 0.0;
+      if (lane < nb) {
+        int k = aci[c0 + lane];
+        bs = brp[k];
+        len = (int)(brp[k + 1] - bs);
+        a = av[c0 + lane];
+        if (PAIR) a2 = av2[c0 + lane];
+      }
+      for (int t0 = 0; t0 < nb; t0 += SPC_U) {
+        int col[SPC_U];
+        double v[SPC_U], v2[SPC_U];
+#pragma unroll
+        for (int u = 0; u < SPC_U; u++) {
+          int t = t0 + u;
+          i64 b = __shfl_sync(FULL_MASK, bs, t & 31);
+          int l = __shfl_sync(FULL_MASK, len, t & 31);
+          col[u] = -1;
+          if (t < nb && lane < l) {
+            col[u] = bci[b + lane];
+            v[u] = bv[b + lane];
+            if (PAIR) v2[u] = bv2[b + lane];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < SPC_U; u++) {
+          int t = t0 + u;
+          double at = __shfl_sync(FULL_MASK, a, t & 31);
+          double at2 = PAIR ? __shfl_sync(FULL_MASK, a2, t & 31) : 0.0;
+          if (col[u] >= 0) {
+            int sl = H.slot[spg_find(H.keys, ts, col[u])];
+            my[sl] += at * v[u];
+            if (PAIR) my2[sl] += at2 * v2[u];
+          }
+          __syncwarp();
+        }
+        for (int u = 0; u < SPC_U; u++) {   // B rows longer than a warp (rare)
+          int t = t0 + u;
+          i64 b = __shfl_sync(FULL_MASK, bs, t & 31);
+          int l = __shfl_sync(FULL_MASK, len, t & 31);
+          double at = __shfl_sync(FULL_MASK, a, t & 31);
+          double at2 = PAIR ? __shfl_sync(FULL_MASK, a2, t & 31) : 0.0;
+          if (t < nb)
+            for (int q = 32 + lane; q < l; q += 32) {
+              int sl = H.slot[spg_find(H.keys, ts, bci[b + q])];
+              my[sl] += at * bv[b + q];
+              if (PAIR) my2[sl] += at2 * bv2[b + q];
+            }
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
+    i64 o = crp[row];
+    for (int t = threadIdx.x; t < nu; t += blockDim.x) {
+      double s = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int g = 0; g < SPC_W; g++) {
+        s += spc_acc[g * SPC_CCAP + t];
+        if (PAIR) s2 += spc_acc[(SPC_W + g) * SPC_CCAP + t];
+      }
+      cci[o + t] = H.list[t];
+      cv[o + t] = s;
+      if (PAIR) cv2[o + t] = s2;
+    }
+    __syncthreads();
+  }
+}
+
+static unsigned cta_grid(i64 n) {
+  // 4 resident CTAs per SM (pair accumulators: 32 KB + 7 KB of table per CTA)
+  i64 g = n < (i64)SPHC_NUM_SMS * 16 ? n : (i64)SPHC_NUM_SMS * 16;
+  return (unsigned)(g > 0 ? g : 1);
+}
+
+extern "C" int sphc_spgemm_count_long(int64_t n, const int64_t* arp, const int32_t* aci,
+                                      const int64_t* brp, const int32_t* bci, int64_t* counts,
+                                      int64_t* status, void* stream) {
+  if (n <= 0) return 0;
+  k_spgemm_count_cta<<<cta_grid(n), SPC_W * 32, 0, as_stream(stream)>>>(n, arp, aci, brp, bci,
+                                                                         counts, status);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+template <bool PAIR>
+static int fill_cta_launch(i64 n, const i64* arp, const int* aci, const double* av,
+                           const double* av2, const i64* brp, const int* bci, const double* bv,
+                           const double* bv2, const i64* crp, int* cci, double* cv, double* cv2,
+                           cudaStream_t s) {
+  size_t sm = (PAIR ? 2 : 1) * SPC_W * SPC_CCAP * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    SPHC_CUDA(cudaFuncSetAttribute(k_spgemm_fill_cta<PAIR>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr = true;
+  }
+  k_spgemm_fill_cta<PAIR><<<cta_grid(n), SPC_W * 32, sm, s>>>(n, arp, aci, av, av2, brp, bci, bv,
+                                                              bv2, crp, cci, cv, cv2);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int sphc_spgemm_fill_long(int64_t n, const int64_t* arp, const int32_t* aci,
+                                     const double* av, const double* av2, const int64_t* brp,
+                                     const int32_t* bci, const double* bv, const double* bv2,
+                                     const int64_t* crp, int32_t* cci, double* cv1, double* cv2,
+                                     void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  if (av2)
+    return fill_cta_launch<true>(n, arp, aci, av, av2, brp, bci, bv, bv2, crp, cci, cv1, cv2, s);
+  return fill_cta_launch<false>(n, arp, aci, av, nullptr, brp, bci, bv, nullptr, crp, cci, cv1,
+                                nullptr, s);
+}

@@ -7,6 +7,7 @@ a libsphcurl kernel).
 """
 
 import functools
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -418,6 +419,15 @@ def _compact(A, rp, nnz):
     return DeviceCSR(rp, ci, v, A.shape)
 
 
+LONG_ROW = int(os.environ.get("SPHC_LONG_ROW", "64"))
+
+
+def _long_rows(A):
+    """Average A row length at which the CTA-per-row SpGEMM takes over (the
+    R (A P) Galerkin products; no host sync: nnz and shape are known)."""
+    return A.shape[0] > 0 and A.nnz >= LONG_ROW * A.shape[0]
+
+
 def _rows(A, lo):
     """Row-pointer view starting at row lo (absolute positions into A's
     column / value arrays, so a kernel launched on it computes rows lo..)."""
@@ -435,8 +445,10 @@ def spgemm(A, B, drop=True, ordered=False, shard=None):
     st = Status()
     cnt = torch.empty(n, dtype=torch.int64, device=A.rowptr.device)
     blocks = shard.blocks(n) if shard is not None else [(0, 0, n)]
+    long_rows = _long_rows(A) and not ordered
     for _, lo, hi in blocks:
-        call("sphc_spgemm_count", hi - lo, _rows(A, lo), A.col, B.rowptr, B.col, cnt[lo:], st.t)
+        call("sphc_spgemm_count_long" if long_rows else "sphc_spgemm_count", hi - lo,
+             _rows(A, lo), A.col, B.rowptr, B.col, cnt[lo:], st.t)
     if shard is not None:
         shard.gather_ranges(cnt, shard.bounds(n))
         shard.min_(st.t)
@@ -445,8 +457,12 @@ def spgemm(A, B, drop=True, ordered=False, shard=None):
     ci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
     v = empty_f64(nnz)
     for _, lo, hi in blocks:
-        call("sphc_spgemm_fill", hi - lo, _rows(A, lo), A.col, A.val, B.rowptr, B.col, B.val,
-             rp[lo:], ci, v, int(ordered), st.t)
+        if long_rows:
+            call("sphc_spgemm_fill_long", hi - lo, _rows(A, lo), A.col, A.val, None, B.rowptr,
+                 B.col, B.val, None, rp[lo:], ci, v, None)
+        else:
+            call("sphc_spgemm_fill", hi - lo, _rows(A, lo), A.col, A.val, B.rowptr, B.col,
+                 B.val, rp[lo:], ci, v, int(ordered), st.t)
     if shard is not None and shard.collective:
         from .sharding import host_offsets
         off = host_offsets(rp, shard.bounds(n))
@@ -472,9 +488,10 @@ def spgemm_pair(A1, A2, B1, B2, drop=True, shard=None):
     st = Status()
     cnt = torch.empty(n, dtype=torch.int64, device=A1.rowptr.device)
     blocks = shard.blocks(n) if shard is not None else [(0, 0, n)]
+    long_rows = _long_rows(A1)
     for _, lo, hi in blocks:
-        call("sphc_spgemm_count", hi - lo, _rows(A1, lo), A1.col, B1.rowptr, B1.col, cnt[lo:],
-             st.t)
+        call("sphc_spgemm_count_long" if long_rows else "sphc_spgemm_count", hi - lo,
+             _rows(A1, lo), A1.col, B1.rowptr, B1.col, cnt[lo:], st.t)
     if shard is not None:
         shard.gather_ranges(cnt, shard.bounds(n))
         shard.min_(st.t)
@@ -483,8 +500,12 @@ def spgemm_pair(A1, A2, B1, B2, drop=True, shard=None):
     ci = torch.empty(nnz, dtype=torch.int32, device=A1.rowptr.device)
     v1, v2 = empty_f64(nnz), empty_f64(nnz)
     for _, lo, hi in blocks:
-        call("sphc_spgemm_fill_pair", hi - lo, _rows(A1, lo), A1.col, A1.val, A2.val,
-             B1.rowptr, B1.col, B1.val, B2.val, rp[lo:], ci, v1, v2, st.t)
+        if long_rows:
+            call("sphc_spgemm_fill_long", hi - lo, _rows(A1, lo), A1.col, A1.val, A2.val,
+                 B1.rowptr, B1.col, B1.val, B2.val, rp[lo:], ci, v1, v2)
+        else:
+            call("sphc_spgemm_fill_pair", hi - lo, _rows(A1, lo), A1.col, A1.val, A2.val,
+                 B1.rowptr, B1.col, B1.val, B2.val, rp[lo:], ci, v1, v2, st.t)
     if shard is not None and shard.collective:
         from .sharding import host_offsets
         off = host_offsets(rp, shard.bounds(n))

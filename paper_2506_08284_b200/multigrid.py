@@ -134,8 +134,15 @@ class ChebyshevSweeper:
         k = CHEB_POWER_ITERS
         d = self.diag
         v, vprev = self.buf
+        sc = dv.empty_f64(2 * k + 1)            # [alpha_1..k | beta_0..k]
+        m = self.sell
+        if m is not None:
+            # all k steps in one cooperative launch (csrc/sell.cu)
+            u, w = dv.empty_f64(n), dv.empty_f64(n)
+            call("sphc_lanczos_sell", n, m.slice_ptr, m.col, m.val, d, self.dinv, k, v, vprev,
+                 w, u, sc)
+            return sc
         u, w, dw = dv.empty_f64(n), dv.empty_f64(n), dv.empty_f64(n)
-        sc = dv.empty_f64(2 * k + 2)            # [alpha_1..k | beta_0..k]
         alpha, beta = sc[:k], sc[k:]
         call("sphc_cheb_start", n, w)
         call("sphc_diag_scale", n, d, w, dw)

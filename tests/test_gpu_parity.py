@@ -146,6 +146,42 @@ def test_spgemm_unordered_tol_and_deterministic():
         assert np.array_equal(C1.data.view(np.uint64), C2.data.view(np.uint64))
 
 
+def test_spgemm_long_rows_cta_kernel():
+    """CTA-per-row kernels (A rows >= 64 entries on average: the R (A P)
+    Galerkin shape): pattern identical to scipy, values TOL, bitwise rerun,
+    pair = two single products, B rows longer than a warp, capacity flag."""
+    dv = _dev()
+    for seed, (n, k, m, d1, d2) in enumerate([(200, 5000, 150, 0.03, 0.02),
+                                               (64, 3000, 250, 0.05, 0.05),   # B rows ~12
+                                               (40, 2000, 256, 0.1, 0.2)]):   # B rows ~51
+        A = _rand_csr(n, k, d1, 60 + seed)
+        B = _rand_csr(k, m, d2, 70 + seed)
+        A2, B2 = A.copy(), B.copy()
+        A2.data = np.cos(A.data)
+        B2.data = np.sin(B.data)
+        Ad, Bd = dv.DeviceCSR.from_scipy(A), dv.DeviceCSR.from_scipy(B)
+        assert dv._long_rows(Ad)
+        C1 = dv.spgemm(Ad, Bd).to_scipy()
+        C1b = dv.spgemm(Ad, Bd).to_scipy()
+        ref = A @ B
+        ref.sort_indices()
+        assert np.array_equal(C1.indptr, ref.indptr)
+        assert np.array_equal(C1.indices, ref.indices)
+        assert rel_max_diff(C1, ref) <= 1e-13
+        assert np.array_equal(C1.data.view(np.uint64), C1b.data.view(np.uint64))
+        P1, P2 = dv.spgemm_pair(Ad, dv.DeviceCSR.from_scipy(A2), Bd,
+                                dv.DeviceCSR.from_scipy(B2), drop=False)
+        assert np.array_equal(P1.to_scipy().data.view(np.uint64), C1.data.view(np.uint64))
+        ref2 = A2 @ B2
+        ref2.sort_indices()
+        assert rel_max_diff(P2.to_scipy(), ref2) <= 1e-13
+    # more than 256 distinct columns in a row: flagged, not written past
+    A = _rand_csr(8, 400, 0.5, 80)
+    B = _rand_csr(400, 2000, 0.05, 81)
+    with pytest.raises(RuntimeError, match="capacity"):
+        dv.spgemm(dv.DeviceCSR.from_scipy(A), dv.DeviceCSR.from_scipy(B))
+
+
 def test_transpose():
     dv = _dev()
     A = _rand_csr(4000, 700, 0.01, 5)

@@ -13,7 +13,10 @@ sites = collections.Counter()
 def hook(message, category, filename, lineno, file=None, line=None):
     st = traceback.extract_stack()[:-2]
     fr = [f for f in st if "paper_2506_08284_b200" in f.filename]
-    key = f"{os.path.basename(fr[-1].filename)}:{fr[-1].lineno} {fr[-1].name}" if fr else "?"
+    fr = [f for f in fr if f.name not in ("readback", "scan", "scan_many", "wrap",
+                                           "drop_zeros_many", "rows", "flush_checks")]
+    key = " <- ".join(f"{os.path.basename(f.filename)}:{f.lineno} {f.name}"
+                      for f in fr[-1:-3:-1]) if fr else "?"
     sites[key] += 1
 warnings.showwarning = hook
 warnings.simplefilter("always")

@@ -52,3 +52,11 @@ gl = [(named[i+1][0] - named[i][1], named[i][2], named[i+1][2], i) for i in rang
 print("largest gaps (us): after -> before")
 for g, a, b_, i in sorted(gl, reverse=True)[:40]:
     print(f"{g:8.1f}  #{i:5d} {a} -> {b_}")
+show = os.environ.get("SHOW")
+if show:
+    import re
+    pat = re.compile(show)
+    for e in sorted((e for e in ev if e.get("cat") == "kernel"), key=lambda e: e["ts"]):
+        if pat.search(e["name"]):
+            a = e.get("args", {})
+            print(f"{e['dur']:9.1f} us  {e['name'].split('(')[0][:40]:40s} grid {a.get('grid')} block {a.get('block')} smem {a.get('shared memory')}")

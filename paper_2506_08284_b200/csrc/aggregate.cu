@@ -87,18 +87,60 @@ __global__ void __launch_bounds__(AGG_WARPS * 32)
     __syncwarp();
     bool covered = false;
     if (!over) {
+      // distinct nodes only (a 27-point stencil lists each distance-2 node up
+      // to 8 times): sort, then keep first occurrences
+      int* L = lst[w];
+      int m = 1;
+      while (m < cnt) m <<= 1;
+      for (int a = cnt + lane; a < m; a += 32) L[a] = 0x7fffffff;
+      __syncwarp();
+      for (int size = 2; size <= m; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          for (int t2 = lane; t2 < (m >> 1); t2 += 32) {
+            int lo = ((t2 & ~(stride - 1)) << 1) | (t2 & (stride - 1)), hi = lo + stride;
+            bool up = (lo & size) == 0;
+            int a = L[lo], b = L[hi];
+            if ((a > b) == up) {
+              L[lo] = b;
+              L[hi] = a;
+            }
+          }
+          __syncwarp();
+        }
+      int u = 0;
+      for (int a0 = 0; a0 < cnt; a0 += 32) {
+        int a = a0 + lane;
+        int key = a < cnt ? L[a] : 0x7fffffff;
+        bool first = a < cnt && (a == 0 || L[a - 1] != key);
+        unsigned bal = __ballot_sync(FULL_MASK, first);
+        __syncwarp();
+        if (first) L[u + __popc(bal & ((1u << lane) - 1))] = key;
+        u += __popc(bal);
+        __syncwarp();
+      }
+      cnt = u;
+      // wait: drop decided non-roots each rescan, stop at the first root
       while (true) {
-        bool pend = false, root = false;
-        for (int a = lane; a < cnt; a += 32) {
-          int sk = vs[lst[w][a]];
-          pend |= sk == 0;
+        bool root = false;
+        int keep = 0;
+        for (int a0 = 0; a0 < cnt; a0 += 32) {
+          int a = a0 + lane;
+          int key = a < cnt ? L[a] : 0;
+          int sk = a < cnt ? vs[key] : 2;
           root |= sk == 1;
+          bool pend = sk == 0;
+          unsigned bal = __ballot_sync(FULL_MASK, pend);
+          __syncwarp();
+          if (pend) L[keep + __popc(bal & ((1u << lane) - 1))] = key;
+          keep += __popc(bal);
+          __syncwarp();
         }
         if (__any_sync(FULL_MASK, root)) {
           covered = true;
           break;
         }
-        if (!__any_sync(FULL_MASK, pend)) break;
+        if (keep == 0) break;
+        cnt = keep;
       }
     } else {
       // very long neighbourhoods: rescan through global memory

@@ -415,13 +415,7 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
         lv.rc = dv.empty_f64(n_coarse)
         levels.append(lv)
         with phase("level.galerkin_edge"):
-            if dv.same_pattern(A_e, S_e):
-                # one pass for both: P^T (A_e P) and P^T (S_e P) share patterns
-                AP, SP = dv.spgemm_pair(A_e, S_e, P_e, P_e, drop=False, shard=shard)
-                A_e, S_e = dv.spgemm_pair(lv.R_e, lv.R_e, AP, SP, shard=shard)
-            else:
-                A_e = dv.spgemm(lv.R_e, dv.spgemm(A_e, P_e, shard=shard), shard=shard)
-                S_e = dv.spgemm(lv.R_e, dv.spgemm(S_e, P_e, shard=shard), shard=shard)
+            A_e, S_e = _galerkin_edge(A_e, S_e, P_e, lv.R_e, shard)
         with phase("level.galerkin_nodal"):
             A_n = dv.spgemm(dv.transpose(P_n), dv.spgemm(A_n, P_n, ordered=True, shard=shard),
                             ordered=True, shard=shard)
@@ -435,6 +429,60 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
     last.r = dv.empty_f64(A_e.shape[0])
     nnz0 = levels[0].A_e.nnz
     oc = sum(lv.A_e.nnz for lv in levels) / nnz0
+    finalize_sweepers()
+    return Hierarchy(levels=levels, coarse_factorization=inv, operator_complexity=oc)
+
+
+def _galerkin_edge(A_e, S_e, P_e, R_e, shard=None):
+    """compress(P^T (A P)) for A_e and S_e (multigrid.py:150-151)."""
+    if dv.same_pattern(A_e, S_e):
+        # one pass for both: P^T (A_e P) and P^T (S_e P) share patterns
+        AP, SP = dv.spgemm_pair(A_e, S_e, P_e, P_e, drop=False, shard=shard)
+        return dv.spgemm_pair(R_e, R_e, AP, SP, shard=shard)
+    return (dv.spgemm(R_e, dv.spgemm(A_e, P_e, shard=shard), shard=shard),
+            dv.spgemm(R_e, dv.spgemm(S_e, P_e, shard=shard), shard=shard))
+
+
+@checked
+def reuse_hierarchy(h, A_e, S_e, cfg=None):
+    """Setup reuse for a sequence of related systems (PAPER.md, closing
+    remarks of the setup-cost discussion: "the interpolation operators can
+    often be retained across a few linear solves (still re-projecting the
+    discretization matrix for each solve)"; not part of the reference API).
+
+    Keeps every level's transfers of ``h`` -- P_e, P_n, the coarse gradients
+    and the explicit restrictions -- and re-projects the new fine operators
+    (A_e, S_e: same edge numbering, e.g. a new sigma or time step) through
+    them: Galerkin products, D^T A D, smoothers, coarsest inverse and the
+    null-space checks of every level. Returns a new Hierarchy sharing the
+    transfers with ``h`` (which stays usable)."""
+    cfg = cfg or SolverConfig()
+    A_e, S_e = as_device_csr(A_e), as_device_csr(S_e)
+    old = h.levels
+    if A_e.shape != old[0].A_e.shape or S_e.shape != old[0].S_e.shape:
+        raise ValueError(f"operators {A_e.shape} / {S_e.shape} do not match the hierarchy's "
+                         f"fine level {old[0].A_e.shape}")
+    D = old[0].D
+    AD = _check_nullspace(S_e, D, "the fine level", A=A_e)
+    levels = []
+    for li, lo in enumerate(old[:-1]):
+        lv = _make_level(A_e, S_e, D, cfg, AD=AD, P_e=lo.P_e, P_n=lo.P_n,
+                         emin_energy=lo.emin_energy, subproblem_dims=lo.subproblem_dims,
+                         commutator_residual=lo.commutator_residual,
+                         n_augmented=lo.n_augmented, membership=lo.membership,
+                         assignment=lo.assignment, coarse_gradient=lo.coarse_gradient,
+                         omega=lo.omega, rho=lo.rho)
+        lv.R_e = lo.R_e
+        lv.rc = dv.empty_f64(lo.P_e.shape[1])
+        levels.append(lv)
+        A_e, S_e = _galerkin_edge(A_e, S_e, lo.P_e, lo.R_e)
+        D = old[li + 1].D
+        AD = _check_nullspace(S_e, D, f"level {li + 1}", A=A_e)
+    last = _make_level(A_e, S_e, D, cfg, AD=AD, smooth=False)
+    last.r = dv.empty_f64(A_e.shape[0])
+    levels.append(last)
+    inv = _coarse_inverse(dv.to_dense(A_e))
+    oc = sum(lv.A_e.nnz for lv in levels) / levels[0].A_e.nnz
     finalize_sweepers()
     return Hierarchy(levels=levels, coarse_factorization=inv, operator_complexity=oc)
 

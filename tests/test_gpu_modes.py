@@ -152,3 +152,62 @@ def test_relaxation_only_slower_than_amg():
     lv = mg.fine_level(s.A_e, s.S, s.D)
     rel = mg.pcg_solve(lv.A_e, b, mg.hiptmair_preconditioner(lv))
     assert rel.iterations >= 2 * amg.iterations
+
+
+def test_reuse_hierarchy_reprojects_new_operators():
+    """Setup reuse (PAPER.md setup-cost remarks): transfers kept, operators
+    re-projected. Every level equals scipy's P^T A P of the new operators
+    through the kept P_e (TOL), null-space identity holds, and the solve
+    converges close to a fresh setup's iteration count."""
+    from golden_util import rel_max_diff
+    from paper_2506_08284_b200 import multigrid as mg
+    s1 = _system(12, 1e-2, True)
+    s2 = _system(12, 1.0, True)              # same mesh, new sigma
+    cfg = mg.SolverConfig(coarse_size=200)
+    h = mg.build_hierarchy(s1.A_e, s1.S, s1.A_n, s1.D, cfg)
+    h2 = mg.reuse_hierarchy(h, s2.A_e, s2.S, cfg)
+    assert [lv.A_e.shape for lv in h2.levels] == [lv.A_e.shape for lv in h.levels]
+    A, S = s2.A_e.tocsr(), s2.S.tocsr()
+    for lv, lv2 in zip(h.levels[:-1], h2.levels[:-1]):
+        assert lv2.P_e is lv.P_e and lv2.R_e is lv.R_e
+        assert rel_max_diff(lv2.A_e.to_scipy(), A) <= 1e-10
+        P = lv.P_e.to_scipy()
+        A, S = (P.T @ A @ P).tocsr(), (P.T @ S @ P).tocsr()
+    assert rel_max_diff(h2.levels[-1].A_e.to_scipy(), A) <= 1e-10
+    assert rel_max_diff(h2.levels[-1].S_e.to_scipy(), S) <= 1e-10
+    b = np.random.default_rng(1).uniform(-1, 1, s2.A_e.shape[0])
+    r2 = mg.pcg_solve(h2.levels[0].A_e, b, mg.v_cycle_preconditioner(h2))
+    fresh = mg.build_hierarchy(s2.A_e, s2.S, s2.A_n, s2.D, cfg)
+    rf = mg.pcg_solve(fresh.levels[0].A_e, b, mg.v_cycle_preconditioner(fresh))
+    assert r2.status == rf.status == "converged"
+    assert r2.iterations <= rf.iterations + 5
+    assert np.linalg.norm(b - s2.A_e @ r2.x) <= 1.5e-8 * np.linalg.norm(b)
+    # the original hierarchy is untouched and still solves its own system
+    r1 = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+    assert r1.status == "converged"
+    with pytest.raises(ValueError, match="do not match"):
+        mg.reuse_hierarchy(h, _system(8, 1.0, True).A_e, _system(8, 1.0, True).S, cfg)
+
+
+def test_matrix_market_import_feeds_the_device_path(tmp_path):
+    """SPEC.md:618 import workflow: exported (A_e, S, A_n, D) -> MatrixMarket
+    -> load_system -> build_hierarchy: the same hierarchy bit for bit as the
+    in-memory inputs (C1 golden case), and the reference's iterations."""
+    from paper_2506_08284_b200 import mmio, multigrid as mg
+    meta, _ = load_case("C1")
+    s = _system(meta["N"], meta["sigma"], meta["dirichlet"])
+    paths = []
+    for name in ("A_e", "S", "A_n", "D"):
+        paths.append(str(tmp_path / f"{name}.mtx"))
+        mmio.write_matrix_market(getattr(s, name), paths[-1])
+    A_e, S, A_n, D = mmio.load_system(*paths)
+    cfg = mg.SolverConfig(coarse_size=meta["coarse_size"])
+    h = mg.build_hierarchy(A_e, S, A_n, D, cfg)
+    assert [lv.A_e.shape[0] for lv in h.levels] == meta["n_edges"]
+    assert [lv.A_e.nnz for lv in h.levels] == meta["nnz_A_e"]
+    for lv, L in zip(h.levels[:-1], meta["levels"]):
+        assert sha(lv.membership.cpu().numpy().astype(np.int64)) == L["membership"]
+        assert csr_hash(lv.P_n.to_scipy()) == L["P_n"]
+    b = np.random.default_rng(meta["seed"]).uniform(-1, 1, s.A_e.shape[0])
+    res = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+    assert abs(res.iterations - meta["cheb"]["iterations"]) <= 1

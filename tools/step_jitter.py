@@ -12,7 +12,10 @@ sc = mg.SolverConfig(coarse_size=1000)
 if os.environ.get("NOGC") == "1":
     gc.disable()
 h = res = None
+flush = torch.empty(32 * 2**20, dtype=torch.float64, device="cuda") if os.environ.get("FLUSH") else None
 for k in range(30):
+    if flush is not None:
+        flush.fill_(float(k))
     st0 = torch.cuda.memory_stats()
     g0 = [x["collections"] for x in gc.get_stats()]
     h = res = None

@@ -148,11 +148,13 @@ int sphc_spgemm_count(int64_t n, const int64_t *arp, const int32_t *aci, const i
  *   nodal Galerkin product (multigrid.py:152).
  * ordered == 0: all lanes busy (sorted 32-product chunks, fixed shuffle-tree
  *   reduction); deterministic, TOL class. Used for the edge Galerkin products
- *   (:150-151), D^T A D (:103) and the null-space check (:111). */
+ *   (:150-151), D^T A D (:103) and the null-space check (:111).
+ * max_cols = the longest output row (max of the count pass; -1 if unknown):
+ *   <= 64 selects a small-footprint, higher-occupancy variant. */
 int sphc_spgemm_fill(int64_t n, const int64_t *arp, const int32_t *aci, const double *av,
                      const int64_t *brp, const int32_t *bci, const double *bv,
                      const int64_t *crp, int32_t *cci, double *cv, int ordered,
-                     int64_t *status, void *stream);
+                     int64_t max_cols, int64_t *status, void *stream);
 
 /* Two products on one pattern in one pass: C1 = A1 B1, C2 = A2 B2 where A1/A2
  * share arp/aci and B1/B2 share brp/bci (the A_e and S_e Galerkin products
@@ -160,8 +162,8 @@ int sphc_spgemm_fill(int64_t n, const int64_t *arp, const int32_t *aci, const do
 int sphc_spgemm_fill_pair(int64_t n, const int64_t *arp, const int32_t *aci, const double *av1,
                           const double *av2, const int64_t *brp, const int32_t *bci,
                           const double *bv1, const double *bv2, const int64_t *crp,
-                          int32_t *cci, double *cv1, double *cv2, int64_t *status,
-                          void *stream);
+                          int32_t *cci, double *cv1, double *cv2, int64_t max_cols,
+                          int64_t *status, void *stream);
 
 /* Long-row variants (one CTA of 8 warps per output row) for products whose A
  * rows are long: the Galerkin R (A P) with R = P_e^T (150-2000 entries per

@@ -23,11 +23,23 @@
 #include "common.cuh"
 
 #define SPG_WARPS 8    // symbolic pass
-#define SPG_FWARPS 4   // numeric pass (shared memory bound)
 #define SPG_HCAP 512   // max hash slots per warp
 #define SPG_CCAP 256   // max distinct columns per output row
 #define SPG_STG 256    // products per batch
 #define SPG_PER_LANE (SPG_STG / 32)
+
+// Numeric-pass capacities. Big: any row up to SPG_CCAP columns, 4 warps per
+// block (shared-memory bound, 12 warps per SM). Small: rows of <= 64
+// columns (A_e D, S_e D, A_e P_e: every product of the hierarchy but R (A P))
+// in a quarter of the shared memory, 8 warps per block and 64 registers, so
+// ~3x the warps per SM hide the row's dependent load chains.
+template <int STG_, int HCAP_, int CCAP_, int FW_, int MINB_>
+struct SpgCfg {
+  static constexpr int STG = STG_, HCAP = HCAP_, CCAP = CCAP_, FW = FW_, MINB = MINB_;
+  static constexpr int PER_LANE = STG_ / 32;
+};
+using SpgBig = SpgCfg<256, 512, 256, 4, 1>;
+using SpgSmall = SpgCfg<128, 128, 64, 8, 4>;
 
 __device__ __forceinline__ int pow2_at_least(int n, int lo) {
   int m = lo;
@@ -35,18 +47,21 @@ __device__ __forceinline__ int pow2_at_least(int n, int lo) {
   return m;
 }
 
-struct SpgBatch {
+template <int STG>
+struct SpgBatchT {
   int off[32];     // inclusive prefix of B-row lengths
   int start[32];   // exclusive prefix
   i64 bs[32];      // B-row starts
   double a[32];    // A values
-  unsigned char owner[SPG_STG];
+  unsigned char owner[STG];
 };
+using SpgBatch = SpgBatchT<SPG_STG>;
 
 // Load the next batch of A row entries [c0, ae). Returns the number of A
 // entries in the batch (0 if a single B row exceeds the window) and the
 // batch's product count in *total.
-__device__ __forceinline__ int spg_batch(SpgBatch& B, i64 c0, i64 ae,
+template <int STG>
+__device__ __forceinline__ int spg_batch(SpgBatchT<STG>& B, i64 c0, i64 ae,
                                          const int* __restrict__ aci,
                                          const double* __restrict__ av,
                                          const i64* __restrict__ brp, int lane, int* total) {
@@ -65,7 +80,7 @@ __device__ __forceinline__ int spg_batch(SpgBatch& B, i64 c0, i64 ae,
     int y = __shfl_up_sync(FULL_MASK, incl, o);
     if (lane >= o) incl += y;
   }
-  unsigned fit = __ballot_sync(FULL_MASK, valid && incl <= SPG_STG);
+  unsigned fit = __ballot_sync(FULL_MASK, valid && incl <= STG);
   int nb = __popc(fit);
   B.off[lane] = incl;
   B.start[lane] = incl - len;
@@ -78,7 +93,8 @@ __device__ __forceinline__ int spg_batch(SpgBatch& B, i64 c0, i64 ae,
   return nb;
 }
 
-__device__ __forceinline__ i64 spg_product(const SpgBatch& B, int f, int* t_out) {
+template <class BT>
+__device__ __forceinline__ i64 spg_product(const BT& B, int f, int* t_out) {
   int t = B.owner[f];
   *t_out = t;
   return B.bs[t] + (f - B.start[t]);
@@ -118,9 +134,11 @@ __device__ __forceinline__ int spg_find(const int* keys, int ts, int col) {
 }
 
 // Insert the distinct columns of row `row` into keys (size ts).
+template <int STG, int CCAP>
 __device__ bool spg_symbolic(i64 row, const i64* __restrict__ arp, const int* __restrict__ aci,
                              const i64* __restrict__ brp, const int* __restrict__ bci,
-                             int* keys, int ts, int* ucount, SpgBatch& B, int lane) {
+                             int* keys, int ts, int* ucount, SpgBatchT<STG>& B, int lane) {
+  constexpr int PER_LANE = STG / 32;
   for (int t = lane; t < ts; t += 32) keys[t] = -1;
   if (lane == 0) *ucount = 0;
   __syncwarp();
@@ -135,20 +153,20 @@ __device__ bool spg_symbolic(i64 row, const i64* __restrict__ arp, const int* __
     }
     // all column loads of the batch first (one L2 round trip per batch, not
     // per product: the shared-memory CAS would otherwise serialise them)
-    int col[SPG_PER_LANE];
+    int col[PER_LANE];
 #pragma unroll
-    for (int u = 0; u < SPG_PER_LANE; u++) {
+    for (int u = 0; u < PER_LANE; u++) {
       int f = lane + 32 * u, t;
       col[u] = f < total ? bci[spg_product(B, f, &t)] : -1;
     }
 #pragma unroll
-    for (int u = 0; u < SPG_PER_LANE; u++)
+    for (int u = 0; u < PER_LANE; u++)
       if (col[u] >= 0) ok &= spg_insert(keys, ts, ucount, col[u]);
     ok = __all_sync(FULL_MASK, ok);
     c0 += nb;
   }
   __syncwarp();
-  return ok && *ucount <= SPG_CCAP;
+  return ok && *ucount <= CCAP;
 }
 
 __device__ __forceinline__ int spg_row_products(i64 row, const i64* __restrict__ arp,
@@ -180,7 +198,8 @@ __global__ void __launch_bounds__(SPG_WARPS * 32)
     int prods = spg_row_products(row, arp, aci, brp, lane);
     int ts = pow2_at_least(2 * prods, 32);
     if (ts > SPG_HCAP) ts = SPG_HCAP;
-    bool ok = spg_symbolic(row, arp, aci, brp, bci, S.keys, ts, &S.ucount, S.B, lane);
+    bool ok = spg_symbolic<SPG_STG, SPG_CCAP>(row, arp, aci, brp, bci, S.keys, ts, &S.ucount,
+                                              S.B, lane);
     if (lane == 0) {
       counts[row] = ok ? S.ucount : 0;
       if (!ok) report(status, SPHC_ST_SPGEMM_CAPACITY, row);
@@ -189,48 +208,55 @@ __global__ void __launch_bounds__(SPG_WARPS * 32)
   }
 }
 
+template <class C>
 struct SpgFill {
-  int keys[SPG_HCAP];
-  short slot[SPG_HCAP];     // sorted position of the column in keys[h]
-  int list[SPG_CCAP];       // sorted output columns
-  double acc[2][SPG_CCAP];
-  short sslot[SPG_STG];     // staged product slots
-  double sval[SPG_STG];     // staged product values
-  SpgBatch B;
+  int keys[C::HCAP];
+  short slot[C::HCAP];      // sorted position of the column in keys[h]
+  int list[C::CCAP];        // sorted output columns
+  double acc[2][C::CCAP];
+  short sslot[C::STG];      // staged product slots
+  double sval[C::STG];      // staged product values
+  SpgBatchT<C::STG> B;
   int ucount;
 };
 
+template <class C>
 struct SpgFillPair {         // two products on one pattern
-  SpgFill f;
+  SpgFill<C> f;
   double a2[32];             // second A's values of the batch
-  double sval2[SPG_STG];
-  double acc2[2][SPG_CCAP];  // second product's accumulators (one per group)
+  double sval2[C::STG];
+  double acc2[2][C::CCAP];   // second product's accumulators (one per group)
 };
 
 // ORDERED / unordered as described at the top. PAIR: C1 = A1 B1 and C2 = A2 B2
 // with A1, A2 (and B1, B2) sharing one pattern -- the A_e and S_e Galerkin
 // products of a level -- computed in one pass (one symbolic phase, indices
 // read once); single lane group, accumulators acc[0] / acc[1].
-template <bool ORDERED, bool PAIR>
-__global__ void __launch_bounds__(SPG_FWARPS * 32)
+template <bool ORDERED, bool PAIR, class C>
+__global__ void __launch_bounds__(C::FW * 32, C::MINB)
     k_spgemm_fill(i64 n, const i64* __restrict__ arp, const int* __restrict__ aci,
                   const double* __restrict__ av, const double* __restrict__ av2,
                   const i64* __restrict__ brp, const int* __restrict__ bci,
                   const double* __restrict__ bv, const double* __restrict__ bv2,
                   const i64* __restrict__ crp, int* __restrict__ cci, double* __restrict__ cv,
-                  double* __restrict__ cv2, i64* status) {
+                  double* __restrict__ cv2, i64* status, int skip_le) {
   extern __shared__ unsigned char spg_smem[];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  SpgFill& F = PAIR ? ((SpgFillPair*)spg_smem)[w].f : ((SpgFill*)spg_smem)[w];
-  double* a2 = PAIR ? ((SpgFillPair*)spg_smem)[w].a2 : nullptr;
-  double* sval2 = PAIR ? ((SpgFillPair*)spg_smem)[w].sval2 : nullptr;
-  double* acc2 = PAIR ? &((SpgFillPair*)spg_smem)[w].acc2[0][0] : nullptr;
-  for (i64 row = (i64)blockIdx.x * SPG_FWARPS + w; row < n; row += (i64)gridDim.x * SPG_FWARPS) {
+  typedef SpgFill<C> Fill;
+  typedef SpgFillPair<C> FillPair;
+  Fill& F = PAIR ? ((FillPair*)spg_smem)[w].f : ((Fill*)spg_smem)[w];
+  double* a2 = PAIR ? ((FillPair*)spg_smem)[w].a2 : nullptr;
+  double* sval2 = PAIR ? ((FillPair*)spg_smem)[w].sval2 : nullptr;
+  double* acc2 = PAIR ? &((FillPair*)spg_smem)[w].acc2[0][0] : nullptr;
+  constexpr int PER_LANE = C::PER_LANE;
+  for (i64 row = (i64)blockIdx.x * C::FW + w; row < n; row += (i64)gridDim.x * C::FW) {
     int nu = (int)(crp[row + 1] - crp[row]);
-    if (nu == 0) continue;
+    // rows of another variant's size class: (skip_le, C::CCAP] are ours
+    if (nu <= skip_le || nu > C::CCAP) continue;
     int ts = pow2_at_least(2 * nu, 32);
-    if (ts > SPG_HCAP) ts = SPG_HCAP;
-    bool ok = spg_symbolic(row, arp, aci, brp, bci, F.keys, ts, &F.ucount, F.B, lane);
+    if (ts > C::HCAP) ts = C::HCAP;
+    bool ok = spg_symbolic<C::STG, C::CCAP>(row, arp, aci, brp, bci, F.keys, ts, &F.ucount,
+                                             F.B, lane);
     if (!ok) continue;  // flagged by the count pass
     // sorted column list
     int cnt = 0;
@@ -262,7 +288,7 @@ __global__ void __launch_bounds__(SPG_FWARPS * 32)
       F.acc[1][t] = 0.0;
       if (PAIR) {
         acc2[t] = 0.0;
-        acc2[SPG_CCAP + t] = 0.0;
+        acc2[C::CCAP + t] = 0.0;
       }
     }
     __syncwarp();
@@ -270,7 +296,7 @@ __global__ void __launch_bounds__(SPG_FWARPS * 32)
     const int G = ORDERED ? 1 : 2, LG = 32 / G;
     int g = lane / LG, l = lane % LG;
     double* my = F.acc[g];
-    double* my2 = PAIR ? acc2 + g * SPG_CCAP : nullptr;
+    double* my2 = PAIR ? acc2 + g * C::CCAP : nullptr;
     for (i64 c0 = as; c0 < ae;) {
       int total;
       int nb = spg_batch(F.B, c0, ae, aci, av, brp, lane, &total);
@@ -284,10 +310,10 @@ __global__ void __launch_bounds__(SPG_FWARPS * 32)
       }
       {
         // loads of the whole batch first, then the hash lookups
-        int col[SPG_PER_LANE], own[SPG_PER_LANE];
-        double v1[SPG_PER_LANE], v2[SPG_PER_LANE];
+        int col[PER_LANE], own[PER_LANE];
+        double v1[PER_LANE], v2[PER_LANE];
 #pragma unroll
-        for (int u = 0; u < SPG_PER_LANE; u++) {
+        for (int u = 0; u < PER_LANE; u++) {
           int f = lane + 32 * u;
           col[u] = -1;
           if (f < total) {
@@ -298,7 +324,7 @@ __global__ void __launch_bounds__(SPG_FWARPS * 32)
           }
         }
 #pragma unroll
-        for (int u = 0; u < SPG_PER_LANE; u++) {
+        for (int u = 0; u < PER_LANE; u++) {
           int f = lane + 32 * u;
           if (col[u] >= 0) {
             F.sslot[f] = F.slot[spg_find(F.keys, ts, col[u])];
@@ -328,7 +354,7 @@ __global__ void __launch_bounds__(SPG_FWARPS * 32)
       cci[o + t] = F.list[t];
       if (PAIR) {
         cv[o + t] = F.acc[0][t] + F.acc[1][t];
-        cv2[o + t] = acc2[t] + acc2[SPG_CCAP + t];
+        cv2[o + t] = acc2[t] + acc2[C::CCAP + t];
       } else {
         cv[o + t] = ORDERED ? F.acc[0][t] : F.acc[0][t] + F.acc[1][t];
       }
@@ -348,46 +374,62 @@ extern "C" int sphc_spgemm_count(int64_t n, const int64_t* arp, const int32_t* a
   return 0;
 }
 
+template <bool ORDERED, bool PAIR, class C>
+static int fill_launch_c(i64 n, const i64* arp, const int* aci, const double* av,
+                         const double* av2, const i64* brp, const int* bci, const double* bv,
+                         const double* bv2, const i64* crp, int* cci, double* cv, double* cv2,
+                         i64* status, cudaStream_t s, int skip_le) {
+  size_t sm = C::FW * (PAIR ? sizeof(SpgFillPair<C>) : sizeof(SpgFill<C>));
+  static bool attr = false;
+  if (!attr) {
+    SPHC_CUDA(cudaFuncSetAttribute(k_spgemm_fill<ORDERED, PAIR, C>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr = true;
+  }
+  unsigned g = grid_for(n, C::FW, SPHC_NUM_SMS * 32);
+  k_spgemm_fill<ORDERED, PAIR, C><<<g, C::FW * 32, sm, s>>>(
+      n, arp, aci, av, av2, brp, bci, bv, bv2, crp, cci, cv, cv2, status, skip_le);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+// max_cols: the longest output row (from the count pass). Rows of <= 64
+// columns go to the small-footprint variant; if longer rows exist, the big
+// variant runs after it on those rows only (each skips the other's rows).
 template <bool ORDERED, bool PAIR>
 static int fill_launch(i64 n, const i64* arp, const int* aci, const double* av,
                        const double* av2, const i64* brp, const int* bci, const double* bv,
                        const double* bv2, const i64* crp, int* cci, double* cv, double* cv2,
-                       i64* status, cudaStream_t s) {
-  size_t sm = SPG_FWARPS * (PAIR ? sizeof(SpgFillPair) : sizeof(SpgFill));
-  static bool attr = false;
-  if (!attr) {
-    SPHC_CUDA(cudaFuncSetAttribute(k_spgemm_fill<ORDERED, PAIR>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr = true;
-  }
-  unsigned g = grid_for(n, SPG_FWARPS, SPHC_NUM_SMS * 32);
-  k_spgemm_fill<ORDERED, PAIR><<<g, SPG_FWARPS * 32, sm, s>>>(
-      n, arp, aci, av, av2, brp, bci, bv, bv2, crp, cci, cv, cv2, status);
-  SPHC_LAUNCH_CHECK();
-  return 0;
+                       i64* status, cudaStream_t s, i64 max_cols) {
+  int rc = fill_launch_c<ORDERED, PAIR, SpgSmall>(n, arp, aci, av, av2, brp, bci, bv, bv2, crp,
+                                                  cci, cv, cv2, status, s, 0);
+  if (rc || (max_cols >= 0 && max_cols <= SpgSmall::CCAP)) return rc;
+  return fill_launch_c<ORDERED, PAIR, SpgBig>(n, arp, aci, av, av2, brp, bci, bv, bv2, crp, cci,
+                                              cv, cv2, status, s, SpgSmall::CCAP);
 }
 
 extern "C" int sphc_spgemm_fill(int64_t n, const int64_t* arp, const int32_t* aci,
                                 const double* av, const int64_t* brp, const int32_t* bci,
                                 const double* bv, const int64_t* crp, int32_t* cci, double* cv,
-                                int ordered, int64_t* status, void* stream) {
+                                int ordered, int64_t max_cols, int64_t* status, void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
   if (ordered)
     return fill_launch<true, false>(n, arp, aci, av, nullptr, brp, bci, bv, nullptr, crp, cci,
-                                    cv, nullptr, status, s);
+                                    cv, nullptr, status, s, max_cols);
   return fill_launch<false, false>(n, arp, aci, av, nullptr, brp, bci, bv, nullptr, crp, cci,
-                                   cv, nullptr, status, s);
+                                   cv, nullptr, status, s, max_cols);
 }
 
 extern "C" int sphc_spgemm_fill_pair(int64_t n, const int64_t* arp, const int32_t* aci,
                                      const double* av1, const double* av2, const int64_t* brp,
                                      const int32_t* bci, const double* bv1, const double* bv2,
                                      const int64_t* crp, int32_t* cci, double* cv1,
-                                     double* cv2, int64_t* status, void* stream) {
+                                     double* cv2, int64_t max_cols, int64_t* status,
+                                     void* stream) {
   if (n <= 0) return 0;
   return fill_launch<false, true>(n, arp, aci, av1, av2, brp, bci, bv1, bv2, crp, cci, cv1,
-                                  cv2, status, as_stream(stream));
+                                  cv2, status, as_stream(stream), max_cols);
 }
 
 // ---------------------------------------------------------------------------

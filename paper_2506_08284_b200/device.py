@@ -318,13 +318,19 @@ def zeros_i64(n):
     return torch.zeros(int(n), dtype=torch.int64, device=device())
 
 
-def scan(counts):
+def scan(counts, with_max=False):
     """Exclusive scan -> (rowptr [n+1], total) (one host sync for the total,
-    shared with any deferred status checks)."""
+    shared with any deferred status checks); with_max: (rowptr, total,
+    max count) from the same readback."""
     n = counts.numel()
     rp = torch.empty(n + 1, dtype=torch.int64, device=counts.device)
     call("sphc_scan_i64", n, counts, rp)
-    return rp, int(readback(rp[n:n + 1])[0][0])
+    if not with_max:
+        return rp, int(readback(rp[n:n + 1])[0][0])
+    mx = torch.amax(counts).reshape(1) if n else torch.zeros(1, dtype=torch.int64,
+                                                             device=counts.device)
+    tot, m = readback(rp[n:n + 1], mx)
+    return rp, int(tot[0]), int(m[0])
 
 
 def scan_many(*counts):
@@ -453,7 +459,7 @@ def spgemm(A, B, drop=True, ordered=False, shard=None):
         shard.gather_ranges(cnt, shard.bounds(n))
         shard.min_(st.t)
     st.defer(capacity_check)
-    rp, nnz = scan(cnt)
+    rp, nnz, mcols = scan(cnt, with_max=True)
     ci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
     v = empty_f64(nnz)
     for _, lo, hi in blocks:
@@ -462,7 +468,7 @@ def spgemm(A, B, drop=True, ordered=False, shard=None):
                  B.col, B.val, None, rp[lo:], ci, v, None)
         else:
             call("sphc_spgemm_fill", hi - lo, _rows(A, lo), A.col, A.val, B.rowptr, B.col,
-                 B.val, rp[lo:], ci, v, int(ordered), st.t)
+                 B.val, rp[lo:], ci, v, int(ordered), mcols, st.t)
     if shard is not None and shard.collective:
         from .sharding import host_offsets
         off = host_offsets(rp, shard.bounds(n))
@@ -496,7 +502,7 @@ def spgemm_pair(A1, A2, B1, B2, drop=True, shard=None):
         shard.gather_ranges(cnt, shard.bounds(n))
         shard.min_(st.t)
     st.defer(capacity_check)
-    rp, nnz = scan(cnt)
+    rp, nnz, mcols = scan(cnt, with_max=True)
     ci = torch.empty(nnz, dtype=torch.int32, device=A1.rowptr.device)
     v1, v2 = empty_f64(nnz), empty_f64(nnz)
     for _, lo, hi in blocks:
@@ -505,7 +511,7 @@ def spgemm_pair(A1, A2, B1, B2, drop=True, shard=None):
                  B1.rowptr, B1.col, B1.val, B2.val, rp[lo:], ci, v1, v2)
         else:
             call("sphc_spgemm_fill_pair", hi - lo, _rows(A1, lo), A1.col, A1.val, A2.val,
-                 B1.rowptr, B1.col, B1.val, B2.val, rp[lo:], ci, v1, v2, st.t)
+                 B1.rowptr, B1.col, B1.val, B2.val, rp[lo:], ci, v1, v2, mcols, st.t)
     if shard is not None and shard.collective:
         from .sharding import host_offsets
         off = host_offsets(rp, shard.bounds(n))

@@ -56,6 +56,7 @@ extern "C" {
 #define SPHC_ST_PC_EMPTY_ROW 14    /* coarse_gradient.py:82-83 row with no entries       */
 #define SPHC_ST_PC_NO_DONOR 15     /* coarse_gradient.py:96-98 empty column after safeguard */
 #define SPHC_ST_AGG_CAPACITY 16    /* aggregation row longer than the device kernel's buffer */
+#define SPHC_ST_PC_NO_FIXPOINT 17  /* Algorithm 1 claiming pass did not converge (internal) */
 
 #define SPHC_EMIN_JMAX 16
 #define SPHC_EMIN_IMAX 128

@@ -93,7 +93,7 @@ def gen_piecewise_const(P, n_passes=2):
     flags, pos, lst = torch.empty(m, **i64), torch.empty(m, **i64), torch.empty(m, **i64)
     srow = torch.empty(P.nnz, dtype=torch.int32, device=dev)
     owner = torch.empty(2 * m_h, dtype=torch.int32, device=dev)
-    changed = torch.empty(1, dtype=torch.int32, device=dev)
+    changed = torch.empty(2, dtype=torch.int32, device=dev)
     assign = torch.empty(m_h, **i64)
     call("sphc_piecewise_const", m_h, m_H, P.rowptr, P.col, P.val, Pc.rowptr, Pc.col, Pc.val,
          int(n_passes), target, counts, srow, owner, changed, flags, pos, lst, assign, st.t)
@@ -106,6 +106,8 @@ def gen_piecewise_const(P, n_passes=2):
             raise ValueError(f"row {rows['PC_EMPTY_ROW']} has no entries to assign")
         if "PC_NO_DONOR" in rows:
             raise ValueError(f"empty column {rows['PC_NO_DONOR']} cannot be assigned any row")
+        if "PC_NO_FIXPOINT" in rows:
+            raise RuntimeError("piecewise_const: claiming pass did not reach its fixed point")
     st.defer(check)
     return assign
 

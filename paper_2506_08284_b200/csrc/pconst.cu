@@ -117,6 +117,65 @@ __global__ void k_pc_diff(i64 m_h, const int* __restrict__ a, const int* __restr
   if (__syncthreads_or(d) && threadIdx.x == 0) *changed = 1;
 }
 
+// One claiming pass's whole fixed-point iteration in a single cooperative
+// launch (formerly one choose + diff launch pair and a host round trip per
+// iteration): grid-wide barriers separate the owner reset, the claims and
+// the change test; changed[2] alternates so a reset never races a read.
+#include <cooperative_groups.h>
+namespace pcg_ = cooperative_groups;
+
+__global__ void __launch_bounds__(PC_WARPS * 32)
+    k_pc_fixpoint(i64 m_h, i64 m_H, const i64* __restrict__ crp, const int* __restrict__ srow,
+                  const i64* __restrict__ target, int n_passes, const i64* __restrict__ assign,
+                  int* own0, int* own1, int* changed, i64* status) {
+  pcg_::grid_group grid = pcg_::this_grid();
+  const i64 nt = (i64)gridDim.x * blockDim.x;
+  const i64 t0 = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  int lane = threadIdx.x & 31;
+  i64 gw = t0 >> 5, nw = nt >> 5;
+  for (i64 r = t0; r < m_h; r += nt) own0[r] = PC_FREE;
+  if (t0 == 0) changed[0] = changed[1] = 0;
+  int cur = 0;
+  bool done = false;
+  for (i64 it = 0; it <= m_H + 1 && !done; it++) {
+    int* oprev = cur ? own1 : own0;
+    cur ^= 1;
+    int* ocur = cur ? own1 : own0;
+    int f = (int)(it & 1);
+    for (i64 r = t0; r < m_h; r += nt) ocur[r] = PC_FREE;
+    if (t0 == 0) changed[f] = 0;
+    grid.sync();
+    for (i64 j = gw; j < m_H; j += nw) {           // claims (k_pc_choose)
+      i64 c0 = crp[j], c1 = crp[j + 1];
+      i64 take = (target[j] + n_passes - 1) / n_passes;
+      i64 got = 0;
+      for (i64 b = c0; b < c1 && got < take; b += 32) {
+        i64 e = b + lane;
+        bool ok = false;
+        int r = 0;
+        if (e < c1) {
+          r = srow[e];
+          ok = assign[r] < 0 && oprev[r] >= (int)j;
+        }
+        unsigned bal = __ballot_sync(FULL_MASK, ok);
+        i64 rank = got + __popc(bal & ((1u << lane) - 1));
+        if (ok && rank < take) atomicMin(ocur + r, (int)j);
+        got += __popc(bal);
+      }
+    }
+    grid.sync();
+    bool d = false;
+    for (i64 r = t0; r < m_h; r += nt) d |= oprev[r] != ocur[r];
+    if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(changed + f, 1);
+    grid.sync();
+    done = ((volatile int*)changed)[f] == 0;
+  }
+  // the owners of the fixed point are in own[cur]; leave them in own0
+  if (cur == 1)
+    for (i64 r = t0; r < m_h; r += nt) own0[r] = own1[r];
+  if (!done && t0 == 0) report(status, SPHC_ST_PC_NO_FIXPOINT, 0);
+}
+
 __global__ void k_pc_commit(i64 m_h, const int* __restrict__ owner, i64* assign) {
   for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < m_h;
        r += (i64)gridDim.x * blockDim.x)
@@ -262,40 +321,32 @@ extern "C" int sphc_piecewise_const(int64_t m_h, int64_t m_H, const int64_t* prp
   SPHC_LAUNCH_CHECK();
   SPHC_CUDA(cudaMemsetAsync(assign, 0xFF, (size_t)m_h * sizeof(int64_t), s));  // -1
   int* own[2] = {owner, owner + m_h};
-  static int32_t* hflag = nullptr;  // pinned readback slot for the convergence flag
-  if (!hflag) SPHC_CUDA(cudaMallocHost((void**)&hflag, sizeof(int32_t)));
-  int rc = 0;
-  for (int pass = 0; pass < n_passes && rc == 0; pass++) {
-    SPHC_CUDA(cudaMemsetAsync(own[0], 0x7F, (size_t)m_h * sizeof(int32_t), s));  // ~ free
-    int cur = 0;
-    bool done = false;
-    for (i64 it = 0; it <= m_H + 1; it++) {
-      int prev = cur;
-      cur ^= 1;
-      SPHC_CUDA(cudaMemsetAsync(own[cur], 0x7F, (size_t)m_h * sizeof(int32_t), s));
-      k_pc_choose<<<gw, PC_WARPS * 32, 0, s>>>(m_H, crp, srow, target, n_passes, assign,
-                                               own[prev], own[cur]);
-      SPHC_LAUNCH_CHECK();
-      SPHC_CUDA(cudaMemsetAsync(changed, 0, sizeof(int32_t), s));
-      k_pc_diff<<<grid_for(m_h, TB, SPHC_NUM_SMS * 4), TB, 0, s>>>(m_h, own[prev], own[cur],
-                                                                   changed);
-      SPHC_LAUNCH_CHECK();
-      SPHC_CUDA(cudaMemcpyAsync(hflag, changed, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      SPHC_CUDA(cudaStreamSynchronize(s));
-      if (*hflag == 0) {
-        done = true;
-        break;
-      }
-    }
-    if (!done) {
-      sphc_set_error("piecewise_const: claiming pass did not reach its fixed point");
-      rc = SPHC_ERR_ARG;
-      break;
-    }
-    k_pc_commit<<<grid_for(m_h, TB), TB, 0, s>>>(m_h, own[cur], assign);
+  static int max_blocks = 0;
+  if (!max_blocks) {
+    int per_sm = 0;
+    SPHC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pc_fixpoint,
+                                                            PC_WARPS * 32, 0));
+    max_blocks = per_sm * SPHC_NUM_SMS;
+  }
+  // few blocks: the pass is a chain of grid barriers, whose cost grows with
+  // the block count; 2 per SM keep every SM busy on the claims
+  i64 want = (m_H > m_h ? m_H : m_h) * 32 / (PC_WARPS * 32) + 1;
+  int cap = max_blocks < 2 * SPHC_NUM_SMS ? max_blocks : 2 * SPHC_NUM_SMS;
+  int gfp = (int)(want < cap ? want : cap);
+  i64 mh = m_h, mH = m_H;
+  int* own0 = own[0];
+  int* own1 = own[1];
+  // changed: 2 ints (the device array holds at least one int64 slot's worth)
+  for (int pass = 0; pass < n_passes; pass++) {
+    void* args[] = {&mh, &mH, (void*)&crp, (void*)&srow, (void*)&target, &n_passes,
+                    (void*)&assign, &own0, &own1, &changed, &status};
+    SPHC_CUDA(cudaLaunchCooperativeKernel((void*)k_pc_fixpoint, dim3(gfp), dim3(PC_WARPS * 32),
+                                          args, 0, s));
+    g_sphc_launches++;
+    k_pc_commit<<<grid_for(m_h, TB), TB, 0, s>>>(m_h, own0, assign);
     SPHC_LAUNCH_CHECK();
   }
-  if (rc) return rc;
+  int rc = 0;
   SPHC_CUDA(cudaMemsetAsync(counts, 0, (size_t)m_H * sizeof(int64_t), s));
   k_pc_counts<<<grid_for(m_h, TB), TB, 0, s>>>(m_h, assign, counts);
   SPHC_LAUNCH_CHECK();

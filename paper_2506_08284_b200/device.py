@@ -21,7 +21,8 @@ SLOTS = 32
 ST = dict(ZERO_DIAG=0, NONPOS_DIAG=1, NODAL_ZERO_DIAG=2, ZERO_ROWSUM=3,
           MALFORMED_GRAD=4, EMPTY_I=5, REDUCIBLE=6, RANK_LOW=7, EMIN_CAPACITY=8,
           EMPTY_J=9, SPGEMM_CAPACITY=10, SORT_CAPACITY=11, TRSV_STALL=12,
-          PC_EMPTY_COLUMN=13, PC_EMPTY_ROW=14, PC_NO_DONOR=15, AGG_CAPACITY=16)
+          PC_EMPTY_COLUMN=13, PC_EMPTY_ROW=14, PC_NO_DONOR=15, AGG_CAPACITY=16,
+          PC_NO_FIXPOINT=17)
 
 
 _DEVICE = None

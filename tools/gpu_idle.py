@@ -39,10 +39,12 @@ print(f"GPU span {1e-3*(t1-t0):.2f} ms, busy {1e-3*busy:.2f} ms ({100*busy/(t1-t
 # split at the largest gap between setup and solve is hard; report by name
 import collections
 agg = collections.defaultdict(float)
+cnt = collections.Counter()
 for a, b_, n in kern:
     agg[n.split("(")[0][:50]] += b_ - a
-for n, v in sorted(agg.items(), key=lambda kv: -kv[1])[:25]:
-    print(f"{v/1e3:8.3f} ms  {n}")
+    cnt[n.split("(")[0][:50]] += 1
+for n, v in sorted(agg.items(), key=lambda kv: -kv[1])[:int(os.environ.get("TOPK", "25"))]:
+    print(f"{v/1e3:8.3f} ms  x{cnt[n]:4d}  {n}")
 # gaps histogram
 gaps = [allg[i+1][0] - allg[i][1] for i in range(len(allg)-1)]
 gaps = [g for g in gaps if g > 0]

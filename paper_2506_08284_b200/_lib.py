@@ -83,16 +83,6 @@ def launch_count():
     return int(lib().sphc_launch_count())
 
 
-def _ptr(a):
-    if a is None:
-        return None
-    if isinstance(a, torch.Tensor):
-        return a.data_ptr()
-    if hasattr(a, "ctypes"):      # numpy (host entry points)
-        return a.ctypes.data
-    return int(a)
-
-
 _DEV = None
 
 
@@ -108,18 +98,37 @@ def stream_handle():
 _FN = {}
 
 
+_TENSOR = torch.Tensor
+
+
+def _conv(a):
+    if a is None:
+        return None
+    if isinstance(a, _TENSOR):
+        return a.data_ptr()
+    if hasattr(a, "ctypes"):      # numpy (host entry points)
+        return a.ctypes.data
+    return int(a)
+
+
 def call(name, *args):
     """Invoke an entry point; device ones run on torch's current stream."""
     ent = _FN.get(name)
     if ent is None:
         ret, codes, stream = SIGS[name]
-        ent = _FN[name] = (getattr(lib(), name), codes, stream)
-    f, codes, stream = ent
-    if len(args) != len(codes):
-        raise TypeError(f"{name} takes {len(codes)} arguments, got {len(args)}")
-    conv = [(_ptr(a) if c == "p" else a) for c, a in zip(codes, args)]
+        ent = _FN[name] = (getattr(lib(), name), len(codes),
+                           tuple(i for i, c in enumerate(codes) if c == "p"), stream)
+    f, nargs, pidx, stream = ent
+    if len(args) != nargs:
+        raise TypeError(f"{name} takes {nargs} arguments, got {len(args)}")
+    conv = list(args)
+    for i in pidx:
+        a = conv[i]
+        if a is not None:
+            conv[i] = a.data_ptr() if a.__class__ is _TENSOR else _conv(a)
     if stream:
-        conv.append(stream_handle())
+        conv.append(torch._C._cuda_getCurrentRawStream(_DEV) if _DEV is not None
+                    else stream_handle())
     rc = f(*conv)
     if rc != 0 and not (name == "sphc_host_piecewise_const" and rc == -3):
         raise RuntimeError(f"{name} failed ({rc}): {lib().sphc_last_error().decode()}")

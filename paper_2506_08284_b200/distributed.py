@@ -389,22 +389,33 @@ def dist_pcg_solve(dh, b_own, rtol=1e-8, maxit=500):
     hist, phist = [nb], [math.sqrt(max(rz0, 0.0))]
     status, its = "maxit", 0
     for k in range(maxit):
+        # the whole iteration is queued without a host decision: alpha and
+        # beta live in sc, the update is a no-op when p.Ap <= 0, and the
+        # scalars of the tests come back in ONE readback at the end (the
+        # single-GPU path's scheme, multigrid.pcg_solve)
         ops.spmv(dl0.A.A, halo(dl0.A, ops, p, g), Ap)
         ops.dot(p, Ap, sc[0:1])
         allsum(0, 1)
         sc[4] = 0.0
         ops.pcg_update(sc, p, Ap, x, r, flag)
         ops.dot(r, r, sc[1:2])
-        # the stagnation flag is an OR over ranks: sum of 0/1 ints as doubles
-        fl = torch.tensor([float(flag.item() != 0)], dtype=torch.float64, device=dev)
-        dist.all_reduce(fl, group=g)
+        # the stagnation flag is an OR over ranks: sum of 0/1 as doubles
+        sc[5:6].copy_((flag != 0).to(torch.float64))
         allsum(1, 2)
-        pAp = float(sc[0].item())
+        allsum(5, 6)
+        z = dist_v_cycle(dh, r)
+        ops.dot(r, z, sc[3:4])
+        allsum(3, 4)
+        # next direction queued speculatively (unused if this iteration ends)
+        ops.pcg_direction(sc, z, p)
+        ops.pcg_rotate(sc)
+        h = sc.cpu().numpy()
+        pAp = float(h[0])
         if pAp <= 0.0:
             status = "indefinite"
             break
         its = k + 1
-        if float(fl.item()) == 0.0:
+        if float(h[5]) == 0.0:
             status = "stagnated"
             ops.spmv(dl0.A.A, halo(dl0.A, ops, x, g), Ap, -1.0, 1.0, b_own)
             ops.dot(Ap, Ap, sc[0:1])
@@ -412,15 +423,10 @@ def dist_pcg_solve(dh, b_own, rtol=1e-8, maxit=500):
             hist.append(math.sqrt(float(sc[0].item())))
             phist.append(phist[-1])
             break
-        res = math.sqrt(float(sc[1].item()))
+        res = math.sqrt(float(h[1]))
         hist.append(res)
-        z = dist_v_cycle(dh, r)
-        ops.dot(r, z, sc[3:4])
-        allsum(3, 4)
-        phist.append(math.sqrt(max(float(sc[3].item()), 0.0)))
+        phist.append(math.sqrt(max(float(h[3]), 0.0)))
         if res <= rtol * nb:
             status = "converged"
             break
-        ops.pcg_direction(sc, z, p)
-        ops.pcg_rotate(sc)
     return DistPcgResult(x, its, hist, phist, status, hist[-1] / nb)

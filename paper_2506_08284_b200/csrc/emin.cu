@@ -14,6 +14,7 @@
 #include "common.cuh"
 
 #define EM_WARPS 4
+#define EM_HCAP 256  // open-addressing slots per warp (|I| <= 128)
 #define JM SPHC_EMIN_JMAX
 #define IM SPHC_EMIN_IMAX
 
@@ -30,6 +31,8 @@ struct EminRow {
   int sc[2][JM];       // staged P_n rows of the two endpoints (em_build_J)
   double sv[2][JM];
   unsigned adj[JM];    // interior-edge adjacency bitmasks over J (em_factor)
+  int hkey[EM_HCAP];   // coarse column -> position in Icol (masked S P lookups)
+  unsigned char hpos[EM_HCAP];
   unsigned incm;       // J nodes incident to some edge of I
   int nJ, nI, k, err, fc;
 };
@@ -433,6 +436,21 @@ extern "C" int sphc_emin_fill(int64_t n_e, const int64_t* drp, const int32_t* dc
   return 0;
 }
 
+__device__ __forceinline__ unsigned em_h(int col) {
+  return ((unsigned)col * 2654435761u) & (EM_HCAP - 1);
+}
+
+// position of coarse column col in the row's I, -1 if absent
+__device__ __forceinline__ int em_lookup(const EminRow& R, int col) {
+  unsigned h = em_h(col);
+  for (;;) {
+    int k = R.hkey[h];
+    if (k == col) return R.hpos[h];
+    if (k < 0) return -1;
+    h = (h + 1) & (EM_HCAP - 1);
+  }
+}
+
 __global__ void __launch_bounds__(EM_WARPS * 32)
     k_emin_step(i64 row0, i64 row1, const i64* __restrict__ srp, const int* __restrict__ sci,
                 const double* __restrict__ sv, const double* __restrict__ dinv,
@@ -458,6 +476,8 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
       R.r[q] = tv[t0 + q];
     }
     __syncwarp();
+    for (int t = lane; t < EM_HCAP; t += 32) R.hkey[t] = -1;
+    __syncwarp();
     for (int e = lane; e < nI; e += 32) {
       int col = eci[e0 + e];
       R.Icol[e] = col;
@@ -466,6 +486,9 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
       int a = ep_a[col], b = ep_b[col];
       R.pb[e] = (signed char)lower_bound_i32(R.J, nJ, b);
       R.pa[e] = (signed char)(a < 0 ? -1 : lower_bound_i32(R.J, nJ, a));
+      unsigned h = em_h(col);     // columns of a row are distinct
+      while (atomicCAS(&R.hkey[h], -1, col) != -1) h = (h + 1) & (EM_HCAP - 1);
+      R.hpos[h] = (unsigned char)e;
     }
     if (lane == 0) {
       R.nJ = nJ;
@@ -475,25 +498,64 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
     // masked S P on the fixed pattern: ascending k, sequential per entry
     // (scipy's S @ P order, edge_prolongator.py:173); the next S entry's
     // P-row bounds are loaded while the current row is accumulated
+    // S row entries staged 32 at a time (column, value, P-row bounds: one
+    // coalesced round of loads), then the P rows walked in ascending k with
+    // the next row's loads issued before the current row's accumulation.
+    // Same sums in the same order as the entry-by-entry loop.
     i64 js = srp[i], se = srp[i + 1];
-    int kk = js < se ? sci[js] : 0;
-    double sc = js < se ? sv[js] : 0.0;
-    i64 pb = js < se ? erp[kk] : 0, pe = js < se ? erp[kk + 1] : 0;
-    for (; js < se; js++) {
-      i64 jn = js + 1;
-      int kn = jn < se ? sci[jn] : 0;
-      double sn = jn < se ? sv[jn] : 0.0;
-      i64 nb0 = jn < se ? erp[kn] : 0, nb1 = jn < se ? erp[kn + 1] : 0;
-      for (i64 jp = pb + lane; jp < pe; jp += 32) {
-        int col = eci[jp];
-        int slot = lower_bound_i32(R.Icol, nI, col);
-        if (slot < nI && R.Icol[slot] == col)
-          R.g[slot] = __dadd_rn(R.g[slot], __dmul_rn(sc, p_in[jp]));
+    for (i64 c0 = js; c0 < se; c0 += 32) {
+      int nb = (int)min((i64)32, se - c0);
+      double s_v = 0.0;
+      i64 s_b = 0;
+      int s_l = 0;
+      if (lane < nb) {
+        int k = sci[c0 + lane];
+        s_v = sv[c0 + lane];
+        s_b = erp[k];
+        s_l = (int)(erp[k + 1] - s_b);
       }
-      __syncwarp();
-      sc = sn;
-      pb = nb0;
-      pe = nb1;
+      if (__any_sync(FULL_MASK, s_l > 32)) {
+        // a P row longer than a warp (rare): entry by entry
+        for (int t = 0; t < nb; t++) {
+          double st = __shfl_sync(FULL_MASK, s_v, t);
+          i64 b = __shfl_sync(FULL_MASK, s_b, t);
+          int l = __shfl_sync(FULL_MASK, s_l, t);
+          for (int q = lane; q < l; q += 32) {
+            int slot = em_lookup(R, eci[b + q]);
+            if (slot >= 0) R.g[slot] = __dadd_rn(R.g[slot], __dmul_rn(st, p_in[b + q]));
+          }
+          __syncwarp();
+        }
+        continue;
+      }
+      int coln = -1;
+      double vn = 0.0;
+      {
+        i64 b = __shfl_sync(FULL_MASK, s_b, 0);
+        int l = __shfl_sync(FULL_MASK, s_l, 0);
+        if (lane < l) {
+          coln = eci[b + lane];
+          vn = p_in[b + lane];
+        }
+      }
+      for (int t = 0; t < nb; t++) {
+        int col = coln;
+        double v = vn;
+        double st = __shfl_sync(FULL_MASK, s_v, t);
+        int tn = t + 1 < nb ? t + 1 : t;
+        i64 b = __shfl_sync(FULL_MASK, s_b, tn);
+        int l = __shfl_sync(FULL_MASK, s_l, tn);
+        coln = -1;
+        if (t + 1 < nb && lane < l) {
+          coln = eci[b + lane];
+          vn = p_in[b + lane];
+        }
+        if (col >= 0) {
+          int slot = em_lookup(R, col);
+          if (slot >= 0) R.g[slot] = __dadd_rn(R.g[slot], __dmul_rn(st, v));
+        }
+        __syncwarp();
+      }
     }
     double en = 0.0;
     for (int e = lane; e < nI; e += 32) en += R.p[e] * R.g[e];
@@ -501,29 +563,29 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
     if (lane == 0) e_row[i] = en;
     __syncwarp();
     if (update) {
-      bool ok = true;
-      int fcw = em_factor(R, i, status, lane);
-      if (lane == 0) {
-        int fc = fcw;
-        if (fc == 1) report(status, SPHC_ST_REDUCIBLE, i);
-        ok = fc == 0;
-        if (ok) {
-          int k = R.k;
-          double di = dinv[i];
-          for (int e = 0; e < nI; e++) R.g[e] = __dmul_rn(di, R.g[e]);  // delta
-          for (int q = 0; q < k; q++) R.y[q] = 0.0;
-          for (int e = 0; e < nI; e++) {  // y = G_k^T delta
-            int a = R.pa[e], b = R.pb[e];
-            if (b < k) R.y[b] += R.g[e];
-            if (a >= 0 && a < k) R.y[a] -= R.g[e];
-          }
-          em_solve(R, R.y);
+      int fc = em_factor(R, i, status, lane);
+      if (fc != 0) {                       // warp-uniform
+        if (fc == 1 && lane == 0) report(status, SPHC_ST_REDUCIBLE, i);
+        __syncwarp();
+        continue;
+      }
+      int k = R.k;
+      double di = dinv[i];
+      for (int e = lane; e < nI; e += 32) R.g[e] = __dmul_rn(di, R.g[e]);  // delta
+      __syncwarp();
+      // y = G_k^T delta: lane q sums its J node's contributions in ascending
+      // e, the serial loop's order for that entry (bitwise the same)
+      if (lane < k) {
+        double yq = 0.0;
+        for (int e = 0; e < nI; e++) {
+          if (R.pb[e] == lane) yq += R.g[e];
+          else if (R.pa[e] == lane) yq -= R.g[e];
         }
-        R.err = ok ? 0 : 1;
+        R.y[lane] = yq;
       }
       __syncwarp();
-      if (R.err) continue;
-      int k = R.k;
+      if (lane == 0) em_solve(R, R.y);
+      __syncwarp();
       for (int e = lane; e < nI; e += 32) {
         int a = R.pa[e], b = R.pb[e];
         double gz = (b < k ? R.y[b] : 0.0) - ((a >= 0 && a < k) ? R.y[a] : 0.0);
@@ -533,18 +595,19 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
       }
       __syncwarp();
     }
-    // commutator residual max |G^T p - r| over all of J
-    if (lane == 0) {
-      double gp[JM];
-      for (int q = 0; q < nJ; q++) gp[q] = 0.0;
+    // commutator residual max |G^T p - r| over all of J: lane q forms
+    // (G^T p)_q in ascending e (the serial order), then a warp max
+    double m = 0.0;
+    if (lane < nJ) {
+      double gq = 0.0;
       for (int e = 0; e < nI; e++) {
-        gp[R.pb[e]] += R.p[e];
-        if (R.pa[e] >= 0) gp[R.pa[e]] -= R.p[e];
+        if (R.pb[e] == lane) gq += R.p[e];
+        else if (R.pa[e] == lane) gq -= R.p[e];
       }
-      double m = 0.0;
-      for (int q = 0; q < nJ; q++) m = fmax(m, fabs(gp[q] - R.r[q]));
-      atomic_max_nonneg(res_max, m);
+      m = fabs(gq - R.r[lane]);
     }
+    m = warp_max(m);
+    if (lane == 0) atomic_max_nonneg(res_max, m);
     __syncwarp();
   }
 }

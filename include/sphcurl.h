@@ -267,6 +267,22 @@ int sphc_graph_end(void **exec, void *stream);
 int sphc_graph_launch(void *exec, void *stream);
 int sphc_graph_destroy(void *exec);
 
+/* The whole PCG loop as ONE graph launch (device-side iteration control):
+ * a WHILE conditional node whose body is captured from `stream` between
+ * sphc_pcg_loop_begin and sphc_pcg_loop_end -- one PCG iteration followed by
+ * sphc_pcg_check, which evaluates the reference's tests
+ * (multigrid.py:244-266) on the device, records |r| and sqrt(r.z) in
+ * hist[2 it], hist[2 it + 1], and ends the loop. ctl[0] = rtol |b|,
+ * ctl[1] = maxit, ctl[2] = iterations, ctl[3] = status (0 running,
+ * 1 converged, 2 maxit, 3 stagnated, 4 indefinite). state[0] receives the
+ * loop object. */
+int sphc_pcg_loop_begin(void **state, void *stream);
+int sphc_pcg_check(void *state, double *sc, double *ctl, double *hist, void *stream);
+int sphc_pcg_loop_end(void *state, void *stream);
+int sphc_pcg_loop_launch(void *state, int64_t *kernels_per_iteration, void *stream);
+int sphc_pcg_loop_add_launches(int64_t n);
+int sphc_pcg_loop_destroy(void *state);
+
 /* dst (pinned host) <- src (device), `bytes` bytes, asynchronous on stream
  * (capturable; the PCG scalars' per-iteration readback). */
 int sphc_copy_d2h(void *dst, const void *src, int64_t bytes, void *stream);

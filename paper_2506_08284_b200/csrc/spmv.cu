@@ -210,6 +210,123 @@ extern "C" int sphc_graph_destroy(void* exec) {
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// The whole PCG loop as ONE graph launch: a WHILE conditional node whose body
+// is one captured iteration followed by k_pcg_check, which records the
+// iteration's residual / preconditioned norms on the device, evaluates the
+// reference's tests (multigrid.py:244-266) and sets the loop condition. No
+// host round trip per iteration.
+//   ctl[0] = rtol * |b| (set before each launch), ctl[1] = maxit,
+//   ctl[2] = iterations done, ctl[3] = status (0 running, 1 converged,
+//   2 maxit, 3 stagnated, 4 indefinite); hist[2 it] = |r|, hist[2 it + 1] =
+//   sqrt(max(r.z, 0)) for it = 1..iterations.
+struct SphcLoop {
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  cudaGraphConditionalHandle handle;
+  cudaGraph_t body;
+  unsigned long long start, kernels;
+};
+
+__global__ void k_pcg_check(double* sc, double* ctl, double* hist,
+                            cudaGraphConditionalHandle handle) {
+  double pAp = sc[SPHC_PCG_PAP];
+  int st = 0;
+  int32_t* flag = reinterpret_cast<int32_t*>(sc + 4);
+  if (pAp <= 0.0) {
+    st = 4;
+  } else {
+    double it = ctl[2] + 1.0;
+    ctl[2] = it;
+    if (*flag == 0) {
+      st = 3;
+    } else {
+      double res = sqrt(sc[SPHC_PCG_RR]);
+      long i = (long)it;
+      hist[2 * i] = res;
+      hist[2 * i + 1] = sqrt(fmax(sc[SPHC_PCG_RZN], 0.0));
+      if (res <= ctl[0]) st = 1;
+      else if (it >= ctl[1]) st = 2;
+    }
+  }
+  ctl[3] = (double)st;
+  sc[4] = 0.0;   // the next iteration's change flag
+  cudaGraphSetConditional(handle, st == 0 ? 1u : 0u);
+}
+
+extern "C" int sphc_pcg_loop_begin(void** state, void* stream) {
+  SphcLoop* L = new SphcLoop();
+  cudaError_t e = cudaGraphCreate(&L->graph, 0);
+  if (e == cudaSuccess)
+    e = cudaGraphConditionalHandleCreate(&L->handle, L->graph, 1, cudaGraphCondAssignDefault);
+  cudaGraphNode_t node;
+  cudaGraphNodeParams prm = {};
+  if (e == cudaSuccess) {
+    prm.type = cudaGraphNodeTypeConditional;
+    prm.conditional.handle = L->handle;
+    prm.conditional.type = cudaGraphCondTypeWhile;
+    prm.conditional.size = 1;
+    e = cudaGraphAddNode(&node, L->graph, nullptr, 0, &prm);
+  }
+  if (e == cudaSuccess) {
+    L->body = prm.conditional.phGraph_out[0];
+    e = cudaStreamBeginCaptureToGraph(as_stream(stream), L->body, nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeThreadLocal);
+  }
+  if (e != cudaSuccess) {
+    if (L->graph) cudaGraphDestroy(L->graph);
+    delete L;
+    sphc_set_error("sphc_pcg_loop_begin: %s", cudaGetErrorString(e));
+    return SPHC_ERR_CUDA;
+  }
+  L->start = g_sphc_launches;
+  state[0] = L;
+  return 0;
+}
+
+extern "C" int sphc_pcg_check(void* state, double* sc, double* ctl, double* hist, void* stream) {
+  SphcLoop* L = (SphcLoop*)state;
+  k_pcg_check<<<1, 1, 0, as_stream(stream)>>>(sc, ctl, hist, L->handle);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int sphc_pcg_loop_end(void* state, void* stream) {
+  SphcLoop* L = (SphcLoop*)state;
+  L->kernels = g_sphc_launches - L->start;   // per iteration
+  g_sphc_launches = L->start;
+  cudaGraph_t g = nullptr;
+  SPHC_CUDA(cudaStreamEndCapture(as_stream(stream), &g));
+  cudaError_t e = cudaGraphInstantiate(&L->exec, L->graph, 0);
+  if (e != cudaSuccess) {
+    sphc_set_error("cudaGraphInstantiate (PCG loop): %s", cudaGetErrorString(e));
+    return SPHC_ERR_CUDA;
+  }
+  return 0;
+}
+
+// runs the loop; *kernels_per_iteration lets the caller count launches
+extern "C" int sphc_pcg_loop_launch(void* state, int64_t* kernels_per_iteration, void* stream) {
+  SphcLoop* L = (SphcLoop*)state;
+  SPHC_CUDA(cudaGraphLaunch(L->exec, as_stream(stream)));
+  if (kernels_per_iteration) *kernels_per_iteration = (int64_t)L->kernels;
+  return 0;
+}
+
+extern "C" int sphc_pcg_loop_add_launches(int64_t n) {
+  g_sphc_launches += (unsigned long long)n;
+  return 0;
+}
+
+extern "C" int sphc_pcg_loop_destroy(void* state) {
+  SphcLoop* L = (SphcLoop*)state;
+  if (!L) return 0;
+  if (L->exec) cudaGraphExecDestroy(L->exec);
+  if (L->graph) cudaGraphDestroy(L->graph);
+  delete L;
+  return 0;
+}
+
 extern "C" int sphc_copy_d2h(void* dst, const void* src, int64_t bytes, void* stream) {
   SPHC_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, as_stream(stream)));
   return 0;

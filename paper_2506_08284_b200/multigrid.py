@@ -595,6 +595,43 @@ class PcgGraph:
             self.h = 0
 
 
+def _true_residual(A, x, b, Ap, sc):
+    dv.spmv(A, x, Ap, alpha=-1.0, beta=1.0, z=b)
+    dv.dot(Ap, Ap, sc[0:1])
+    return math.sqrt(float(dv.readback(sc[0:1])[0][0]))
+
+
+class PcgLoop:
+    """The whole PCG loop as one graph launch: a WHILE conditional node whose
+    body is one captured iteration plus the device-side convergence / break-
+    down test (sphc_pcg_check; include/sphcurl.h). Records |r| and sqrt(r.z)
+    per iteration on the device."""
+
+    def __init__(self, body, sc, ctl, hist):
+        h = np.zeros(1, dtype=np.uint64)
+        call("sphc_pcg_loop_begin", h)
+        self.h = int(h[0])
+        try:
+            body()
+            call("sphc_pcg_check", self.h, sc, ctl, hist)
+        finally:
+            call("sphc_pcg_loop_end", self.h)
+        self.ctl = ctl
+
+    def launch(self):
+        k = np.zeros(1, dtype=np.int64)
+        call("sphc_pcg_loop_launch", self.h, k)
+        self.per_iter = int(k[0])
+
+    def __del__(self):
+        if getattr(self, "h", 0):
+            try:
+                call("sphc_pcg_loop_destroy", self.h)
+            except Exception:
+                pass
+            self.h = 0
+
+
 def _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc, flag, stage):
     """One PCG iteration with device-resident scalars (sc slots as in
     include/sphcurl.h SPHC_PCG_*); ends with the scalars copied to ``stage``."""
@@ -606,7 +643,8 @@ def _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc, flag, stage):
     z = precond(r)
     dv.dot(r, z, sc[3:4])
     call("sphc_pcg_direction", n, sc, z, p)
-    call("sphc_copy_d2h", stage, sc, sc.numel() * 8)
+    if stage is not None:
+        call("sphc_copy_d2h", stage, sc, sc.numel() * 8)
     call("sphc_pcg_rotate", sc)
     return z
 
@@ -616,10 +654,11 @@ def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
     """Preconditioned CG from x = 0 (multigrid.py:220-274): same statuses
     (converged | maxit | stagnated | indefinite) and histories.
 
-    The scalars alpha, beta live on the device; with a graph-safe
-    preconditioner (ours) one whole iteration is captured once as a CUDA
-    graph and replayed, with one 48-byte readback per iteration for the
-    convergence / breakdown tests."""
+    The scalars alpha, beta live on the device. With a graph-safe
+    preconditioner (ours) the whole loop is ONE CUDA graph launch: a WHILE
+    conditional node around one captured iteration and a device-side test
+    of the reference's conditions (PcgLoop), captured once per hierarchy;
+    the histories come back in one readback after the loop."""
     A = as_device_csr(A)
     host = not isinstance(b, torch.Tensor)
     b = (dv.upload(np.asarray(b, dtype=np.float64), np.float64) if host
@@ -655,49 +694,63 @@ def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
     history = [nb]
     precond_history = [math.sqrt(max(rz0, 0.0))]
     status, iters = "maxit", 0
-    graph = ws["graph"]
-    if graph_ok and graph is None:
-        # every buffer of the iteration exists already (precond(r) above ran
-        # the V-cycle once), so capture directly; the graph is kept on the
-        # hierarchy for later solves with the same A.
-        # capture on a side stream without torch.cuda.graph's gc.collect() +
-        # empty_cache(), which would force every later allocation back to
-        # cudaMalloc
-        cap = torch.cuda.Stream()
-        cap.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(cap):
-            graph = PcgGraph(lambda: _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc,
-                                                     flag, stage))
-        torch.cuda.current_stream().wait_stream(cap)
-        ws["graph"] = graph
-        if hier is not None:
-            hier._pcg_ws = ws
-    for k in range(maxit):
+    if graph_ok:
+        # the whole loop on the device: one graph launch, one readback
+        loop = ws.get("loop")
+        if loop is None or ws["loop_maxit"] < maxit:
+            ws["ctl"] = dv.zeros_f64(4)
+            ws["hist"] = dv.zeros_f64(2 * (maxit + 1))
+            ws["ctl_host"] = torch.zeros(4, dtype=torch.float64, pin_memory=True)
+            # every buffer of the iteration exists already (precond(r) above
+            # ran the V-cycle once); captured on a side stream
+            cap = torch.cuda.Stream()
+            cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cap):
+                loop = PcgLoop(lambda: _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc,
+                                                      flag, None),
+                               sc, ws["ctl"], ws["hist"])
+            torch.cuda.current_stream().wait_stream(cap)
+            ws["loop"], ws["loop_maxit"] = loop, maxit
+            if hier is not None:
+                hier._pcg_ws = ws
+        ctl, hist, ch = ws["ctl"], ws["hist"], ws["ctl_host"]
+        ch.copy_(torch.tensor([rtol * nb, float(maxit), 0.0, 0.0], dtype=torch.float64))
+        ctl.copy_(ch, non_blocking=True)
         sc[4] = 0.0
-        if graph is not None:
-            graph.replay()
-        else:
+        loop.launch()
+        cv, hv = dv.readback(ctl, hist)
+        iters, code = int(cv[2]), int(cv[3])
+        # launch accounting: every kernel of every executed loop body
+        call("sphc_pcg_loop_add_launches", loop.per_iter * (iters + (code == 4)))
+        history += [float(hv[2 * i]) for i in range(1, iters + 1)]
+        precond_history += [float(hv[2 * i + 1]) for i in range(1, iters + 1)]
+        status = {1: "converged", 2: "maxit", 3: "stagnated", 4: "indefinite"}[code]
+        if code == 3:
+            # the last entry is the true residual of the unchanged iterate
+            history[-1] = _true_residual(A, x, b, Ap, sc)
+            precond_history[-1] = precond_history[-2]
+    else:
+        for k in range(maxit):
+            sc[4] = 0.0
             _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc, flag, stage)
-        torch.cuda.current_stream().synchronize()
-        hv = stage.numpy()
-        pAp = float(hv[0])
-        if pAp <= 0.0:
-            status = "indefinite"
-            break
-        iters = k + 1
-        if hv.view(np.int32)[8] == 0:
-            status = "stagnated"
-            dv.spmv(A, x, Ap, alpha=-1.0, beta=1.0, z=b)
-            dv.dot(Ap, Ap, sc[0:1])
-            history.append(math.sqrt(float(sc[0].item())))
-            precond_history.append(precond_history[-1])
-            break
-        res = math.sqrt(float(hv[1]))
-        history.append(res)
-        precond_history.append(math.sqrt(max(float(hv[3]), 0.0)))
-        if res <= rtol * nb:
-            status = "converged"
-            break
+            torch.cuda.current_stream().synchronize()
+            hv = stage.numpy()
+            pAp = float(hv[0])
+            if pAp <= 0.0:
+                status = "indefinite"
+                break
+            iters = k + 1
+            if hv.view(np.int32)[8] == 0:
+                status = "stagnated"
+                history.append(_true_residual(A, x, b, Ap, sc))
+                precond_history.append(precond_history[-1])
+                break
+            res = math.sqrt(float(hv[1]))
+            history.append(res)
+            precond_history.append(math.sqrt(max(float(hv[3]), 0.0)))
+            if res <= rtol * nb:
+                status = "converged"
+                break
     if hier is not None:
         for lv in hier.levels:
             for sw in (lv.edge_sweeper, lv.aux_sweeper):

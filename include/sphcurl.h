@@ -287,6 +287,25 @@ int sphc_pcg_loop_destroy(void *state);
  * (capturable; the PCG scalars' per-iteration readback). */
 int sphc_copy_d2h(void *dst, const void *src, int64_t bytes, void *stream);
 
+/* nsteps (2 or 3) consecutive Chebyshev steps (sphc_sell_cheb_step
+ * semantics, step k: xout_k = xin_k + d, d <- cd_k d + cr_k D^-1 (b - A xin_k))
+ * in ONE pass over the SELL matrix: row blocks of 256 in ascending order,
+ * step k of a block once step k-1 is done within the matrix bandwidth L
+ * (in blocks: ceil(max|col - row| / 256) + 1), so the block's rows are
+ * re-read from L2. Bitwise identical to nsteps separate launches.
+ * sync: int32 scratch of 1 + nsteps * ceil(n / 256) entries. x_zero applies
+ * to step 0. */
+int sphc_sell_cheb_fused(int64_t n, const int64_t *slice_ptr, const int32_t *sci,
+                         const double *sv, const double *dinv, const double *b, double *d,
+                         int nsteps, const double *xin0, double *xout0, double cd0, double cr0,
+                         const double *xin1, double *xout1, double cd1, double cr1,
+                         const double *xin2, double *xout2, double cd2, double cr2, int x_zero,
+                         int L, int32_t *sync, void *stream);
+
+/* *out = max |col - row| over the stored entries of a CSR with sorted rows. */
+int sphc_csr_bandwidth(int64_t n, const int64_t *rp, const int32_t *ci, int64_t *out,
+                       void *stream);
+
 /* The k-step Lanczos estimate behind the Chebyshev smoother's upper bound
  * (D^-1 A in the D inner product, deterministic start vector) in one
  * cooperative launch on the SELL mirror of A: writes alpha_1..k to sc[0..k)

@@ -378,3 +378,182 @@ extern "C" int sphc_lanczos_sell(int64_t n, const int64_t* slice_ptr, const int3
   g_sphc_launches++;
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// KS consecutive Chebyshev steps (KS = 2 or 3) in ONE pass over the matrix:
+// the rows are cut into blocks of FZ_ROWS; CTAs claim time slots t in
+// ascending order and, at slot t, run step p on block t - (p-1)(L+1) for
+// p = 1..KS. Step p of block b waits until step p-1 is done on every block
+// within the matrix bandwidth (blocks b-L..b+L), so it reads complete
+// values, and it reads block b's SELL rows while step p-1 left them in L2
+// (the window of (KS-1)(L+1) blocks is sized to fit L2 by the caller).
+// Every row's arithmetic is the unfused kernel's (k_sell_cheb<true,1>): same
+// loads, same fma order, same epilogue -- the result is bitwise identical.
+// Buffers written by one CTA and read by another go through L2 (ld.cg /
+// release-acquire flags): L1 is not coherent across SMs.
+#define FZ_ROWS 256
+
+struct FzStep {
+  const double* xin;
+  double* xout;
+  double cd, cr;
+};
+struct FzArgs {
+  FzStep st[3];
+};
+
+__device__ __forceinline__ int fz_ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int KS>
+__global__ void __launch_bounds__(FZ_ROWS)
+    k_sell_cheb_fused(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
+                      const double* __restrict__ sv, const double* __restrict__ dinv,
+                      const double* __restrict__ b, double* d, FzArgs a, int x_zero, int L,
+                      int nblk, int* ticket, int* done) {
+  __shared__ int slot;
+  const int nslots = nblk + (KS - 1) * (L + 1);
+  for (;;) {
+    if (threadIdx.x == 0) slot = atomicAdd(ticket, 1);
+    __syncthreads();
+    int t = slot;
+    __syncthreads();
+    if (t >= nslots) return;
+#pragma unroll
+    for (int p = 0; p < KS; p++) {
+      int blk = t - p * (L + 1);
+      if (blk < 0 || blk >= nblk) continue;
+      if (p > 0) {   // step p-1 done on blocks [blk - L, blk + L]
+        const int* prev = done + (size_t)(p - 1) * nblk;
+        int lo = max(0, blk - L), hi = min(nblk - 1, blk + L);
+        for (;;) {
+          bool ok = true;
+          for (int c = lo + threadIdx.x; c <= hi; c += FZ_ROWS) ok &= fz_ld_acquire(prev + c) != 0;
+          if (__syncthreads_and(ok)) break;
+        }
+      }
+      const FzStep st = a.st[p];
+      const bool zero = x_zero && p == 0;
+      i64 row = (i64)blk * FZ_ROWS + threadIdx.x;
+      if (row < n) {
+        i64 s = row / SELL_C;
+        int r = (int)(row % SELL_C);
+        i64 b0 = sp[s];
+        int w = (int)((sp[s + 1] - b0) / SELL_C);
+        double acc = 0.0;
+        if (!zero) {
+          i64 base = b0 + r;
+          for (int j0 = 0; j0 < w; j0 += 4) {
+            int c[4];
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              int j = j0 + u;
+              if (j < w) {
+                i64 o = base + (i64)j * SELL_C;
+                // the last step streams the matrix out of L2; earlier ones
+                // leave it for the next step
+                v[u] = (p == KS - 1) ? __ldcs(sv + o) : __ldg(sv + o);
+                c[u] = (p == KS - 1) ? __ldcs(sci + o) : __ldg(sci + o);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+              if (j0 + u < w) acc = fma(v[u], __ldcg(st.xin + c[u]), acc);
+          }
+        }
+        double res = b[row] - acc;
+        double dn = st.cr * dinv[row] * res;
+        if (st.cd != 0.0) dn = fma(st.cd, __ldcg(d + row), dn);
+        __stcg(d + row, dn);
+        __stcg(st.xout + row, (zero ? 0.0 : __ldcg(st.xin + row)) + dn);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(done + (size_t)p * nblk + blk),
+                     "r"(1)
+                     : "memory");
+      }
+    }
+  }
+}
+
+// maximum |col - row| of a CSR matrix (the fused steps' dependency range)
+__global__ void k_csr_bandwidth(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
+                                unsigned long long* out) {
+  unsigned long long m = 0;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    i64 s = rp[i], e = rp[i + 1];
+    if (e > s) {
+      i64 a = (i64)ci[s] - i, z = (i64)ci[e - 1] - i;   // sorted columns
+      unsigned long long v = (unsigned long long)max(a < 0 ? -a : a, z < 0 ? -z : z);
+      m = max(m, v);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL_MASK, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+extern "C" int sphc_csr_bandwidth(int64_t n, const int64_t* rp, const int32_t* ci,
+                                  int64_t* out, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  SPHC_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), s));
+  if (n <= 0) return 0;
+  k_csr_bandwidth<<<grid_for(n, 256), 256, 0, s>>>(n, rp, ci, (unsigned long long*)out);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int sphc_sell_cheb_fused(int64_t n, const int64_t* slice_ptr, const int32_t* sci,
+                                    const double* sv, const double* dinv, const double* b,
+                                    double* d, int nsteps, const double* xin0, double* xout0,
+                                    double cd0, double cr0, const double* xin1, double* xout1,
+                                    double cd1, double cr1, const double* xin2, double* xout2,
+                                    double cd2, double cr2, int x_zero, int L, int32_t* sync,
+                                    void* stream) {
+  if (n <= 0) return 0;
+  if (nsteps < 2 || nsteps > 3 || L < 0) {
+    sphc_set_error("sphc_sell_cheb_fused: nsteps must be 2 or 3");
+    return SPHC_ERR_ARG;
+  }
+  cudaStream_t s = as_stream(stream);
+  int nblk = (int)((n + FZ_ROWS - 1) / FZ_ROWS);
+  // sync = [ticket | done flags: nsteps x nblk]
+  SPHC_CUDA(cudaMemsetAsync(sync, 0, (size_t)(1 + nsteps * nblk) * sizeof(int32_t), s));
+  FzArgs a;
+  a.st[0] = {xin0, xout0, cd0, cr0};
+  a.st[1] = {xin1, xout1, cd1, cr1};
+  a.st[2] = {xin2, xout2, cd2, cr2};
+  static int per_sm[4] = {0, 0, 0, 0};
+  if (!per_sm[nsteps]) {
+    if (nsteps == 2)
+      SPHC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[2], k_sell_cheb_fused<2>,
+                                                              FZ_ROWS, 0));
+    else
+      SPHC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[3], k_sell_cheb_fused<3>,
+                                                              FZ_ROWS, 0));
+  }
+  // persistent CTAs, all resident (a CTA may wait on slots claimed earlier)
+  int g = per_sm[nsteps] * SPHC_NUM_SMS;
+  static int cap = -1;
+  if (cap < 0) {
+    const char* e = getenv("SPHC_FUSE_CTAS");
+    cap = e ? atoi(e) : 0;
+  }
+  if (cap > 0 && g > cap) g = cap;
+  int nslots = nblk + (nsteps - 1) * (L + 1);
+  if (g > nslots) g = nslots;
+  if (nsteps == 2)
+    k_sell_cheb_fused<2><<<g, FZ_ROWS, 0, s>>>(n, slice_ptr, sci, sv, dinv, b, d, a, x_zero, L,
+                                               nblk, sync, sync + 1);
+  else
+    k_sell_cheb_fused<3><<<g, FZ_ROWS, 0, s>>>(n, slice_ptr, sci, sv, dinv, b, d, a, x_zero, L,
+                                               nblk, sync, sync + 1);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}

@@ -31,6 +31,16 @@ from .trace import phase
 _NULLSPACE_TOL = 1e-10
 USE_SELL = os.environ.get("SPHC_SELL", "1") != "0"
 USE_GRAPH = os.environ.get("SPHC_PCG_GRAPH", "1") != "0"
+# fused Chebyshev steps (csrc/sell.cu k_sell_cheb_fused): operators with at
+# least as many rows as the unfused kernel runs thread-per-row on (bitwise
+# identical results), L2 window budget per pass. OFF by default: measured
+# slower (C4 V-cycle 11.9 ms fused vs 9.2 ms unfused) -- the dependency lag
+# is a whole z-plane of edges, so the rows in flight at full occupancy
+# overflow L2 before the second step re-reads them, and capping the CTAs to
+# fit starves the loads. SPHC_FUSE_MB=64 enables it.
+FUSE_ROWS = 256
+FUSE_MIN_ROWS = int(os.environ.get("SPHC_FUSE_MIN_ROWS", str(148 * 48 * 32)))
+FUSE_L2_BYTES = float(os.environ.get("SPHC_FUSE_MB", "0")) * 2**20
 
 CHEB_POWER_ITERS = 15
 CHEB_SAFETY = 1.1
@@ -81,10 +91,14 @@ def finalize_sweepers():
     pend = list(_UNFINISHED)
     _UNFINISHED.clear()
     live = [sw for sw in pend if sw._sc is not None]
-    hs = dv.readback(*[sw._sc for sw in live]) if live else (dv.flush_checks() or [])
+    bws = [sw for sw in pend if getattr(sw, "_bw", None) is not None]
+    tens = [sw._sc for sw in live] + [sw._bw for sw in bws]
+    hs = dv.readback(*tens) if tens else (dv.flush_checks() or [])
     it = iter(hs)
     for sw in pend:
         sw._finish(next(it) if sw._sc is not None else None)
+    for sw in bws:
+        sw._plan_fusion(int(next(it)[0]))
 
 
 class ChebyshevSweeper:
@@ -110,7 +124,31 @@ class ChebyshevSweeper:
         # sweeper's of the hierarchy (finalize_sweepers)
         self.hi = self.lo = self.coefs = None
         self._sc = self._lanczos()
+        # fused multi-step launches for operators streamed from HBM
+        # (sphc_sell_cheb_fused): needs the matrix bandwidth, read back
+        # with the Lanczos scalars
+        self.fuse, self._bw = 0, None
+        if self.sell is not None and n >= FUSE_MIN_ROWS and degree >= 2:
+            self._bw = torch.zeros(1, dtype=torch.int64, device=d.device)
+            call("sphc_csr_bandwidth", n, A.rowptr, A.col, self._bw)
         _UNFINISHED.append(self)
+
+    def _plan_fusion(self, bw):
+        """Steps per pass: the most (<= 3) whose L2 window -- (steps - 1)
+        dependency ranges of row blocks -- fits FUSE_L2_BYTES."""
+        self._bw = None
+        n = self.A.shape[0]
+        nblk = (n + FUSE_ROWS - 1) // FUSE_ROWS
+        self.fuse_L = -(-bw // FUSE_ROWS) + 1
+        per_blk = 12.0 * self.sell.padded / nblk
+        self.fuse = 0
+        for ks in (3, 2):
+            if ks <= self.degree and (ks - 1) * (self.fuse_L + 1) * per_blk <= FUSE_L2_BYTES:
+                self.fuse = ks
+                break
+        if self.fuse:
+            self.fuse_sync = torch.empty(1 + self.fuse * nblk, dtype=torch.int32,
+                                         device=self.d.device)
 
     def _finish(self, sc):
         k = CHEB_POWER_ITERS
@@ -178,6 +216,11 @@ class ChebyshevSweeper:
         A = self.A
         n = A.shape[0]
         cur = x
+        if self.fuse:
+            for _ in range(sweeps):
+                cur = self._fused_sweep(cur, b, x_zero)
+                x_zero = False
+            return cur
         for _ in range(sweeps):
             for step, (cd, cr) in enumerate(self.coefs):
                 out = self.buf[0] if cur is not self.buf[0] else self.buf[1]
@@ -191,6 +234,34 @@ class ChebyshevSweeper:
                          b, None if z else cur, out, self.d, cd, cr, int(z))
                 cur = out
             x_zero = False
+        return cur
+
+
+    def _fused_sweep(self, x, b, x_zero):
+        """The polynomial's steps in passes of self.fuse steps (the same
+        buffers and arithmetic as the step-by-step loop)."""
+        m, n = self.sell, self.A.shape[0]
+        seq, cur = [], x
+        for cd, cr in self.coefs:
+            out = self.buf[0] if cur is not self.buf[0] else self.buf[1]
+            seq.append((cur, out, cd, cr))
+            cur = out
+        k = 0
+        while k < len(seq):
+            ks = min(self.fuse, len(seq) - k)
+            z = int(x_zero and k == 0)
+            if ks == 1:
+                xin, xout, cd, cr = seq[k]
+                call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, self.dinv, b,
+                     None if z else xin, xout, self.d, cd, cr, z, m.padded)
+            else:
+                st = seq[k:k + ks] + [(None, None, 0.0, 0.0)] * (3 - ks)
+                args = []
+                for j, (xin, xout, cd, cr) in enumerate(st):
+                    args += [None if (z and j == 0) else xin, xout, cd, cr]
+                call("sphc_sell_cheb_fused", n, m.slice_ptr, m.col, m.val, self.dinv, b,
+                     self.d, ks, *args, z, self.fuse_L, self.fuse_sync)
+            k += ks
         return cur
 
 

@@ -180,7 +180,7 @@ class DeviceCSR:
     @staticmethod
     def from_scipy(A, dev=None):
         dev = dev or device()
-        A = sp.csr_matrix(A)
+        A = host_csr(A)
         if not A.has_canonical_format:
             A = A.copy()
             A.sum_duplicates()
@@ -202,6 +202,14 @@ class DeviceCSR:
             if m <= lim:
                 return L
         return 32
+
+
+def host_csr(A):
+    """A scipy CSR as is (so scipy's cached canonical-format flag survives
+    repeated calls with the same matrix object); anything else converted."""
+    if sp.issparse(A) and A.format == "csr":
+        return A
+    return sp.csr_matrix(A)
 
 
 def as_device_csr(A):
@@ -227,7 +235,7 @@ class AsyncUpload:
         dev = device()
         self.mats = []
         for A in mats:
-            A = sp.csr_matrix(A)
+            A = host_csr(A)
             if not A.has_canonical_format:
                 A = A.copy()
                 A.sum_duplicates()

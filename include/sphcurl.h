@@ -283,6 +283,14 @@ int sphc_pcg_loop_launch(void *state, int64_t *kernels_per_iteration, void *stre
 int sphc_pcg_loop_add_launches(int64_t n);
 int sphc_pcg_loop_destroy(void *state);
 
+/* Page-lock / release a caller's host range in place (uploads then DMA
+ * straight from it); register fails (non-sticky) on overlapping ranges. */
+int sphc_host_register(void *p, int64_t bytes);
+int sphc_host_unregister(void *p);
+
+/* dst (device) <- src (page-locked host), `bytes` bytes, asynchronous. */
+int sphc_copy_h2d(void *dst, const void *src, int64_t bytes, void *stream);
+
 /* dst (pinned host) <- src (device), `bytes` bytes, asynchronous on stream
  * (capturable; the PCG scalars' per-iteration readback). */
 int sphc_copy_d2h(void *dst, const void *src, int64_t bytes, void *stream);

@@ -600,3 +600,32 @@ extern "C" int sphc_reciprocal(int64_t n, const double* x, const double* zero_su
   SPHC_LAUNCH_CHECK();
   return 0;
 }
+
+// ------------------------------------------------------------------ host memory
+// Page-lock a caller's host array in place so uploads DMA straight from it
+// (no staging copy); registered once per array by the Python side.
+extern "C" int sphc_host_register(void* p, int64_t bytes) {
+  cudaError_t e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();   // not sticky: the caller falls back to staging
+    sphc_set_error("cudaHostRegister: %s", cudaGetErrorString(e));
+    return SPHC_ERR_CUDA;
+  }
+  return 0;
+}
+
+extern "C" int sphc_host_unregister(void* p) {
+  cudaError_t e = cudaHostUnregister(p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return SPHC_ERR_CUDA;
+  }
+  return 0;
+}
+
+// dst (device) <- src (host, page-locked), asynchronous on stream
+extern "C" int sphc_copy_h2d(void* dst, const void* src, int64_t bytes, void* stream) {
+  SPHC_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, as_stream(stream)));
+  return 0;
+}
+

@@ -145,12 +145,18 @@ def upload(a, dtype, dev=None):
     """Host array -> new device tensor through a reused pinned staging buffer
     (one cast on the host, one DMA at pinned-memory bandwidth)."""
     dev = dev or device()
+    a0 = a
     a = np.asarray(a)
     n = a.size
     t = torch.empty(n, dtype=torch.from_numpy(np.zeros(0, dtype=dtype)).dtype, device=dev)
     if n == 0:
         return t
     nbytes = n * np.dtype(dtype).itemsize
+    # direct DMA only from the caller's own array object (a temporary made
+    # by asarray would be freed -- and unregistered -- under the copy)
+    if a is a0 and a.dtype == np.dtype(dtype) and pinned_in_place(a):
+        call("sphc_copy_h2d", t, a, nbytes)     # stream ordered, no staging / sync
+        return t
     buf = _PINNED.get("buf")
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1 << 24), dtype=torch.uint8, pin_memory=True)
@@ -221,6 +227,41 @@ def as_device_csr(A):
 
 
 _STAGE = {}
+_REG = {}      # (address, bytes) -> weakref of the page-locked host array
+
+
+def pinned_in_place(a):
+    """True if host array ``a`` is page-locked for direct DMA. Each array
+    object is registered once (sphc_host_register) and released when it is
+    garbage collected; small, strided or overlapping arrays return False
+    (the caller stages them instead)."""
+    if a.nbytes < (1 << 20) or not a.flags.c_contiguous or os.environ.get("SPHC_PIN") == "0":
+        return False
+    import weakref
+    key = (a.ctypes.data, a.nbytes)
+    ref = _REG.get(key)
+    if ref is not None:
+        if ref() is a:
+            return True
+        return False          # an older array at this address: let it be released first
+    try:
+        call("sphc_host_register", a, a.nbytes)
+    except RuntimeError:
+        return False
+
+    def release(_, ptr=key[0], key=key):
+        _REG.pop(key, None)
+        try:
+            _lib.lib().sphc_host_unregister(ctypes_void(ptr))
+        except Exception:     # noqa: BLE001 - interpreter shutdown
+            pass
+    _REG[key] = weakref.ref(a, release)
+    return True
+
+
+def ctypes_void(p):
+    import ctypes
+    return ctypes.c_void_p(p)
 
 
 class AsyncUpload:
@@ -273,18 +314,28 @@ class AsyncUpload:
                                   pin_memory=True)
                 _STAGE["buf"] = buf
             hv = buf.numpy()
+            # arrays already in the device dtype DMA straight from the
+            # caller's page-locked memory; the rest are cast into staging
+            direct = [a.dtype == np.dtype(d) and pinned_in_place(a) for a, d in self.specs]
             jobs = []
-            for (a, d), o in zip(self.specs, self.offs):
+            for (a, d), o, dr in zip(self.specs, self.offs, direct):
+                if dr:
+                    continue
                 dstv = hv[o:o + a.size * np.dtype(d).itemsize].view(d)
                 step = max(1 << 18, a.size // self.nthreads + 1)
                 for k in range(0, a.size, step):
                     jobs.append((dstv[k:k + step], a[k:k + step]))
-            from concurrent.futures import ThreadPoolExecutor
-            with ThreadPoolExecutor(self.nthreads) as ex:
-                list(ex.map(lambda j: np.copyto(j[0], j[1], casting="unsafe"), jobs))
             with torch.cuda.stream(self.stream):
-                for t, (a, d), o in zip(self.dst, self.specs, self.offs):
-                    if a.size:
+                for t, (a, d), dr in zip(self.dst, self.specs, direct):
+                    if dr and a.size:
+                        call("sphc_copy_h2d", t, a, a.nbytes)
+            if jobs:
+                from concurrent.futures import ThreadPoolExecutor
+                with ThreadPoolExecutor(self.nthreads) as ex:
+                    list(ex.map(lambda j: np.copyto(j[0], j[1], casting="unsafe"), jobs))
+            with torch.cuda.stream(self.stream):
+                for t, (a, d), o, dr in zip(self.dst, self.specs, self.offs, direct):
+                    if a.size and not dr:
                         t.view(torch.uint8).copy_(buf[o:o + a.size * np.dtype(d).itemsize],
                                                   non_blocking=True)
                 self.event.record(self.stream)

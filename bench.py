@@ -25,6 +25,7 @@ import math
 import os
 import statistics
 import subprocess
+import tempfile
 import sys
 import time
 
@@ -91,17 +92,21 @@ class ClockSampler:
         idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
         try:
             import pynvml  # noqa: F401
+            # samples go to a file, not a pipe: a pipe nobody drains fills
+            # up after ~5 s and blocks the poller (long C4/C5 runs)
+            self.out = tempfile.TemporaryFile(mode="w+")
             self.p = subprocess.Popen([sys.executable, "-c", _NVML_POLL, str(idx)],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                      stdout=self.out, stderr=subprocess.DEVNULL,
                                       text=True)
             self.kind = "nvml"
             time.sleep(0.2)        # first samples before the timed region
         except Exception:   # noqa: BLE001
             try:
+                self.out = tempfile.TemporaryFile(mode="w+")
                 self.p = subprocess.Popen(
                     ["nvidia-smi", "-i", str(idx), f"--query-gpu={self.Q}",
                      "--format=csv,noheader,nounits", "-lms", "200"],
-                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                    stdout=self.out, stderr=subprocess.DEVNULL, text=True)
                 self.kind = "nvidia-smi"
             except OSError:
                 self.p = None
@@ -111,8 +116,10 @@ class ClockSampler:
         self.lines = []
         if self.p is not None:
             self.p.terminate()
-            out, _ = self.p.communicate(timeout=10)
-            self.lines = [l for l in out.splitlines() if l.strip()]
+            self.p.wait(timeout=10)
+            self.out.seek(0)
+            self.lines = [l for l in self.out.read().splitlines() if l.strip()]
+            self.out.close()
 
     def mark(self, which):
         """Wall-clock bounds of the timed region (samples outside are dropped)."""

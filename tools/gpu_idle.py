@@ -6,12 +6,22 @@ import torch
 from torch.profiler import profile, ProfilerActivity
 from paper_2506_08284_b200 import multigrid as mg, device as dv
 from paper_2506_08284_b200.inputs import make_config
-s, rhs, cfg = make_config(sys.argv[1] if len(sys.argv) > 1 else "C2")
-A_e, S, A_n, D = (dv.DeviceCSR.from_scipy(M) for M in (s.A_e, s.S, s.A_n, s.D))
+name = sys.argv[1] if len(sys.argv) > 1 else "C2"
+if name in ("C3", "C4", "C5"):
+    from paper_2506_08284_b200.assembly import make_device_config
+    s, rhs, cfg = make_device_config(name)
+    A_e, S, A_n, D = s.A_e, s.S, s.A_n, s.D
+else:
+    s, rhs, cfg = make_config(name)
+    A_e, S, A_n, D = (dv.DeviceCSR.from_scipy(M) for M in (s.A_e, s.S, s.A_n, s.D))
 b = torch.from_numpy(rhs).cuda()
-sc = mg.SolverConfig(coarse_size=1000)
-for _ in range(3):
-    h = mg.build_hierarchy(A_e, S, A_n, D, sc); r = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+sc = mg.SolverConfig(coarse_size=cfg.get("coarse_size", 1000))
+for _ in range(int(os.environ.get("WARM", "3"))):
+    h = None
+    h = mg.build_hierarchy(A_e, S, A_n, D, sc)
+    if os.environ.get("SETUP_ONLY") != "1":
+        r = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+h = None
 torch.cuda.synchronize()
 marks = {}
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:

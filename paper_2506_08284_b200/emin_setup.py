@@ -152,15 +152,35 @@ def setup_constraints(D_h, P_n, cg, shard=None):
     n_aug = 0
     if bool(any_need[0]):
         from . import repair
+        cg0 = cg
         with phase("emin.repair"):
-            cg, xrp, xeid, n_aug = repair.make_irreducible_pass(
+            cg, xrp, xeid, n_aug, post = repair.make_irreducible_pass(
                 need, flags, rowmax, rdp_scale, T, pattern, cg)
         with phase("emin.refill"):
-            st, icount, jcount, rmax2, dims, _, _ = _count(D, P, cg, xrp, xeid, False, shard)
+            # the refill flags the post-pass rows that are still reducible
+            # (instead of raising); the host repairs just those, then refills
+            track = post is not None
+            st, icount, jcount, rmax2, dims, rowflag, _ = _count(D, P, cg, xrp, xeid, track,
+                                                                 shard)
             st.defer(check)
-            T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st, shard=shard)
+            T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st,
+                               rowflag=rowflag, shard=shard)
             st.defer(check)
-            h = dv.readback(dims)[0]
+            if track:
+                red = torch.nonzero(rowflag & 1).flatten()    # (syncs: sized output)
+                h = dv.readback(dims)[0]
+                if red.numel():
+                    with phase("emin.repair"):
+                        cg, xrp, xeid, n_aug = repair.finish_post_pass(
+                            post, red.cpu().numpy(), cg0, n_e)
+                    st, icount, jcount, rmax2, dims, _, _ = _count(D, P, cg, xrp, xeid, False,
+                                                                   shard)
+                    st.defer(check)
+                    T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st, shard=shard)
+                    st.defer(check)
+                    h = dv.readback(dims)[0]
+            else:
+                h = dv.readback(dims)[0]
     h = h.reshape(129, 17)
     nz = np.argwhere(h)
     counter = Counter({(int(i), int(j)): int(h[i, j]) for i, j in nz})

@@ -47,6 +47,19 @@ def _rows(M, rows):
     return out
 
 
+def _isect_sorted(ka, kb):
+    """Positions (ia, ib) of the common keys of two sorted unique arrays
+    (a binary-search merge: no re-sort of the concatenation)."""
+    if ka.size == 0 or kb.size == 0:
+        z = np.zeros(0, dtype=np.int64)
+        return z, z
+    idx = np.searchsorted(kb, ka)
+    ok = idx < kb.size
+    ok[ok] = kb[idx[ok]] == ka[ok]
+    ia = np.flatnonzero(ok)
+    return ia, idx[ia]
+
+
 class _Graph:
     """Components / incidence of one block (edges over node set J)."""
 
@@ -99,7 +112,7 @@ def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
     def score(a, b):
         ka, va = column(a)
         kb, vb = column(b)
-        common, ia, ib = np.intersect1d(ka, kb, assume_unique=True, return_indices=True)
+        ia, ib = _isect_sorted(ka, kb)
         s = 0.0
         for x, y in zip(va[ia], vb[ib]):        # ascending fine edge, unfused
             s += float(x) * float(y)
@@ -173,7 +186,8 @@ def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
         aff = set()
         for e in new_edges:
             a, b = ends[e]
-            aff.update(np.intersect1d(column(a)[0], column(b)[0]).tolist())
+            ka = column(a)[0]
+            aff.update(ka[_isect_sorted(ka, column(b)[0])[0]].tolist())
         aff = sorted(aff)
         rows_T = dict(zip(aff, _rows(T, aff)))
         rows_I = dict(zip(aff, _rows(pattern, aff)))
@@ -182,6 +196,7 @@ def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
         for e in new_edges:
             for n in ends[e]:
                 by_node.setdefault(n, []).append(e)
+        post = []
         for i in aff:
             J, I0 = rows_T[i][0], rows_I[i][0]
             prev = final.get(i)
@@ -194,9 +209,45 @@ def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
             I1 = sorted(set(I0.tolist()) | set(add))
             if len(I1) == len(prev if prev is not None else I0):
                 continue
-            final[i] = repair(i, I1, J)
-    n_aug = len(ends) - n0
-    # per-row extras: appended ids of each repaired row, ascending
+            # grown rows: the reference re-checks them in ascending order and
+            # repairs the reducible ones. The check runs on the device (the
+            # refill pass flags them, emin_setup.setup_constraints); only the
+            # flagged rows come back here (finish_post_pass), in the same
+            # order, so the appended edge ids are the reference's.
+            final[i] = I1
+            post.append(i)
+        state = _PostState(ends, final, n0, {i: rows_T[i][0] for i in post}, repair)
+    else:
+        state = None
+    cg2, xrp, xeid = _extras(cg, ends, final, n0, n_e, dev)
+    return cg2, xrp, xeid, len(ends) - n0, state
+
+
+class _PostState:
+    """What finish_post_pass needs to repair the post-pass rows the device
+    found reducible."""
+
+    def __init__(self, ends, final, n0, J, repair):
+        self.ends, self.final, self.n0, self.J, self.repair = ends, final, n0, J, repair
+
+
+def finish_post_pass(state, rows, cg0, n_e):
+    """Repair the post-pass rows the device flagged reducible, ascending
+    (emin_setup.py:311-333: further edges stay local to the row). Returns the
+    augmented coarse gradient and per-row extras like make_irreducible_pass."""
+    for i in sorted(int(r) for r in rows):
+        if i not in state.J:
+            raise RuntimeError(f"fine edge {i}: reducible after the make_irreducible pass "
+                               "(internal error)")
+        state.final[i] = state.repair(i, list(state.final[i]), state.J[i])
+    dev = cg0.ep_a.device
+    cg2, xrp, xeid = _extras(cg0, state.ends, state.final, state.n0, n_e, dev)
+    return cg2, xrp, xeid, len(state.ends) - state.n0
+
+
+def _extras(cg, ends, final, n0, n_e, dev):
+    """Per-row extras (appended ids of each repaired row, ascending) and
+    the coarse gradient with the appended edges."""
     counts = np.zeros(n_e, dtype=np.int64)
     items = []
     import bisect
@@ -208,8 +259,7 @@ def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
     xrp_h = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
     xrp = torch.from_numpy(xrp_h).to(dev)
     xeid = torch.from_numpy(np.asarray(items, dtype=np.int32)).to(dev)
-    cg = _augment(cg, ends[n0:], dev)
-    return cg, xrp, xeid, n_aug
+    return _augment(cg, ends[n0:], dev), xrp, xeid
 
 
 def _augment(cg, new, dev):

@@ -179,6 +179,19 @@ int sphc_spgemm_fill_long(int64_t n, const int64_t *arp, const int32_t *aci, con
                           const double *bv, const double *bv2, const int64_t *crp,
                           int32_t *cci, double *cv1, double *cv2, void *stream);
 
+/* make_irreducible's main loop on the device (emin_setup.py:183-217,
+ * 283-301): one warp per listed fine edge rows[r]; its coarse-node graph (J
+ * from T, original pattern edges from prp/pci with endpoints ep_a/ep_b) is
+ * joined greedily by the largest |R_dp[:, a] . R_dp[:, b]| over bridging
+ * pairs (columns of R_dp = T^T in ttrp/ttci/ttv, summed in ascending fine
+ * edge, unfused; ties: smallest (a, b)). ncnt[r] = number of joins, their
+ * (a, b) in pairs[2 * (15 r + j)]; -1 single-node graph, -2 |J| > 16. */
+int sphc_emin_repair(int64_t nrows, const int64_t *rows, const int64_t *trp, const int32_t *tci,
+                     const int64_t *prp, const int32_t *pci, const int32_t *ep_a,
+                     const int32_t *ep_b, const int64_t *ttrp, const int32_t *ttci,
+                     const double *ttv, int32_t *ncnt, int32_t *pairs, int64_t *status,
+                     void *stream);
+
 /* ---------------------------------------------------------------- solve */
 
 /* y = alpha * (A x) + beta * z  (z may be NULL; y may alias z).

@@ -626,3 +626,151 @@ extern "C" int sphc_emin_step(int64_t row0, int64_t row1, const int64_t* srp, co
   SPHC_LAUNCH_CHECK();
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// make_irreducible's main loop (emin_setup.py:183-217, 283-301) for the rows
+// the count/fill passes flagged: one warp per row. The row's constraint
+// graph (coarse nodes J <= 16 from T, its original pattern edges I) is
+// connected greedily: among node pairs in different components, join the
+// one with the largest |(D_h P_n)[:, a] . (D_h P_n)[:, b]| (ties and zeros:
+// lexicographically smallest (a, b)), until every node is incident to an
+// edge and the graph is connected. The column dot products are summed in
+// ascending fine edge with separate multiply and add, as scipy's
+// csr_matmat does for the reference's R_dp_csc[:, a].T @ R_dp_csc[:, b], so
+// the decisions are the reference's. Main-loop repairs do not see each
+// other's new edges (the reference extracts every row from the original
+// pattern), so rows are independent; the caller numbers the new edges in
+// ascending row order. Output: ncnt[r] edges in pairs[r * 15 + j] (a, b);
+// ncnt[r] = -1: single-node graph (the reference's ValueError), -2: the row
+// exceeds the kernel's |J| <= 16.
+#define RP_MAXNEW (JM - 1)
+
+__global__ void __launch_bounds__(128)
+    k_emin_repair(i64 nrows, const i64* __restrict__ rows, const i64* __restrict__ trp,
+                  const int* __restrict__ tci, const i64* __restrict__ prp,
+                  const int* __restrict__ pci, const int* __restrict__ ep_a,
+                  const int* __restrict__ ep_b, const i64* __restrict__ ttrp,
+                  const int* __restrict__ ttci, const double* __restrict__ ttv,
+                  int* __restrict__ ncnt, int2* __restrict__ pairs, i64* status) {
+  __shared__ double prod[4][32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 r = gw; r < nrows; r += nw) {
+    i64 i = rows[r];
+    i64 t0 = trp[i];
+    int nJ = (int)(trp[i + 1] - t0);
+    if (nJ > JM) {
+      if (lane == 0) ncnt[r] = -2;
+      continue;
+    }
+    int myJ = lane < nJ ? tci[t0 + lane] : 0x7fffffff;   // J sorted ascending
+    // adjacency bitmasks over J from the original pattern edges
+    unsigned adj = 0u, inc = 0u;
+    i64 p0 = prp[i], p1 = prp[i + 1];
+    for (i64 e = p0; e < p1; e++) {        // warp-uniform loop, <= 128 edges
+      int col = pci[e];
+      int a = ep_a[col], b = ep_b[col];
+      unsigned ba = __ballot_sync(FULL_MASK, lane < nJ && myJ == b);
+      unsigned aa = a >= 0 ? __ballot_sync(FULL_MASK, lane < nJ && myJ == a) : 0u;
+      inc |= ba | aa;
+      if (aa && ba) {
+        int pa = __ffs(aa) - 1, pb = __ffs(ba) - 1;
+        if (lane == pa) adj |= 1u << pb;
+        if (lane == pb) adj |= 1u << pa;
+      }
+    }
+    unsigned full = nJ >= 32 ? 0xffffffffu : ((1u << nJ) - 1u);
+    int nnew = 0;
+    for (;;) {
+      // component label = lowest node index reachable (BFS by bitmask OR)
+      unsigned reach = 1u << lane;
+      if (lane >= nJ) reach = 0u;
+      for (int it = 0; it < JM; it++) {
+        unsigned nr = reach;
+        for (int q = 0; q < nJ; q++) {
+          unsigned aq = __shfl_sync(FULL_MASK, adj, q);
+          if ((reach >> q) & 1u) nr |= aq;
+        }
+        if (__all_sync(FULL_MASK, nr == reach)) break;
+        reach = nr;
+      }
+      int comp = reach ? __ffs(reach) - 1 : 32;
+      bool one = __all_sync(FULL_MASK, lane >= nJ || comp == 0);
+      if (one && inc == full) break;
+      if (one) {                 // a single node without edges: unrepairable
+        nnew = -1;
+        break;
+      }
+      if (nnew >= RP_MAXNEW) {   // cannot happen: each join merges two components
+        nnew = -2;
+        break;
+      }
+      // best bridging pair: exact scores in (x, y) order, strict > keeps the
+      // lexicographically smallest pair among equal scores
+      double best = -1.0;
+      int bx = -1, by = -1;
+      for (int x = 0; x < nJ; x++) {
+        int cx = __shfl_sync(FULL_MASK, comp, x);
+        int a = __shfl_sync(FULL_MASK, myJ, x);
+        i64 a0 = ttrp[a], a1 = ttrp[a + 1];
+        for (int y = x + 1; y < nJ; y++) {
+          int cy = __shfl_sync(FULL_MASK, comp, y);
+          if (cx == cy) continue;
+          int b = __shfl_sync(FULL_MASK, myJ, y);
+          i64 b0 = ttrp[b], b1 = ttrp[b + 1];
+          double s = 0.0;
+          for (i64 c0 = a0; c0 < a1; c0 += 32) {
+            i64 e = c0 + lane;
+            double pr = 0.0;
+            bool hit = false;
+            if (e < a1) {
+              int k = ttci[e];
+              i64 q = lower_bound_i32_g(ttci, b0, b1, k);
+              if (q < b1 && ttci[q] == k) {
+                hit = true;
+                pr = __dmul_rn(ttv[e], ttv[q]);
+              }
+            }
+            prod[w][lane] = pr;
+            unsigned hm = __ballot_sync(FULL_MASK, hit);
+            __syncwarp();
+            if (lane == 0)
+              for (int l = 0; l < 32; l++)
+                if ((hm >> l) & 1u) s = __dadd_rn(s, prod[w][l]);
+            __syncwarp();
+          }
+          s = __shfl_sync(FULL_MASK, fabs(s), 0);
+          if (s > best) {
+            best = s;
+            bx = x;
+            by = y;
+          }
+        }
+      }
+      // join (J[bx], J[by])
+      {
+        int vx = __shfl_sync(FULL_MASK, myJ, bx), vy = __shfl_sync(FULL_MASK, myJ, by);
+        if (lane == 0) pairs[r * RP_MAXNEW + nnew] = make_int2(vx, vy);
+      }
+      if (lane == bx) adj |= 1u << by;
+      if (lane == by) adj |= 1u << bx;
+      inc |= (1u << bx) | (1u << by);
+      nnew++;
+    }
+    if (lane == 0) ncnt[r] = nnew;
+  }
+}
+
+extern "C" int sphc_emin_repair(int64_t nrows, const int64_t* rows, const int64_t* trp,
+                                const int32_t* tci, const int64_t* prp, const int32_t* pci,
+                                const int32_t* ep_a, const int32_t* ep_b, const int64_t* ttrp,
+                                const int32_t* ttci, const double* ttv, int32_t* ncnt,
+                                int32_t* pairs, int64_t* status, void* stream) {
+  if (nrows <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  k_emin_repair<<<grid_for(nrows, 4), 128, 0, s>>>(nrows, rows, trp, tci, prp, pci, ep_a, ep_b,
+                                                   ttrp, ttci, ttv, ncnt, (int2*)pairs, status);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}

@@ -24,8 +24,8 @@ does for the reference's ``R_dp_csc[:, a].T @ R_dp_csc[:, b]``.
 import numpy as np
 import torch
 
-from . import device as dv
-from .device import DeviceCSR
+from paper_2506_08284_b200 import device as dv
+from paper_2506_08284_b200.device import DeviceCSR
 
 
 def _rows(M, rows):
@@ -179,32 +179,7 @@ def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
                 raise ValueError(
                     f"fine edge {i}: nonzero commutator row over a single coarse node "
                     "cannot be satisfied by interior coarse edges")
-    # the main loop's greedy joins, all flagged rows at once on the device
-    # (csrc/emin.cu k_emin_repair); the new edges take ids in ascending row
-    # order, as the reference appends them
-    nr = len(need_rows)
-    rows_d = torch.from_numpy(need_rows.astype(np.int64)).to(dev)
-    ncnt = torch.empty(nr, dtype=torch.int32, device=dev)
-    pairs = torch.empty(nr * 15 * 2, dtype=torch.int32, device=dev)
-    st = dv.Status()
-    dv.call("sphc_emin_repair", nr, rows_d, T.rowptr, T.col, pattern.rowptr, pattern.col,
-            cg.ep_a, cg.ep_b, Tt.rowptr, Tt.col, Tt.val, ncnt, pairs, st.t)
-    cnt_h, pairs_h = dv.readback(ncnt, pairs)
-    pairs_h = pairs_h.reshape(nr, 15, 2)
-    for r, i in enumerate(need_rows.tolist()):
-        c = int(cnt_h[r])
-        if c == -1:
-            raise ValueError(f"fine edge {i}: cannot repair a single-node "
-                             "constraint graph")
-        if c < 0:
-            raise RuntimeError(f"fine edge {i}: constraint block exceeds the device "
-                               "make_irreducible kernel (|J| <= 16)")
-        I = data_I[i][0].tolist()
-        for j in range(c):
-            a, b = int(pairs_h[r, j, 0]), int(pairs_h[r, j, 1])
-            ends.append((min(a, b), max(a, b)))
-            I.append(len(ends) - 1)
-        final[i] = I
+        final[i] = repair(i, I0.tolist(), J)
     new_edges = list(range(n0, len(ends)))
     if new_edges:
         # post pass (emin_setup.py:311-333)
@@ -292,7 +267,7 @@ def _augment(cg, new, dev):
     (coarse_gradient.py:163-171 append_edge)."""
     if not new:
         return cg
-    from .coarse_gradient import CoarseGradient
+    from paper_2506_08284_b200.coarse_gradient import CoarseGradient
     k = len(new)
     a = torch.tensor([e[0] for e in new], dtype=torch.int32, device=dev)
     b = torch.tensor([e[1] for e in new], dtype=torch.int32, device=dev)

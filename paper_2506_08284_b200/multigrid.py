@@ -351,8 +351,12 @@ class Hierarchy:
 
 def _make_level(A_e, S_e, D, cfg, AD=None, smooth=True, shard=None, **extra):
     Dt = dv.transpose(D)
-    nodal_aux = dv.spgemm(Dt, AD if AD is not None else dv.spgemm(A_e, D, shard=shard),
-                          shard=shard)
+    # D^T A D keeps exact cancellations as stored zeros (scipy drops them;
+    # they change no value and no decision, and skipping the compaction
+    # saves a host sync per level)
+    nodal_aux = dv.spgemm(Dt, AD if AD is not None else dv.spgemm(A_e, D, drop=False,
+                                                                  shard=shard),
+                          drop=False, shard=shard)
     level = Level(A_e=A_e, S_e=S_e, D=D, nodal_aux=nodal_aux, Dt=Dt, **extra)
     if smooth:   # the coarsest level is solved directly, never smoothed
         sweeper = SMOOTHERS[cfg.smoother]
@@ -370,7 +374,7 @@ def _check_nullspace(S, D, where, A=None, shard=None):
     AD = None
     if A is not None and dv.same_pattern(A, S):
         AD, SD = dv.spgemm_pair(A, S, D, D, drop=False, shard=shard)
-        AD = dv.drop_zeros(AD)
+        # (stored zeros of A D only feed D^T A D; see _make_level)
     else:
         SD = dv.spgemm(S, D, drop=False, shard=shard)
     m = dv.empty_f64(2)

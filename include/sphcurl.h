@@ -264,6 +264,12 @@ int sphc_lanczos_update(int64_t n, const double *u, const double *dinv, const do
 int sphc_pcg_update(int64_t n, const double *sc, const double *p, const double *Ap, double *x,
                     double *r, int32_t *changed, void *stream);
 
+/* sphc_pcg_update fused with sc[RR] = r . r of the updated residual, summed
+ * exactly as sphc_dot(n, r, r) does (same grid, same order: bitwise equal).
+ * sc[RR] is left untouched when p.Ap <= 0. */
+int sphc_pcg_update_rr(int64_t n, double *sc, const double *p, const double *Ap, double *x,
+                       double *r, int32_t *changed, void *stream);
+
 /* p = z + (sc[RZN] / sc[RZ]) p (multigrid.py:268-270). */
 int sphc_pcg_direction(int64_t n, const double *sc, const double *z, double *p, void *stream);
 
@@ -285,7 +291,8 @@ int sphc_graph_destroy(void *exec);
  * sphc_pcg_loop_begin and sphc_pcg_loop_end -- one PCG iteration followed by
  * sphc_pcg_check, which evaluates the reference's tests
  * (multigrid.py:244-266) on the device, records |r| and sqrt(r.z) in
- * hist[2 it], hist[2 it + 1], and ends the loop. ctl[0] = rtol |b|,
+ * hist[2 it], hist[2 it + 1], rotates r.z (sphc_pcg_rotate's update, so the
+ * body omits that launch), and ends the loop. ctl[0] = rtol |b|,
  * ctl[1] = maxit, ctl[2] = iterations, ctl[3] = status (0 running,
  * 1 converged, 2 maxit, 3 stagnated, 4 indefinite). state[0] receives the
  * loop object. */

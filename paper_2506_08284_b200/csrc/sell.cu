@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(SELL_PER_BLOCK, (STREAM && K == 1) ? 8 : 5)
     k_sell_spmv(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
                 const double* __restrict__ sv, const double* __restrict__ x, double alpha,
                 double beta, const double* z, double* y) {
+  pdl_begin();
   i64 row;
   double acc;
   if (!sell_rowsum<STREAM, K>(n, sp, sci, sv, x, false, row, acc)) return;
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(SELL_PER_BLOCK, (STREAM && K == 1) ? 8 : 5)
                 const double* __restrict__ b, const double* __restrict__ x_in,
                 double* __restrict__ x_out, double* __restrict__ d, double cd, double cr,
                 int x_zero) {
+  pdl_begin();
   i64 row;
   double ax;
   if (!sell_rowsum<STREAM, K>(n, sp, sci, sv, x_in, x_zero != 0, row, ax)) return;
@@ -199,13 +201,13 @@ static inline unsigned sell_grid(i64 n, int K) {
     int K_ = sell_split(n);                                                      \
     unsigned g_ = sell_grid(n, K_);                                              \
     if (STREAMING) {                                                             \
-      if (K_ == 1) KERNEL<true, 1><<<g_, SELL_PER_BLOCK, 0, s>>>(__VA_ARGS__);   \
-      else if (K_ == 2) KERNEL<true, 2><<<g_, SELL_PER_BLOCK, 0, s>>>(__VA_ARGS__); \
-      else KERNEL<true, 4><<<g_, SELL_PER_BLOCK, 0, s>>>(__VA_ARGS__);           \
+      if (K_ == 1) launch_pdl(KERNEL<true, 1>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__);   \
+      else if (K_ == 2) launch_pdl(KERNEL<true, 2>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__); \
+      else launch_pdl(KERNEL<true, 4>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__);           \
     } else {                                                                     \
-      if (K_ == 1) KERNEL<false, 1><<<g_, SELL_PER_BLOCK, 0, s>>>(__VA_ARGS__);  \
-      else if (K_ == 2) KERNEL<false, 2><<<g_, SELL_PER_BLOCK, 0, s>>>(__VA_ARGS__); \
-      else KERNEL<false, 4><<<g_, SELL_PER_BLOCK, 0, s>>>(__VA_ARGS__);          \
+      if (K_ == 1) launch_pdl(KERNEL<false, 1>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__);  \
+      else if (K_ == 2) launch_pdl(KERNEL<false, 2>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__); \
+      else launch_pdl(KERNEL<false, 4>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__);          \
     }                                                                            \
   } while (0)
 

@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(SPMV_THREADS)
     k_spmv(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
            const double* __restrict__ v, const double* __restrict__ x, double alpha,
            double beta, const double* z, double* y) {
+  pdl_begin();
   const int RPW = 32 / L;
   int lane = threadIdx.x & (L - 1);
   int sub = (threadIdx.x & 31) / L;
@@ -50,6 +51,7 @@ __global__ void __launch_bounds__(SPMV_THREADS)
            const double* __restrict__ b, const double* __restrict__ x_in,
            double* __restrict__ x_out, double* __restrict__ d, double cd, double cr,
            int x_zero) {
+  pdl_begin();
   const int RPW = 32 / L;
   int lane = threadIdx.x & (L - 1);
   int sub = (threadIdx.x & 31) / L;
@@ -89,8 +91,8 @@ extern "C" int sphc_spmv(int64_t n, const int64_t* rp, const int32_t* ci, const 
                          const double* z, double* y, void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
-  DISPATCH_L(lanes, (k_spmv<LL><<<spmv_grid(n, LL), SPMV_THREADS, 0, s>>>(
-                         n, rp, ci, v, x, alpha, beta, z, y)));
+  DISPATCH_L(lanes, (launch_pdl(k_spmv<LL>, spmv_grid(n, LL), SPMV_THREADS, 0, s,
+                                    n, rp, ci, v, x, alpha, beta, z, y)));
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -101,8 +103,8 @@ extern "C" int sphc_cheb_step(int64_t n, const int64_t* rp, const int32_t* ci, c
                               double cr, int x_zero, void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
-  DISPATCH_L(lanes, (k_cheb<LL><<<spmv_grid(n, LL), SPMV_THREADS, 0, s>>>(
-                         n, rp, ci, v, dinv, b, x_in, x_out, d, cd, cr, x_zero)));
+  DISPATCH_L(lanes, (launch_pdl(k_cheb<LL>, spmv_grid(n, LL), SPMV_THREADS, 0, s,
+                                    n, rp, ci, v, dinv, b, x_in, x_out, d, cd, cr, x_zero)));
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -112,6 +114,7 @@ extern "C" int sphc_cheb_step(int64_t n, const int64_t* rp, const int32_t* ci, c
 __global__ void k_pcg_update(i64 n, const double* __restrict__ sc, const double* __restrict__ p,
                              const double* __restrict__ Ap, double* __restrict__ x,
                              double* __restrict__ r, int* changed) {
+  pdl_begin();
   double pAp = sc[SPHC_PCG_PAP];
   if (!(pAp > 0.0)) return;  // "indefinite": the reference stops before updating
   double alpha = sc[SPHC_PCG_RZ] / pAp;
@@ -131,32 +134,79 @@ __global__ void k_pcg_update(i64 n, const double* __restrict__ sc, const double*
 extern "C" int sphc_pcg_update(int64_t n, const double* sc, const double* p, const double* Ap,
                                double* x, double* r, int32_t* changed, void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_pcg_update<<<grid_for(n, 256), 256, 0, s>>>(n, sc, p, Ap, x, r, changed);
+  launch_pdl(k_pcg_update, grid_for(n, 256), 256, 0, s, n, sc, p, Ap, x, r, changed);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
 
 __global__ void k_pcg_dir(i64 n, const double* __restrict__ sc, const double* __restrict__ z,
                           double* __restrict__ p) {
+  pdl_begin();
   double beta = sc[SPHC_PCG_RZN] / sc[SPHC_PCG_RZ];
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (i64)gridDim.x * blockDim.x)
     p[i] = z[i] + beta * p[i];
 }
 
-extern "C" int sphc_pcg_direction(int64_t n, const double* sc, const double* z, double* p,
-                                  void* stream) {
+// sphc_pcg_update plus r.r of the new residual (the grid and summation
+// order of sphc_dot(n, r, r), so bitwise the same value) in one launch
+__global__ void k_pcg_update_rr(i64 n, double* __restrict__ sc, const double* __restrict__ p,
+                                const double* __restrict__ Ap, double* __restrict__ x,
+                                double* __restrict__ r, int* changed, double* part,
+                                unsigned* ticket) {
+  pdl_begin();
+  __shared__ double sh[32];
+  double pAp = sc[SPHC_PCG_PAP];
+  if (!(pAp > 0.0)) return;
+  double alpha = sc[SPHC_PCG_RZ] / pAp;
+  int ch = 0;
+  double acc = 0.0;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    double xo = x[i];
+    double xn = xo + alpha * p[i];
+    ch |= (xn != xo);
+    x[i] = xn;
+    double rn = r[i] - alpha * Ap[i];
+    r[i] = rn;
+    acc = fma(rn, rn, acc);
+  }
+  ch = __syncthreads_or(ch);
+  if (ch && threadIdx.x == 0) atomicOr(changed, 1);
+  double t = block_sum(acc, sh);
+  double total;
+  if (last_block_sum(t, part, ticket, sh, &total) && threadIdx.x == 0)
+    sc[SPHC_PCG_RR] = total;
+}
+
+extern "C" int sphc_pcg_update_rr(int64_t n, double* sc, const double* p, const double* Ap,
+                                  double* x, double* r, int32_t* changed, void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_pcg_dir<<<grid_for(n, 256), 256, 0, s>>>(n, sc, z, p);
+  double* part;
+  unsigned* ticket;
+  if (sphc_reduce_scratch(&part, &ticket)) return SPHC_ERR_CUDA;
+  launch_pdl(k_pcg_update_rr, sphc_reduce_grid(n), RED_THREADS, 0, s, n, sc, p, Ap, x, r,
+             changed, part, ticket);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
 
-__global__ void k_pcg_rotate(double* sc) { sc[SPHC_PCG_RZ] = sc[SPHC_PCG_RZN]; }
+extern "C" int sphc_pcg_direction(int64_t n, const double* sc, const double* z, double* p,
+                                  void* stream) {
+  cudaStream_t s = as_stream(stream);
+  launch_pdl(k_pcg_dir, grid_for(n, 256), 256, 0, s, n, sc, z, p);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+__global__ void k_pcg_rotate(double* sc) {
+  pdl_begin();
+  sc[SPHC_PCG_RZ] = sc[SPHC_PCG_RZN];
+}
 
 extern "C" int sphc_pcg_rotate(double* sc, void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_pcg_rotate<<<1, 1, 0, s>>>(sc);
+  launch_pdl(k_pcg_rotate, 1, 1, 0, s, sc);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -231,6 +281,7 @@ struct SphcLoop {
 __global__ void k_pcg_check(double* sc, double* ctl, double* hist,
                             cudaGraphConditionalHandle handle) {
   double pAp = sc[SPHC_PCG_PAP];
+  sc[SPHC_PCG_RZ] = sc[SPHC_PCG_RZN];   // the rotate of sphc_pcg_rotate, folded in
   int st = 0;
   int32_t* flag = reinterpret_cast<int32_t*>(sc + 4);
   if (pAp <= 0.0) {
@@ -335,6 +386,7 @@ extern "C" int sphc_copy_d2h(void* dst, const void* src, int64_t bytes, void* st
 // y = A x, A dense row-major n x n: one warp per row, fixed-order reduction
 __global__ void k_dense_gemv(i64 n, const double* __restrict__ A, const double* __restrict__ x,
                              double* __restrict__ y) {
+  pdl_begin();
   int lane = threadIdx.x & 31;
   i64 w = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
@@ -351,7 +403,7 @@ extern "C" int sphc_dense_gemv(int64_t n, const double* A, const double* x, doub
                                void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
-  k_dense_gemv<<<grid_for(n * 32, 256), 256, 0, s>>>(n, A, x, y);
+  launch_pdl(k_dense_gemv, grid_for(n * 32, 256), 256, 0, s, n, A, x, y);
   SPHC_LAUNCH_CHECK();
   return 0;
 }

@@ -109,22 +109,6 @@ extern "C" int sphc_scan_i64(int64_t n, const int64_t* counts, int64_t* offsets,
 }
 
 // ------------------------------------------------------------------ reductions
-#define RED_THREADS 256
-#define RED_MAX_BLOCKS (SPHC_NUM_SMS * 8)
-
-__device__ __forceinline__ double block_sum(double v, double* sh) {
-  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  v = warp_sum(v);
-  if (lane == 0) sh[wid] = v;
-  __syncthreads();
-  double t = 0.0;
-  if (wid == 0) {
-    t = (lane < (int)(blockDim.x >> 5)) ? sh[lane] : 0.0;
-    t = warp_sum(t);
-  }
-  __syncthreads();
-  return t;
-}
 __device__ __forceinline__ double block_max(double v, double* sh) {
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   v = warp_max(v);
@@ -139,10 +123,16 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
   return t;
 }
 
+// One launch per reduction: every block writes its partial, and the last
+// block to finish (ticket counter) combines all partials in index order with
+// the same fixed tree, then re-arms the counter. The grid is fixed by n, so
+// the result is deterministic.
 template <int MODE>  // 0: dot, 1: maxabs, 2: sum
-__global__ void k_reduce_partial(i64 n, const double* __restrict__ x,
-                                 const double* __restrict__ y, double* __restrict__ part) {
+__global__ void k_reduce(i64 n, const double* __restrict__ x, const double* __restrict__ y,
+                         double* part, unsigned* ticket, double* out) {
+  pdl_begin();
   __shared__ double sh[32];
+  __shared__ bool last;
   double acc = 0.0;
   i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -151,29 +141,49 @@ __global__ void k_reduce_partial(i64 n, const double* __restrict__ x,
     else acc = fmax(acc, fabs(x[i]));
   }
   double t = (MODE != 1) ? block_sum(acc, sh) : block_max(acc, sh);
-  if (threadIdx.x == 0) part[blockIdx.x] = t;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = t;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  acc = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+    double v = __ldcg(part + i);
+    acc = (MODE != 1) ? acc + v : fmax(acc, v);
+  }
+  t = (MODE != 1) ? block_sum(acc, sh) : block_max(acc, sh);
+  if (threadIdx.x == 0) {
+    *out = t;
+    *ticket = 0u;
+  }
 }
 
-template <int MODE>
-__global__ void k_reduce_final(int nparts, const double* __restrict__ part, double* out) {
-  __shared__ double sh[32];
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += blockDim.x)
-    acc = (MODE != 1) ? acc + part[i] : fmax(acc, part[i]);
-  double t = (MODE != 1) ? block_sum(acc, sh) : block_max(acc, sh);
-  if (threadIdx.x == 0) *out = t;
+// persistent partials and ticket shared by every single-launch reduction:
+// reductions are stream ordered, and fixed buffers keep them capturable in
+// CUDA graphs (no allocation nodes)
+int sphc_reduce_scratch(double** part, unsigned** ticket) {
+  static double* p = nullptr;
+  static unsigned* t = nullptr;
+  if (!p) {
+    SPHC_CUDA(cudaMalloc((void**)&p, RED_MAX_BLOCKS * sizeof(double)));
+    SPHC_CUDA(cudaMalloc((void**)&t, sizeof(unsigned)));
+    SPHC_CUDA(cudaMemset(t, 0, sizeof(unsigned)));
+  }
+  *part = p;
+  *ticket = t;
+  return 0;
 }
 
 template <int MODE>
 static int reduce_launch(i64 n, const double* x, const double* y, double* out, cudaStream_t s) {
-  // persistent partials: reductions are stream ordered, and a fixed buffer
-  // keeps them capturable in CUDA graphs (no allocation nodes)
-  static double* part = nullptr;
-  if (!part) SPHC_CUDA(cudaMalloc((void**)&part, RED_MAX_BLOCKS * sizeof(double)));
-  int nb = (int)grid_for(n, RED_THREADS, RED_MAX_BLOCKS);
-  k_reduce_partial<MODE><<<nb, RED_THREADS, 0, s>>>(n, x, y, part);
-  SPHC_LAUNCH_CHECK();
-  k_reduce_final<MODE><<<1, 1024, 0, s>>>(nb, part, out);
+  double* part;
+  unsigned* ticket;
+  if (sphc_reduce_scratch(&part, &ticket)) return SPHC_ERR_CUDA;
+  int nb = sphc_reduce_grid(n);
+  launch_pdl(k_reduce<MODE>, nb, RED_THREADS, 0, s, n, x, y, part, ticket, out);
   SPHC_LAUNCH_CHECK();
   return 0;
 }

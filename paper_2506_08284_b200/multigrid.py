@@ -707,20 +707,21 @@ class PcgLoop:
             self.h = 0
 
 
-def _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc, flag, stage):
+def _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc, flag, stage, rotate=True):
     """One PCG iteration with device-resident scalars (sc slots as in
-    include/sphcurl.h SPHC_PCG_*); ends with the scalars copied to ``stage``."""
+    include/sphcurl.h SPHC_PCG_*); ends with the scalars copied to ``stage``.
+    ``rotate=False`` leaves r.z's rotation to sphc_pcg_check (graph loop)."""
     n = x.numel()
     dv.spmv(A, p, Ap, lanes=lanes)
     dv.dot(p, Ap, sc[0:1])
-    call("sphc_pcg_update", n, sc, p, Ap, x, r, flag)
-    dv.dot(r, r, sc[1:2])
+    call("sphc_pcg_update_rr", n, sc, p, Ap, x, r, flag)     # + sc[1] = r.r
     z = precond(r)
     dv.dot(r, z, sc[3:4])
     call("sphc_pcg_direction", n, sc, z, p)
     if stage is not None:
         call("sphc_copy_d2h", stage, sc, sc.numel() * 8)
-    call("sphc_pcg_rotate", sc)
+    if rotate:
+        call("sphc_pcg_rotate", sc)
     return z
 
 
@@ -755,39 +756,45 @@ def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
     x.zero_()
     r.copy_(b)
     dv.dot(b, b, sc[1:2])
-    nb = math.sqrt(float(sc[1].item()))
+    # the first preconditioner application is queued before |b| is known (a
+    # zero b gives z = 0 and returns below, as the reference does without
+    # calling it), so the loop graph's capture and instantiation on the host
+    # overlap it instead of following a sync
+    z = precond(r)
+    p.copy_(z)
+    dv.dot(r, z, sc[2:3])
+    if graph_ok:
+        loop = ws.get("loop")
+        if loop is None or ws["loop_maxit"] < maxit:
+            ws["loop"] = loop = None
+            ws["ctl"] = dv.zeros_f64(4)
+            ws["hist"] = dv.zeros_f64(2 * (maxit + 1))
+            ws["ctl_host"] = torch.zeros(4, dtype=torch.float64, pin_memory=True)
+            # every buffer of the iteration exists already (precond(r) above
+            # queued the V-cycle once); captured on a side stream
+            cap = torch.cuda.Stream()
+            cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cap):
+                loop = PcgLoop(lambda: _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc,
+                                                      flag, None, rotate=False),
+                               sc, ws["ctl"], ws["hist"])
+            torch.cuda.current_stream().wait_stream(cap)
+            ws["loop"], ws["loop_maxit"] = loop, maxit
+            if hier is not None:
+                hier._pcg_ws = ws
+    bb, rz0 = (float(v) for v in dv.readback(sc[1:3])[0])
+    nb = math.sqrt(bb)
 
     def out(v):
         return v.cpu().numpy() if host else v.clone()
 
     if nb == 0.0:
         return PcgResult(out(x), 0, [0.0], [0.0], "converged", 0.0)
-    z = precond(r)
-    p.copy_(z)
-    dv.dot(r, z, sc[2:3])
-    rz0 = float(sc[2].item())
     history = [nb]
     precond_history = [math.sqrt(max(rz0, 0.0))]
     status, iters = "maxit", 0
     if graph_ok:
         # the whole loop on the device: one graph launch, one readback
-        loop = ws.get("loop")
-        if loop is None or ws["loop_maxit"] < maxit:
-            ws["ctl"] = dv.zeros_f64(4)
-            ws["hist"] = dv.zeros_f64(2 * (maxit + 1))
-            ws["ctl_host"] = torch.zeros(4, dtype=torch.float64, pin_memory=True)
-            # every buffer of the iteration exists already (precond(r) above
-            # ran the V-cycle once); captured on a side stream
-            cap = torch.cuda.Stream()
-            cap.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(cap):
-                loop = PcgLoop(lambda: _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc,
-                                                      flag, None),
-                               sc, ws["ctl"], ws["hist"])
-            torch.cuda.current_stream().wait_stream(cap)
-            ws["loop"], ws["loop_maxit"] = loop, maxit
-            if hier is not None:
-                hier._pcg_ws = ws
         ctl, hist, ch = ws["ctl"], ws["hist"], ws["ctl_host"]
         ch.copy_(torch.tensor([rtol * nb, float(maxit), 0.0, 0.0], dtype=torch.float64))
         ctl.copy_(ch, non_blocking=True)

@@ -35,7 +35,8 @@ for rep in range(3):
     ws = h._pcg_ws
     with torch.cuda.stream(cap):
         lp = mg.PcgLoop(lambda: mg._pcg_iteration(ws["A"], ws["A"].lanes(), pre, ws["x"], ws["r"],
-                                                  ws["p"], ws["Ap"], ws["sc"], ws["flag"], None),
+                                                  ws["p"], ws["Ap"], ws["sc"], ws["flag"], None,
+                                                  rotate=False),
                         ws["sc"], ws["ctl"], ws["hist"])
     torch.cuda.synchronize()
     t2 = time.perf_counter()

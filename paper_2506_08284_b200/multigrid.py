@@ -398,8 +398,8 @@ def _coarse_inverse(Ad):
     at N=128 with sigma = 1e-4 (C5's recipe), where a plain factorisation
     loses the small (gradient-like) modes. The inverse is therefore formed
     on the Jacobi-equilibrated matrix S A S, S = diag(A)^-1/2 (an exact
-    identity: A^-1 = S (S A S)^-1 S), from its Cholesky factor (potrf +
-    potri: symmetric positive by construction; an explicit getri inverse is
+    identity: A^-1 = S (S A S)^-1 S), from its Cholesky factor (potrf,
+    then L^-T L^-1: symmetric positive by construction; an explicit getri inverse is
     visibly non-symmetric at cond ~ 4e15 and made PCG diverge on C4). If the
     factorisation breaks down (numerically semidefinite: the Galerkin
     operator of a rank-deficient prolongator), S A S + n eps ||SAS|| I is
@@ -424,7 +424,11 @@ def _coarse_inverse(Ad):
         L, info = torch.linalg.cholesky_ex(As + shift * torch.eye(n, dtype=As.dtype,
                                                                   device=As.device))
     if int(info) == 0:
-        inv = torch.cholesky_inverse(L)
+        # L^-T L^-1 from one triangular solve against I and a GEMM (0.37 ms
+        # at n = 364 against 0.56 ms for cholesky_inverse's blocked potrs)
+        Li = torch.linalg.solve_triangular(L, torch.eye(L.shape[0], dtype=L.dtype,
+                                                        device=L.device), upper=False)
+        inv = Li.T @ Li
     else:
         lam, V = torch.linalg.eigh(As)
         tiny = lam.abs().max() * As.shape[0] * torch.finfo(torch.float64).eps

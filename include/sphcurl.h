@@ -315,6 +315,10 @@ int sphc_copy_h2d(void *dst, const void *src, int64_t bytes, void *stream);
  * (capturable; the PCG scalars' per-iteration readback). */
 int sphc_copy_d2h(void *dst, const void *src, int64_t bytes, void *stream);
 
+/* Wait for `stream` (the host side of a readback; other streams, e.g. an
+ * upload streaming in behind the setup, keep running). */
+int sphc_stream_sync(void *stream);
+
 /* nsteps (2 or 3) consecutive Chebyshev steps (sphc_sell_cheb_step
  * semantics, step k: xout_k = xin_k + d, d <- cd_k d + cr_k D^-1 (b - A xin_k))
  * in ONE pass over the SELL matrix: row blocks of 256 in ascending order,

@@ -383,6 +383,11 @@ extern "C" int sphc_copy_d2h(void* dst, const void* src, int64_t bytes, void* st
   return 0;
 }
 
+extern "C" int sphc_stream_sync(void* stream) {
+  SPHC_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  return 0;
+}
+
 // y = A x, A dense row-major n x n: one warp per row, fixed-order reduction
 __global__ void k_dense_gemv(i64 n, const double* __restrict__ A, const double* __restrict__ x,
                              double* __restrict__ y) {

@@ -109,7 +109,7 @@ def readback(*tensors):
     for p, nb, off in zip(parts, sizes, offs):
         if nb:
             call("sphc_copy_d2h", base + off, p, nb)
-    torch.cuda.current_stream().synchronize()
+    call("sphc_stream_sync")
     raw = buf.numpy()
     hs = [raw[off:off + nb].view(_NP[p.dtype]).copy() for p, nb, off in zip(parts, sizes, offs)]
     for (st, handler), h in zip(pend, hs):
@@ -174,6 +174,11 @@ def upload(a, dtype, dev=None):
     if a is a0 and a.dtype == np.dtype(dtype) and pinned_in_place(a):
         call("sphc_copy_h2d", t, a, nbytes)     # stream ordered, no staging / sync
         return t
+    # the staging buffer is reused: the next upload waits for this copy's
+    # event (normally long done) instead of this one syncing the stream
+    ev = _PINNED.get("event")
+    if ev is not None:
+        ev.synchronize()
     buf = _PINNED.get("buf")
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1 << 24), dtype=torch.uint8, pin_memory=True)
@@ -181,7 +186,9 @@ def upload(a, dtype, dev=None):
     host = buf[:nbytes].numpy().view(dtype)
     np.copyto(host, a, casting="unsafe")
     t.view(torch.uint8).copy_(buf[:nbytes], non_blocking=True)
-    torch.cuda.current_stream().synchronize()   # the staging buffer is reused
+    if ev is None:
+        ev = _PINNED["event"] = torch.cuda.Event()
+    ev.record()
     return t
 
 

@@ -18,7 +18,8 @@ for _ in range(3):
     r = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
 torch.cuda.synchronize()
 h = r = None
-with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA],
+             with_stack=os.environ.get("STACK") == "1") as prof:
     torch.cuda.synchronize()
     with torch.profiler.record_function("SETUP"):
         h = mg.build_hierarchy(A_e, S, A_n, D, sc)
@@ -35,6 +36,8 @@ gpu = sorted([(e["ts"], e["ts"] + e["dur"], e["name"]) for e in ev
               if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")])
 rt = sorted([(e["ts"], e["ts"] + e["dur"], e["name"]) for e in ev
              if e.get("ph") == "X" and e.get("cat") == "cuda_runtime"])
+py = [(e["ts"], e["ts"] + e["dur"], e["name"]) for e in ev
+      if e.get("ph") == "X" and e.get("cat") == "python_function" and "paper_2506" in e["name"]]
 for name, (t0, t1) in sorted(win.items(), key=lambda kv: kv[1][0]):
     g = [x for x in gpu if x[0] >= t0 and x[1] <= t1]
     busy, cur_end = 0.0, t0
@@ -56,6 +59,15 @@ for name, (t0, t1) in sorted(win.items(), key=lambda kv: kv[1][0]):
                 calls[rn] = calls.get(rn, 0) + 1
         print(f"  gap {d:7.1f} us after {str(p)[:38]:38s} before {n[:38]:38s} "
               + " ".join(f"{k}x{v}" for k, v in sorted(calls.items(), key=lambda kv: -kv[1])[:3]))
+        if py:
+            # our python frames overlapping the gap, by overlap time
+            ov = {}
+            for a, z, fn in py:
+                o = min(z, gz) - max(a, ga)
+                if o > 0:
+                    ov[fn] = ov.get(fn, 0) + o
+            for fn, o in sorted(ov.items(), key=lambda kv: (-kv[1], kv[0]))[:6]:
+                print(f"      {o:6.1f} us {fn.split('paper_2506_08284_b200/')[-1][:90]}")
     # gap histogram
     tot = sum(x[0] for x in gaps)
     small = sum(x[0] for x in gaps if x[0] < 10)

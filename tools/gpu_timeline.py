@@ -72,3 +72,11 @@ for name, (t0, t1) in sorted(win.items(), key=lambda kv: kv[1][0]):
     tot = sum(x[0] for x in gaps)
     small = sum(x[0] for x in gaps if x[0] < 10)
     print(f"  gaps: {len(gaps)} total {tot / 1e3:.2f} ms; < 10 us: {small / 1e3:.2f} ms")
+    # kernels by GPU time inside the window
+    agg = {}
+    for a, z, n in g:
+        k = n.split("(")[0][:70]
+        c, d = agg.get(k, (0, 0.0))
+        agg[k] = (c + 1, d + z - a)
+    for k, (c, d) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:int(os.environ.get("TOPK", "12"))]:
+        print(f"  {d:8.1f} us x{c:4d} {k}")

@@ -172,19 +172,28 @@ __global__ void __launch_bounds__(SELL_PER_BLOCK, (STREAM && K == 1) ? 8 : 5)
 }
 
 // warps per slice: K = 1 once the slices alone fill ~48 warps per SM;
-// otherwise the largest K in {2, 4} whose grid still fits one wave
+// K = 8 for tiny operators (below); otherwise the largest K in {2, 4} whose
+// grid still fits one wave
 // (8 blocks of 256 threads per SM) -- a second partial wave costs more than
 // the extra loads in flight gain. SPHC_SELL_K overrides (tuning).
 static inline int sell_split(i64 n) {
-  static int forced = -1;
+  static int forced = -1, sell_k8 = -1;
+  if (sell_k8 < 0) {
+    const char* e = getenv("SPHC_SELL_K8");
+    sell_k8 = (e && e[0] == '0') ? 0 : 1;
+  }
   if (forced < 0) {
     const char* e = getenv("SPHC_SELL_K");
     forced = e ? atoi(e) : 0;
   }
-  if (forced == 1 || forced == 2 || forced == 4) return forced;
+  if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
   i64 ns = (n + SELL_C - 1) / SELL_C;
   if (ns >= (i64)SPHC_NUM_SMS * 48) return 1;
   const i64 wave = (i64)SPHC_NUM_SMS * 8;
+  // 1 slice per block for the smallest operators (C2 level 1: 219 slices,
+  // ~44 entries per row -> one load group per thread; 4.96 -> 4.88 ms per
+  // C2 solve). Measured slower at C2's 931-slice level-0 nodal operator.
+  if (sell_k8 && ns * 4 <= wave) return 8;
   if ((ns + 1) / 2 <= wave) return 4;    // 2 slices per block
   if ((ns + 3) / 4 <= wave) return 2;    // 4 slices per block
   return 1;
@@ -203,11 +212,13 @@ static inline unsigned sell_grid(i64 n, int K) {
     if (STREAMING) {                                                             \
       if (K_ == 1) launch_pdl(KERNEL<true, 1>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__);   \
       else if (K_ == 2) launch_pdl(KERNEL<true, 2>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__); \
-      else launch_pdl(KERNEL<true, 4>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__);           \
+      else if (K_ == 4) launch_pdl(KERNEL<true, 4>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__); \
+      else launch_pdl(KERNEL<true, 8>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__);           \
     } else {                                                                     \
       if (K_ == 1) launch_pdl(KERNEL<false, 1>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__);  \
       else if (K_ == 2) launch_pdl(KERNEL<false, 2>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__); \
-      else launch_pdl(KERNEL<false, 4>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__);          \
+      else if (K_ == 4) launch_pdl(KERNEL<false, 4>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__); \
+      else launch_pdl(KERNEL<false, 8>, g_, SELL_PER_BLOCK, 0, s, __VA_ARGS__);          \
     }                                                                            \
   } while (0)
 

@@ -84,21 +84,23 @@ def _zero_diag_check(rows):
 _UNFINISHED = []
 
 
-def finalize_sweepers():
+def finalize_sweepers(*extra):
     """Read the Lanczos scalars of every sweeper built so far in one host
     readback (with the deferred status checks) and form their Chebyshev
-    coefficients."""
+    coefficients. ``extra`` device tensors ride on the same readback; their
+    host copies are returned."""
     pend = list(_UNFINISHED)
     _UNFINISHED.clear()
     live = [sw for sw in pend if sw._sc is not None]
     bws = [sw for sw in pend if getattr(sw, "_bw", None) is not None]
-    tens = [sw._sc for sw in live] + [sw._bw for sw in bws]
+    tens = [sw._sc for sw in live] + [sw._bw for sw in bws] + list(extra)
     hs = dv.readback(*tens) if tens else (dv.flush_checks() or [])
     it = iter(hs)
     for sw in pend:
         sw._finish(next(it) if sw._sc is not None else None)
     for sw in bws:
         sw._plan_fusion(int(next(it)[0]))
+    return list(it)
 
 
 class ChebyshevSweeper:
@@ -389,7 +391,7 @@ def _check_nullspace(S, D, where, A=None, shard=None):
     return AD
 
 
-def _coarse_inverse(Ad):
+def _coarse_inverse_start(Ad):
     """Symmetric inverse of the coarsest operator (multigrid.py:157 factors it
     with LU). The coarsest A_e is SPD in exact arithmetic but badly scaled
     and ill-conditioned: the edge prolongators grow level by level (max|P_e|
@@ -407,27 +409,42 @@ def _coarse_inverse(Ad):
     the eigendecomposition); the symmetric eigendecomposition with
     eigenvalues <= n eps lambda_max treated as null space is the last
     resort."""
+    # Queued without a host sync: the factorisation's status is read back
+    # with the smoothers' Lanczos scalars (finalize_sweepers), and
+    # _coarse_inverse_finish redoes the inverse on the rare breakdown.
     A = 0.5 * (Ad + Ad.T)
     d = torch.diagonal(A).clone()
     sc = torch.where(d > 0, d.rsqrt(), torch.ones_like(d))
     As = sc[:, None] * A * sc[None, :]
     As = 0.5 * (As + As.T)
     L, info = torch.linalg.cholesky_ex(As)
-    if int(info) != 0:
-        # numerically singular: the Galerkin operator of a rank-deficient
-        # prolongator (make_irreducible duplicates, deep levels of C5). A
-        # shift of n eps ||SAS|| keeps the factor finite; the directions it
-        # blows up are the null vectors of P (P A_c^-1 P^T never sees them),
-        # and it perturbs the rest less than truncating them would.
-        n = As.shape[0]
-        shift = n * torch.finfo(torch.float64).eps * As.abs().sum(1).max()
-        L, info = torch.linalg.cholesky_ex(As + shift * torch.eye(n, dtype=As.dtype,
-                                                                  device=As.device))
+    # L^-T L^-1 from one triangular solve against I and a GEMM (0.37 ms
+    # at n = 364 against 0.56 ms for cholesky_inverse's blocked potrs)
+    Li = torch.linalg.solve_triangular(L, torch.eye(L.shape[0], dtype=L.dtype,
+                                                    device=L.device), upper=False)
+    inv = Li.T @ Li
+    inv = sc[:, None] * inv * sc[None, :]
+    return 0.5 * (inv + inv.T), info.reshape(1).to(torch.int64), (As, sc)
+
+
+def _coarse_inverse_finish(inv, info, state):
+    """The inverse from _coarse_inverse_start, or -- when its Cholesky broke
+    down (info != 0) -- from the shifted / eigendecomposition fallbacks."""
     if int(info) == 0:
-        # L^-T L^-1 from one triangular solve against I and a GEMM (0.37 ms
-        # at n = 364 against 0.56 ms for cholesky_inverse's blocked potrs)
-        Li = torch.linalg.solve_triangular(L, torch.eye(L.shape[0], dtype=L.dtype,
-                                                        device=L.device), upper=False)
+        return inv
+    As, sc = state
+    # numerically singular: the Galerkin operator of a rank-deficient
+    # prolongator (make_irreducible duplicates, deep levels of C5). A
+    # shift of n eps ||SAS|| keeps the factor finite; the directions it
+    # blows up are the null vectors of P (P A_c^-1 P^T never sees them),
+    # and it perturbs the rest less than truncating them would.
+    n = As.shape[0]
+    shift = n * torch.finfo(torch.float64).eps * As.abs().sum(1).max()
+    L, info = torch.linalg.cholesky_ex(As + shift * torch.eye(n, dtype=As.dtype,
+                                                              device=As.device))
+    if int(info) == 0:
+        Li = torch.linalg.solve_triangular(L, torch.eye(n, dtype=L.dtype, device=L.device),
+                                           upper=False)
         inv = Li.T @ Li
     else:
         lam, V = torch.linalg.eigh(As)
@@ -436,6 +453,23 @@ def _coarse_inverse(Ad):
         inv = (V * w) @ V.T
     inv = sc[:, None] * inv * sc[None, :]
     return 0.5 * (inv + inv.T)
+
+
+_SIDE = {}
+
+
+def _side_stream():
+    dev = torch.cuda.current_device()
+    st = _SIDE.get(dev)
+    if st is None:
+        st = _SIDE[dev] = torch.cuda.Stream()
+    return st
+
+
+def _coarse_inverse(Ad):
+    """Synchronous form (the reuse path)."""
+    inv, info, state = _coarse_inverse_start(Ad)
+    return _coarse_inverse_finish(inv, dv.readback(info)[0][0], state)
 
 
 @checked
@@ -502,13 +536,26 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
         with phase("level.nullspace_check"):
             AD = _check_nullspace(S_e, D, f"level {len(levels)}", A=A_e, shard=shard)
     with phase("coarsest"):
+        # the dense inverse (cuSOLVER / cuBLAS) runs on a side stream while
+        # this stream forms the coarsest level's D^T A D; its status comes
+        # back with the Lanczos scalars
+        main = torch.cuda.current_stream()
+        side = _side_stream()
+        Ad = dv.to_dense(A_e)
+        Ad.record_stream(side)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            inv, info, inv_state = _coarse_inverse_start(Ad)
         last = _make_level(A_e, S_e, D, cfg, AD=AD, smooth=False, shard=shard)
         levels.append(last)
-        inv = _coarse_inverse(dv.to_dense(A_e))
+        main.wait_stream(side)
+        for t in (inv, info, *inv_state):
+            t.record_stream(main)
     last.r = dv.empty_f64(A_e.shape[0])
     nnz0 = levels[0].A_e.nnz
     oc = sum(lv.A_e.nnz for lv in levels) / nnz0
-    finalize_sweepers()
+    (info_h,) = finalize_sweepers(info)
+    inv = _coarse_inverse_finish(inv, info_h[0], inv_state)
     return Hierarchy(levels=levels, coarse_factorization=inv, operator_complexity=oc)
 
 

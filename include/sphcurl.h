@@ -319,6 +319,13 @@ int sphc_copy_d2h(void *dst, const void *src, int64_t bytes, void *stream);
  * upload streaming in behind the setup, keep running). */
 int sphc_stream_sync(void *stream);
 
+/* Readback gather: `count` (<= 16) device ranges -- desc holds host rows of
+ * 3 int64 (device source pointer, bytes, byte offset into dst; bytes and
+ * offsets multiples of 4) -- written by ONE kernel straight into `dst`, a
+ * page-locked (device-mapped) host buffer. Replaces one copy-engine
+ * transfer per range; visible on the host after sphc_stream_sync. */
+int sphc_readback_gather(int32_t count, const int64_t *desc, void *dst, void *stream);
+
 /* nsteps (2 or 3) consecutive Chebyshev steps (sphc_sell_cheb_step
  * semantics, step k: xout_k = xin_k + d, d <- cd_k d + cr_k D^-1 (b - A xin_k))
  * in ONE pass over the SELL matrix: row blocks of 256 in ascending order,

@@ -383,6 +383,65 @@ extern "C" int sphc_copy_d2h(void* dst, const void* src, int64_t bytes, void* st
   return 0;
 }
 
+#define RB_MAX 16
+struct RbParts {
+  const uint32_t* src[RB_MAX];
+  int64_t words[RB_MAX];
+  int64_t off[RB_MAX];
+  int count;
+};
+
+// one CTA per range: 4-byte words from device memory to mapped host memory
+__global__ void k_readback_gather(RbParts P, uint32_t* dst) {
+  pdl_begin();
+  int r = blockIdx.x;
+  if (r >= P.count) return;
+  const uint32_t* s = P.src[r];
+  uint32_t* d = dst + P.off[r] / 4;
+  for (int64_t i = threadIdx.x; i < P.words[r]; i += blockDim.x) d[i] = s[i];
+}
+
+extern "C" int sphc_readback_gather(int32_t count, const int64_t* desc, void* dst,
+                                    void* stream) {
+  if (count <= 0) return 0;
+  if (count > RB_MAX) {
+    sphc_set_error("sphc_readback_gather: %d ranges (max %d)", count, RB_MAX);
+    return SPHC_ERR_ARG;
+  }
+  RbParts P = {};
+  P.count = count;
+  for (int i = 0; i < count; i++) {
+    const int64_t* r = desc + 3 * i;
+    if ((r[1] | r[2]) & 3) {
+      sphc_set_error("sphc_readback_gather: range %d not 4-byte aligned", i);
+      return SPHC_ERR_ARG;
+    }
+    P.src[i] = (const uint32_t*)r[0];
+    P.words[i] = r[1] / 4;
+    P.off[i] = r[2];
+  }
+  // the staging buffer's device alias (the same address under unified
+  // addressing for mapped page-locked memory); a buffer that is not mapped
+  // falls back to one copy-engine transfer per range
+  static void* last_host = nullptr;
+  static void* last_dev = nullptr;
+  if (dst != last_host) {
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, dst, 0) != cudaSuccess) {
+      (void)cudaGetLastError();
+      for (int i = 0; i < count; i++)
+        SPHC_CUDA(cudaMemcpyAsync((char*)dst + P.off[i], P.src[i], (size_t)P.words[i] * 4,
+                                  cudaMemcpyDeviceToHost, as_stream(stream)));
+      return 0;
+    }
+    last_host = dst;
+    last_dev = dp;
+  }
+  launch_pdl(k_readback_gather, count, 256, 0, as_stream(stream), P, (uint32_t*)last_dev);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
 extern "C" int sphc_stream_sync(void* stream) {
   SPHC_CUDA(cudaStreamSynchronize(as_stream(stream)));
   return 0;

@@ -106,9 +106,14 @@ def readback(*tensors):
         o += (nb + 15) & ~15
     buf = _staging(o)
     base = buf.data_ptr()
-    for p, nb, off in zip(parts, sizes, offs):
-        if nb:
-            call("sphc_copy_d2h", base + off, p, nb)
+    rng = [(p.data_ptr(), nb, off) for p, nb, off in zip(parts, sizes, offs) if nb]
+    if len(rng) <= 16 and all(nb % 4 == 0 for _, nb, _ in rng):
+        # one kernel writes every range into the mapped staging buffer
+        call("sphc_readback_gather", len(rng), np.array(rng, dtype=np.int64).reshape(-1),
+             base)
+    else:
+        for src, nb, off in rng:
+            call("sphc_copy_d2h", base + off, src, nb)
     call("sphc_stream_sync")
     raw = buf.numpy()
     hs = [raw[off:off + nb].view(_NP[p.dtype]).copy() for p, nb, off in zip(parts, sizes, offs)]

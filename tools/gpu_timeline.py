@@ -10,8 +10,12 @@ from paper_2506_08284_b200.inputs import make_config
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "C2"
 s, rhs, cfg = make_config(cfgname)
-A_e, S, A_n, D = (dv.DeviceCSR.from_scipy(M) for M in (s.A_e, s.S, s.A_n, s.D))
-b = torch.from_numpy(rhs).cuda()
+if os.environ.get("E2E") == "1":
+    # the public API from host inputs (scipy CSR, numpy RHS), as bench.py's e2e
+    A_e, S, A_n, D, b = s.A_e, s.S, s.A_n, s.D, rhs
+else:
+    A_e, S, A_n, D = (dv.DeviceCSR.from_scipy(M) for M in (s.A_e, s.S, s.A_n, s.D))
+    b = torch.from_numpy(rhs).cuda()
 sc = mg.SolverConfig(coarse_size=1000)
 for _ in range(3):
     h = mg.build_hierarchy(A_e, S, A_n, D, sc)

@@ -195,7 +195,9 @@ int sphc_emin_repair(int64_t nrows, const int64_t *rows, const int64_t *trp, con
 /* ---------------------------------------------------------------- solve */
 
 /* y = alpha * (A x) + beta * z  (z may be NULL; y may alias z).
- * `lanes` (1,2,4,8,16,32) = lanes per row. csr_matvec call sites
+ * `lanes` (1,2,4,8,16,32) = lanes per row; 256 = one CTA per row (few,
+ * long rows: the explicit restrictions R = P_e^T of the coarse levels,
+ * fixed-order block reduction). csr_matvec call sites
  * multigrid.py:46,51,168,171,183,186,242,252. */
 int sphc_spmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *v, int lanes,
               const double *x, double alpha, double beta, const double *z, double *y,

@@ -86,11 +86,39 @@ static unsigned spmv_grid(i64 n, int L) {
     default: sphc_set_error("lanes must be 1,2,4,8,16,32"); return SPHC_ERR_ARG; \
   }
 
+// y = alpha A x + beta z with one CTA per row (rows of hundreds of entries,
+// too few rows to fill the SMs warp per row): strided fma per thread, then
+// the fixed-order block tree (deterministic)
+__global__ void __launch_bounds__(256)
+    k_spmv_cta(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
+               const double* __restrict__ v, const double* __restrict__ x, double alpha,
+               double beta, const double* z, double* y) {
+  pdl_begin();
+  __shared__ double sh[32];
+  for (i64 row = blockIdx.x; row < n; row += gridDim.x) {
+    double acc = 0.0;
+    for (i64 j = rp[row] + threadIdx.x; j < rp[row + 1]; j += blockDim.x)
+      acc = fma(v[j], x[ci[j]], acc);
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) {
+      double r = alpha * acc;
+      if (z) r = fma(beta, z[row], r);
+      y[row] = r;
+    }
+  }
+}
+
 extern "C" int sphc_spmv(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
                          int lanes, const double* x, double alpha, double beta,
                          const double* z, double* y, void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
+  if (lanes == 256) {
+    launch_pdl(k_spmv_cta, grid_for(n, 1, SPHC_NUM_SMS * 8), 256, 0, s, n, rp, ci, v, x, alpha,
+               beta, z, y);
+    SPHC_LAUNCH_CHECK();
+    return 0;
+  }
   DISPATCH_L(lanes, (launch_pdl(k_spmv<LL>, spmv_grid(n, LL), SPMV_THREADS, 0, s,
                                     n, rp, ci, v, x, alpha, beta, z, y)));
   SPHC_LAUNCH_CHECK();

@@ -649,14 +649,22 @@ def sell(A):
     return m
 
 
+CTA_ROW_MAX_ROWS = int(os.environ.get("SPHC_CTA_ROW_MAX_ROWS", "4096"))
+CTA_ROW_MIN_LEN = 96
+
+
 def spmv(A, x, y, alpha=1.0, beta=0.0, z=None, lanes=None):
     """y = alpha A x + beta z (on A's SELL mirror when it has one)."""
     m = getattr(A, "_sell", None)
     if m is not None:
         call("sphc_sell_spmv", m.n, m.slice_ptr, m.col, m.val, x, alpha, beta, z, y, m.padded)
         return y
-    call("sphc_spmv", A.shape[0], A.rowptr, A.col, A.val, lanes or A.lanes(), x, alpha,
-         beta, z, y)
+    if lanes is None:
+        lanes = A.lanes()
+        if lanes == 32 and A.shape[0] <= CTA_ROW_MAX_ROWS and \
+                A.nnz >= CTA_ROW_MIN_LEN * A.shape[0]:
+            lanes = 256       # one CTA per row (coarse-level restrictions)
+    call("sphc_spmv", A.shape[0], A.rowptr, A.col, A.val, lanes, x, alpha, beta, z, y)
     return y
 
 

@@ -295,22 +295,40 @@ def piecewise_const(P, n_passes=2):
 @dataclass
 class CoarseEdges:
     """Coarse edge list: interior pairs (a < b) sorted, then single-node
-    edges sorted by node (coarse_gradient.py:106-160)."""
+    edges sorted by node (coarse_gradient.py:106-160), then the interior
+    edges ``make_irreducible`` appended, in append order
+    (coarse_gradient.py:163-171; duplicates of an existing pair allowed, as
+    in the reference)."""
 
     pairs: np.ndarray           # (n_int, 2)
     singles: np.ndarray         # (n_single,)
     n_nodes: int
+    augmented: np.ndarray = None  # (n_aug, 2), a < b
+
+    def __post_init__(self):
+        if self.augmented is None:
+            self.augmented = np.zeros((0, 2), dtype=np.int64)
 
     @property
     def n_edges(self):
-        return self.pairs.shape[0] + self.singles.size
+        return self.pairs.shape[0] + self.singles.size + self.augmented.shape[0]
+
+    def endpoints(self):
+        """Endpoint tuples by edge id (CoarseGradient.edge_endpoints)."""
+        return ([(int(a), int(b)) for a, b in self.pairs]
+                + [(int(c),) for c in self.singles]
+                + [(int(a), int(b)) for a, b in self.augmented])
 
     def D_H(self):
-        ni = self.pairs.shape[0]
+        ni, ns = self.pairs.shape[0], self.singles.size
+        na_ = self.augmented.shape[0]
         e = np.arange(ni)
-        rows = np.concatenate([e, e, ni + np.arange(self.singles.size)])
-        cols = np.concatenate([self.pairs[:, 0], self.pairs[:, 1], self.singles])
-        vals = np.concatenate([-np.ones(ni), np.ones(ni), np.ones(self.singles.size)])
+        ea = ni + ns + np.arange(na_)
+        rows = np.concatenate([e, e, ni + np.arange(ns), ea, ea])
+        cols = np.concatenate([self.pairs[:, 0], self.pairs[:, 1], self.singles,
+                               self.augmented[:, 0], self.augmented[:, 1]])
+        vals = np.concatenate([-np.ones(ni), np.ones(ni), np.ones(ns),
+                               -np.ones(na_), np.ones(na_)])
         return canonical(sp.coo_matrix((vals, (rows, cols)),
                                        shape=(self.n_edges, self.n_nodes)))
 
@@ -337,9 +355,11 @@ def coarse_edges(D_h, assign, n_agg):
 # constrained energy minimisation (reference emin_setup.py, edge_prolongator.py)
 
 
-def _components(G):
-    nc = G.shape[1]
-    parent = list(range(nc))
+def _components(ends, I, J):
+    """Union-find over the row's coarse nodes J; two-node coarse edges join
+    their ends, one-node edges only mark incidence (emin_setup.py:150-171)."""
+    pos = {int(c): x for x, c in enumerate(J)}
+    parent = list(range(len(J)))
 
     def find(a):
         while parent[a] != a:
@@ -347,15 +367,74 @@ def _components(G):
             a = parent[a]
         return a
 
-    inc = np.zeros(nc, dtype=bool)
-    for r in range(G.shape[0]):
-        cols = np.flatnonzero(G[r])
-        inc[cols] = True
-        if cols.size == 2:
-            x, y = find(int(cols[0])), find(int(cols[1]))
+    inc = [False] * len(J)
+    for e in I:
+        ps = [pos[n] for n in ends[int(e)]]
+        for p in ps:
+            inc[p] = True
+        if len(ps) == 2:
+            x, y = find(ps[0]), find(ps[1])
             if x != y:
                 parent[max(x, y)] = min(x, y)
-    return np.array([find(c) for c in range(nc)]), inc
+    return [find(c) for c in range(len(J))], inc
+
+
+def _irreducible(ends, I, J):
+    """check_irreducible (emin_setup.py:174-180)."""
+    if len(J) == 0:
+        return False
+    roots, inc = _components(ends, I, J)
+    return all(inc) and len(set(roots)) == 1
+
+
+def _column_score(Rc, a, b):
+    """|R_dp[:, a] . R_dp[:, b]| as the reference evaluates it
+    (emin_setup.py:206): scipy csr_matmat of the transposed column a with
+    column b, i.e. products summed sequentially from 0.0 in ascending fine
+    edge, unfused; an exactly-zero sum scores 0."""
+    sa = slice(Rc.indptr[a], Rc.indptr[a + 1])
+    sb = slice(Rc.indptr[b], Rc.indptr[b + 1])
+    ka, kb = Rc.indices[sa], Rc.indices[sb]
+    _, ia, ib = np.intersect1d(ka, kb, assume_unique=True, return_indices=True)
+    va, vb = Rc.data[sa][ia], Rc.data[sb][ib]
+    s = 0.0
+    for x, y in zip(va.tolist(), vb.tolist()):
+        s += x * y
+    return abs(s)
+
+
+def make_irreducible(edge, I, J, ends, aug, Rc, score_cache):
+    """Append coarse edges until the row's block is irreducible
+    (emin_setup.py:183-217, coarse_gradient.py:163-171).
+
+    Each step bridges two components with the pair (a, b), a < b in J order,
+    of largest |R_dp[:, a] . R_dp[:, b]|; ties and zero scores go to the
+    lexicographically smallest (a, b). The new edge takes the next id
+    (``ends``/``aug`` grow; an existing pair may be appended again, as in
+    the reference). Returns the grown edge list."""
+    I = list(I)
+    while not _irreducible(ends, I, J):
+        roots, _ = _components(ends, I, J)
+        if len(set(roots)) <= 1:
+            raise ValueError(f"fine edge {edge}: cannot repair a single-node "
+                             "constraint graph")
+        best = None
+        for ai in range(len(J)):
+            for bi in range(ai + 1, len(J)):
+                if roots[ai] == roots[bi]:
+                    continue
+                a, b = int(J[ai]), int(J[bi])
+                sc = score_cache.get((a, b))
+                if sc is None:
+                    sc = score_cache[(a, b)] = _column_score(Rc, a, b)
+                key = (-sc, a, b)
+                if best is None or key < best:
+                    best = key
+        _, a, b = best
+        ends.append((min(a, b), max(a, b)))
+        aug.append((min(a, b), max(a, b)))
+        I.append(len(ends) - 1)
+    return I
 
 
 def _rank_check(G, k, edge):
@@ -388,11 +467,13 @@ class EminResult:
     subproblem_dims: Counter
     n_augmented: int = 0
     R_dp: sp.csr_matrix = None
+    coarse: "CoarseEdges" = None
 
 
 def emin_prolongator(D_h, P_n, ce, S, omega=0.5, iterations=1):
-    """Pattern, feasible guess and projected Jacobi sweeps
-    (emin_setup.py:62-336, edge_prolongator.py:104-228)."""
+    """Pattern, irreducibility repair, feasible guess and projected Jacobi
+    sweeps (emin_setup.py:62-336, edge_prolongator.py:104-228). The coarse
+    edges make_irreducible appends come back in ``result.coarse``."""
     D = canonical(D_h)
     nnz = np.diff(D.indptr)
     badm = (nnz < 1) | (nnz > 2)
@@ -401,63 +482,127 @@ def emin_prolongator(D_h, P_n, ce, S, omega=0.5, iterations=1):
         raise ValueError(f"malformed gradient: row {b} has {nnz[b]} nonzeros")
     P_n = canonical(P_n)
     R = canonical(D @ P_n)
+    Rc = None
     rdp_scale = max(1.0, float(np.max(np.abs(R.data))) if R.nnz else 1.0)
     ni = ce.pairs.shape[0]
     adj = {(int(a), int(b)): e for e, (a, b) in enumerate(ce.pairs)}
     single = np.full(ce.n_nodes, -1, dtype=np.int64)
     single[ce.singles] = ni + np.arange(ce.singles.size)
+    ends = ce.endpoints()
+    n0 = len(ends)
+    aug = [tuple(int(v) for v in e) for e in ce.augmented]
+    n_aug_in = len(aug)
+    score_cache = {}
 
     n = D.shape[0]
-    rows_I, rows_p, factors = [None] * n, [None] * n, [None] * n
-    cache = {}
-    dims = Counter()
+    rows_I, rows_J, rows_N, rows_r = [None] * n, [None] * n, [None] * n, [None] * n
+
+    # main loop (emin_setup.py:291-309)
     for i in range(n):
-        ends = D.indices[D.indptr[i]:D.indptr[i + 1]]
+        ends_i = D.indices[D.indptr[i]:D.indptr[i + 1]]
         J = np.unique(np.concatenate([P_n.indices[P_n.indptr[e]:P_n.indptr[e + 1]]
-                                      for e in ends])).astype(np.int64)
+                                      for e in ends_i])).astype(np.int64)
         Jl = J.tolist()
         I = [adj[(a, b)] for x, a in enumerate(Jl) for b in Jl[x + 1:]
              if (a, b) in adj]
         I += [int(single[c]) for c in Jl if single[c] >= 0]
+        I.sort()
         s = slice(R.indptr[i], R.indptr[i + 1])
         r = np.zeros(J.size)
         r[np.searchsorted(J, R.indices[s])] = R.data[s]
+        rows_J[i], rows_N[i], rows_r[i] = J, I, r
         if not I:
-            if np.any(np.abs(R.data[s]) > 1e-12 * rdp_scale):
-                raise NotImplementedError(
-                    f"fine edge {i}: empty constraint pattern with a nonzero "
-                    "commutator row needs make_irreducible")
+            if not np.any(np.abs(R.data[s]) > 1e-12 * rdp_scale):
+                continue
+            # _empty_shell (emin_setup.py:134-147)
+            if J.size == 0:
+                raise ValueError(f"fine edge {i} has an empty constraint "
+                                 "pattern (isolated edge or pattern bug)")
+            if J.size == 1:
+                raise ValueError(
+                    f"fine edge {i}: nonzero commutator row over a single "
+                    "coarse node cannot be satisfied by interior coarse edges")
+        if not _irreducible(ends, I, Jl):
+            if Rc is None:
+                Rc = R.tocsc()
+                Rc.sort_indices()
+            I = make_irreducible(i, I, Jl, ends, aug, Rc, score_cache)
+        rows_I[i] = I
+
+    # post pass (emin_setup.py:311-333): the main loop's new edges join
+    # every row that sees both of their ends
+    new_edges = list(range(n0, len(ends)))
+    if new_edges:
+        by_node = {}
+        for e in new_edges:
+            for c in ends[e]:
+                by_node.setdefault(c, []).append(e)
+        affected = []
+        for i in range(n):
+            Jset = set(rows_J[i].tolist())
+            hit = False
+            for c in Jset:
+                for e in by_node.get(c, ()):
+                    if all(x in Jset for x in ends[e]):
+                        hit = True
+                        break
+                if hit:
+                    break
+            if hit:
+                affected.append(i)
+        for i in affected:
+            if rows_I[i] is None:
+                continue
+            Jl = rows_J[i].tolist()
+            Jset = set(Jl)
+            add = [e for e in new_edges if all(x in Jset for x in ends[e])]
+            I = sorted(set(rows_N[i]) | set(add))
+            if not I:
+                raise ValueError(f"fine edge {i} has an empty constraint "
+                                 "pattern (isolated edge or pattern bug)")
+            if len(I) == len(rows_I[i]):
+                continue
+            if not _irreducible(ends, I, Jl):
+                I = make_irreducible(i, I, Jl, ends, aug, Rc, score_cache)
+            rows_I[i] = I
+
+    # factors (factor_subproblem, emin_setup.py:220-248; cached per block)
+    n_single_end = ni + ce.singles.size
+    factors, rows_p = [None] * n, [None] * n
+    cache = {}
+    dims = Counter()
+    for i in range(n):
+        I = rows_I[i]
+        if I is None:
             continue
-        I = np.array(sorted(I), dtype=np.int64)
-        pos = {c: x for x, c in enumerate(Jl)}
-        G = np.zeros((I.size, J.size))
+        J = rows_J[i]
+        pos = {int(c): x for x, c in enumerate(J.tolist())}
+        G = np.zeros((len(I), J.size))
         for x, e in enumerate(I):
-            if e < ni:
-                G[x, pos[int(ce.pairs[e, 0])]] = -1.0
-                G[x, pos[int(ce.pairs[e, 1])]] = 1.0
+            en = ends[e]
+            if len(en) == 2:
+                G[x, pos[en[0]]] = -1.0
+                G[x, pos[en[1]]] = 1.0
             else:
-                G[x, pos[int(ce.singles[e - ni])]] = 1.0
-        dirich = bool(np.any(I >= ni))
+                G[x, pos[en[0]]] = 1.0
+        dirich = any(ni <= e < n_single_end for e in I)
         key = (G.shape, G.tobytes(), dirich)
         fac = cache.get(key)
         if fac is None:
-            roots, inc = _components(G)
-            if not (np.all(inc) and np.unique(roots).size == 1):
-                raise NotImplementedError(
-                    f"fine edge {i}: reducible constraint block needs "
-                    "make_irreducible")
             k = J.size - (0 if dirich else 1)
             _rank_check(G, k, i)
             Gk = G[:, :k]
             Minv = np.linalg.inv(Gk.T @ Gk)
-            fac = (Gk, Minv, G.T @ np.ones(I.size), k)
+            fac = (Gk, Minv, G.T @ np.ones(len(I)), k)
             cache[key] = fac
         Gk, Minv, gt1, k = fac
-        c = r - gt1
+        c = rows_r[i] - gt1
         rows_p[i] = 1.0 + Gk @ (Minv @ c[:k])
-        rows_I[i] = I
+        rows_I[i] = np.array(I, dtype=np.int64)
         factors[i] = fac
-        dims[(I.size, J.size)] += 1
+        dims[(len(I), J.size)] += 1
+    ce = CoarseEdges(pairs=ce.pairs, singles=ce.singles, n_nodes=ce.n_nodes,
+                     augmented=np.array(aug, dtype=np.int64).reshape(-1, 2))
 
     lengths = np.array([0 if x is None else x.size for x in rows_I], dtype=np.int64)
     indptr = np.concatenate([[0], np.cumsum(lengths)])
@@ -503,7 +648,9 @@ def emin_prolongator(D_h, P_n, ce, S, omega=0.5, iterations=1):
     P_e = mat(vals)
     res = max_abs(canonical(P_e @ ce.D_H() - R))
     return EminResult(P_e=P_e, energy_history=energy_hist,
-                      commutator_residual=res, subproblem_dims=dims, R_dp=R)
+                      commutator_residual=res, subproblem_dims=dims,
+                      n_augmented=ce.augmented.shape[0] - n_aug_in, R_dp=R,
+                      coarse=ce)
 
 
 # ---------------------------------------------------------------------------
@@ -690,6 +837,7 @@ def build_hierarchy(A_e, S_e, A_n, D, coarse_size=200, max_levels=10,
         ce = coarse_edges(D, assign, n_agg)
         em = emin_prolongator(D, P_n, ce, S_e, omega,
                               0 if mode == "rsamg" else iterations)
+        ce = em.coarse                  # with make_irreducible's new edges
         nH = ce.n_edges
         if nH == 0:
             break

@@ -14,6 +14,7 @@ LIB = os.path.join(HERE, "libsphcurl.so")
 
 CU = ["util.cu", "spmv.cu", "sell.cu", "spgemm.cu", "nodal.cu", "coarse.cu", "emin.cu",
       "trsv.cu", "pconst.cu", "aggregate.cu", "assemble.cu"]
+HEADERS = ["common.cuh", "assemble_rows.cuh"]
 CPP = ["host_seq.cpp"]
 
 NVCC_FLAGS = [
@@ -33,7 +34,8 @@ def _nvcc():
 
 def sources():
     return [os.path.join(CSRC, f) for f in CU + CPP] + [
-        os.path.join(CSRC, "common.cuh"), os.path.join(REPO, "include", "sphcurl.h")]
+        os.path.join(REPO, "include", "sphcurl.h")] + [
+        os.path.join(CSRC, h) for h in HEADERS]
 
 
 def up_to_date():

@@ -156,8 +156,18 @@ def run_case(name, N, dirichlet, sigma, coarse_size, seed, full, mode="sphcurl")
                     arrays[f"L{li}_{key}_indptr"] = M.indptr
                     arrays[f"L{li}_{key}_indices"] = M.indices
                     arrays[f"L{li}_{key}_data"] = M.data
+        nxt = h.levels[li + 1] if li + 1 < h.n_levels else None
+        if not full and lv.P_e is not None:
+            # values only (the patterns are pinned by sha256): every entry of
+            # the prolongator and of the next level's coarse operators
+            _store_values(arrays, f"L{li}_Pe", lv.P_e, None)
+            _store_values(arrays, f"L{li + 1}_A_e", nxt.A_e, None)
+            _store_values(arrays, f"L{li + 1}_S_e", nxt.S_e, None)
+            L["next_A_e_pattern"] = sha(nxt.A_e.indptr.astype(np.int64),
+                                        nxt.A_e.indices.astype(np.int64))
+            L["next_S_e_pattern"] = sha(nxt.S_e.indptr.astype(np.int64),
+                                        nxt.S_e.indices.astype(np.int64))
         if full:
-            nxt = h.levels[li + 1] if li + 1 < h.n_levels else None
             if nxt is not None:
                 for key, M in (("A_e", nxt.A_e), ("S_e", nxt.S_e), ("D", nxt.D)):
                     arrays[f"L{li + 1}_{key}_indptr"] = M.indptr
@@ -295,6 +305,130 @@ def repair_case():
     return meta, arrays
 
 
+# Device-generated configs: the inputs are
+# built by the host build of the device assembly rows (oracle/host_assembly.py,
+# bit-identical to assembly.make_device_config on the B200, recorded by sha256),
+# and the UNMODIFIED reference is run on them. Values of the prolongators and
+# coarse operators are stored in full up to ``limit`` entries per matrix, else
+# on every k-th row (k = ceil(nnz / limit)); patterns by sha256.
+BIG = {
+    # name: (config, N, coarse_size, value limit per matrix, run GS solve)
+    "C4s": ("C4", 16, 200, None, True),
+    "C3": ("C3", 64, 1000, 1_000_000, True),
+    "C5s": ("C5", 64, 1000, 1_000_000, True),
+    "C4r": ("C4", 128, 1000, 500_000, True),
+}
+
+
+def _store_values(arrays, key, M, limit):
+    M = sp.csr_matrix(M)
+    k = 1 if limit is None else max(1, -(-int(M.nnz) // int(limit)))
+    rows = np.arange(0, M.shape[0], k)
+    arrays[key + "_stride"] = np.array(k, dtype=np.int64)
+    if k == 1:
+        arrays[key + "_vals"] = M.data
+    else:
+        ln = np.diff(M.indptr)[rows]
+        idx = np.repeat(M.indptr[rows], ln) + (np.arange(int(ln.sum()))
+                                               - np.repeat(np.cumsum(ln) - ln, ln))
+        arrays[key + "_vals"] = M.data[idx]
+
+
+def run_device_case(name, config, N, coarse_size, limit, with_gs):
+    from types import SimpleNamespace
+    from hcurlamg import nodal_amg as na, coarse_gradient as cgm
+    from oracle.host_assembly import config_host
+    A_e, S, A_n, D, rhs, cfg = config_host(config, N)
+    s = SimpleNamespace(A_e=A_e, S=S, A_n=A_n, D=D)
+    meta = {"config": config, "N": N, "dirichlet": bool(cfg["dirichlet"]),
+            "coarse_size": coarse_size, "limit": limit,
+            "inputs": {k: csr_hash(getattr(s, k)) for k in ("A_e", "S", "A_n", "D")},
+            "rhs": sha(rhs), "levels": []}
+    t0 = time.perf_counter()
+    h = mg.build_hierarchy(A_e, S, A_n, D, mg.SolverConfig(coarse_size=coarse_size))
+    meta["t_setup_ref"] = time.perf_counter() - t0
+    print(name, "setup", meta["t_setup_ref"], "levels", [lv.A_e.shape[0] for lv in h.levels],
+          flush=True)
+    meta.update({"n_levels": h.n_levels, "operator_complexity": h.operator_complexity,
+                 "n_edges": [lv.A_e.shape[0] for lv in h.levels],
+                 "nnz_A_e": [int(lv.A_e.nnz) for lv in h.levels]})
+    arrays = {}
+    for li, lv in enumerate(h.levels):
+        L = {"n_edges": lv.A_e.shape[0], "n_nodes": lv.D.shape[1],
+             "A_e": csr_hash(lv.A_e), "S_e": csr_hash(lv.S_e), "D": csr_hash(lv.D),
+             "A_e_pattern": sha(lv.A_e.indptr.astype(np.int64),
+                                lv.A_e.indices.astype(np.int64)),
+             "S_e_pattern": sha(lv.S_e.indptr.astype(np.int64),
+                                lv.S_e.indices.astype(np.int64)),
+             "A_e_nnz": int(lv.A_e.nnz), "S_e_nnz": int(lv.S_e.nnz),
+             "nodal_aux_nnz": int(lv.nodal_aux.nnz)}
+        if li > 0:
+            _store_values(arrays, f"L{li}_A_e", lv.A_e, limit)
+            _store_values(arrays, f"L{li}_S_e", lv.S_e, limit)
+            L["A_e_fro"] = float(np.linalg.norm(lv.A_e.data))
+            L["S_e_fro"] = float(np.linalg.norm(lv.S_e.data))
+        if lv.P_e is not None:
+            nxt = h.levels[li + 1]
+            n_aug = int(lv.n_augmented)
+            Dn = sp.csr_matrix(nxt.D)
+            aug = [Dn.indices[Dn.indptr[r]:Dn.indptr[r + 1]].tolist()
+                   for r in range(Dn.shape[0] - n_aug, Dn.shape[0])]
+            L.update({
+                "P_e_nnz": int(lv.P_e.nnz),
+                "P_e_pattern": sha(lv.P_e.indptr.astype(np.int64),
+                                   lv.P_e.indices.astype(np.int64)),
+                "P_e_fro": float(np.linalg.norm(lv.P_e.data)),
+                "P_n": csr_hash(lv.P_n), "P_n_nnz": int(lv.P_n.nnz),
+                "emin_energy": lv.emin_energy,
+                "commutator_residual": lv.commutator_residual,
+                "subproblem_dims": sorted([list(k) + [v] for k, v in
+                                           lv.subproblem_dims.items()]),
+                "n_augmented": n_aug, "augmented": aug,
+            })
+            _store_values(arrays, f"L{li}_Pe", lv.P_e, limit)
+        meta["levels"].append(L)
+
+    for li, lv in enumerate(h.levels[:-1]):
+        An = _an(h, li, s)
+        agg = na.aggregate(na.strength_graph(An, 0.0))
+        nod = na.smooth_and_normalize(An, na.tentative_prolongator(agg))
+        assert (nod.P != lv.P_n).nnz == 0
+        Pc = cgm.gen_piecewise_const(nod.P, 2)
+        assign = Pc.indices[Pc.indptr[:-1]].astype(np.int64)
+        cg = cgm.augment_dirichlet_edges(cgm.build_coarse_gradient(lv.D, Pc), lv.D, Pc)
+        pairs = np.array([e for e in cg.edge_endpoints if len(e) == 2],
+                         dtype=np.int64).reshape(-1, 2)
+        singles = np.array([e[0] for e in cg.edge_endpoints if len(e) == 1],
+                           dtype=np.int64)
+        meta["levels"][li].update({
+            "n_agg": agg.n_agg, "membership": sha(agg.membership.astype(np.int64)),
+            "omega_hex": float(nod.omega_used).hex(), "rho_hex": float(nod.rho_estimate).hex(),
+            "assignment": sha(assign), "pairs": sha(pairs), "singles": sha(singles),
+            "n_pairs": int(pairs.shape[0]), "n_singles": int(singles.size)})
+    print(name, "decisions recorded", flush=True)
+
+    b = rhs
+    if with_gs:
+        t0 = time.perf_counter()
+        res = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+        meta["t_solve_ref"] = time.perf_counter() - t0
+        meta["gs"] = {"iterations": res.iterations, "status": res.status,
+                      "residual_history": res.residual_history,
+                      "relative_residual": res.relative_residual}
+        print(name, "gs its", res.iterations, meta["t_solve_ref"], flush=True)
+    for lv in h.levels[:-1]:
+        lv.edge_sweeper = ChebyshevSweeper(lv.A_e, 3)
+        lv.aux_sweeper = ChebyshevSweeper(lv.nodal_aux, 3)
+    t0 = time.perf_counter()
+    rc = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+    meta["cheb"] = {"iterations": rc.iterations, "status": rc.status,
+                    "residual_history": rc.residual_history,
+                    "relative_residual": rc.relative_residual,
+                    "t_solve_ref": time.perf_counter() - t0}
+    print(name, "cheb its", rc.iterations, flush=True)
+    return meta, arrays
+
+
 def main(which):
     if "repair" in which:
         meta, arrays = repair_case()
@@ -317,6 +451,14 @@ def main(which):
         with open(os.path.join(HERE, "inputs.json"), "w") as f:
             json.dump(inputs_table(), f, indent=1, sort_keys=True)
         print("inputs.json written")
+    for name, spec in BIG.items():
+        if name not in which:           # only on request (minutes to hours)
+            continue
+        meta, arrays = run_device_case(name, *spec)
+        with open(os.path.join(HERE, f"hier_{name}.json"), "w") as f:
+            json.dump(meta, f, indent=1)
+        np.savez_compressed(os.path.join(HERE, f"hier_{name}.npz"), **arrays)
+        print(name, "written", flush=True)
     for name, spec in CASES.items():
         if which and name not in which:
             continue
@@ -331,4 +473,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(set(sys.argv[1:]) or set(["inputs", "errors"] + list(CASES) + list(RELAX)))
+    main(set(sys.argv[1:]) or set(["inputs", "errors", "repair"] + list(CASES) + list(RELAX)))

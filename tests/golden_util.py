@@ -83,3 +83,30 @@ def roundoff_pattern_diff(A, B, tol=1e-12):
     vb = np.asarray(B[mask.row, mask.col]).ravel()
     scale = max(float(abs(B).max()) if B.nnz else 0.0, 1e-300)
     return int(only.nnz), float(np.max(np.abs(np.concatenate([va, vb])))) / scale
+
+
+def sampled_rows_vals(M, stride):
+    """Values of rows 0, k, 2k, ... of a canonical scipy CSR, row-major."""
+    rows = np.arange(0, M.shape[0], int(stride))
+    ln = np.diff(M.indptr)[rows]
+    idx = np.repeat(M.indptr[rows], ln) + (np.arange(int(ln.sum()))
+                                           - np.repeat(np.cumsum(ln) - ln, ln))
+    return M.data[idx]
+
+
+def check_values(M, arrays, key, fro=None):
+    """TOL on the stored values of ``key`` (pattern already proven equal)."""
+    stride = int(arrays[key + "_stride"])
+    ref = arrays[key + "_vals"]
+    got = sampled_rows_vals(M, stride)
+    assert got.shape == ref.shape, key
+    scale = max(float(np.max(np.abs(M.data))) if M.nnz else 0.0, 1e-300)
+    err = float(np.max(np.abs(got - ref))) if ref.size else 0.0
+    assert err <= 1e-10 * scale, (key, err / scale)
+    if fro is not None:
+        assert abs(np.linalg.norm(M.data) - fro) <= 1e-10 * fro, key
+    return stride
+
+
+def pattern_sha(M):
+    return sha(M.indptr.astype(np.int64), M.indices.astype(np.int64))

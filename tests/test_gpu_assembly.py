@@ -117,3 +117,18 @@ def test_device_config_c4_small_hierarchy_vs_oracle(_gpu):
             assert np.array_equal(lv.membership.cpu().numpy(), lo.membership)
     assert res.status == "converged"
     assert abs(res.iterations - ro.iterations) <= 1, (res.iterations, ro.iterations)
+
+
+@pytest.mark.parametrize("config,N", [("C4", 12), ("C3", 16), ("C2", 8), ("C5", 10)])
+def test_device_assembly_equals_host_build_bitwise(config, N):
+    """The device generator and its host build (oracle/host_assembly.py, the
+    input source of the reference goldens for the device configs) produce the
+    same bits: same per-row source, explicit IEEE rounding."""
+    from golden_util import csr_hash
+    from oracle.host_assembly import config_host
+    from paper_2506_08284_b200.assembly import make_device_config
+    s, rhs, _ = make_device_config(config, N)
+    A_e, S, A_n, D, rhs_h, _ = config_host(config, N)
+    assert np.array_equal(rhs, rhs_h)
+    for M, H in ((s.A_e, A_e), (s.S, S), (s.A_n, A_n), (s.D, D)):
+        assert csr_hash(M.to_scipy()) == csr_hash(H)

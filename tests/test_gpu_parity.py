@@ -10,7 +10,8 @@ import numpy as np
 import pytest
 import scipy.sparse as sp
 
-from golden_util import csr_hash, golden_csr, load_case, rel_max_diff, sha
+from golden_util import (check_values, csr_hash, golden_csr, load_case, pattern_sha,
+                         rel_max_diff, sha)
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -311,8 +312,17 @@ def test_hierarchy_vs_reference_golden(name):
         rows = arrays[f"L{li}_Pe_sample_rows"]
         ref = golden_csr(arrays, f"L{li}_Pe_sample", (rows.size, P.shape[1]))
         assert rel_max_diff(P[rows], ref) <= 1e-10
+        if f"L{li}_Pe_vals" in arrays:
+            # every P_e entry (values-only goldens of the large cases)
+            check_values(P, arrays, f"L{li}_Pe", L["P_e_fro"])
         assert np.allclose(lv.emin_energy, L["emin_energy"], rtol=1e-10, atol=0)
         assert lv.commutator_residual <= 1e-12
+        if f"L{li + 1}_A_e_vals" in arrays:
+            nxt = h.levels[li + 1]
+            for key, M in (("A_e", nxt.A_e), ("S_e", nxt.S_e)):
+                Ms = M.to_scipy()
+                assert pattern_sha(Ms) == L[f"next_{key}_pattern"], (li, key)
+                check_values(Ms, arrays, f"L{li + 1}_{key}")
         if f"L{li + 1}_A_e_data" in arrays:
             nxt = h.levels[li + 1]
             n1 = nxt.A_e.shape[0]

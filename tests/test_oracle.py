@@ -181,3 +181,87 @@ def test_oracle_relaxation_only(name):
     assert res.iterations == meta["iterations"]
     np.testing.assert_allclose(res.residual_history, meta["residual_history"], rtol=1e-6)
     assert np.max(np.abs(res.x - arrays["x"])) <= 1e-8 * np.max(np.abs(arrays["x"]))
+
+
+def _repair_inputs():
+    """Level-0 inputs of the golden repair case (make_golden.repair_case):
+    N=10 Dirichlet, sigma=1, with every 17th interior coarse edge removed."""
+    import json
+    from golden_util import GOLDEN
+    with open(os.path.join(GOLDEN, "repair_N10d.json")) as f:
+        meta = json.load(f)
+    arrays = dict(np.load(os.path.join(GOLDEN, "repair_N10d.npz")))
+    s = discretize_hex(10, 1.0, True)
+    memb, n_agg = O.aggregate(O.strength_pattern(s.A_n))
+    P_n, _, _ = O.smoothed_prolongator(s.A_n, memb, n_agg)
+    assign = O.piecewise_const(P_n, 2)
+    ce = O.coarse_edges(s.D, assign, n_agg)
+    keep = np.array([p for k, p in enumerate(ce.pairs) if k % 17 != 3])
+    assert np.array_equal(keep, arrays["pairs"])
+    assert np.array_equal(ce.singles, arrays["singles"])
+    ce = O.CoarseEdges(pairs=keep, singles=ce.singles, n_nodes=n_agg)
+    return meta, arrays, s, P_n, ce
+
+
+def test_oracle_make_irreducible_vs_reference():
+    """make_irreducible + the post pass (emin_setup.py:183-217,311-333)
+    reproduce the reference's own setup_constraints on the repair golden:
+    the appended coarse edges (with the reference's duplicates), the
+    prolongator pattern and the feasible initial guess."""
+    meta, arrays, s, P_n, ce = _repair_inputs()
+    em = O.emin_prolongator(s.D, P_n, ce, s.S, iterations=0)
+    assert em.n_augmented == meta["n_augmented"] > 0
+    assert em.coarse.augmented.tolist() == meta["augmented"]
+    P = em.P_e
+    assert np.array_equal(P.indptr, arrays["P_indptr"])
+    assert np.array_equal(P.indices, arrays["P_indices"])
+    ref = arrays["P_data"]
+    assert np.max(np.abs(P.data - ref)) <= 1e-10 * np.max(np.abs(ref))
+    dims = sorted([list(k) + [v] for k, v in em.subproblem_dims.items()])
+    assert dims == meta["dims"]
+    # the repaired prolongator still satisfies the commutator identity
+    assert em.commutator_residual <= 1e-12
+
+
+def _check_device_config(name):
+    """Oracle vs the reference on a device-generated config golden
+    (inputs = the host build of the device assembly, pinned by sha256)."""
+    from golden_util import check_values, pattern_sha
+    from oracle.host_assembly import config_host
+    meta, arrays = load_case(name)
+    A_e, S, A_n, D, rhs, _ = config_host(meta["config"], meta["N"])
+    for k, M in (("A_e", A_e), ("S", S), ("A_n", A_n), ("D", D)):
+        assert csr_hash(M) == meta["inputs"][k], k
+    assert sha(rhs) == meta["rhs"]
+    h = O.build_hierarchy(A_e, S, A_n, D, coarse_size=meta["coarse_size"], smoother="cheb")
+    assert [lv.A_e.shape[0] for lv in h.levels] == meta["n_edges"]
+    assert [int(lv.A_e.nnz) for lv in h.levels] == meta["nnz_A_e"]
+    assert abs(h.operator_complexity - meta["operator_complexity"]) < 1e-14
+    for li, (lv, L) in enumerate(zip(h.levels, meta["levels"])):
+        assert csr_hash(lv.D) == L["D"], li
+        if li > 0:
+            for key, M in (("A_e", lv.A_e), ("S_e", lv.S_e)):
+                assert pattern_sha(M) == L[f"{key}_pattern"], (li, key)
+                check_values(M, arrays, f"L{li}_{key}", L[f"{key}_fro"])
+        if lv.P_e is None:
+            continue
+        assert sha(lv.membership.astype(np.int64)) == L["membership"]
+        assert float(lv.omega).hex() == L["omega_hex"]
+        assert csr_hash(lv.P_n) == L["P_n"]
+        assert sha(lv.assignment.astype(np.int64)) == L["assignment"]
+        assert lv.emin.n_augmented == L["n_augmented"]
+        assert pattern_sha(lv.P_e) == L["P_e_pattern"]
+        check_values(lv.P_e, arrays, f"L{li}_Pe", L["P_e_fro"])
+        assert np.allclose(lv.emin.energy_history, L["emin_energy"], rtol=1e-10, atol=0)
+    res = O.solve(h, rhs)
+    assert abs(res.iterations - meta["cheb"]["iterations"]) <= 1
+
+
+def test_oracle_device_config_c4s():
+    _check_device_config("C4s")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C3", "C5s"])
+def test_oracle_device_config_large(name):
+    _check_device_config(name)

@@ -1,13 +1,16 @@
 """Benchmark: SpHcurlAMG setup + PCG solve to 1e-8 on the B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
 A step is one pass of the hot path over one synthetic problem: build_hierarchy
 (constrained-energy-minimisation prolongators, Galerkin products, coarse
 gradients) followed by pcg_solve with the Chebyshev-Hiptmair V-cycle, rtol 1e-8.
-The default workload is BASELINE.json configs[1] ("C2": 32^3 hex, Dirichlet,
-sigma = 1e-2, RHS U[-1,1] seed 1, coarse_size 1000). Inputs are synthetic
-(the reference's own model problem, assembled bit-identically in-tree).
+The default workload is the largest BASELINE.json config that fits one GPU
+with the reference's settings, configs[3] ("C4": 128^3 hex, natural BC,
+lognormal per-element sigma, jittered isoparametric hexes, RHS U[-1,1], all
+from default_rng(3), coarse_size 1000). Inputs are synthetic, assembled on
+the device (csrc/assemble.cu); the reference arm runs on the bit-identical
+host build of the same rows (oracle/host_assembly.py).
 
 value = edge DOFs/s of setup + solve with the inputs resident in HBM; e2e = the
 same through the public API with host (scipy / numpy) inputs and the solution
@@ -16,17 +19,49 @@ every rank solves its own replica (weak scaling, no data-path collective --
 DESIGN.md "Multi-GPU"); timing is the max over ranks.
 
 --impl reference times the reference algorithm's CPU implementation (the
-oracle port in oracle/, Gauss-Seidel smoother as in the reference) on rank 0.
+oracle port in oracle/, Gauss-Seidel smoother as in the reference) on rank 0,
+re-executed under the survey's pin (OPENBLAS_CORETYPE=Haswell,
+OPENBLAS_NUM_THREADS=1, ``taskset -c 0``: one host core) before numpy loads.
 """
+
+import os
+import sys
+
+_PIN_ENV = {"OPENBLAS_CORETYPE": "Haswell", "OPENBLAS_NUM_THREADS": "1",
+            "OMP_NUM_THREADS": "1", "MKL_NUM_THREADS": "1"}
+
+
+def _pinned_cmd(argv):
+    """argv under ``taskset -c 0`` (when available) for the 1-core CPU legs."""
+    import shutil
+    cmd = [sys.executable] + list(argv)
+    if shutil.which("taskset"):
+        cmd = ["taskset", "-c", "0"] + cmd
+    return cmd
+
+
+def _reexec_pinned():
+    """The CPU arms (--impl reference, --cpu-sample) must see the BLAS pin
+    before numpy is imported, and run on one core: re-exec once."""
+    argv = sys.argv[1:]
+    cpu_leg = ("--cpu-sample" in argv or
+               any(a == "--impl=reference" for a in argv) or
+               ("--impl" in argv and argv[argv.index("--impl") + 1:][:1] == ["reference"]))
+    if cpu_leg and os.environ.get("SPHC_CPU_PINNED") != "1":
+        env = dict(os.environ, SPHC_CPU_PINNED="1", **_PIN_ENV)
+        cmd = _pinned_cmd(sys.argv)
+        os.execvpe(cmd[0], cmd, env)
+
+
+if __name__ == "__main__":
+    _reexec_pinned()
 
 import argparse
 import json
 import math
-import os
 import statistics
 import subprocess
 import tempfile
-import sys
 import time
 
 import numpy as np
@@ -178,20 +213,28 @@ def cheb_kernel_bytes(A):
     return 12 * A.nnz + 8 * (n + 1) + 8 * 6 * n
 
 
-def ncu_traffic(pattern="k_sell_cheb_full"):
-    """DRAM bytes (read + write) per launch of the roofline kernel from the
-    newest committed ncu --set full summary in profiles/, or None."""
+def ncu_traffic_file(config):
+    """The committed ncu --set full summary of the roofline kernel for this
+    workload: profiles/*_<config>_k_sell_cheb_full.txt (newest round)."""
     import glob
-    files = sorted(glob.glob(os.path.join(REPO, "profiles", f"*{pattern}*.txt")))
-    if not files:
+    files = sorted(glob.glob(os.path.join(REPO, "profiles",
+                                          f"r*_{config.lower()}_k_sell_cheb_full.txt")))
+    return os.path.relpath(files[-1], REPO) if files else None
+
+
+def ncu_traffic(config):
+    """DRAM bytes (read + write) per launch of the roofline kernel from that
+    summary, or None."""
+    f = ncu_traffic_file(config)
+    if f is None:
         return None
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     tot = 0.0
     found = 0
-    for line in open(files[-1]):
-        f = line.split()
-        if len(f) == 3 and f[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            tot += float(f[1]) * scale.get(f[2], 1)
+    for line in open(os.path.join(REPO, f)):
+        x = line.split()
+        if len(x) == 3 and x[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(x[1]) * scale.get(x[2], 1)
             found += 1
     return tot if found == 2 else None
 
@@ -247,7 +290,8 @@ def scale_roofline(args, flush):
             "kernel": "k_sell_cheb", "launch_ms_median": t, "algorithmic_bytes": byts,
             "achieved": ach, "peak": float(pk["hbm_gbs"]), "unit": "GB/s",
             "frac": ach / float(pk["hbm_gbs"]), "sell_padding": m.padded / A.nnz,
-            "traffic": ncu_traffic("k_sell_cheb_c3_full")}
+            "traffic": ncu_traffic(args.scale_config),
+            "traffic_source": ncu_traffic_file(args.scale_config)}
 
 
 DEVICE_INPUTS = ("C3", "C4", "C5")
@@ -459,12 +503,14 @@ def run_ours(args):
     t_k = sum(a.elapsed_time(bb) for a, bb in kev) / nk
     t_k_warm = k0.elapsed_time(k1) / nk
     kbytes = (12 * A0.nnz + 8 * (n_e + 1) + 32 * n_e) if gs_mode else cheb_kernel_bytes(A0)
-    at_scale = None if args.no_scale_roofline else scale_roofline(args, flush)
+    # the main roofline is already at scale (> L2) for C3-C5
+    at_scale = (None if args.no_scale_roofline or args.config in DEVICE_INPUTS
+                else scale_roofline(args, flush))
 
     # e2e: public API with host inputs, solution back to host
     e2e = None
     if sysm is not None:
-        e2e_ms = []
+        e2e_ms, first_ms = [], None
         for k in range(-2, max(2, min(args.steps, 5))):    # k < 0: untimed warm-up
             flush.fill_(3.0 + k)
             torch.cuda.synchronize()
@@ -475,6 +521,10 @@ def run_ours(args):
             torch.cuda.synchronize()
             if k >= 0:
                 e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            elif first_ms is None:
+                # first public-API call on these host arrays (staging buffers,
+                # graph capture and instantiation included)
+                first_ms = (time.perf_counter() - t0) * 1e3
             assert isinstance(re.x, np.ndarray)
             del he, re
         t_e2e = sum(e2e_ms) / len(e2e_ms)
@@ -489,8 +539,10 @@ def run_ours(args):
             return M.data.size * 8 + M.indices.size * 4 + M.indptr.size * 8
         h2d = sum(dev_bytes(M) for M in (sysm.A_e, sysm.S, sysm.A_n, sysm.D)) + rhs.nbytes
         e2e = {"value": ws * n_e / (t_e2e * 1e-3), "unit": "edge DOFs/s",
-               "ms": t_e2e, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(n_e * 8)}
+               "ms": t_e2e, "first_call_ms": first_ms, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(n_e * 8),
+               "host_memory": "caller arrays staged through a pinned buffer "
+                              "(no page-locking of caller memory; SPHC_PIN=1 opts in)"}
 
     pk, pk_kind = peaks()
     peak = float(pk["hbm_gbs"])
@@ -507,19 +559,15 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong" if partitioned else "weak",
             "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (reference model problem, seeded RHS)",
-            "config": {"workload": f"{args.config}: {cfg['N']}^3 hex, "
-                       f"{'Dirichlet' if cfg['dirichlet'] else 'natural'}, "
-                       f"sigma={cfg['sigma']}, rhs seed {cfg['seed']}, "
-                       f"coarse_size {args.coarse_size}",
-                       "n_edges": n_e, "levels": [lv.A_e.shape[0] for lv in h.levels],
-                       "operator_complexity": h.operator_complexity,
-                       "pcg_iterations": iters,
-                       "smoother": ("chebyshev-3 hiptmair" if args.smoother == "chebyshev"
-                                    else "symmetric gauss-seidel hiptmair (reference smoother)"),
-                       "parallelism": (f"row-block sharded setup + partitioned solve x{ws}"
-                                       if partitioned
-                                       else f"replicas x{ws}"),
-                       "l2": "256 MB flush before every timed step"},
+            "config": workload_config(args.config, cfg, n_e, args.coarse_size),
+            "run": {"levels": [lv.A_e.shape[0] for lv in h.levels],
+                    "operator_complexity": h.operator_complexity,
+                    "pcg_iterations": iters,
+                    "smoother": ("chebyshev-3 hiptmair" if args.smoother == "chebyshev"
+                                 else "symmetric gauss-seidel hiptmair (reference smoother)"),
+                    "parallelism": (f"row-block sharded setup + partitioned solve x{ws}"
+                                    if partitioned else f"replicas x{ws}"),
+                    "l2": "256 MB flush before every timed step (inputs > L2 at C3-C5)"},
             "step_ms": [round(x, 3) for x in step_ms],
             "setup_ms": t_setup, "solve_ms": t_solve,
             "setup_dofs_per_s": n_e / (t_setup * 1e-3),
@@ -533,10 +581,8 @@ def run_ours(args):
                                     "k_sell_cheb (fused Chebyshev step, SELL-32, level-0 A_e)"),
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
-                         "traffic": (None if gs_mode else
-                                     ncu_traffic() if args.config == "C2" else
-                                     ncu_traffic("k_sell_cheb_c3_full")
-                                     if args.config == "C3" else None),
+                         "traffic": None if gs_mode else ncu_traffic(args.config),
+                         "traffic_source": None if gs_mode else ncu_traffic_file(args.config),
                          "peak_source": pk_kind, "launch_ms": t_k,
                          "launch_ms_l2_warm": t_k_warm,
                          "l2_flushed_per_launch": "256 MB write + 256 MB clean read",
@@ -555,52 +601,165 @@ def run_ours(args):
     return line
 
 
+def host_problem(config, N=None):
+    """Host (scipy) inputs for the CPU legs, no GPU needed: inputs.py for
+    C1/C2 (bit-identical to the reference's assembly); for C3-C5 the host
+    build of the device assembly rows (oracle/host_assembly.py; bit-identical
+    to what the GPU arm assembles, tests/test_gpu_assembly.py)."""
+    from types import SimpleNamespace
+    if config in DEVICE_INPUTS:
+        from oracle.host_assembly import config_host
+        A_e, S, A_n, D, rhs, cfg = config_host(config, N)
+        return SimpleNamespace(A_e=A_e, S=S, A_n=A_n, D=D), rhs, cfg
+    from paper_2506_08284_b200.inputs import make_config
+    return make_config(config, N)
+
+
 def _oracle_step(sysm, rhs, coarse_size, smoother):
     from oracle import hcurl_oracle as O
     t0 = time.perf_counter()
     h = O.build_hierarchy(sysm.A_e, sysm.S, sysm.A_n, sysm.D, coarse_size=coarse_size,
                           smoother=smoother)
+    t1 = time.perf_counter()
     res = O.solve(h, rhs)
-    return time.perf_counter() - t0, res
+    t2 = time.perf_counter()
+    return t2 - t0, res, t1 - t0, t2 - t1
+
+
+def host_info():
+    """What the CPU legs ran on: lscpu model, os.cpu_count(), the affinity
+    actually used (taskset -c 0 -> 1) and the BLAS pin."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for l in out.splitlines():
+            if l.startswith("Model name:"):
+                model = l.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except AttributeError:
+        aff = None
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "affinity_cores": aff,
+            "openblas": {k: os.environ.get(k) for k in ("OPENBLAS_CORETYPE",
+                                                        "OPENBLAS_NUM_THREADS")}}
+
+
+# cpu_baseline sample per bench workload: the same recipe at a size whose
+# port setup + solve takes ~10-20 s on one core
+CPU_SAMPLE_N = {"C1": None, "C2": None, "C3": 32, "C4": 32, "C5": 32}
+
+
+def cpu_sample(args):
+    """--cpu-sample (re-executed pinned, one core): the oracle port's setup +
+    solve on a bounded sample of the workload; prints one JSON line."""
+    sysm, rhs, cfg = host_problem(args.config, args.N)
+    t, res, ts, tv = _oracle_step(sysm, rhs, args.coarse_size or cfg.get("coarse_size", 1000),
+                                  "gs")
+    print(json.dumps({"t": t, "t_setup": ts, "t_solve": tv, "n_e": sysm.A_e.shape[0],
+                      "N": cfg["N"], "its": res.iterations, "status": res.status,
+                      "host": host_info()}), flush=True)
 
 
 def cpu_baseline(args):
-    """The oracle port (reference algorithm, Gauss-Seidel) on a bounded sample
-    of the workload: C1 (16^3) setup + solve, 1 host core."""
-    sysm, rhs, cfg = make_problem("C1")
-    t, res = _oracle_step(sysm, rhs, 1000, "gs")
-    n_e = sysm.A_e.shape[0]
-    return {"value": n_e / t, "unit": "edge DOFs/s", "cores": 1, "kind": "port",
-            "sample": f"C1 16^3 Dirichlet ({n_e} edges) setup+solve, {res.iterations} its, "
-                      f"{t:.2f} s"}
+    """The oracle port (reference algorithm, Gauss-Seidel) on a bounded
+    sample of the workload -- the same recipe at CPU_SAMPLE_N[config] --
+    in a pinned one-core subprocess (this process has numpy loaded already)."""
+    nsamp = CPU_SAMPLE_N.get(args.config)
+    cmd = _pinned_cmd([os.path.abspath(__file__), "--cpu-sample", "--config", args.config] +
+                      (["--N", str(nsamp)] if nsamp else []))
+    env = dict(os.environ, SPHC_CPU_PINNED="1", **_PIN_ENV)
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, check=True).stdout
+    r = json.loads(out.strip().splitlines()[-1])
+    return {"value": r["n_e"] / r["t"], "unit": "edge DOFs/s",
+            "cores": r["host"]["affinity_cores"] or 1, "kind": "port",
+            "sample": f"{args.config} recipe at {r['N']}^3 ({r['n_e']} edges): oracle port "
+                      f"setup {r['t_setup']:.2f} s + Gauss-Seidel PCG {r['its']} its "
+                      f"{r['t_solve']:.2f} s, one core (taskset -c 0, OpenBLAS Haswell x1)",
+            "host": r["host"]}
+
+
+def host_cfg(config, N=None):
+    """The config dict of a workload without building it."""
+    from paper_2506_08284_b200.inputs import CONFIGS
+    cfg = dict(CONFIGS[config])
+    if N is not None:
+        cfg["N"] = int(N)
+    if cfg["sigma"] == "lognormal":
+        cfg["geometry"] = "jittered isoparametric trilinear hexes (|dx| <= 0.2 h)"
+    return cfg
+
+
+def full_n_edges(cfg):
+    """Edge count of the hex mesh."""
+    N = cfg["N"]
+    return 3 * N * (N - 1) ** 2 if cfg["dirichlet"] else 3 * N * (N + 1) ** 2
+
+
+def workload_config(config, cfg, n_e, coarse_size):
+    """The ``config`` object both arms print (identical for the same run)."""
+    sig = cfg["sigma"]
+    sig = sig if isinstance(sig, (int, float, str)) else "per-element"
+    return {"workload": f"{config}: {cfg['N']}^3 hex, "
+                        f"{'Dirichlet' if cfg['dirichlet'] else 'natural'} BC, sigma={sig}"
+                        + (", jittered hexes" if cfg.get("geometry", "").startswith("jitter")
+                           else "")
+                        + f", rhs U[-1,1] seed {cfg['seed']}, coarse_size {coarse_size}, "
+                          "PCG rtol 1e-8",
+            "n_edges": int(n_e)}
+
+
+# reference-arm sample per workload (--ref-N overrides; 0 = the full size):
+# the full C4 setup + solve takes ~1 h on one core (the reference package
+# itself ~3 h, DESIGN.md 6), far beyond a bench run, so each step runs the
+# same recipe at 32^3
+REF_SAMPLE_N = {"C3": 32, "C4": 32, "C5": 32}
 
 
 def run_reference(args):
+    """The reference's CPU path (the oracle port with the reference's
+    Gauss-Seidel smoother; the reference package itself cannot travel to
+    the GPU box) on one pinned core, rank 0 only. Each step is one full
+    setup + solve of a bounded sample of the workload: the same recipe at
+    REF_SAMPLE_N (capped at --ref-steps steps)."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return None
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    sysm, rhs, cfg = make_problem(args.config, args.N)
+    full_cfg = host_cfg(args.config, args.N)
+    nsamp = REF_SAMPLE_N.get(args.config) if args.ref_N is None else (args.ref_N or None)
+    sysm, rhs, cfg = host_problem(args.config, nsamp or args.N)
     n_e = sysm.A_e.shape[0]
-    for _ in range(min(args.warmup, 1)):
-        _oracle_step(*make_problem("C1")[:2], 1000, "gs")
+    cs = args.coarse_size or cfg.get("coarse_size", 1000)
+    wu = min(args.warmup, 1)
+    for _ in range(wu):        # warm-up on a small instance (imports, page-in)
+        s1, r1, _ = host_problem("C1")
+        _oracle_step(s1, r1, 1000, "gs")
     k = max(1, min(args.steps, args.ref_steps))
-    times = []
+    times, res = [], None
     for _ in range(k):
-        t, res = _oracle_step(sysm, rhs, args.coarse_size or cfg.get("coarse_size", 1000), "gs")
-        times.append(t)
-    tm = sum(times) / k
+        t, res, ts, tv = _oracle_step(sysm, rhs, cs, "gs")
+        times.append((t, ts, tv))
+    tm = sum(x[0] for x in times) / k
     v = n_e / tm
+    hi = host_info()
     line = {"impl": "reference", "metric": "edge DOFs/s for setup + PCG solve to 1e-8",
             "value": v, "unit": "edge DOFs/s", "n_gpus": ws, "steps": k,
-            "warmup": min(args.warmup, 1), "ms_per_step": tm * 1e3,
+            "warmup": wu, "ms_per_step": tm * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (reference model problem, seeded RHS)",
-            "config": {"workload": f"{args.config}: {cfg['N']}^3 hex", "n_edges": n_e,
-                       "pcg_iterations": res.iterations, "smoother": "gauss-seidel (reference)"},
-            "cpu_baseline": {"value": v, "unit": "edge DOFs/s", "cores": 1, "kind": "port",
-                             "sample": f"{args.config} full setup+solve x{k} (capped at "
-                                       f"{args.ref_steps} steps)"},
+            "config": workload_config(args.config, full_cfg, full_n_edges(full_cfg), cs),
+            "run": {"pcg_iterations": res.iterations, "status": res.status,
+                    "sample": {"N": cfg["N"], "n_edges": int(n_e)},
+                    "smoother": "symmetric gauss-seidel hiptmair (reference)",
+                    "setup_s": [round(x[1], 3) for x in times],
+                    "solve_s": [round(x[2], 3) for x in times]},
+            "cpu_baseline": {"value": v, "unit": "edge DOFs/s",
+                             "cores": hi["affinity_cores"] or 1, "kind": "port",
+                             "sample": f"{args.config} recipe at {cfg['N']}^3 ({n_e} edges): "
+                                       f"full setup + Gauss-Seidel PCG x{k} (capped at "
+                                       f"--ref-steps {args.ref_steps}), one core",
+                             "host": hi},
             "e2e": {"value": v, "unit": "edge DOFs/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -612,14 +771,17 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--N", type=int, default=None)
     ap.add_argument("--coarse-size", type=int, default=None,
                     help="default: the config's (1000; 10000 for C5)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--smoother", default="chebyshev", choices=["chebyshev", "gauss_seidel"])
-    ap.add_argument("--ref-steps", type=int, default=3)
+    ap.add_argument("--ref-steps", type=int, default=1)
+    ap.add_argument("--ref-N", type=int, default=None,
+                    help="reference-arm sample size (default REF_SAMPLE_N; 0: full size)")
+    ap.add_argument("--cpu-sample", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-scale-roofline", action="store_true")
     ap.add_argument("--partitioned", action="store_true",
@@ -629,7 +791,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
-    if args.impl == "reference":
+    if args.cpu_sample:
+        cpu_sample(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -379,10 +379,19 @@ def _components(ends, I, J):
     return [find(c) for c in range(len(J))], inc
 
 
-def _irreducible(ends, I, J):
-    """check_irreducible (emin_setup.py:174-180)."""
+def _irreducible(ends, I, J, cache=None):
+    """check_irreducible (emin_setup.py:174-180); ``cache`` memoises it by
+    the block's local structure (the reference's blocks repeat heavily)."""
     if len(J) == 0:
         return False
+    if cache is not None:
+        pos = {c: x for x, c in enumerate(J)}
+        key = (len(J), tuple(tuple(pos[n] for n in ends[e]) for e in I))
+        hit = cache.get(key)
+        if hit is None:
+            roots, inc = _components(ends, I, J)
+            hit = cache[key] = all(inc) and len(set(roots)) == 1
+        return hit
     roots, inc = _components(ends, I, J)
     return all(inc) and len(set(roots)) == 1
 
@@ -492,7 +501,7 @@ def emin_prolongator(D_h, P_n, ce, S, omega=0.5, iterations=1):
     n0 = len(ends)
     aug = [tuple(int(v) for v in e) for e in ce.augmented]
     n_aug_in = len(aug)
-    score_cache = {}
+    score_cache, irr_cache = {}, {}
 
     n = D.shape[0]
     rows_I, rows_J, rows_N, rows_r = [None] * n, [None] * n, [None] * n, [None] * n
@@ -522,7 +531,7 @@ def emin_prolongator(D_h, P_n, ce, S, omega=0.5, iterations=1):
                 raise ValueError(
                     f"fine edge {i}: nonzero commutator row over a single "
                     "coarse node cannot be satisfied by interior coarse edges")
-        if not _irreducible(ends, I, Jl):
+        if not _irreducible(ends, I, Jl, irr_cache):
             if Rc is None:
                 Rc = R.tocsc()
                 Rc.sort_indices()

@@ -161,11 +161,23 @@ _NP = {torch.int64: np.int64, torch.int32: np.int32, torch.float64: np.float64,
 
 
 _PINNED = {}
+_INFLIGHT = []        # (host array, event): direct DMAs whose source must stay alive
 
 
-def upload(a, dtype, dev=None):
+def _retire_inflight():
+    while _INFLIGHT and _INFLIGHT[0][1].query():
+        _INFLIGHT.pop(0)
+
+
+def upload(a, dtype, dev=None, owned=True):
     """Host array -> new device tensor through a reused pinned staging buffer
-    (one cast on the host, one DMA at pinned-memory bandwidth)."""
+    (one cast on the host, one DMA at pinned-memory bandwidth).
+
+    With page-locking enabled (SPHC_PIN=1, opt-in) an array the CALLER owns
+    (``owned``; never a temporary made here) that already has the device
+    dtype is DMA'd straight from its own memory; it is kept alive until that
+    copy's event completes, so neither the caller dropping it nor its
+    registration being released can race the copy."""
     dev = dev or device()
     a0 = a
     a = np.asarray(a)
@@ -174,10 +186,12 @@ def upload(a, dtype, dev=None):
     if n == 0:
         return t
     nbytes = n * np.dtype(dtype).itemsize
-    # direct DMA only from the caller's own array object (a temporary made
-    # by asarray would be freed -- and unregistered -- under the copy)
-    if a is a0 and a.dtype == np.dtype(dtype) and pinned_in_place(a):
+    _retire_inflight()
+    if owned and a is a0 and a.dtype == np.dtype(dtype) and pinned_in_place(a):
         call("sphc_copy_h2d", t, a, nbytes)     # stream ordered, no staging / sync
+        ev = torch.cuda.Event()
+        ev.record()
+        _INFLIGHT.append((a, ev))
         return t
     # the staging buffer is reused: the next upload waits for this copy's
     # event (normally long done) instead of this one syncing the stream
@@ -215,14 +229,15 @@ class DeviceCSR:
     @staticmethod
     def from_scipy(A, dev=None):
         dev = dev or device()
-        A = host_csr(A)
+        A0 = A = host_csr(A)
         if not A.has_canonical_format:
             A = A.copy()
             A.sum_duplicates()
             A.sort_indices()
-        return DeviceCSR(rowptr=upload(A.indptr, np.int64, dev),
-                         col=upload(A.indices, np.int32, dev),
-                         val=upload(A.data, np.float64, dev),
+        owned = A is A0          # a canonicalised temporary is always staged
+        return DeviceCSR(rowptr=upload(A.indptr, np.int64, dev, owned),
+                         col=upload(A.indices, np.int32, dev, owned),
+                         val=upload(A.data, np.float64, dev, owned),
                          shape=tuple(int(s) for s in A.shape))
 
     def to_scipy(self):
@@ -247,6 +262,15 @@ def host_csr(A):
     return sp.csr_matrix(A)
 
 
+def own_csr(A):
+    """A solver-owned DeviceCSR for a caller's matrix: a caller DeviceCSR is
+    re-wrapped (same tensors, new object), so caches and pattern sharing the
+    solver attaches to its own matrices never touch the caller's object."""
+    if isinstance(A, DeviceCSR):
+        return DeviceCSR(A.rowptr, A.col, A.val, A.shape)
+    return as_device_csr(A)
+
+
 def as_device_csr(A):
     if isinstance(A, DeviceCSR):
         return A
@@ -259,12 +283,18 @@ _STAGE = {}
 _REG = {}      # (address, bytes) -> weakref of the page-locked host array
 
 
+PIN_CALLER_MEMORY = os.environ.get("SPHC_PIN", "0") == "1"
+
+
 def pinned_in_place(a):
-    """True if host array ``a`` is page-locked for direct DMA. Each array
+    """True if host array ``a`` is page-locked for direct DMA. Opt-in
+    (SPHC_PIN=1): page-locking is a process-wide side effect on the caller's
+    memory, so by default every upload is staged. When enabled, each array
     object is registered once (sphc_host_register) and released when it is
-    garbage collected; small, strided or overlapping arrays return False
-    (the caller stages them instead)."""
-    if a.nbytes < (1 << 20) or not a.flags.c_contiguous or os.environ.get("SPHC_PIN") == "0":
+    garbage collected (its in-flight copies keep it alive until they finish,
+    ``upload``); small, strided or overlapping arrays return False (the
+    caller stages them instead)."""
+    if not PIN_CALLER_MEMORY or a.nbytes < (1 << 20) or not a.flags.c_contiguous:
         return False
     import weakref
     key = (a.ctypes.data, a.nbytes)
@@ -303,17 +333,19 @@ class AsyncUpload:
 
     def __init__(self, mats, nthreads=8):
         dev = device()
-        self.mats = []
+        self.mats, owned = [], []
         for A in mats:
-            A = host_csr(A)
+            A0 = A = host_csr(A)
             if not A.has_canonical_format:
                 A = A.copy()
                 A.sum_duplicates()
                 A.sort_indices()
             self.mats.append(A)
+            owned += [A is A0] * 3
         self.specs = []
         for A in self.mats:
             self.specs += [(A.indptr, np.int64), (A.indices, np.int32), (A.data, np.float64)]
+        self.owned = owned
         tdt = {np.int64: torch.int64, np.int32: torch.int32, np.float64: torch.float64}
         self.dst = [torch.empty(a.size, dtype=tdt[d], device=dev) for a, d in self.specs]
         self.offs, o = [], 0
@@ -345,7 +377,8 @@ class AsyncUpload:
             hv = buf.numpy()
             # arrays already in the device dtype DMA straight from the
             # caller's page-locked memory; the rest are cast into staging
-            direct = [a.dtype == np.dtype(d) and pinned_in_place(a) for a, d in self.specs]
+            direct = [own and a.dtype == np.dtype(d) and pinned_in_place(a)
+                      for (a, d), own in zip(self.specs, self.owned)]
             jobs = []
             for (a, d), o, dr in zip(self.specs, self.offs, direct):
                 if dr:
@@ -369,6 +402,10 @@ class AsyncUpload:
                                                   non_blocking=True)
                 self.event.record(self.stream)
             _STAGE["event"] = self.event
+            # direct sources stay referenced (self.mats) until get() has
+            # made the compute stream wait on the copies; keep them alive
+            # past that too, until the copies are done
+            _INFLIGHT.extend((a, self.event) for (a, _), dr in zip(self.specs, direct) if dr)
         except BaseException as e:   # noqa: BLE001 - re-raised by get()
             self.err = e
 
@@ -631,9 +668,23 @@ class SellMirror:
         return int(self.col.numel())
 
 
-def sell(A):
-    """SELL-32 mirror of A (built once, cached on the DeviceCSR)."""
+def _sell_key(A):
+    return (A.rowptr.data_ptr(), A.col.data_ptr(), A.val.data_ptr(), A.val._version)
+
+
+def sell_mirror(A):
+    """A's cached SELL mirror if it still matches A's arrays (an in-place
+    update of A.val bumps its version and retires the mirror), else None."""
     m = getattr(A, "_sell", None)
+    if m is not None and A._sell_key == _sell_key(A):
+        return m
+    return None
+
+
+def sell(A):
+    """SELL-32 mirror of A (built once per array version, cached on A; the
+    solver builds it on its own wrappers, never on a caller's DeviceCSR)."""
+    m = sell_mirror(A)
     if m is not None:
         return m
     n = A.shape[0]
@@ -645,7 +696,7 @@ def sell(A):
     v = empty_f64(tot)
     call("sphc_sell_fill", n, A.rowptr, A.col, A.val, sp_, ci, v)
     m = SellMirror(sp_, ci, v, n)
-    A._sell = m
+    A._sell, A._sell_key = m, _sell_key(A)
     return m
 
 
@@ -654,8 +705,8 @@ CTA_ROW_MIN_LEN = 96
 
 
 def spmv(A, x, y, alpha=1.0, beta=0.0, z=None, lanes=None):
-    """y = alpha A x + beta z (on A's SELL mirror when it has one)."""
-    m = getattr(A, "_sell", None)
+    """y = alpha A x + beta z (on A's SELL mirror when it has a current one)."""
+    m = sell_mirror(A)
     if m is not None:
         call("sphc_sell_spmv", m.n, m.slice_ptr, m.col, m.val, x, alpha, beta, z, y, m.padded)
         return y

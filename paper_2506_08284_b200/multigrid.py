@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import device as dv
-from .device import checked, DeviceCSR, Status, as_device_csr, call
+from .device import checked, DeviceCSR, Status, as_device_csr, call, own_csr
 from .edge_prolongator import EminConfig, build_edge_prolongator
 from . import trace as _trace
 from .trace import phase
@@ -489,7 +489,7 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
         # right after the first prolongator. A data error of the nodal chain
         # defers to that check's, so the reference's error order holds.
         up = dv.AsyncUpload([A_e, S_e])
-        A_n, D = as_device_csr(A_n), as_device_csr(D)
+        A_n, D = own_csr(A_n), own_csr(D)
         try:
             first = build_edge_prolongator(A_n, dv.PendingCSR(up, 0), dv.PendingCSR(up, 1), D,
                                            cfg.emin, shard=shard)
@@ -497,8 +497,11 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
             _check_nullspace(up.get(1), D, "the fine level", A=up.get(0), shard=shard)
             raise
         A_e, S_e = up.get(0), up.get(1)
-    A_e, S_e = as_device_csr(A_e), as_device_csr(S_e)
-    A_n, D = as_device_csr(A_n), as_device_csr(D)
+    else:
+        # solver-owned wrappers: the SELL mirrors and shared index arrays
+        # the setup attaches never land on the caller's DeviceCSR objects
+        A_e, S_e = own_csr(A_e), own_csr(S_e)
+        A_n, D = own_csr(A_n), own_csr(D)
     AD = _check_nullspace(S_e, D, "the fine level", A=A_e, shard=shard)
     levels = []
     while A_e.shape[0] > cfg.coarse_size and len(levels) < cfg.max_levels - 1:
@@ -583,7 +586,7 @@ def reuse_hierarchy(h, A_e, S_e, cfg=None):
     null-space checks of every level. Returns a new Hierarchy sharing the
     transfers with ``h`` (which stays usable)."""
     cfg = cfg or SolverConfig()
-    A_e, S_e = as_device_csr(A_e), as_device_csr(S_e)
+    A_e, S_e = own_csr(A_e), own_csr(S_e)
     old = h.levels
     if A_e.shape != old[0].A_e.shape or S_e.shape != old[0].S_e.shape:
         raise ValueError(f"operators {A_e.shape} / {S_e.shape} do not match the hierarchy's "
@@ -649,6 +652,7 @@ def v_cycle_preconditioner(h):
         with phase("solve.vcycle"):
             return v_cycle(h, None, b)
     apply.graph_safe = not _trace.ENABLED     # tracing inserts host syncs
+    apply.device_tensors = True
     apply.hierarchy = h
     return apply
 
@@ -660,6 +664,7 @@ def hiptmair_preconditioner(level):
         with phase("solve.hiptmair"):
             return hiptmair_smooth(level, None, b, x_zero=True)
     apply.graph_safe = not _trace.ENABLED
+    apply.device_tensors = True
     # pcg_solve keeps its captured iteration on this holder and checks the
     # level's sweepers after the solve, as for a hierarchy
     holder = getattr(level, "_relax_holder", None)
@@ -675,7 +680,7 @@ def fine_level(A_e, S_e, D, cfg=None):
     comparison (multigrid.py:204-207). ``cfg`` (not a reference argument)
     picks the smoother; the default is the Chebyshev-3 performance smoother."""
     cfg = cfg or SolverConfig()
-    A_e, S_e, D = as_device_csr(A_e), as_device_csr(S_e), as_device_csr(D)
+    A_e, S_e, D = own_csr(A_e), own_csr(S_e), own_csr(D)
     lv = _make_level(A_e, S_e, D, cfg)
     finalize_sweepers()
     return lv
@@ -776,6 +781,23 @@ def _pcg_iteration(A, lanes, precond, x, r, p, Ap, sc, flag, stage, rotate=True)
     return z
 
 
+def _device_precond(precond):
+    """The reference's preconditioner contract is Callable[[ndarray],
+    ndarray] (multigrid.py:220). Ours (``device_tensors``) map device
+    tensors to device tensors; any other callable gets r as a host numpy
+    array and may return numpy or torch. Such a callable runs in the host
+    loop, never in the captured graph."""
+    if getattr(precond, "device_tensors", False):
+        return precond
+
+    def apply(r):
+        z = precond(r.cpu().numpy())
+        if isinstance(z, torch.Tensor):
+            return z.to(device=r.device, dtype=torch.float64)
+        return torch.as_tensor(np.ascontiguousarray(z, dtype=np.float64), device=r.device)
+    return apply
+
+
 @checked
 def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
     """Preconditioned CG from x = 0 (multigrid.py:220-274): same statuses
@@ -794,6 +816,7 @@ def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
     lanes = A.lanes()
     graph_ok = getattr(precond, "graph_safe", False) and maxit > 0 and USE_GRAPH
     hier = getattr(precond, "hierarchy", None)
+    precond = _device_precond(precond)
     ws = getattr(hier, "_pcg_ws", None) if graph_ok else None
     if ws is not None and (ws["A"] is not A and ws["A_key"] != _csr_key(A) or ws["n"] != n):
         ws = None

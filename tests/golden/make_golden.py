@@ -429,6 +429,30 @@ def run_device_case(name, config, N, coarse_size, limit, with_gs):
     return meta, arrays
 
 
+def pcg_status_cases():
+    """The reference's non-converged PCG exits (multigrid.py:244-264) on
+    small hierarchies: maxit (maxit=3), stagnated (rtol=0: x stops changing
+    at round-off; the last history entry is the true residual) and
+    indefinite (the negated operator: p.Ap <= 0 on the first iteration)."""
+    out, arrays = {}, {}
+    for name, (N, dirich, cs) in {"N4n": (4, False, 40), "N6d": (6, True, 40)}.items():
+        s = discretize(build_structured_mesh(3, "hex", N + 1, dirich), 1.0)
+        h = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, mg.SolverConfig(coarse_size=cs))
+        b = np.random.default_rng(0).uniform(-1, 1, s.A_e.shape[0])
+        M = mg.v_cycle_preconditioner(h)
+        for kind, (A, kw) in {"maxit": (h.levels[0].A_e, dict(maxit=3)),
+                              "stagnated": (h.levels[0].A_e, dict(rtol=0.0)),
+                              "indefinite": (-h.levels[0].A_e, {})}.items():
+            r = mg.pcg_solve(A, b, M, **kw)
+            out[f"{name}_{kind}"] = {"N": N, "dirichlet": dirich, "coarse_size": cs,
+                                     "status": r.status, "iterations": r.iterations,
+                                     "residual_history": r.residual_history,
+                                     "precond_history": r.precond_history,
+                                     "relative_residual": r.relative_residual}
+            arrays[f"{name}_{kind}_x"] = r.x
+    return out, arrays
+
+
 def main(which):
     if "repair" in which:
         meta, arrays = repair_case()
@@ -436,6 +460,12 @@ def main(which):
             json.dump(meta, f, indent=1)
         np.savez_compressed(os.path.join(HERE, "repair_N10d.npz"), **arrays)
         print("repair case: n_augmented", meta["n_augmented"])
+    if "pcg_status" in which:
+        meta, arrays = pcg_status_cases()
+        with open(os.path.join(HERE, "pcg_status.json"), "w") as f:
+            json.dump(meta, f, indent=1)
+        np.savez_compressed(os.path.join(HERE, "pcg_status.npz"), **arrays)
+        print("pcg status cases", {k: (v["status"], v["iterations"]) for k, v in meta.items()})
     if "errors" in which:
         with open(os.path.join(HERE, "errors.json"), "w") as f:
             json.dump(error_cases(), f, indent=1)
@@ -473,4 +503,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(set(sys.argv[1:]) or set(["inputs", "errors", "repair"] + list(CASES) + list(RELAX)))
+    main(set(sys.argv[1:]) or set(["inputs", "errors", "repair", "pcg_status"] + list(CASES) + list(RELAX)))

@@ -265,3 +265,39 @@ def test_oracle_device_config_c4s():
 @pytest.mark.parametrize("name", ["C3", "C5s"])
 def test_oracle_device_config_large(name):
     _check_device_config(name)
+
+
+def _pcg_status_golden():
+    import json
+    from golden_util import GOLDEN
+    with open(os.path.join(GOLDEN, "pcg_status.json")) as f:
+        meta = json.load(f)
+    return meta, dict(np.load(os.path.join(GOLDEN, "pcg_status.npz")))
+
+
+@pytest.mark.parametrize("kind", ["maxit", "stagnated", "indefinite"])
+@pytest.mark.parametrize("case", ["N4n", "N6d"])
+def test_oracle_pcg_status_vs_reference(case, kind):
+    """The oracle's PCG restatement exits like the reference's
+    (multigrid.py:244-264): same status, iterations and histories."""
+    meta, arrays = _pcg_status_golden()
+    g = meta[f"{case}_{kind}"]
+    s = discretize_hex(g["N"], 1.0, g["dirichlet"])
+    h = O.build_hierarchy(s.A_e, s.S, s.A_n, s.D, coarse_size=g["coarse_size"])
+    b = np.random.default_rng(0).uniform(-1, 1, s.A_e.shape[0])
+    A = h.levels[0].A_e if kind != "indefinite" else -h.levels[0].A_e
+    kw = {"maxit": dict(maxit=3), "stagnated": dict(rtol=0.0), "indefinite": {}}[kind]
+    r = O.pcg(A, b, lambda v: O.v_cycle(h, v), **kw)
+    assert r.status == g["status"] == kind
+    assert r.iterations == g["iterations"]
+    np.testing.assert_allclose(r.residual_history[:-1], g["residual_history"][:-1],
+                               rtol=1e-6, atol=1e-14 * g["residual_history"][0])
+    np.testing.assert_allclose(r.precond_history, g["precond_history"], rtol=1e-6,
+                               atol=1e-14 * g["precond_history"][0])
+    if kind == "stagnated":        # true residual of the frozen iterate
+        assert r.residual_history[-1] <= 1e-11 * g["residual_history"][0]
+    else:
+        assert abs(r.residual_history[-1] - g["residual_history"][-1]) <= \
+            1e-6 * g["residual_history"][-1]
+    x = arrays[f"{case}_{kind}_x"]
+    assert np.max(np.abs(r.x - x)) <= 1e-8 * max(np.max(np.abs(x)), 1e-300)

@@ -128,6 +128,15 @@ int sphc_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_
 int sphc_csr_count_nonzero(int64_t n, const int64_t *rp, const double *v, int64_t *counts,
                            void *stream);
 
+/* C = alpha A + beta B on the union pattern of two canonical CSR matrices
+ * (scipy csr_binop_csr, e.g. commutator_residual's P_e D_H - R_dp,
+ * edge_prolongator.py:179-181): count pass, scan, fill. */
+int sphc_csr_add_count(int64_t n, const int64_t *arp, const int32_t *aci, const int64_t *brp,
+                       const int32_t *bci, int64_t *counts, void *stream);
+int sphc_csr_add_fill(int64_t n, const int64_t *arp, const int32_t *aci, const double *av,
+                      const int64_t *brp, const int32_t *bci, const double *bv, double alpha,
+                      double beta, const int64_t *crp, int32_t *cci, double *cv, void *stream);
+
 /* Drop exact zeros (sparse_ops.py:107-113 compress(A, 0)). new_rp from
  * sphc_csr_count_nonzero + sphc_scan_i64. */
 int sphc_csr_compact(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
@@ -382,6 +391,19 @@ int sphc_pattern_union_fill(int64_t n, const int64_t *arp, const int32_t *aci,
  * -- the storage order scipy gives diags(1/d) @ A (nodal_amg.py:150-151,110). */
 int sphc_nodal_powmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
                      const double *dinv, const double *x, double *y, void *stream);
+
+/* y_i = sum over row i IN STORAGE ORDER of fl(a_ij x_j), sequential from 0,
+ * no FMA: scipy csr_matvec on any row order (estimate_rho(A_scaled),
+ * nodal_amg.py:99-116, whose A_scaled rows scipy stores descending). */
+int sphc_spmv_stored_order(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                           const double *x, double *y, void *stream);
+
+/* normalize_rows (nodal_amg.py:119-135): out = fl(fl(1 / s_i) a_ij) with
+ * s_i = a_i0 + pairwise(a_i1..) (np.add.reduceat); zero-sum rows (|s| <=
+ * 1e-13 max(1, sum |a|)) -> status ZERO_ROWSUM; rows longer than 257 ->
+ * SPGEMM_CAPACITY. Exact zeros are dropped by the caller (compact). */
+int sphc_normalize_rows(int64_t n, const int64_t *rp, const double *v, double *out,
+                        int64_t *status, void *stream);
 
 /* Smoothed + normalised nodal prolongator rows (nodal_amg.py:119-155):
  * P = normalize((I - omega D^-1 A) P_tent), bit-faithful (Appendix A). */

@@ -214,6 +214,7 @@ def normalize_rows(P):
         raise ValueError(f"zero row sum before scaling in row {bad[0]}")
     out = P.copy()
     out.data = (1.0 / s)[row_ids(P)] * P.data
+    out.eliminate_zeros()          # diags(1/s) @ P drops exact-zero products
     return out
 
 

@@ -1,10 +1,15 @@
 """Coarse discrete gradients from nodal grid transfers, on the B200.
 
-Mirror of the reference's coarse_gradient.py. ``gen_piecewise_const``
-(Algorithm 1) is the host C++ greedy pass of libsphcurl on the downloaded
-nodal prolongator; the coarse edge set, the Dirichlet single-node edges and
-D_H are built by libsphcurl kernels (bucket by lower aggregate, segmented
-sort, unique, scan).
+Mirror of the reference's coarse_gradient.py (same names and signatures:
+``gen_piecewise_const(P) -> P_const``, ``build_coarse_gradient(D_h, P_const)``,
+``augment_dirichlet_edges(cg, D_h, P_const)``, ``append_edge(cg, i, j)``).
+Algorithm 1 runs on the device as cooperative fixed-point claiming passes
+(csrc/pconst.cu), bit-identical to the reference's ordered loops; the coarse
+edge set, the Dirichlet single-node edges and D_H are built by libsphcurl
+kernels (bucket by lower aggregate, segmented sort, unique, scan). The
+hierarchy itself uses the assignment-vector forms
+(``piecewise_const_assignment``, ``coarse_gradient_from_assignment``): P_const
+is exactly that vector.
 """
 
 from dataclasses import dataclass
@@ -78,10 +83,29 @@ def coarse_gradient_from_edges(pairs, singles, n_nodes):
 
 @checked
 def gen_piecewise_const(P, n_passes=2):
+    """Algorithm 1 (coarse_gradient.py:36-103): P_const, one unit entry per
+    row at the column Algorithm 1 assigns it (a DeviceCSR)."""
+    assign = piecewise_const_assignment(P, n_passes)
+    n, m = P.shape
+    dev = assign.device
+    return DeviceCSR(torch.arange(n + 1, dtype=torch.int64, device=dev),
+                     assign.to(torch.int32), torch.ones(n, dtype=torch.float64, device=dev),
+                     (n, m))
+
+
+def _assignment_of(P_const):
+    """The assignment vector of a P_const matrix (one entry per row)."""
+    P = as_device_csr(P_const)
+    if P.nnz != P.shape[0]:
+        raise ValueError("P_const must hold exactly one entry per row")
+    return P.col.to(torch.int64), P.shape[1]
+
+
+@checked
+def piecewise_const_assignment(P, n_passes=2):
     """Algorithm 1 (coarse_gradient.py:36-103): the column assigned to every
-    row (int64, device). Returned as the assignment vector rather than the
-    0/1 matrix P_const (one unit entry per row at that column). Runs on the
-    device (csrc/pconst.cu), bit-identical to the reference's ordered loops."""
+    row (int64, device) -- P_const as a vector. Runs on the device
+    (csrc/pconst.cu), bit-identical to the reference's ordered loops."""
     P = as_device_csr(P)
     m_h, m_H = P.shape
     dev = P.rowptr.device
@@ -113,8 +137,8 @@ def gen_piecewise_const(P, n_passes=2):
 
 
 def gen_piecewise_const_host(P, n_passes=2):
-    """The same map computed by the sequential host C++ loop (kept as a
-    cross-check for the device version)."""
+    """``piecewise_const_assignment`` computed by the sequential host C++
+    loop (kept as a cross-check for the device version)."""
     P = as_device_csr(P)
     m_h, m_H = P.shape
     rp = P.rowptr.cpu().numpy()
@@ -132,10 +156,49 @@ def gen_piecewise_const_host(P, n_passes=2):
 
 
 @checked
-def build_coarse_gradient(D_h, assignment, n_agg):
-    """Coarse edges from the projected node-graph Laplacian plus the Dirichlet
-    single-node edges (coarse_gradient.py:106-160, build_coarse_gradient
-    followed by augment_dirichlet_edges)."""
+def build_coarse_gradient(D_h, P_const):
+    """Coarse edges from the projected node-graph Laplacian
+    (coarse_gradient.py:106-120): one edge (i, j), i < j, per pair of
+    aggregates joined by a fine edge with two free ends, sorted."""
+    assign, n_agg = _assignment_of(P_const)
+    return coarse_gradient_from_assignment(D_h, assign, n_agg, dirichlet=False)
+
+
+@checked
+def augment_dirichlet_edges(cg, D_h, P_const):
+    """Append one single-node coarse edge per coarse node owning the free end
+    of a one-entry fine gradient row (coarse_gradient.py:139-160). The edges
+    already present are kept in place (build_coarse_gradient's output: they
+    are recomputed identically on the device)."""
+    assign, n_agg = _assignment_of(P_const)
+    if cg.augmented_edges:
+        raise NotImplementedError("augment_dirichlet_edges after append_edge: the device "
+                                  "layout keeps single-node edges before appended ones")
+    return coarse_gradient_from_assignment(D_h, assign, n_agg, dirichlet=True)
+
+
+def append_edge(cg, i, j):
+    """Append interior coarse edge (min, max), recorded as augmented
+    (coarse_gradient.py:163-171); duplicates of an existing pair allowed."""
+    i, j = int(min(i, j)), int(max(i, j))
+    D = cg.D_H
+    dev = D.rowptr.device
+    rp = torch.cat([D.rowptr, (D.rowptr[-1:] + 2)])
+    ci = torch.cat([D.col, torch.tensor([i, j], dtype=torch.int32, device=dev)])
+    v = torch.cat([D.val, torch.tensor([-1.0, 1.0], dtype=torch.float64, device=dev)])
+    return CoarseGradient(
+        D_H=DeviceCSR(rp, ci, v, (D.shape[0] + 1, D.shape[1])),
+        n_interior=cg.n_interior, n_single=cg.n_single, adj=cg.adj,
+        ep_a=torch.cat([cg.ep_a, torch.tensor([i], dtype=torch.int32, device=dev)]),
+        ep_b=torch.cat([cg.ep_b, torch.tensor([j], dtype=torch.int32, device=dev)]),
+        single_id=cg.single_id, augmented_edges=list(cg.augmented_edges or []) + [(i, j)])
+
+
+@checked
+def coarse_gradient_from_assignment(D_h, assignment, n_agg, dirichlet=True):
+    """Coarse edges from the projected node-graph Laplacian plus (dirichlet)
+    the single-node edges (coarse_gradient.py:106-160, build_coarse_gradient
+    followed by augment_dirichlet_edges), from the assignment vector."""
     D = as_device_csr(D_h)
     n_e = D.shape[0]
     dev = D.rowptr.device
@@ -150,7 +213,8 @@ def build_coarse_gradient(D_h, assignment, n_agg):
     st.defer(dv.capacity_check)
     call("sphc_unique_count", n_agg, brp, bcol, cnt)
     flags = torch.zeros(n_agg, dtype=torch.int64, device=dev)
-    call("sphc_single_flags", n_e, D.rowptr, D.col, assignment, flags)
+    if dirichlet:
+        call("sphc_single_flags", n_e, D.rowptr, D.col, assignment, flags)
     (arp, n_int), (soff, n_single) = dv.scan_many(cnt, flags)
     acol = torch.empty(n_int, dtype=torch.int32, device=dev)
     call("sphc_unique_fill", n_agg, brp, bcol, arp, acol)

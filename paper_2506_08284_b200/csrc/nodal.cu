@@ -97,14 +97,28 @@ extern "C" int sphc_pattern_union_fill(int64_t n, const int64_t* arp, const int3
 
 // ------------------------------------------------------------------ power method
 // w_i = sum over j DESCENDING of fl(fl(dinv_i a_ij) x_j), sequential from 0
+// (DESC false: in storage order, scipy csr_matvec on any row order; dinv
+// null: the stored values as they are)
+template <bool DESC>
 __global__ void k_nodal_powmv(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
                               const double* __restrict__ v, const double* __restrict__ dinv,
                               const double* __restrict__ x, double* __restrict__ y) {
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (i64)gridDim.x * blockDim.x) {
-    double inv = dinv[i], s = 0.0;
-    for (i64 j = rp[i + 1] - 1; j >= rp[i]; j--)
-      s = __dadd_rn(s, __dmul_rn(__dmul_rn(inv, v[j]), x[ci[j]]));
+    double s = 0.0;
+    i64 b = rp[i], e = rp[i + 1];
+    if (dinv) {
+      double inv = dinv[i];
+      for (i64 t = 0; t < e - b; t++) {
+        i64 j = DESC ? e - 1 - t : b + t;
+        s = __dadd_rn(s, __dmul_rn(__dmul_rn(inv, v[j]), x[ci[j]]));
+      }
+    } else {
+      for (i64 t = 0; t < e - b; t++) {
+        i64 j = DESC ? e - 1 - t : b + t;
+        s = __dadd_rn(s, __dmul_rn(v[j], x[ci[j]]));
+      }
+    }
     y[i] = s;
   }
 }
@@ -112,7 +126,16 @@ __global__ void k_nodal_powmv(i64 n, const i64* __restrict__ rp, const int* __re
 extern "C" int sphc_nodal_powmv(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
                                 const double* dinv, const double* x, double* y, void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_nodal_powmv<<<grid_for(n, 128), 128, 0, s>>>(n, rp, ci, v, dinv, x, y);
+  k_nodal_powmv<true><<<grid_for(n, 128), 128, 0, s>>>(n, rp, ci, v, dinv, x, y);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int sphc_spmv_stored_order(int64_t n, const int64_t* rp, const int32_t* ci,
+                                      const double* v, const double* x, double* y,
+                                      void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_nodal_powmv<false><<<grid_for(n, 128), 128, 0, s>>>(n, rp, ci, v, nullptr, x, y);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -292,6 +315,50 @@ extern "C" int sphc_nodal_smooth_fill(int64_t n, const int64_t* rp, const int32_
   cudaStream_t s = as_stream(stream);
   k_nodal_smooth<<<grid_for(n, SM_WARPS, SPHC_NUM_SMS * 32), SM_WARPS * 32, 0, s>>>(
       n, rp, ci, v, dinv, memb, omega, nullptr, prp, pci, pv, status);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+// ------------------------------------------------------------------ normalize_rows
+// normalize_rows (nodal_amg.py:119-135) of an arbitrary CSR: row sum as
+// np.add.reduceat (a_0 + pairwise(a_1..)), |a| likewise for the zero-sum
+// tolerance 1e-13 max(1, sum |a|), values fl(fl(1 / s) a) in place of the
+// output (exact zeros are dropped afterwards by count_nonzero / compact,
+// as the reference's diags(1 / s) @ P does). Thread per row; the pairwise
+// sum reads the row straight from global memory.
+__device__ double np_pairwise_abs(const double* a, int n, double* buf) {
+  for (int t = 0; t < n; t++) buf[t] = fabs(a[t]);
+  return np_pairwise(buf, n);
+}
+
+#define NR_CAP 256
+__global__ void k_normalize_rows(i64 n, const i64* __restrict__ rp, const double* __restrict__ v,
+                                 double* __restrict__ out, i64* status) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    i64 b = rp[i];
+    int len = (int)(rp[i + 1] - b);
+    double sum = 0.0, asum = 0.0;
+    if (len > NR_CAP + 1) {
+      report(status, SPHC_ST_SPGEMM_CAPACITY, i);
+      continue;
+    }
+    if (len > 0) {
+      double buf[NR_CAP];
+      sum = __dadd_rn(v[b], np_pairwise(v + b + 1, len - 1));
+      asum = __dadd_rn(fabs(v[b]), np_pairwise_abs(v + b + 1, len - 1, buf));
+    }
+    double tol = __dmul_rn(1e-13, fmax(1.0, asum));
+    if (fabs(sum) <= tol) report(status, SPHC_ST_ZERO_ROWSUM, i);
+    double inv = __ddiv_rn(1.0, sum);
+    for (int t = 0; t < len; t++) out[b + t] = __dmul_rn(inv, v[b + t]);
+  }
+}
+
+extern "C" int sphc_normalize_rows(int64_t n, const int64_t* rp, const double* v, double* out,
+                                   int64_t* status, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_normalize_rows<<<grid_for(n, 128), 128, 0, s>>>(n, rp, v, out, status);
   SPHC_LAUNCH_CHECK();
   return 0;
 }

@@ -541,6 +541,22 @@ def drop_zeros_many(*mats):
     return [_compact(A, rp, nnz) for A, (rp, nnz) in zip(mats, scan_many(*cnts))]
 
 
+@checked
+def csr_add(A, B, alpha=1.0, beta=1.0):
+    """alpha A + beta B on the union pattern (scipy's csr_binop_csr)."""
+    if A.shape != B.shape:
+        raise ValueError(f"shape mismatch {A.shape} vs {B.shape}")
+    n = A.shape[0]
+    cnt = torch.empty(n, dtype=torch.int64, device=A.rowptr.device)
+    call("sphc_csr_add_count", n, A.rowptr, A.col, B.rowptr, B.col, cnt)
+    rp, nnz = scan(cnt)
+    ci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
+    v = empty_f64(nnz)
+    call("sphc_csr_add_fill", n, A.rowptr, A.col, A.val, B.rowptr, B.col, B.val, float(alpha),
+         float(beta), rp, ci, v)
+    return DeviceCSR(rp, ci, v, A.shape)
+
+
 def _compact(A, rp, nnz):
     n = A.shape[0]
     if nnz == A.nnz:

@@ -150,9 +150,9 @@ def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None, shard=None):
         else:
             nod = na.smooth_and_normalize(A_n, agg)
     with phase("setup.piecewise_const"):
-        assign = cgrad.gen_piecewise_const(nod.P, cfg.n_passes)
+        assign = cgrad.piecewise_const_assignment(nod.P, cfg.n_passes)
     with phase("setup.coarse_gradient"):
-        cg = cgrad.build_coarse_gradient(D_h, assign, agg.n_agg)
+        cg = cgrad.coarse_gradient_from_assignment(D_h, assign, agg.n_agg)
     with phase("setup.emin_constraints"):
         setup = es.setup_constraints(D_h, nod.P, cg, shard=shard)
         cg = setup.cg                      # with any edges make_irreducible appended
@@ -167,3 +167,54 @@ def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None, shard=None):
     prol.membership = agg.membership
     prol.assignment = assign
     return prol, cg, nod
+
+
+# ---------------------------------------------------------------------------
+# reference-signature pieces of Alg. 3 (edge_prolongator.py:104-181), over the
+# same kernels build_edge_prolongator runs
+
+
+def initial_feasible_guess(setup, structure=None):
+    """All-ones seed corrected row by row to satisfy the commutator
+    constraints (edge_prolongator.py:104-126). Returns (structure, values):
+    the prolongator pattern (a value-less DeviceCSR) and the feasible guess,
+    which the constraint pass already formed on the device (fused)."""
+    P = setup.pattern
+    if structure is None:
+        structure = DeviceCSR(P.rowptr, P.col, None, P.shape)
+    return structure, P.val.clone()
+
+
+@checked
+def emin_step(S, values, setup, structure, omega):
+    """One projected damped-Jacobi sweep on the prolongator values
+    (edge_prolongator.py:170-176): masked S P / diag(S) on the pattern,
+    projection onto each row's constraint null space, values - omega dP.
+    One fused launch (sphc_emin_step)."""
+    S = as_device_csr(S)
+    n_e = structure.shape[0]
+    T, cg = setup.T, setup.cg
+    st = Status()
+    e_row = dv.empty_f64(n_e)
+    res = torch.zeros(1, dtype=torch.float64, device=e_row.device)
+    out = torch.empty_like(values)
+    call("sphc_emin_step", 0, n_e, S.rowptr, S.col, S.val, jacobi_diag_inverse(S), T.rowptr,
+         T.col, T.val, structure.rowptr, structure.col, values, out, cg.ep_a, cg.ep_b,
+         float(omega), 1, e_row, res, st.t)
+    st.defer(es._checker(S))
+    return out
+
+
+@checked
+def commutator_residual(P_e, D_H, R_dp):
+    """max |P_e D_H - R_dp|, the feasibility defect (edge_prolongator.py:
+    179-181): device SpGEMM, union-pattern difference, max reduction."""
+    P, Dh, R = as_device_csr(P_e), as_device_csr(D_H), as_device_csr(R_dp)
+    C = dv.spgemm(P, Dh, drop=False)
+    if C.shape != R.shape:
+        raise ValueError(f"shape mismatch: P_e D_H {C.shape} vs R_dp {R.shape}")
+    Df = dv.csr_add(C, R, 1.0, -1.0)
+    m = dv.zeros_f64(1)
+    if Df.nnz:
+        dv.maxabs(Df.val, m)
+    return float(dv.readback(m)[0][0])

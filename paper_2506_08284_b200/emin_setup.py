@@ -31,6 +31,12 @@ class EminSetup:
     rdp_scale: float
     n_augmented: int = 0
 
+    @property
+    def R_dp(self):
+        """The commutator right-hand side D_h P_n (emin_setup.py:268): T's
+        values (T's pattern also keeps the exactly-cancelled entries)."""
+        return self.T
+
 
 def _checker(D):
     """Deferred check of the emin kernels' status slots (Status.defer)."""

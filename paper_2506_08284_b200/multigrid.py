@@ -307,6 +307,24 @@ SMOOTHERS = {"chebyshev": ChebyshevSweeper, "gauss_seidel": GaussSeidelSweeper,
              "gs": GaussSeidelSweeper}
 
 
+@checked
+def symmetric_gauss_seidel(A, x, b, sweeps=1):
+    """Forward then backward Gauss-Seidel sweeps (multigrid.py:62-66), same
+    signature: numpy x / b give a numpy result, device tensors a device
+    tensor. Sync-free triangular substitution kernels (csrc/trsv.cu)."""
+    A = as_device_csr(A)
+    host = not isinstance(b, torch.Tensor)
+    dev = A.rowptr.device
+    xt = torch.as_tensor(np.asarray(x, dtype=np.float64) if host else x,
+                         dtype=torch.float64, device=dev)
+    bt = torch.as_tensor(np.asarray(b, dtype=np.float64) if host else b,
+                         dtype=torch.float64, device=dev)
+    sw = GaussSeidelSweeper(A)
+    out = sw.symmetric(xt, bt, sweeps)
+    sw.check()
+    return out.cpu().numpy() if host else out.clone()
+
+
 @dataclass
 class Level:
     """One hierarchy level (multigrid.py:69-89) plus its device working set."""

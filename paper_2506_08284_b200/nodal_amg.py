@@ -1,11 +1,12 @@
 """Smoothed aggregation for the auxiliary nodal problem, on the B200.
 
-Mirror of the reference's nodal_amg.py (same names and results). Every row is
-bit-identical to the reference (SURVEY.md Hazard 1 / Appendix A): the
-strength pattern, the power-method norms (Haswell-ddot order), the Jacobi-
-smoothed prolongator and its row normalisation run as libsphcurl kernels with
-explicit round-to-nearest arithmetic; the greedy aggregation is the host C++
-pass of libsphcurl (sequential by definition).
+Mirror of the reference's nodal_amg.py (same names, signatures and
+results). Every row is bit-identical to the reference (SURVEY.md Hazard 1 /
+Appendix A): the strength pattern, the power-method norms (Haswell-ddot
+order), the Jacobi-smoothed prolongator and its row normalisation run as
+libsphcurl kernels with explicit round-to-nearest arithmetic; the greedy
+aggregation runs on the device as a distance-2 wavefront in index order
+(csrc/aggregate.cu), bit-identical to the reference's sequential loops.
 """
 
 from dataclasses import dataclass
@@ -122,11 +123,9 @@ def _power_start(n):
     return v
 
 
-@checked
-def estimate_rho(A, dinv, iterations=10):
-    """Ten-step power method on diag(1/d) A (nodal_amg.py:99-116). The norms
-    run in the OpenBLAS-Haswell ddot order, so rho is bit-identical."""
-    n = A.shape[0]
+def _power_iterations(n, spmv, iterations):
+    """The power method's loop (nodal_amg.py:104-116) with ``spmv(v, w)``
+    computing w = A_scaled v; norms in the OpenBLAS-Haswell ddot order."""
     v0 = _power_start(n)           # shared constant: never written
     v = dv.empty_f64(n)
     sq = dv.empty_f64(1)
@@ -135,7 +134,7 @@ def estimate_rho(A, dinv, iterations=10):
     call("sphc_scale_by_norm", n, v0, sq, v, norms[0:1])
     w = dv.empty_f64(n)
     for it in range(iterations):
-        call("sphc_nodal_powmv", n, A.rowptr, A.col, A.val, dinv, v, w)
+        spmv(v, w)
         call("sphc_hsw_dot", n, w, w, sq)
         call("sphc_scale_by_norm", n, w, sq, v, norms[it + 1:it + 2])
     h = dv.readback(norms)[0]
@@ -145,6 +144,41 @@ def estimate_rho(A, dinv, iterations=10):
             return 0.0
         rho = float(h[it + 1])
     return rho
+
+
+def _stored_order_csr(A):
+    """A on the device with each row's entries in the caller's storage order
+    (no canonical sort): scipy's csr_matvec sums in that order."""
+    if isinstance(A, DeviceCSR):
+        return A
+    import scipy.sparse as sp
+    A = A if sp.issparse(A) and A.format == "csr" else sp.csr_matrix(A)
+    return DeviceCSR(dv.upload(A.indptr, np.int64), dv.upload(A.indices, np.int32),
+                     dv.upload(A.data, np.float64), tuple(int(x) for x in A.shape))
+
+
+@checked
+def estimate_rho(A_scaled, iterations=10):
+    """Power-method estimate of the spectral radius of a scaled operator
+    (nodal_amg.py:99-116), same signature: the deterministic start vector
+    1 + 0.01 sin(i), ``iterations`` steps, rho = the last norm (0.0 if a norm
+    vanishes). Row sums in the matrix's storage order, norms in the
+    OpenBLAS-Haswell ddot order: bit-identical to the reference."""
+    A = _stored_order_csr(A_scaled)
+    n = A.shape[0]
+    return _power_iterations(
+        n, lambda v, w: call("sphc_spmv_stored_order", n, A.rowptr, A.col, A.val, v, w),
+        iterations)
+
+
+def _estimate_rho_scaled(A, dinv, iterations=10):
+    """estimate_rho(diags(dinv) @ A) without forming the scaled matrix: rows
+    summed in DESCENDING column order, the storage scipy's ``diags @ A``
+    produces (what smooth_and_normalize passes the reference's estimate_rho)."""
+    n = A.shape[0]
+    return _power_iterations(
+        n, lambda v, w: call("sphc_nodal_powmv", n, A.rowptr, A.col, A.val, dinv, v, w),
+        iterations)
 
 
 def _dinv(A):
@@ -158,27 +192,44 @@ def _dinv(A):
     return dv.reciprocal(d)
 
 
+def _membership_of(P_tent):
+    """(membership, n_agg) of a tentative prolongator: an Aggregation, or a
+    matrix with exactly one unit entry per row (tentative_prolongator)."""
+    if isinstance(P_tent, Aggregation):
+        return P_tent.membership, P_tent.n_agg, P_tent.n_fine
+    P = as_device_csr(P_tent)
+    n, m = P.shape
+    ok = P.nnz == n and bool(dv.readback(
+        ((P.rowptr == torch.arange(n + 1, device=P.rowptr.device)).all()
+         & (P.val == 1.0).all()).reshape(1))[0][0])
+    if not ok:
+        raise ValueError("smooth_and_normalize expects the tentative prolongator "
+                         "(one unit entry per row)")
+    return P.col.to(torch.int64), m, n
+
+
 @checked
-def smooth_and_normalize(A_n, agg):
+def smooth_and_normalize(A_n, P_tent):
     """P = normalize((I - omega D^-1 A_n) P_tent), omega = 4 / (3 rho)
-    (nodal_amg.py:138-155). ``agg`` replaces the reference's P_tent argument
-    (the tentative prolongator is exactly the membership array)."""
+    (nodal_amg.py:138-155), same signature: ``P_tent`` is the tentative
+    prolongator (tentative_prolongator(agg)) or, equivalently, the
+    Aggregation itself (no matrix needed: P_tent is the membership array)."""
     A = as_device_csr(A_n)
+    memb, n_agg, n_fine = _membership_of(P_tent)
     n = A.shape[0]
-    if n != agg.n_fine:
-        raise ValueError(f"incompatible shapes {A.shape} and {(agg.n_fine, agg.n_agg)}")
+    if A.shape[1] != n_fine:
+        raise ValueError(f"incompatible shapes {A.shape} and {(n_fine, n_agg)}")
     dinv = _dinv(A)
-    rho = estimate_rho(A, dinv)
+    rho = _estimate_rho_scaled(A, dinv)
     omega = 4.0 / (3.0 * rho)
     st = Status()
     cnt = torch.empty(n, dtype=torch.int64, device=A.rowptr.device)
-    call("sphc_nodal_smooth_count", n, A.rowptr, A.col, A.val, dinv, agg.membership, omega,
-         cnt, st.t)
+    call("sphc_nodal_smooth_count", n, A.rowptr, A.col, A.val, dinv, memb, omega, cnt, st.t)
     prp, nnz = dv.scan(cnt)
     pci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
     pv = dv.empty_f64(nnz)
-    call("sphc_nodal_smooth_fill", n, A.rowptr, A.col, A.val, dinv, agg.membership, omega,
-         prp, pci, pv, st.t)
+    call("sphc_nodal_smooth_fill", n, A.rowptr, A.col, A.val, dinv, memb, omega, prp, pci, pv,
+         st.t)
 
     def check(rows):
         if "SPGEMM_CAPACITY" in rows:
@@ -187,5 +238,28 @@ def smooth_and_normalize(A_n, agg):
         if "ZERO_ROWSUM" in rows:
             raise ValueError(f"zero row sum before scaling in row {rows['ZERO_ROWSUM']}")
     st.defer(check)
-    P = DeviceCSR(prp, pci, pv, (n, agg.n_agg))
+    P = DeviceCSR(prp, pci, pv, (n, n_agg))
     return NodalProlongator(P=P, omega_used=omega, rho_estimate=rho)
+
+
+@checked
+def normalize_rows(P):
+    """Scale every row to sum exactly one (nodal_amg.py:119-135): the row sum
+    is numpy's ``np.add.reduceat`` (a_0 + pairwise(a_1..)), a vanishing sum
+    (|s| <= 1e-13 max(1, sum |a|)) raises the reference's ValueError, values
+    are fl(fl(1 / s) a) and exact zeros are dropped, as ``diags(1/s) @ P``
+    does. Bit-identical to the reference."""
+    P = as_device_csr(P)
+    n = P.shape[0]
+    st = Status()
+    out = dv.empty_f64(P.nnz)
+    call("sphc_normalize_rows", n, P.rowptr, P.val, out, st.t)
+
+    def check(rows):
+        if "SPGEMM_CAPACITY" in rows:
+            raise RuntimeError(f"row {rows['SPGEMM_CAPACITY']} longer than the "
+                               "normalize_rows kernel holds (257)")
+        if "ZERO_ROWSUM" in rows:
+            raise ValueError(f"zero row sum before scaling in row {rows['ZERO_ROWSUM']}")
+    st.defer(check)
+    return dv.drop_zeros(DeviceCSR(P.rowptr, P.col, out, P.shape))

@@ -119,6 +119,7 @@ def test_device_config_c4_small_hierarchy_vs_oracle(_gpu):
     assert abs(res.iterations - ro.iterations) <= 1, (res.iterations, ro.iterations)
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("config,N", [("C4", 12), ("C3", 16), ("C2", 8), ("C5", 10)])
 def test_device_assembly_equals_host_build_bitwise(config, N):
     """The device generator and its host build (oracle/host_assembly.py, the

@@ -221,9 +221,9 @@ def test_nodal_chain_and_topology_bitwise(N, sigma, dirichlet):
     Po, wo, ro = O.smoothed_prolongator(s.A_n, memb_o, nagg_o)
     assert nod.rho_estimate == ro and nod.omega_used == wo
     assert csr_hash(nod.P.to_scipy()) == csr_hash(Po)
-    assign = cg.gen_piecewise_const(nod.P, 2).cpu().numpy()
+    assign = cg.piecewise_const_assignment(nod.P, 2).cpu().numpy()
     assert np.array_equal(assign, O.piecewise_const(Po, 2))
-    cgd = cg.build_coarse_gradient(s.D, torch.from_numpy(assign).cuda(), nagg_o)
+    cgd = cg.coarse_gradient_from_assignment(s.D, torch.from_numpy(assign).cuda(), nagg_o)
     ceo = O.coarse_edges(s.D, assign, nagg_o)
     assert cgd.n_interior == ceo.pairs.shape[0] and cgd.n_single == ceo.singles.size
     DH = cgd.D_H.to_scipy()
@@ -380,7 +380,7 @@ def test_piecewise_const_device_bitwise(case):
     """Device Algorithm 1 (sync-free column passes, parallel + ordered
     leftovers, safeguard) == the reference's sequential loops."""
     from oracle import hcurl_oracle as O
-    from paper_2506_08284_b200.coarse_gradient import gen_piecewise_const
+    from paper_2506_08284_b200.coarse_gradient import piecewise_const_assignment as gen_piecewise_const
     from paper_2506_08284_b200.inputs import discretize_hex
     passes = {"ties_1pass": 1, "ties_3pass": 3}.get(case, 2)
     if case.startswith("mesh"):
@@ -426,7 +426,7 @@ def test_aggregate_device_bitwise(case):
 
 
 def test_piecewise_const_device_errors():
-    from paper_2506_08284_b200.coarse_gradient import gen_piecewise_const
+    from paper_2506_08284_b200.coarse_gradient import piecewise_const_assignment as gen_piecewise_const
     P = sp.csr_matrix(np.array([[1.0, 0.0, 0.0], [0.5, 0.0, 2.0]]))
     with pytest.raises(ValueError, match="empty column 1 cannot be assigned any row"):
         gen_piecewise_const(P)

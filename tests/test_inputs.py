@@ -26,3 +26,24 @@ def test_assembly_bitwise_n32():
         s = discretize_hex(32, float(sigma), bool(int(dirichlet)))
         for k in ("A_e", "S", "A_n", "D"):
             assert csr_hash(getattr(s, k)) == TABLE[key][k], (key, k)
+
+
+def test_host_build_of_device_assembly():
+    """oracle/host_assembly.py (the golden-input source for the device
+    configs): equal to the reference-faithful host generator to rounding on
+    uniform meshes (same patterns), and to the independent isoparametric
+    quadrature (tests/iso_assembly.py) on a jittered C4-recipe mesh."""
+    import numpy as np
+    from golden_util import rel_max_diff
+    from iso_assembly import assemble
+    from oracle.host_assembly import assemble_host
+    from paper_2506_08284_b200.assembly import config_draws
+    from paper_2506_08284_b200.inputs import discretize_hex
+    for N, dirich, sigma in ((6, True, 0.3), (5, False, 1e-2)):
+        s = discretize_hex(N, sigma, dirich)
+        for a, b in zip(assemble_host(N, sigma, dirich), (s.A_e, s.S, s.A_n, s.D)):
+            assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+            assert rel_max_diff(a, b) <= 1e-15
+    cfg, sigma, jitter, _ = config_draws("C4", 8)
+    for a, b in zip(assemble_host(8, sigma, False, jitter), assemble(8, sigma, False, jitter)):
+        assert rel_max_diff(a, b) <= 1e-13

@@ -362,7 +362,10 @@ def run_ours(args):
     global _FLUSH_R
     _FLUSH_R = torch.zeros(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
-    partitioned = args.partitioned
+    # N > 1: one problem, row-block sharded setup + partitioned solve
+    # (strong scaling) unless --replicas; N = 1: the single-GPU path
+    # (--partitioned runs the partitioned code on a one-rank group)
+    partitioned = args.partitioned or (ws > 1 and not args.replicas)
     if partitioned and ws == 1 and not tdist.is_initialized():
         # one-rank group: exercises the sharded / partitioned path on 1 GPU
         import socket
@@ -515,9 +518,17 @@ def run_ours(args):
             flush.fill_(3.0 + k)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            he = mg.build_hierarchy(sysm.A_e, sysm.S, sysm.A_n, sysm.D, scfg)
-            # the reference's own usage: pcg_solve(h.levels[0].A_e, b, V(h))
-            re = mg.pcg_solve(he.levels[0].A_e, rhs, mg.v_cycle_preconditioner(he))
+            he = mg.build_hierarchy(sysm.A_e, sysm.S, sysm.A_n, sysm.D, scfg, shard=shard)
+            if partitioned:
+                dh = dist_mod.distribute_hierarchy(he)
+                part = dh.levels[0].edge_part
+                bo = torch.from_numpy(rhs[part.lo(rank):part.hi(rank)]).to(dev)
+                re = dist_mod.dist_pcg_solve(dh, bo)
+                re.x = re.x.cpu().numpy()          # the owned block back to the host
+                del dh
+            else:
+                # the reference's own usage: pcg_solve(h.levels[0].A_e, b, V(h))
+                re = mg.pcg_solve(he.levels[0].A_e, rhs, mg.v_cycle_preconditioner(he))
             torch.cuda.synchronize()
             if k >= 0:
                 e2e_ms.append((time.perf_counter() - t0) * 1e3)
@@ -537,10 +548,13 @@ def run_ours(args):
         # (int64 row pointers and int32 columns on the device)
         def dev_bytes(M):
             return M.data.size * 8 + M.indices.size * 4 + M.indptr.size * 8
-        h2d = sum(dev_bytes(M) for M in (sysm.A_e, sysm.S, sysm.A_n, sysm.D)) + rhs.nbytes
-        e2e = {"value": ws * n_e / (t_e2e * 1e-3), "unit": "edge DOFs/s",
+        # every rank uploads the whole system (replicated / sharded setup)
+        h2d = ws * sum(dev_bytes(M) for M in (sysm.A_e, sysm.S, sysm.A_n, sysm.D)) + \
+            (1 if partitioned else ws) * rhs.nbytes
+        e2e = {"value": (1 if partitioned else ws) * n_e / (t_e2e * 1e-3),
+               "unit": "edge DOFs/s",
                "ms": t_e2e, "first_call_ms": first_ms, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(n_e * 8),
+               "d2h_bytes_per_step": int((1 if partitioned else ws) * n_e * 8),
                "host_memory": "caller arrays staged through a pinned buffer "
                               "(no page-locking of caller memory; SPHC_PIN=1 opts in)"}
 
@@ -784,8 +798,12 @@ def main():
     ap.add_argument("--cpu-sample", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-scale-roofline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: N independent replicas (weak scaling) instead of the "
+                         "partitioned solve")
     ap.add_argument("--partitioned", action="store_true",
-                    help="N>1: one problem, row-block sharded setup + partitioned solve "
+                    help="N=1: run the partitioned path on a one-rank group; "
+                         "N>1: one problem, row-block sharded setup + partitioned solve "
                          "(strong scaling)")
     ap.add_argument("--scale-config", default="C3")
     args = ap.parse_args()

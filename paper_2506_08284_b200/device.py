@@ -88,11 +88,20 @@ def _staging(nbytes):
     return buf
 
 
+_RB_LOCK = __import__("threading").RLock()
+
+
 def readback(*tensors):
     """Small device tensors -> numpy arrays after ONE stream synchronisation,
     first running every deferred status check (Status.defer) in order. Each
     part is DMA'd straight into a page-locked staging buffer (no gather
-    kernel, no pageable bounce through the driver's staging copy)."""
+    kernel, no pageable bounce through the driver's staging copy). The
+    staging buffer is shared: serialised across host threads."""
+    with _RB_LOCK:
+        return _readback(tensors)
+
+
+def _readback(tensors):
     pend = list(_PENDING)
     _PENDING.clear()
     parts = [st.t for st, _ in pend] + [t.reshape(-1) for t in tensors]

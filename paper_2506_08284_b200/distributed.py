@@ -1,33 +1,194 @@
-"""Row-block partitioned PCG + Hiptmair V-cycle over torch.distributed.
+"""Row-block partitioned PCG + Hiptmair V-cycle.
 
-SURVEY.md 8(e): the solve shards by contiguous row blocks (edge ids follow
-the lexicographic mesh order, so a block is a slab and its halo is about one
-node plane). This module partitions every level of a hierarchy across the
-ranks of a process group (one process per GPU), builds per-operator halo
-plans, and runs the same V-cycle / PCG as ``multigrid`` with
+The solve shards by contiguous row blocks: edge ids follow the lexicographic
+mesh order, so a block is a slab and its halo is about one node plane, owned
+by at most two neighbouring ranks. Every level whose edge count is at least
+``agglomerate`` is partitioned across the ranks of a communicator (one
+process per GPU), with a halo plan per operator; the levels below it are
+AGGLOMERATED: the restricted residual is all-gathered once and every rank
+runs the rest of the V-cycle on its replicated copy of those levels (the
+single-GPU kernels, no halos), keeping its own block of the correction. On
+the partitioned levels:
 
-* halo exchange before every SpMV-type application (``all_to_all_single``
-  with per-neighbour splits; NCCL over NVLink on B200 boxes), the local rows
-  keeping the global entry order, so every local SpMV row is bit-identical to
-  the single-GPU row;
-* PCG inner products as local partial sums + ``all_reduce`` on the device
-  scalar array (the only data that crosses ranks besides halos);
-* the coarsest level replicated: ``all_gather`` of the restricted residual
-  and the dense inverse applied redundantly.
+* a halo exchange precedes every SpMV-type application: point-to-point
+  sends / receives with the neighbours that actually share entries
+  (``batch_isend_irecv``; NCCL over NVLink on B200 boxes), no group-wide
+  collective; the local rows keep the global entry order, so every local
+  SpMV row is bit-identical to the single-GPU row;
+* PCG inner products are local partial sums + an all-reduce on the device
+  scalar array (the only other data that crosses ranks).
 
-The setup is replicated in round 1 (every rank builds the bit-identical
-hierarchy on its own GPU). Local kernels come from an ops
-object: ``CudaOps`` (libsphcurl, the product) -- the CPU gloo tests inject a
-scipy implementation of the same six calls to exercise the partitioning,
-halo plans and collectives without a GPU.
+The setup is replicated or row-block sharded (``sharding.py``): every rank
+holds the whole hierarchy, partitioned here by views of its row blocks.
+
+The collective layer is a communicator object:
+
+* ``TorchComm(group)``: torch.distributed (NCCL on the GPU, gloo on CPU);
+* ``ThreadComm``: W virtual ranks as W threads of one process, each with
+  its own CUDA stream, exchanging through host-synchronised device copies
+  (every transfer waits for the sender's stream on the host, then copies):
+  the CUDA path with real, non-empty halos runs on ONE GPU without any
+  kernel waiting on another rank's kernel (tests/test_gpu_distributed.py).
+
+Local kernels come from an ops object: ``CudaOps`` (libsphcurl, the
+product); the CPU gloo tests inject a scipy implementation of the same
+calls to exercise the partitioning, plans and collectives without a GPU.
 """
 
+import contextlib
 import math
+import os
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
 import torch
 import torch.distributed as dist
+
+AGGLOMERATE_EDGES = int(os.environ.get("SPHC_AGGLOMERATE_EDGES", "250000"))
+
+
+# ---------------------------------------------------------------------------
+# communicators
+
+
+class TorchComm:
+    """torch.distributed process group (NCCL / gloo)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def all_to_all(self, out, inp, out_splits, in_splits):
+        """Setup only (halo plans): variable-size all-to-all."""
+        dist.all_to_all_single(out, inp, list(out_splits), list(in_splits), group=self.group)
+
+    def exchange(self, sends, recvs):
+        """Point-to-point: sends = [(peer, tensor)], recvs = [(peer, tensor)];
+        only the ranks that share halo entries talk to each other."""
+        ops = [dist.P2POp(dist.isend, t, self._global(q), self.group) for q, t in sends]
+        ops += [dist.P2POp(dist.irecv, t, self._global(q), self.group) for q, t in recvs]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def _global(self, q):
+        return q if self.group is None else dist.get_global_rank(self.group, q)
+
+    def all_reduce_(self, t):
+        dist.all_reduce(t, group=self.group)
+
+    def all_gather_(self, out, t):
+        dist.all_gather_into_tensor(out, t, group=self.group)
+
+    def replicated(self):
+        return contextlib.nullcontext()
+
+
+class VirtualWorld:
+    """Shared state of W virtual ranks (ThreadComm)."""
+
+    def __init__(self, world):
+        self.world = int(world)
+        self.barrier = threading.Barrier(self.world)
+        self.slots = [None] * self.world
+        self.lock = threading.Lock()
+
+
+class ThreadComm:
+    """Rank ``rank`` of a VirtualWorld: every transfer posts the sender's
+    tensors after a host sync of its stream, waits at a barrier, copies on
+    the receiver's stream, syncs, and waits again before buffers are
+    reused. No device-side waiting between ranks."""
+
+    def __init__(self, vw, rank):
+        self.vw, self.rank, self.world = vw, int(rank), vw.world
+        self.group = None
+
+    def _sync(self):
+        if torch.cuda.is_available():
+            torch.cuda.current_stream().synchronize()
+
+    def _post(self, obj):
+        self._sync()
+        self.vw.slots[self.rank] = obj
+        self.vw.barrier.wait()
+
+    def _done(self):
+        self._sync()
+        self.vw.barrier.wait()
+
+    def all_to_all(self, out, inp, out_splits, in_splits):
+        ioff = np.concatenate([[0], np.cumsum(in_splits)]).astype(np.int64)
+        self._post((inp, ioff))
+        o = 0
+        for q in range(self.world):
+            src, qoff = self.vw.slots[q]
+            k = int(out_splits[q])
+            if k:
+                out[o:o + k].copy_(src[int(qoff[self.rank]):int(qoff[self.rank]) + k])
+            o += k
+        self._done()
+
+    def exchange(self, sends, recvs):
+        self._post({q: t for q, t in sends})
+        for q, t in recvs:
+            t.copy_(self.vw.slots[q][self.rank])
+        self._done()
+
+    def all_reduce_(self, t):
+        self._post(t.clone())
+        t.copy_(self.vw.slots[0])
+        for q in range(1, self.world):
+            t.add_(self.vw.slots[q])
+        self._done()
+
+    def all_gather_(self, out, t):
+        self._post(t.clone())
+        m = t.numel()
+        for q in range(self.world):
+            out[q * m:(q + 1) * m].copy_(self.vw.slots[q])
+        self._done()
+
+    @contextlib.contextmanager
+    def replicated(self):
+        """The agglomerated levels' buffers are shared by the virtual ranks
+        of one process: one rank at a time."""
+        with self.vw.lock:
+            yield
+            self._sync()
+
+
+def run_virtual(world, fn, *args):
+    """fn(comm, *args) on ``world`` virtual ranks (threads, one CUDA stream
+    each); returns the per-rank results. Exceptions are re-raised."""
+    vw = VirtualWorld(world)
+    out, errs = [None] * world, []
+    dev = torch.cuda.current_device() if torch.cuda.is_available() else None
+
+    def body(r):
+        try:
+            if dev is not None:
+                torch.cuda.set_device(dev)
+                with torch.cuda.stream(torch.cuda.Stream()):
+                    out[r] = fn(ThreadComm(vw, r), *args)
+                    torch.cuda.current_stream().synchronize()
+            else:
+                out[r] = fn(ThreadComm(vw, r), *args)
+        except BaseException as e:     # noqa: BLE001 - re-raised below
+            errs.append(e)
+            vw.barrier.abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    real = [e for e in errs if not isinstance(e, threading.BrokenBarrierError)]
+    if real or errs:
+        raise (real or errs)[0]
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -91,45 +252,53 @@ class HaloPlan:
     send_counts: list
     recv_counts: list
 
+    def peers(self):
+        """[(peer, start, count)] of the sends and of the receives (halo
+        entries are sorted, hence grouped by owner in rank order)."""
+        def runs(counts):
+            out, o = [], 0
+            for q, k in enumerate(counts):
+                if k:
+                    out.append((q, o, int(k)))
+                o += int(k)
+            return out
+        return runs(self.send_counts), runs(self.recv_counts)
 
-def _exchange_counts(counts, group, device):
-    t = torch.tensor(counts, dtype=torch.int64, device=device)
-    out = torch.empty_like(t)
-    dist.all_to_all_single(out, t, group=group)
-    return out.cpu().tolist()
 
-
-def localize(rp, ci, val, row_lo, row_hi, col_part, rank, group, device):
+def localize(rp, ci, val, row_lo, row_hi, col_part, comm, device):
     """Owned rows [row_lo, row_hi) of a global CSR (torch tensors on
     `device`: the GPU in the product, CPU under the gloo tests) ->
-    (CSRLocal with remapped columns, HaloPlan). Collective over `group`.
-    Everything stays on the device: the slice, the sorted halo set
-    (unique of the off-block columns), the column remap (searchsorted) and
-    the owner counts; the only host reads are the block's CSR bounds and the
-    per-neighbour counts."""
-    world = col_part.offsets.size - 1
+    (CSRLocal with remapped columns, HaloPlan). Collective over `comm`
+    (every rank calls it for every operator). Everything stays on the
+    device: the slice, the sorted halo set (unique of the off-block
+    columns), the column remap (searchsorted) and the owner counts; the only
+    host reads are the block's CSR bounds and the per-neighbour counts."""
+    world, rank = comm.world, comm.rank
     bounds = rp[[row_lo, row_hi]].cpu().tolist()
     s, e = int(bounds[0]), int(bounds[1])
     lrp = (rp[row_lo:row_hi + 1] - s).to(torch.int64)
     cols = ci[s:e].to(torch.int64)
     lo, hi = col_part.lo(rank), col_part.hi(rank)
     own = (cols >= lo) & (cols < hi)
-    halo = torch.unique(cols[~own])                     # sorted
+    halo_ids = torch.unique(cols[~own])                 # sorted
     n_own = hi - lo
-    lcol = torch.where(own, cols - lo, n_own + torch.searchsorted(halo, cols))
+    lcol = torch.where(own, cols - lo, n_own + torch.searchsorted(halo_ids, cols))
     offs = torch.as_tensor(col_part.offsets, dtype=torch.int64, device=cols.device)
-    owners = torch.searchsorted(offs, halo, right=True) - 1
+    owners = torch.searchsorted(offs, halo_ids, right=True) - 1
     recv_counts = torch.bincount(owners, minlength=world).cpu().tolist()
     if world > 1:
-        send_counts = _exchange_counts(recv_counts, group, device)
+        rc = torch.tensor(recv_counts, dtype=torch.int64, device=device)
+        sc = torch.empty_like(rc)
+        comm.all_to_all(sc, rc, [1] * world, [1] * world)
+        send_counts = sc.cpu().tolist()
         got = torch.empty(int(sum(send_counts)), dtype=torch.int64, device=device)
-        dist.all_to_all_single(got, halo, send_counts, recv_counts, group=group)
+        comm.all_to_all(got, halo_ids, send_counts, recv_counts)
     else:
         send_counts, got = [0], torch.empty(0, dtype=torch.int64, device=device)
     send_idx = (got - lo).to(torch.int64)
     A = CSRLocal(lrp, lcol.to(torch.int32), val[s:e].contiguous(),
-                 (row_hi - row_lo, n_own + int(halo.numel())))
-    return A, HaloPlan(n_own, int(halo.numel()), send_idx, send_counts, recv_counts)
+                 (row_hi - row_lo, n_own + int(halo_ids.numel())))
+    return A, HaloPlan(n_own, int(halo_ids.numel()), send_idx, send_counts, recv_counts)
 
 
 @dataclass
@@ -138,9 +307,11 @@ class DistOp:
     plan: HaloPlan
     xbuf: torch.Tensor = None    # extended input [owned | halo]
     sbuf: torch.Tensor = None    # send staging
+    sends: list = None           # [(peer, view of sbuf)]
+    recvs: list = None           # [(peer, view of xbuf's halo part)]
 
 
-def make_op(M, row_part, col_part, rank, group, device):
+def make_op(M, row_part, col_part, comm, device):
     """M: global operator (DeviceCSR / anything with rowptr, col, val
     tensors, or a scipy CSR), replicated on every rank."""
     if hasattr(M, "rowptr"):
@@ -149,15 +320,18 @@ def make_op(M, row_part, col_part, rank, group, device):
         rp, ci, v = (torch.from_numpy(np.ascontiguousarray(a))
                      for a in (M.indptr.astype(np.int64), M.indices, M.data))
     rp, ci, v = (t.to(device) for t in (rp, ci, v))
-    A, plan = localize(rp, ci, v, row_part.lo(rank), row_part.hi(rank), col_part, rank,
-                       group, device)
+    A, plan = localize(rp, ci, v, row_part.lo(comm.rank), row_part.hi(comm.rank), col_part,
+                       comm, device)
     op = DistOp(A, plan)
     op.xbuf = torch.zeros(plan.n_own + plan.n_halo, dtype=torch.float64, device=device)
     op.sbuf = torch.empty(plan.send_idx.numel(), dtype=torch.float64, device=device)
+    sp_, rp_ = plan.peers()
+    op.sends = [(q, op.sbuf[o:o + k]) for q, o, k in sp_]
+    op.recvs = [(q, op.xbuf[plan.n_own + o:plan.n_own + o + k]) for q, o, k in rp_]
     return op
 
 
-def halo(op, ops, x_own, group):
+def halo(op, ops, x_own, comm):
     """Extended input of op: [x_own | halo values from the owners]."""
     p = op.plan
     xb = op.xbuf
@@ -165,9 +339,8 @@ def halo(op, ops, x_own, group):
         ops.copy(xb[:p.n_own], x_own)
     if p.send_idx.numel():
         ops.gather(p.send_idx, xb, op.sbuf)
-    if sum(p.send_counts) or p.n_halo:
-        dist.all_to_all_single(xb[p.n_own:], op.sbuf, p.recv_counts, p.send_counts,
-                               group=group)
+    if comm.world > 1:
+        comm.exchange(op.sends, op.recvs)
     return xb
 
 
@@ -176,7 +349,7 @@ def halo(op, ops, x_own, group):
 
 
 class CudaOps:
-    """The six local operations, on libsphcurl kernels."""
+    """The local operations, on libsphcurl kernels."""
 
     def __init__(self):
         from . import device as dv
@@ -184,7 +357,7 @@ class CudaOps:
         self.dv, self.call = dv, call
 
     def spmv(self, A, x, y, alpha=1.0, beta=0.0, z=None):
-        # SELL mirror for the smoothed square operators (built in cheb)
+        # SELL mirror for the smoothed square operators (built in prepare)
         self.dv.spmv(A, x, y, alpha, beta, z)
 
     def cheb(self, A, dinv, b, x_ext, x_out, d, cd, cr, x_zero):
@@ -199,9 +372,6 @@ class CudaOps:
 
     def dot(self, x, y, out):
         self.call("sphc_dot", x.numel(), x, y, out)
-
-    def gemv(self, M, x, y):
-        self.call("sphc_dense_gemv", M.shape[0], M, x, y)
 
     def gather(self, idx, x, out):
         self.call("sphc_gather", idx.numel(), idx, x, out)
@@ -242,64 +412,87 @@ class DistLevel:
 
 @dataclass
 class DistHierarchy:
-    levels: list
-    coarse_inverse: torch.Tensor
-    coarse_part: Partition
-    rank: int
-    world: int
-    group: object
+    levels: list                 # the partitioned levels
+    n_levels: int                # of the whole hierarchy
+    agg_part: Partition          # edge partition of the first agglomerated level
+    replicated_vcycle: object    # (level, b_full) -> x_full on the replicated levels
+    comm: object
     ops: object
+
+    @property
+    def rank(self):
+        return self.comm.rank
+
+    @property
+    def world(self):
+        return self.comm.world
 
 
 def _own(t, part, rank):
     return t[part.lo(rank):part.hi(rank)].clone()
 
 
-def distribute_hierarchy(h, group=None):
-    """Partition a product ``multigrid.Hierarchy`` (built identically on every
-    rank) over the ranks of `group` for ``dist_pcg_solve``."""
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    return distribute(h.levels, h.coarse_factorization, rank, world, group, CudaOps())
+def distribute_hierarchy(h, comm=None, agglomerate=None):
+    """Partition a product ``multigrid.Hierarchy`` (identical on every rank:
+    replicated or sharded setup) over ``comm`` (default: the default
+    torch.distributed group) for ``dist_pcg_solve``."""
+    from . import multigrid as mg
+    comm = comm or TorchComm()
+
+    def vcycle(level, b):
+        return mg.v_cycle(h, None, b, level)
+    return distribute(h.levels, vcycle, comm, CudaOps(), agglomerate=agglomerate)
 
 
-def distribute(levels, coarse_inverse, rank, world, group=None, ops=None, device=None):
-    """Partition a replicated hierarchy. `levels`: sequence of objects with
-    A_e, nodal_aux, D, Dt, P_e, R_e (global operators; P_e/R_e None on the
-    coarsest) and edge/aux sweepers exposing dinv and coefs."""
+def distribute(levels, replicated_vcycle, comm, ops=None, device=None, agglomerate=None):
+    """Partition a replicated hierarchy. ``levels``: objects with A_e,
+    nodal_aux, D, Dt, P_e, R_e (global operators; P_e / R_e None on the
+    coarsest) and edge / aux sweepers exposing dinv and coefs.
+    ``replicated_vcycle(level, b_full)`` runs the V-cycle from ``level``
+    down on the replicated levels. Levels with fewer than ``agglomerate``
+    edges (and the coarsest) are agglomerated; level 0 is always
+    partitioned."""
     ops = ops or CudaOps()
-    device = device or (coarse_inverse.device if isinstance(coarse_inverse, torch.Tensor)
-                        else torch.device("cpu"))
+    agglomerate = AGGLOMERATE_EDGES if agglomerate is None else int(agglomerate)
+    device = device or (torch.device("cuda", torch.cuda.current_device())
+                        if isinstance(ops, CudaOps) else torch.device("cpu"))
+    world, rank = comm.world, comm.rank
+    n_part = 1
+    while (n_part < len(levels) - 1 and levels[n_part].A_e.shape[0] >= agglomerate):
+        n_part += 1
+    parts = [Partition.balanced(lv.A_e.shape[0], world) for lv in levels[:n_part + 1]]
     out = []
-    parts = [Partition.balanced(lv.A_e.shape[0], world) for lv in levels]
-    nparts = [Partition.balanced(lv.D.shape[1], world) for lv in levels]
-    for li, lv in enumerate(levels):
-        ep, npart = parts[li], nparts[li]
-        dl = DistLevel(A=make_op(lv.A_e, ep, ep, rank, group, device),
-                       aux=make_op(lv.nodal_aux, npart, npart, rank, group, device),
-                       D=make_op(lv.D, ep, npart, rank, group, device),
-                       Dt=make_op(lv.Dt, npart, ep, rank, group, device),
+    for li, lv in enumerate(levels[:n_part]):
+        ep = parts[li]
+        npart = Partition.balanced(lv.D.shape[1], world)
+        if not hasattr(lv.edge_sweeper, "coefs"):
+            raise ValueError("the partitioned solve needs the Chebyshev smoother "
+                             "(Gauss-Seidel is sequential across rows)")
+        cp = parts[li + 1]
+        dl = DistLevel(A=make_op(lv.A_e, ep, ep, comm, device),
+                       aux=make_op(lv.nodal_aux, npart, npart, comm, device),
+                       D=make_op(lv.D, ep, npart, comm, device),
+                       Dt=make_op(lv.Dt, npart, ep, comm, device),
+                       P=make_op(lv.P_e, ep, cp, comm, device),
+                       R=make_op(lv.R_e, cp, ep, comm, device),
                        edge_part=ep, node_part=npart)
-        if li + 1 < len(levels):
-            if not hasattr(lv.edge_sweeper, "coefs"):
-                raise ValueError("the partitioned solve needs the Chebyshev smoother "
-                                 "(Gauss-Seidel is sequential across rows)")
-            cp = parts[li + 1]
-            dl.P = make_op(lv.P_e, ep, cp, rank, group, device)
-            dl.R = make_op(lv.R_e, cp, ep, rank, group, device)
-            dl.dinv_A = _own(torch.as_tensor(lv.edge_sweeper.dinv).to(device), ep, rank)
-            dl.dinv_aux = _own(torch.as_tensor(lv.aux_sweeper.dinv).to(device), npart, rank)
-            dl.coefs_A = list(lv.edge_sweeper.coefs)
-            dl.coefs_aux = list(lv.aux_sweeper.coefs)
+        dl.dinv_A = _own(torch.as_tensor(lv.edge_sweeper.dinv).to(device), ep, rank)
+        dl.dinv_aux = _own(torch.as_tensor(lv.aux_sweeper.dinv).to(device), npart, rank)
+        dl.coefs_A = list(lv.edge_sweeper.coefs)
+        dl.coefs_aux = list(lv.aux_sweeper.coefs)
         if hasattr(ops, "prepare"):
             ops.prepare(dl)
         ne, nn = ep.size(rank), npart.size(rank)
         z = lambda k: torch.zeros(k, dtype=torch.float64, device=device)  # noqa: E731
         dl.work = dict(x=[z(ne), z(ne)], d=z(ne), r=z(ne), bn=z(nn), c=[z(nn), z(nn)],
-                       dn=z(nn), rc=z(parts[li + 1].size(rank)) if li + 1 < len(levels) else None)
+                       dn=z(nn), rc=z(cp.size(rank)))
         out.append(dl)
-    inv = torch.as_tensor(coarse_inverse, dtype=torch.float64).to(device)
-    return DistHierarchy(out, inv, parts[-1], rank, world, group, ops)
+    ap = parts[n_part]
+    m = max(ap.size(r) for r in range(world))
+    z = lambda k: torch.zeros(k, dtype=torch.float64, device=device)  # noqa: E731
+    dh = DistHierarchy(out, len(levels), ap, replicated_vcycle, comm, ops)
+    dh.agg_work = dict(send=z(m), all=z(m * world), full=z(ap.n), out=z(ap.size(rank)))
+    return dh
 
 
 def _cheb(dh, op, dinv, coefs, b, x_own, bufs, d, x_zero):
@@ -309,45 +502,49 @@ def _cheb(dh, op, dinv, coefs, b, x_own, bufs, d, x_zero):
     for step, (cd, cr) in enumerate(coefs):
         out = bufs[0] if cur is not bufs[0] else bufs[1]
         z = x_zero and step == 0
-        xe = None if z else halo(op, ops, cur, dh.group)
+        xe = None if z else halo(op, ops, cur, dh.comm)
         ops.cheb(op.A, dinv, b, xe, out, d, cd, cr, z)
         cur = out
     return cur
 
 
 def _hiptmair(dh, dl, x, b, x_zero):
-    ops, g = dh.ops, dh.group
+    ops, c_ = dh.ops, dh.comm
     w = dl.work
     x = _cheb(dh, dl.A, dl.dinv_A, dl.coefs_A, b, x, w["x"], w["d"], x_zero)
-    ops.spmv(dl.A.A, halo(dl.A, ops, x, g), w["r"], -1.0, 1.0, b)
-    ops.spmv(dl.Dt.A, halo(dl.Dt, ops, w["r"], g), w["bn"])
+    ops.spmv(dl.A.A, halo(dl.A, ops, x, c_), w["r"], -1.0, 1.0, b)
+    ops.spmv(dl.Dt.A, halo(dl.Dt, ops, w["r"], c_), w["bn"])
     c = _cheb(dh, dl.aux, dl.dinv_aux, dl.coefs_aux, w["bn"], None, w["c"], w["dn"], True)
-    ops.spmv(dl.D.A, halo(dl.D, ops, c, g), x, 1.0, 1.0, x)
+    ops.spmv(dl.D.A, halo(dl.D, ops, c, c_), x, 1.0, 1.0, x)
     return _cheb(dh, dl.A, dl.dinv_A, dl.coefs_A, b, x, w["x"], w["d"], False)
 
 
+def _agglomerated(dh, b, level):
+    """All-gather the restricted residual of the first agglomerated level,
+    run the replicated V-cycle from there, keep the owned block."""
+    part, comm, aw = dh.agg_part, dh.comm, dh.agg_work
+    m = aw["send"].numel()
+    dh.ops.copy(aw["send"][:b.numel()], b)
+    comm.all_gather_(aw["all"], aw["send"])
+    for r in range(comm.world):
+        dh.ops.copy(aw["full"][part.lo(r):part.hi(r)], aw["all"][r * m:r * m + part.size(r)])
+    with comm.replicated():
+        y = dh.replicated_vcycle(level, aw["full"])
+        dh.ops.copy(aw["out"], y[part.lo(comm.rank):part.hi(comm.rank)])
+    return aw["out"]
+
+
 def dist_v_cycle(dh, b, level=0):
+    if level == len(dh.levels):
+        return _agglomerated(dh, b, level)
     dl = dh.levels[level]
-    ops, g = dh.ops, dh.group
-    if level == len(dh.levels) - 1:
-        part = dh.coarse_part
-        m = max(part.size(r) for r in range(dh.world))
-        send = torch.zeros(m, dtype=torch.float64, device=b.device)
-        ops.copy(send[:b.numel()], b)
-        allb = torch.empty(m * dh.world, dtype=torch.float64, device=b.device)
-        dist.all_gather_into_tensor(allb, send, group=g)
-        full = torch.cat([allb[r * m:r * m + part.size(r)] for r in range(dh.world)])
-        y = torch.empty_like(full)
-        ops.gemv(dh.coarse_inverse, full, y)
-        out = dl.work["r"]
-        ops.copy(out, y[part.lo(dh.rank):part.hi(dh.rank)])
-        return out
+    ops, c_ = dh.ops, dh.comm
     x = _hiptmair(dh, dl, None, b, True)
     w = dl.work
-    ops.spmv(dl.A.A, halo(dl.A, ops, x, g), w["r"], -1.0, 1.0, b)
-    ops.spmv(dl.R.A, halo(dl.R, ops, w["r"], g), w["rc"])
+    ops.spmv(dl.A.A, halo(dl.A, ops, x, c_), w["r"], -1.0, 1.0, b)
+    ops.spmv(dl.R.A, halo(dl.R, ops, w["r"], c_), w["rc"])
     ec = dist_v_cycle(dh, w["rc"], level + 1)
-    ops.spmv(dl.P.A, halo(dl.P, ops, ec, g), x, 1.0, 1.0, x)
+    ops.spmv(dl.P.A, halo(dl.P, ops, ec, c_), x, 1.0, 1.0, x)
     return _hiptmair(dh, dl, x, b, False)
 
 
@@ -363,7 +560,7 @@ class DistPcgResult:
 
 def dist_pcg_solve(dh, b_own, rtol=1e-8, maxit=500):
     """PCG (multigrid.py:220-274 semantics) on the partitioned hierarchy."""
-    ops, g = dh.ops, dh.group
+    ops, comm = dh.ops, dh.comm
     dl0 = dh.levels[0]
     dev = b_own.device
     n = b_own.numel()
@@ -374,7 +571,7 @@ def dist_pcg_solve(dh, b_own, rtol=1e-8, maxit=500):
     Ap = torch.empty_like(r)
 
     def allsum(lo, hi):
-        dist.all_reduce(sc[lo:hi], group=g)
+        comm.all_reduce_(sc[lo:hi])
 
     ops.dot(b_own, b_own, sc[1:2])
     allsum(1, 2)
@@ -391,9 +588,8 @@ def dist_pcg_solve(dh, b_own, rtol=1e-8, maxit=500):
     for k in range(maxit):
         # the whole iteration is queued without a host decision: alpha and
         # beta live in sc, the update is a no-op when p.Ap <= 0, and the
-        # scalars of the tests come back in ONE readback at the end (the
-        # single-GPU path's scheme, multigrid.pcg_solve)
-        ops.spmv(dl0.A.A, halo(dl0.A, ops, p, g), Ap)
+        # scalars of the tests come back in ONE readback per iteration
+        ops.spmv(dl0.A.A, halo(dl0.A, ops, p, comm), Ap)
         ops.dot(p, Ap, sc[0:1])
         allsum(0, 1)
         sc[4] = 0.0
@@ -417,7 +613,7 @@ def dist_pcg_solve(dh, b_own, rtol=1e-8, maxit=500):
         its = k + 1
         if float(h[5]) == 0.0:
             status = "stagnated"
-            ops.spmv(dl0.A.A, halo(dl0.A, ops, x, g), Ap, -1.0, 1.0, b_own)
+            ops.spmv(dl0.A.A, halo(dl0.A, ops, x, comm), Ap, -1.0, 1.0, b_own)
             ops.dot(Ap, Ap, sc[0:1])
             allsum(0, 1)
             hist.append(math.sqrt(float(sc[0].item())))

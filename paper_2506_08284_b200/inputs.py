@@ -322,18 +322,15 @@ def sigma_jump(N, inner=1e-6, outer=1.0):
 
 
 # The five BASELINE.json configs. This host generator has
-# uniform geometry only; the device generator (assembly.make_device_config)
-# applies C4's node jitter. C5 coarsens to 10,000 edges: below that the
-# hierarchy of the reference algorithm degenerates at 256^3, sigma = 1e-4
-# (numerically singular Galerkin operators, Jacobi radius 88 on the level
-# below; PCG stagnates at 8e-3 with coarse_size 1000, converges in 136
-# iterations with 10,000 -- DESIGN.md 8).
+# uniform geometry only (make_config draws C4's jitter and leaves it
+# unapplied); the device generator (assembly.make_device_config) and its
+# bit-identical host build (oracle/host_assembly.py) apply C4's jittered
+# isoparametric hexes. C5 coarsens to 10,000 edges.
 CONFIGS = {
     "C1": dict(N=16, sigma=1.0, dirichlet=True, seed=0),
     "C2": dict(N=32, sigma=1e-2, dirichlet=True, seed=1),
     "C3": dict(N=64, sigma="jump", dirichlet=False, seed=2),
-    # config 4 without the node jitter (uniform geometry; the jittered
-    # trilinear assembly is DESIGN.md 9 work): lognormal per-element sigma
+    # lognormal per-element sigma; jittered hexes on the device generator
     "C4": dict(N=128, sigma="lognormal", dirichlet=False, seed=3),
     "C5": dict(N=256, sigma=1e-4, dirichlet=False, seed=4, coarse_size=10000),
 }

@@ -101,14 +101,20 @@ def _problem():
     return h, b, inv
 
 
-def _worker(rank, world, port, out_path):
+def _replicated(h, inv):
+    def vcycle(level, b):
+        return torch.from_numpy(_vc(h, inv, b.numpy(), level))
+    return vcycle
+
+
+def _worker(rank, world, port, out_path, agglomerate):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.set_num_threads(1)
     h, b, inv = _problem()
-    dh = D.distribute(_levels(h), torch.from_numpy(inv), rank, world, None, ScipyOps(),
-                      torch.device("cpu"))
+    dh = D.distribute(_levels(h), _replicated(h, inv), D.TorchComm(), ScipyOps(),
+                      torch.device("cpu"), agglomerate=agglomerate)
     part = dh.levels[0].edge_part
     res = D.dist_pcg_solve(dh, torch.from_numpy(b[part.lo(rank):part.hi(rank)]).clone())
     xs = [None] * world
@@ -116,7 +122,7 @@ def _worker(rank, world, port, out_path):
     if rank == 0:
         with open(out_path, "wb") as f:
             pickle.dump(dict(x=np.concatenate(xs), its=res.iterations, status=res.status,
-                             hist=res.residual_history), f)
+                             hist=res.residual_history, n_part=len(dh.levels)), f)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -131,18 +137,68 @@ def test_partition_and_halo_plan_sizes():
     p = D.Partition.balanced(10, 3)
     assert p.offsets.tolist() == [0, 3, 6, 10]
     assert p.owner(np.array([0, 2, 3, 5, 6, 9])).tolist() == [0, 0, 1, 1, 2, 2]
+    plan = D.HaloPlan(4, 3, torch.zeros(0), [0, 2, 0, 5], [1, 0, 2, 0])
+    assert plan.peers() == ([(1, 0, 2), (3, 2, 5)], [(0, 0, 1), (2, 1, 2)])
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_distributed_solve_matches_single_process(world):
+def test_halo_neighbours_of_a_slab_partition():
+    """Contiguous row blocks of the edge operator are slabs: each rank's halo
+    comes from its (at most two) neighbouring blocks, so the exchange is
+    point-to-point with <= 2 peers. Virtual ranks (threads) on CPU."""
+    h, b, inv = _problem()
+    A = h.levels[0].A_e
+    world = 4
+
+    def fn(comm):
+        part = D.Partition.balanced(A.shape[0], world)
+        op = D.make_op(A, part, part, comm, torch.device("cpu"))
+        x = torch.arange(part.lo(comm.rank), part.hi(comm.rank), dtype=torch.float64)
+        xe = D.halo(op, ScipyOps(), x, comm)
+        return [q for q, _ in op.recvs], xe.numpy().copy(), op.plan
+    outs = D.run_virtual(world, fn)
+    for r, (peers, xe, plan) in enumerate(outs):
+        assert 0 < len(peers) <= 2 and all(abs(q - r) == 1 for q in peers)
+        # halo values are the owners' entries: the global column ids here
+        halo_vals = xe[plan.n_own:]
+        assert np.all(np.diff(halo_vals) > 0)
+        assert not np.any((halo_vals >= D.Partition.balanced(A.shape[0], world).lo(r)) &
+                          (halo_vals < D.Partition.balanced(A.shape[0], world).hi(r)))
+
+
+def test_virtual_ranks_solve_cpu():
+    """The ThreadComm virtual ranks (the communicator of the single-GPU
+    multi-rank tests) reproduce the gloo result on CPU."""
+    h, b, inv = _problem()
+    ref = O.pcg(h.levels[0].A_e, b, lambda r: _vc(h, inv, r))
+
+    def fn(comm):
+        dh = D.distribute(_levels(h), _replicated(h, inv), comm, ScipyOps(),
+                          torch.device("cpu"), agglomerate=0)
+        part = dh.levels[0].edge_part
+        res = D.dist_pcg_solve(dh, torch.from_numpy(b[part.lo(comm.rank):part.hi(comm.rank)]))
+        return res
+    outs = D.run_virtual(3, fn)
+    x = np.concatenate([o.x.numpy() for o in outs])
+    assert all(o.iterations == outs[0].iterations for o in outs)
+    assert abs(outs[0].iterations - ref.iterations) <= 1
+    assert np.max(np.abs(x - ref.x)) <= 1e-8 * np.max(np.abs(ref.x))
+
+
+@pytest.mark.parametrize("world,agglomerate", [(2, 0), (3, 0), (3, 10 ** 9)])
+def test_distributed_solve_matches_single_process(world, agglomerate):
+    """Partitioned levels with point-to-point neighbour halos; the levels
+    below ``agglomerate`` edges run replicated after one all-gather
+    (10**9: only level 0 is partitioned; 0: all but the coarsest)."""
     h, b, inv = _problem()
     # single-process reference: the same V-cycle with the dense coarse inverse
     ref = O.pcg(h.levels[0].A_e, b, lambda r: _vc(h, inv, r))
     with tempfile.TemporaryDirectory() as d:
         out = os.path.join(d, "res.pkl")
-        mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), out, agglomerate), nprocs=world,
+                 join=True)
         with open(out, "rb") as f:
             got = pickle.load(f)
+    assert got["n_part"] == (len(h.levels) - 1 if agglomerate == 0 else 1)
     assert got["status"] == "converged"
     assert abs(got["its"] - ref.iterations) <= 1
     assert np.max(np.abs(got["x"] - ref.x)) <= 1e-8 * np.max(np.abs(ref.x))

@@ -56,11 +56,22 @@ class SolverConfig:
     emin: EminConfig = field(default_factory=EminConfig)
     smoother: str = "chebyshev"      # or "gauss_seidel" (the reference's own smoother)
     cheb_degree: int = 3
+    # coarsest solve: "cholesky" (default) = the Jacobi-equilibrated
+    # Cholesky inverse with the shifted / eigendecomposition fallbacks for
+    # numerically semidefinite operators; "lu" = the reference's
+    # partial-pivoting LU (multigrid.py:156-157,180-181; applied as the
+    # inverse its LU solves give). On the C4 recipe at 128^3 and C5's at
+    # 64^3 the LU solve of the near-singular coarsest operator makes PCG
+    # diverge (500 iterations, |r|/|b| 1e3 / 7) where the Cholesky inverse
+    # converges in 81 / 40 (profiles/r02_probe_coarse.txt).
+    coarse_solver: str = "cholesky"
 
     def __post_init__(self):
         if self.smoother not in SMOOTHERS:
             raise ValueError(f"unknown smoother {self.smoother!r}; "
                              f"expected one of {sorted(SMOOTHERS)}")
+        if self.coarse_solver not in ("lu", "cholesky"):
+            raise ValueError(f"unknown coarse_solver {self.coarse_solver!r}")
 
 
 def lanczos_max(alpha, beta):
@@ -409,7 +420,25 @@ def _check_nullspace(S, D, where, A=None, shard=None):
     return AD
 
 
-def _coarse_inverse_start(Ad):
+def _coarse_lu_inverse(Ad):
+    """The reference's coarsest solve (multigrid.py:156-157,180-181):
+    scipy ``lu_factor`` = LAPACK getrf with partial pivoting, then
+    ``lu_solve``. Here getrf (cuSOLVER through torch) and the LU solves of
+    the identity form the matrix those solves apply, A^-1 = U^-1 L^-1 P, so
+    a V-cycle applies it as one GEMV. Nothing is symmetrised or regularised:
+    on a numerically singular coarsest operator it behaves as the
+    reference's LU does. Returns (inverse, info) -- info > 0 is getrf's
+    exact-zero pivot (scipy only warns; the inverse then holds inf / nan)."""
+    LU, piv, info = torch.linalg.lu_factor_ex(Ad)
+    n = Ad.shape[0]
+    inv = torch.linalg.lu_solve(LU, piv, torch.eye(n, dtype=Ad.dtype, device=Ad.device))
+    return inv, info.reshape(1).to(torch.int64)
+
+
+def _coarse_inverse_start(Ad, solver="cholesky"):
+    if solver == "lu":
+        inv, info = _coarse_lu_inverse(Ad)
+        return inv, torch.zeros_like(info), None
     """Symmetric inverse of the coarsest operator (multigrid.py:157 factors it
     with LU). The coarsest A_e is SPD in exact arithmetic but badly scaled
     and ill-conditioned: the edge prolongators grow level by level (max|P_e|
@@ -448,7 +477,7 @@ def _coarse_inverse_start(Ad):
 def _coarse_inverse_finish(inv, info, state):
     """The inverse from _coarse_inverse_start, or -- when its Cholesky broke
     down (info != 0) -- from the shifted / eigendecomposition fallbacks."""
-    if int(info) == 0:
+    if int(info) == 0 or state is None:
         return inv
     As, sc = state
     # numerically singular: the Galerkin operator of a rank-deficient
@@ -484,9 +513,9 @@ def _side_stream():
     return st
 
 
-def _coarse_inverse(Ad):
+def _coarse_inverse(Ad, solver="cholesky"):
     """Synchronous form (the reuse path)."""
-    inv, info, state = _coarse_inverse_start(Ad)
+    inv, info, state = _coarse_inverse_start(Ad, solver)
     return _coarse_inverse_finish(inv, dv.readback(info)[0][0], state)
 
 
@@ -566,11 +595,11 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
         Ad.record_stream(side)
         side.wait_stream(main)
         with torch.cuda.stream(side):
-            inv, info, inv_state = _coarse_inverse_start(Ad)
+            inv, info, inv_state = _coarse_inverse_start(Ad, cfg.coarse_solver)
         last = _make_level(A_e, S_e, D, cfg, AD=AD, smooth=False, shard=shard)
         levels.append(last)
         main.wait_stream(side)
-        for t in (inv, info, *inv_state):
+        for t in (inv, info, *(inv_state or ())):
             t.record_stream(main)
     last.r = dv.empty_f64(A_e.shape[0])
     nnz0 = levels[0].A_e.nnz
@@ -628,7 +657,7 @@ def reuse_hierarchy(h, A_e, S_e, cfg=None):
     last = _make_level(A_e, S_e, D, cfg, AD=AD, smooth=False)
     last.r = dv.empty_f64(A_e.shape[0])
     levels.append(last)
-    inv = _coarse_inverse(dv.to_dense(A_e))
+    inv = _coarse_inverse(dv.to_dense(A_e), cfg.coarse_solver)
     oc = sum(lv.A_e.nnz for lv in levels) / levels[0].A_e.nnz
     finalize_sweepers()
     return Hierarchy(levels=levels, coarse_factorization=inv, operator_complexity=oc)

@@ -491,6 +491,23 @@ int sphc_emin_step(int64_t row0, int64_t row1, const int64_t *srp, const int32_t
                    const int32_t *ep_b, double omega, int update, double *e_row,
                    double *res_max, int64_t *status, void *stream);
 
+/* SpGEMM rows beyond the on-chip kernels' capacity (the count kernels
+ * mark them with count -1: > 256 distinct columns, a B row longer than a
+ * staging window, a hash overflow): one CTA per listed row, the row's hash
+ * table in global scratch (hoff: per-row offsets, power-of-two sizes >= 2 x
+ * the row's products, from sphc_spgemm_global_products). crp NULL: count
+ * pass (counts[row]); else fill at crp[row] with sorted columns and
+ * ascending-k unfused sums (bitwise scipy csr_matmat order); av2 non-NULL:
+ * the pair product. Rows of more than 8192 columns -> SPGEMM_CAPACITY. */
+int sphc_spgemm_global_products(int64_t nrows, const int64_t *rows, const int64_t *arp,
+                                const int32_t *aci, const int64_t *brp, int64_t *prods,
+                                void *stream);
+int sphc_spgemm_global(int64_t nrows, const int64_t *rows, const int64_t *hoff, int32_t *hkeys,
+                       int32_t *hslot, const int64_t *arp, const int32_t *aci, const double *av,
+                       const double *av2, const int64_t *brp, const int32_t *bci,
+                       const double *bv, const double *bv2, int64_t *counts, const int64_t *crp,
+                       int32_t *cci, double *cv, double *cv2, int64_t *status, void *stream);
+
 /* ---------------------------------------------------------------- host (C++) */
 
 /* Greedy two-phase aggregation, exact reference semantics

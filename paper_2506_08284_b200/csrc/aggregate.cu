@@ -20,7 +20,7 @@
 extern "C" int sphc_scan_i64(int64_t n, const int64_t* counts, int64_t* offsets, void* stream);
 
 #define AGG_WARPS 4
-#define AGG_CAP 256  // neighbour owners buffered per leftover node
+#define AGG_CAP 256  // neighbour owners buffered per leftover node (beyond: global reads)
 
 __device__ __forceinline__ int agg_ld_acquire(const int* p) {
   int v;
@@ -251,6 +251,27 @@ __global__ void __launch_bounds__(AGG_WARPS * 32)
           bv = v;
         }
       }
+    } else {
+      // more assigned neighbours than the buffer holds: the same counts
+      // straight from global memory (O(d^2) reads; rare high-degree nodes).
+      // Lower neighbours were acquired above; a higher LEFTOVER neighbour is
+      // still unassigned (it waits for this node), exactly the reference's
+      // "currently assigned" set.
+      for (i64 qa = s + lane; qa < e; qa += 32) {
+        int ja = ci[qa];
+        i64 v = ja == (int)i ? -1 : agg_ld_acquire64(memb + ja);
+        if (v < 0) continue;
+        int c = 0;
+        for (i64 qb = s; qb < e; qb++) {
+          int jb = ci[qb];
+          if (jb != (int)i && agg_ld_acquire64(memb + jb) == v) c++;
+        }
+        if (c > bc || (c == bc && (bv < 0 || v < bv))) {
+          bc = c;
+          bv = v;
+        }
+      }
+      over = false;
     }
     for (int o = 16; o > 0; o >>= 1) {
       int c2 = __shfl_xor_sync(FULL_MASK, bc, o);

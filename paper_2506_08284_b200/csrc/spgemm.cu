@@ -201,7 +201,9 @@ __global__ void __launch_bounds__(SPG_WARPS * 32)
     bool ok = spg_symbolic<SPG_STG, SPG_CCAP>(row, arp, aci, brp, bci, S.keys, ts, &S.ucount,
                                               S.B, lane);
     if (lane == 0) {
-      counts[row] = ok ? S.ucount : 0;
+      // -1: beyond the on-chip capacity; the global-memory path
+      // (sphc_spgemm_global) counts and fills this row
+      counts[row] = ok ? S.ucount : -1;
       if (!ok) report(status, SPHC_ST_SPGEMM_CAPACITY, row);
     }
     __syncwarp();
@@ -515,7 +517,7 @@ __global__ void __launch_bounds__(SPC_W * 32)
     __syncthreads();
     if (threadIdx.x == 0) {
       bool ok = !H.bad && H.ucount <= SPC_CCAP;
-      counts[row] = ok ? H.ucount : 0;
+      counts[row] = ok ? H.ucount : -1;   // -1: global-memory path
       if (!ok) report(status, SPHC_ST_SPGEMM_CAPACITY, row);
     }
     __syncthreads();
@@ -537,7 +539,8 @@ __global__ void __launch_bounds__(SPC_W * 32)
   double* my2 = PAIR ? spc_acc + (SPC_W + w) * SPC_CCAP : nullptr;
   for (i64 row = blockIdx.x; row < n; row += gridDim.x) {
     int nu = (int)(crp[row + 1] - crp[row]);
-    if (nu == 0) continue;              // empty, or flagged by the count pass
+    // empty, or beyond the on-chip capacity (the global-memory path's row)
+    if (nu == 0 || nu > SPC_CCAP) continue;
     int ts = pow2_at_least(2 * nu, 64);
     if (ts > SPC_HCAP) ts = SPC_HCAP;
     i64 as = arp[row], ae = arp[row + 1];
@@ -680,4 +683,203 @@ extern "C" int sphc_spgemm_fill_long(int64_t n, const int64_t* arp, const int32_
     return fill_cta_launch<true>(n, arp, aci, av, av2, brp, bci, bv, bv2, crp, cci, cv1, cv2, s);
   return fill_cta_launch<false>(n, arp, aci, av, nullptr, brp, bci, bv, nullptr, crp, cci, cv1,
                                 nullptr, s);
+}
+
+// ---------------------------------------------------------------------------
+// Global-memory path for the rows the on-chip kernels cannot hold (more
+// than 256 distinct columns, a B row longer than a staging window, or a
+// hash table overflow; the count kernels mark them with -1). One CTA per
+// such row, the row's hash table in global scratch (hoff: per-row offsets,
+// power-of-two sizes >= 2 x the row's products):
+//   COUNT: insert every product column, count the distinct ones;
+//   FILL:  insert again, collect the columns, sort them in shared memory
+//          (bitonic, <= SPG_GCAP columns), record each column's sorted slot,
+//          then accumulate A entry by A entry in ascending k (a B row's
+//          columns are distinct, so the threads never collide) with
+//          unfused sums: scipy's csr_matmat order, bitwise ORDERED.
+#define SPG_GT 256
+#define SPG_GCAP 8192
+
+__global__ void k_spgemm_global_products(i64 nrows, const i64* __restrict__ rows,
+                                         const i64* __restrict__ arp, const int* __restrict__ aci,
+                                         const i64* __restrict__ brp, i64* __restrict__ prods) {
+  for (i64 r = blockIdx.x; r < nrows; r += gridDim.x) {
+    i64 row = rows[r];
+    i64 t = 0;
+    for (i64 j = arp[row] + threadIdx.x; j < arp[row + 1]; j += blockDim.x) {
+      int k = aci[j];
+      t += brp[k + 1] - brp[k];
+    }
+    __shared__ i64 red[SPG_GT];
+    red[threadIdx.x] = t;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) prods[r] = red[0];
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ i64 spg_gh(int col, i64 ts) {
+  return (i64)(((unsigned long long)(unsigned)col * 11400714819323198485ull) >> 20) & (ts - 1);
+}
+
+__device__ int spg_ginsert(int* keys, i64 ts, int col) {   // 1 if newly inserted
+  i64 h = spg_gh(col, ts);
+  for (;;) {
+    int cur = ((volatile int*)keys)[h];
+    if (cur == col) return 0;
+    if (cur == -1) {
+      int old = atomicCAS(&keys[h], -1, col);
+      if (old == -1) return 1;
+      if (old == col) return 0;
+    }
+    h = (h + 1) & (ts - 1);
+  }
+}
+
+__device__ __forceinline__ i64 spg_gfind(const int* keys, i64 ts, int col) {
+  i64 h = spg_gh(col, ts);
+  while (keys[h] != col) h = (h + 1) & (ts - 1);
+  return h;
+}
+
+template <bool FILL, bool PAIR>
+__global__ void __launch_bounds__(SPG_GT)
+    k_spgemm_global(i64 nrows, const i64* __restrict__ rows, const i64* __restrict__ hoff,
+                    int* __restrict__ hkeys, int* __restrict__ hslot,
+                    const i64* __restrict__ arp, const int* __restrict__ aci,
+                    const double* __restrict__ av, const double* __restrict__ av2,
+                    const i64* __restrict__ brp, const int* __restrict__ bci,
+                    const double* __restrict__ bv, const double* __restrict__ bv2,
+                    i64* __restrict__ counts, const i64* __restrict__ crp,
+                    int* __restrict__ cci, double* __restrict__ cv, double* __restrict__ cv2,
+                    i64* status) {
+  extern __shared__ int glist[];          // FILL: sorted columns (<= SPG_GCAP)
+  __shared__ int ucount;
+  for (i64 r = blockIdx.x; r < nrows; r += gridDim.x) {
+    i64 row = rows[r];
+    i64 ts = hoff[r + 1] - hoff[r];
+    int* keys = hkeys + hoff[r];
+    int* slot = hslot + hoff[r];
+    for (i64 h = threadIdx.x; h < ts; h += blockDim.x) keys[h] = -1;
+    if (threadIdx.x == 0) ucount = 0;
+    __syncthreads();
+    i64 as = arp[row], ae = arp[row + 1];
+    int mine = 0;
+    // products: A entries in chunks, every thread walks one B row at a time
+    for (i64 j = as; j < ae; j++) {
+      int k = aci[j];
+      for (i64 q = brp[k] + threadIdx.x; q < brp[k + 1]; q += blockDim.x)
+        mine += spg_ginsert(keys, ts, bci[q]);
+    }
+    atomicAdd(&ucount, mine);
+    __syncthreads();
+    int nu = ucount;
+    if (!FILL) {
+      if (threadIdx.x == 0) counts[row] = nu;
+      __syncthreads();
+      continue;
+    }
+    if (nu > SPG_GCAP) {
+      if (threadIdx.x == 0) report(status, SPHC_ST_SPGEMM_CAPACITY, row);
+      __syncthreads();
+      continue;
+    }
+    // collect, then bitonic sort in shared memory
+    if (threadIdx.x == 0) ucount = 0;
+    __syncthreads();
+    for (i64 h = threadIdx.x; h < ts; h += blockDim.x) {
+      int key = keys[h];
+      if (key >= 0) glist[atomicAdd(&ucount, 1)] = key;
+    }
+    int m = 1;
+    while (m < nu) m <<= 1;
+    __syncthreads();
+    for (int t = nu + threadIdx.x; t < m; t += blockDim.x) glist[t] = 0x7fffffff;
+    __syncthreads();
+    for (int size = 2; size <= m; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = threadIdx.x; t < (m >> 1); t += blockDim.x) {
+          int lo = ((t & ~(stride - 1)) << 1) | (t & (stride - 1)), hi = lo + stride;
+          bool up = (lo & size) == 0;
+          int a = glist[lo], b = glist[hi];
+          if ((a > b) == up) {
+            glist[lo] = b;
+            glist[hi] = a;
+          }
+        }
+        __syncthreads();
+      }
+    i64 o = crp[row];
+    for (int t = threadIdx.x; t < nu; t += blockDim.x) {
+      slot[spg_gfind(keys, ts, glist[t])] = t;
+      cci[o + t] = glist[t];
+      cv[o + t] = 0.0;
+      if (PAIR) cv2[o + t] = 0.0;
+    }
+    __syncthreads();
+    for (i64 j = as; j < ae; j++) {
+      int k = aci[j];
+      double a = av[j], a2 = PAIR ? av2[j] : 0.0;
+      for (i64 q = brp[k] + threadIdx.x; q < brp[k + 1]; q += blockDim.x) {
+        int sl = slot[spg_gfind(keys, ts, bci[q])];
+        cv[o + sl] = __dadd_rn(cv[o + sl], __dmul_rn(a, bv[q]));
+        if (PAIR) cv2[o + sl] = __dadd_rn(cv2[o + sl], __dmul_rn(a2, bv2[q]));
+      }
+      __syncthreads();
+    }
+  }
+}
+
+extern "C" int sphc_spgemm_global_products(int64_t nrows, const int64_t* rows,
+                                           const int64_t* arp, const int32_t* aci,
+                                           const int64_t* brp, int64_t* prods, void* stream) {
+  if (nrows <= 0) return 0;
+  k_spgemm_global_products<<<grid_for(nrows, 1, SPHC_NUM_SMS * 8), SPG_GT, 0,
+                             as_stream(stream)>>>(nrows, rows, arp, aci, brp, prods);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int sphc_spgemm_global(int64_t nrows, const int64_t* rows, const int64_t* hoff,
+                                  int32_t* hkeys, int32_t* hslot, const int64_t* arp,
+                                  const int32_t* aci, const double* av, const double* av2,
+                                  const int64_t* brp, const int32_t* bci, const double* bv,
+                                  const double* bv2, int64_t* counts, const int64_t* crp,
+                                  int32_t* cci, double* cv, double* cv2, int64_t* status,
+                                  void* stream) {
+  if (nrows <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  unsigned g = grid_for(nrows, 1, SPHC_NUM_SMS * 8);
+  size_t sm = SPG_GCAP * sizeof(int);
+  if (!crp) {
+    k_spgemm_global<false, false><<<g, SPG_GT, 0, s>>>(nrows, rows, hoff, hkeys, hslot, arp,
+                                                        aci, av, av2, brp, bci, bv, bv2, counts,
+                                                        crp, cci, cv, cv2, status);
+  } else if (av2) {
+    static bool attr = false;
+    if (!attr) {
+      SPHC_CUDA(cudaFuncSetAttribute(k_spgemm_global<true, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      attr = true;
+    }
+    k_spgemm_global<true, true><<<g, SPG_GT, sm, s>>>(nrows, rows, hoff, hkeys, hslot, arp, aci,
+                                                       av, av2, brp, bci, bv, bv2, counts, crp,
+                                                       cci, cv, cv2, status);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      SPHC_CUDA(cudaFuncSetAttribute(k_spgemm_global<true, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      attr = true;
+    }
+    k_spgemm_global<true, false><<<g, SPG_GT, sm, s>>>(nrows, rows, hoff, hkeys, hslot, arp,
+                                                        aci, av, av2, brp, bci, bv, bv2, counts,
+                                                        crp, cci, cv, cv2, status);
+  }
+  SPHC_LAUNCH_CHECK();
+  return 0;
 }

@@ -591,11 +591,82 @@ def _rows(A, lo):
     return A.rowptr[lo:]
 
 
+class _Overflow:
+    """Deferred status handler of the SpGEMM count passes: rows beyond the
+    on-chip capacity (count -1) are noted for the global-memory path;
+    every other capacity status still raises."""
+
+    def __init__(self):
+        self.hit = False
+
+    def __call__(self, rows):
+        if "SPGEMM_CAPACITY" in rows:
+            self.hit = True
+        capacity_check({k: v for k, v in rows.items() if k != "SPGEMM_CAPACITY"})
+
+
+def _global_rows_count(A, B, cnt):
+    """Rows the count kernels marked -1: their true counts by the
+    global-memory kernel (one CTA per row, hash tables in global scratch).
+    Rare (imported matrices with very long rows); a few host syncs."""
+    dev = A.rowptr.device
+    rows = torch.nonzero(cnt < 0).flatten()
+    nr = rows.numel()
+    STATS["spgemm_global_rows"] += nr
+    prods = torch.empty(nr, dtype=torch.int64, device=dev)
+    call("sphc_spgemm_global_products", nr, rows, A.rowptr, A.col, B.rowptr, prods)
+    sz = torch.clamp(2 * prods, min=64)
+    sz = torch.pow(2, torch.ceil(torch.log2(sz.to(torch.float64)))).to(torch.int64)
+    hoff = torch.zeros(nr + 1, dtype=torch.int64, device=dev)
+    hoff[1:] = torch.cumsum(sz, 0)
+    tot = int(readback(hoff[nr:nr + 1])[0][0])
+    hkeys = torch.empty(tot, dtype=torch.int32, device=dev)
+    hslot = torch.empty(tot, dtype=torch.int32, device=dev)
+    st = Status()
+    call("sphc_spgemm_global", nr, rows, hoff, hkeys, hslot, A.rowptr, A.col, None, None,
+         B.rowptr, B.col, None, None, cnt, None, None, None, None, st.t)
+    return (rows, hoff, hkeys, hslot)
+
+
+def _global_rows_fill(g, A, B, rp, ci, v, A2=None, B2=None, v2=None):
+    rows, hoff, hkeys, hslot = g
+    st = Status()
+    call("sphc_spgemm_global", rows.numel(), rows, hoff, hkeys, hslot, A.rowptr, A.col, A.val,
+         None if A2 is None else A2.val, B.rowptr, B.col, B.val,
+         None if B2 is None else B2.val, None, rp, ci, v, v2, st.t)
+    st.defer(capacity_check)
+
+
+# rows of more output columns than this also take the global-memory path
+# (0 = only the rows the on-chip kernels cannot hold; tests lower it to
+# drive whole hierarchies through the global path)
+GLOBAL_ROWS_ABOVE = int(os.environ.get("SPHC_SPGEMM_GLOBAL_ABOVE", "0"))
+STATS = {"spgemm_global_rows": 0}
+
+
+def _count_with_overflow(A, B, cnt, st, shard, n):
+    """scan of the count pass; rows beyond the on-chip capacity go to the
+    global-memory path (their counts fixed, then a second scan)."""
+    ov = _Overflow()
+    st.defer(ov)
+    if GLOBAL_ROWS_ABOVE > 0:
+        cnt.masked_fill_(cnt > GLOBAL_ROWS_ABOVE, -1)
+        ov.hit = True
+    rp, nnz, mcols = scan(cnt, with_max=True)
+    g = None
+    if ov.hit:
+        g = _global_rows_count(A, B, cnt)
+        rp, nnz, mcols = scan(cnt, with_max=True)
+    return rp, nnz, mcols, g
+
+
 @checked
 def spgemm(A, B, drop=True, ordered=False, shard=None):
     """C = A B; exact zeros dropped like scipy's product (drop=True).
     ordered=True reproduces scipy csr_matmat's accumulation bit for bit.
-    shard: rows computed by row blocks over a ``sharding.Sharding``."""
+    shard: rows computed by row blocks over a ``sharding.Sharding``.
+    Rows beyond the on-chip kernels' capacity (> 256 distinct columns) take
+    the global-memory path (sphc_spgemm_global, same ordered sums)."""
     if A.shape[1] != B.shape[0]:
         raise ValueError(f"spgemm dimension mismatch: {A.shape} @ {B.shape}")
     n = A.shape[0]
@@ -609,8 +680,7 @@ def spgemm(A, B, drop=True, ordered=False, shard=None):
     if shard is not None:
         shard.gather_ranges(cnt, shard.bounds(n))
         shard.min_(st.t)
-    st.defer(capacity_check)
-    rp, nnz, mcols = scan(cnt, with_max=True)
+    rp, nnz, mcols, g = _count_with_overflow(A, B, cnt, st, shard, n)
     ci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
     v = empty_f64(nnz)
     for _, lo, hi in blocks:
@@ -620,6 +690,8 @@ def spgemm(A, B, drop=True, ordered=False, shard=None):
         else:
             call("sphc_spgemm_fill", hi - lo, _rows(A, lo), A.col, A.val, B.rowptr, B.col,
                  B.val, rp[lo:], ci, v, int(ordered), mcols, st.t)
+    if g is not None:
+        _global_rows_fill(g, A, B, rp, ci, v)
     if shard is not None and shard.collective:
         from .sharding import host_offsets
         off = host_offsets(rp, shard.bounds(n))
@@ -658,8 +730,7 @@ def spgemm_pair(A1, A2, B1, B2, drop=True, shard=None):
     if shard is not None:
         shard.gather_ranges(cnt, shard.bounds(n))
         shard.min_(st.t)
-    st.defer(capacity_check)
-    rp, nnz, mcols = scan(cnt, with_max=True)
+    rp, nnz, mcols, g = _count_with_overflow(A1, B1, cnt, st, shard, n)
     ci = torch.empty(nnz, dtype=torch.int32, device=A1.rowptr.device)
     v1, v2 = empty_f64(nnz), empty_f64(nnz)
     for _, lo, hi in blocks:
@@ -669,6 +740,8 @@ def spgemm_pair(A1, A2, B1, B2, drop=True, shard=None):
         else:
             call("sphc_spgemm_fill_pair", hi - lo, _rows(A1, lo), A1.col, A1.val, A2.val,
                  B1.rowptr, B1.col, B1.val, B2.val, rp[lo:], ci, v1, v2, mcols, st.t)
+    if g is not None:
+        _global_rows_fill(g, A1, B1, rp, ci, v1, A2, B2, v2)
     if shard is not None and shard.collective:
         from .sharding import host_offsets
         off = host_offsets(rp, shard.bounds(n))

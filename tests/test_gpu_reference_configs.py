@@ -2,7 +2,7 @@
 (row X1 of the round-1 verdict: parity where the performance is claimed).
 
 Goldens ``hier_C4s`` (C4 recipe at 16^3), ``hier_C3`` (64^3, sigma jump),
-``hier_C5s`` (C5 recipe at 64^3) and ``hier_C4r`` (the C4 recipe at 128^3,
+``hier_C5s`` (C5 recipe at 64^3) and ``hier_C4rh`` (the C4 recipe at 128^3,
 the smallest size where ``make_irreducible`` fires: 154 coarse edges appended
 on level 2) were made by running the reference on the host build of the
 device assembly (oracle/host_assembly.py, tests/golden/make_golden.py BIG).
@@ -20,8 +20,11 @@ public API and checks:
   (``<key>_stride``) plus the Frobenius norm of the whole matrix; emin
   energies rtol 1e-10; commutator residual <= 1e-12;
 * ITER: PCG iterations within +-1 of the reference hierarchy with the same
-  Chebyshev sweeper in its seam, and converged like the reference's own
-  Gauss-Seidel solve.
+  Chebyshev sweeper in its seam. Where the reference's LU coarsest solve
+  does not converge (the near-singular coarsest operators of the C4 / C5
+  recipes), the device's LU mode (``coarse_solver="lu"``) reproduces that
+  exit within the same iteration cap, and the default equilibrated
+  Cholesky coarsest solve converges (the documented deviation).
 """
 
 import os
@@ -34,7 +37,7 @@ from golden_util import GOLDEN, check_values, csr_hash, load_case, pattern_sha, 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-CASES = ["C4s", "C5s", "C3", "C4r"]
+CASES = ["C4s", "C5s", "C3", "C4rh"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -96,10 +99,22 @@ def test_device_config_vs_reference(name):
                    for r in range(Dn.shape[0] - L["n_augmented"], Dn.shape[0])]
             assert got == L["augmented"], li
 
-    res = mg.pcg_solve(h.levels[0].A_e, torch.from_numpy(rhs).cuda(),
-                       mg.v_cycle_preconditioner(h))
-    assert res.status == meta["cheb"]["status"] == "converged"
-    assert abs(res.iterations - meta["cheb"]["iterations"]) <= 1, (
-        res.iterations, meta["cheb"]["iterations"])
-    if "gs" in meta:
-        assert meta["gs"]["status"] == "converged"
+    if "cheb" not in meta:
+        pytest.fail(f"golden hier_{name} has no solve yet (reference still running)")
+    b = torch.from_numpy(rhs).cuda()
+    ref = meta["cheb"]
+    res = mg.pcg_solve(h.levels[0].A_e, b, mg.v_cycle_preconditioner(h))
+    if ref["status"] == "converged":
+        assert res.status == "converged"
+        assert abs(res.iterations - ref["iterations"]) <= 1, (res.iterations,
+                                                              ref["iterations"])
+    else:
+        # the reference's LU coarsest solve fails here; so does ours in LU
+        # mode, while the default coarsest solve converges
+        assert res.status == "converged"
+        hl = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D,
+                                mg.SolverConfig(coarse_size=meta["coarse_size"],
+                                                coarse_solver="lu"))
+        rl = mg.pcg_solve(hl.levels[0].A_e, b, mg.v_cycle_preconditioner(hl),
+                          maxit=ref.get("maxit", 500))
+        assert rl.status == ref["status"], (rl.status, ref["status"])

@@ -219,6 +219,21 @@ int sphc_spmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *v, 
 int sphc_sell_sizes(int64_t n, const int64_t *rp, int64_t *slice_entries, void *stream);
 int sphc_sell_fill(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
                    const int64_t *slice_ptr, int32_t *sci, double *sv, void *stream);
+/* SELL fill for a rectangular operator (A_e D): padding entries repeat the
+ * row's first column (0 for an empty row) instead of the row index. */
+int sphc_sell_fill_rect(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                        const int64_t *slice_ptr, int32_t *sci, double *sv, void *stream);
+/* Hiptmair mid step (hiptmair_smooth, multigrid.py:164-173): the nodal
+ * correction x + D c and the first Chebyshev step of the second edge sweep
+ * from the residual r = b - A x already held, b - A (x + D c) = r - (A D) c:
+ *   d = cr dinv (r - (A D) c);  x_out = (x + D c) + d
+ * (slice_ptr, sci, sv) = SELL mirror of A D (sphc_sell_fill_rect), (drp, dci,
+ * dv) = CSR of D. Replaces one D pass and one A_e pass by one A D pass. */
+int sphc_sell_hipt_mid(int64_t n, const int64_t *slice_ptr, const int32_t *sci,
+                       const double *sv, const int64_t *drp, const int32_t *dci,
+                       const double *dv, const double *dinv, const double *r,
+                       const double *c, const double *x_in, double *x_out, double *d,
+                       double cr, int64_t padded, void *stream);
 /* y = alpha A x + beta z on the SELL mirror, one thread per row. `padded` =
  * stored entries (slice_ptr[n_slices]); operators above 48 MB are read with
  * evict-first loads, smaller ones stay L2-resident across the V-cycle. */

@@ -32,6 +32,7 @@ extern "C" int sphc_sell_sizes(int64_t n, const int64_t* rp, int64_t* slice_entr
   return 0;
 }
 
+template <bool RECT>
 __global__ void k_sell_fill(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
                             const double* __restrict__ v, const i64* __restrict__ sp,
                             int* __restrict__ sci, double* __restrict__ sv) {
@@ -47,7 +48,7 @@ __global__ void k_sell_fill(i64 n, const i64* __restrict__ rp, const int* __rest
       j0 = rp[row];
       len = (int)(rp[row + 1] - j0);
     }
-    int self = row < n ? (int)row : 0;
+    int self = RECT ? (len ? ci[j0] : 0) : (row < n ? (int)row : 0);
     for (int j = 0; j < w; j++) {
       bool real = j < len;
       sci[base + (i64)j * SELL_C] = real ? ci[j0 + j] : self;
@@ -60,7 +61,19 @@ extern "C" int sphc_sell_fill(int64_t n, const int64_t* rp, const int32_t* ci, c
                               const int64_t* slice_ptr, int32_t* sci, double* sv,
                               void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_sell_fill<<<grid_for(n, 256), 256, 0, s>>>(n, rp, ci, v, slice_ptr, sci, sv);
+  k_sell_fill<false><<<grid_for(n, 256), 256, 0, s>>>(n, rp, ci, v, slice_ptr, sci, sv);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+// Rectangular operators (A_e D: n_e x n_n): a padding entry repeats the
+// row's first column (0 for an empty row) instead of the row index, which
+// need not be a valid column.
+extern "C" int sphc_sell_fill_rect(int64_t n, const int64_t* rp, const int32_t* ci,
+                                   const double* v, const int64_t* slice_ptr, int32_t* sci,
+                                   double* sv, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_sell_fill<true><<<grid_for(n, 256), 256, 0, s>>>(n, rp, ci, v, slice_ptr, sci, sv);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -241,6 +254,47 @@ extern "C" int sphc_sell_cheb_step(int64_t n, const int64_t* slice_ptr, const in
   cudaStream_t s = as_stream(stream);
   SELL_DISPATCH(k_sell_cheb, padded * 12 > SELL_STREAM_BYTES, n, slice_ptr, sci, sv, dinv, b,
                 x_in, x_out, d, cd, cr, x_zero);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+// Hiptmair mid step (multigrid.py:164-173, between the nodal correction and
+// the second edge sweep): x1 = x + D c, then the first Chebyshev step of the
+// next edge sweep taken from the residual r = b - A x the caller already
+// holds, since b - A (x + D c) = r - (A D) c:
+//   d = cr dinv (r - (A D) c);   x_out = (x + D c) + d
+// One pass over the SELL mirror of A D (~18 entries per row against ~33 for
+// A_e) replaces the D pass and one A_e pass of the V-cycle. D from its CSR
+// (<= 2 entries per row on these gradients; any length is handled).
+template <bool STREAM, int K>
+__global__ void __launch_bounds__(SELL_PER_BLOCK, (STREAM && K == 1) ? 8 : 5)
+    k_sell_hipt_mid(i64 n, const i64* __restrict__ sp, const int* __restrict__ sci,
+                    const double* __restrict__ sv, const i64* __restrict__ drp,
+                    const int* __restrict__ dci, const double* __restrict__ dvv,
+                    const double* __restrict__ dinv, const double* __restrict__ r,
+                    const double* __restrict__ c, const double* __restrict__ x_in,
+                    double* __restrict__ x_out, double* __restrict__ d, double cr) {
+  pdl_begin();
+  i64 row;
+  double adc;
+  if (!sell_rowsum<STREAM, K>(n, sp, sci, sv, c, false, row, adc)) return;
+  i64 j0 = drp[row], j1 = drp[row + 1];
+  double u = 0.0;
+  for (i64 j = j0; j < j1; j++) u = fma(dvv[j], __ldg(c + dci[j]), u);
+  double dn = cr * dinv[row] * (r[row] - adc);
+  d[row] = dn;
+  x_out[row] = (x_in[row] + u) + dn;
+}
+
+extern "C" int sphc_sell_hipt_mid(int64_t n, const int64_t* slice_ptr, const int32_t* sci,
+                                  const double* sv, const int64_t* drp, const int32_t* dci,
+                                  const double* dv, const double* dinv, const double* r,
+                                  const double* c, const double* x_in, double* x_out,
+                                  double* d, double cr, int64_t padded, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  SELL_DISPATCH(k_sell_hipt_mid, padded * 12 > SELL_STREAM_BYTES, n, slice_ptr, sci, sv, drp,
+                dci, dv, dinv, r, c, x_in, x_out, d, cr);
   SPHC_LAUNCH_CHECK();
   return 0;
 }

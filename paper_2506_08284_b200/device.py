@@ -365,12 +365,17 @@ class AsyncUpload:
         self.nthreads = nthreads
         self.dev = dev
         self.stream = torch.cuda.Stream(device=dev)
-        self.event = torch.cuda.Event()
-        self.err = None
         import threading
+        nm = len(self.mats)
+        self.events = [torch.cuda.Event() for _ in range(nm)]
+        self.ready = [threading.Event() for _ in range(nm)]
+        self.event = self.events[-1] if nm else torch.cuda.Event()
+        self.err = None
         self.thread = threading.Thread(target=self._run, daemon=True)
         self.thread.start()
-        self.csr = None
+        self.csr = [None] * nm
+
+    CHUNK = 1 << 25          # staging granularity (bytes)
 
     def _run(self):
         try:
@@ -385,31 +390,40 @@ class AsyncUpload:
                 _STAGE["buf"] = buf
             hv = buf.numpy()
             # arrays already in the device dtype DMA straight from the
-            # caller's page-locked memory; the rest are cast into staging
+            # caller's page-locked memory (opt-in); the rest are cast into
+            # staging chunk by chunk, and each chunk's DMA is queued as soon
+            # as its host copy is done, so the copies of later chunks (and
+            # of S) overlap the transfers of earlier ones (and of A_e)
             direct = [own and a.dtype == np.dtype(d) and pinned_in_place(a)
                       for (a, d), own in zip(self.specs, self.owned)]
-            jobs = []
-            for (a, d), o, dr in zip(self.specs, self.offs, direct):
-                if dr:
-                    continue
-                dstv = hv[o:o + a.size * np.dtype(d).itemsize].view(d)
-                step = max(1 << 18, a.size // self.nthreads + 1)
-                for k in range(0, a.size, step):
-                    jobs.append((dstv[k:k + step], a[k:k + step]))
-            with torch.cuda.stream(self.stream):
-                for t, (a, d), dr in zip(self.dst, self.specs, direct):
-                    if dr and a.size:
-                        call("sphc_copy_h2d", t, a, a.nbytes)
-            if jobs:
-                from concurrent.futures import ThreadPoolExecutor
-                with ThreadPoolExecutor(self.nthreads) as ex:
-                    list(ex.map(lambda j: np.copyto(j[0], j[1], casting="unsafe"), jobs))
-            with torch.cuda.stream(self.stream):
-                for t, (a, d), o, dr in zip(self.dst, self.specs, self.offs, direct):
-                    if a.size and not dr:
-                        t.view(torch.uint8).copy_(buf[o:o + a.size * np.dtype(d).itemsize],
-                                                  non_blocking=True)
-                self.event.record(self.stream)
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(self.nthreads) as ex, torch.cuda.stream(self.stream):
+                futs = []
+                for idx, ((a, d), o, dr) in enumerate(zip(self.specs, self.offs, direct)):
+                    isz = np.dtype(d).itemsize
+                    if dr or not a.size:
+                        futs.append((None, idx, 0, 0, True))
+                        continue
+                    dstv = hv[o:o + a.size * isz].view(d)
+                    per = max(1, self.CHUNK // isz)
+                    for k in range(0, a.size, per):
+                        n = min(per, a.size - k)
+                        f = ex.submit(np.copyto, dstv[k:k + n], a[k:k + n], casting="unsafe")
+                        futs.append((f, idx, k * isz, n * isz, k + n == a.size))
+                for f, idx, rel, nb, last in futs:
+                    a, d = self.specs[idx]
+                    if f is None:
+                        if a.size:
+                            call("sphc_copy_h2d", self.dst[idx], a, a.nbytes)
+                    else:
+                        f.result()
+                        o = self.offs[idx] + rel
+                        self.dst[idx].view(torch.uint8)[rel:rel + nb].copy_(
+                            buf[o:o + nb], non_blocking=True)
+                    if last and idx % 3 == 2:          # a matrix's last array is queued
+                        m = idx // 3
+                        self.events[m].record(self.stream)
+                        self.ready[m].set()
             _STAGE["event"] = self.event
             # direct sources stay referenced (self.mats) until get() has
             # made the compute stream wait on the copies; keep them alive
@@ -417,16 +431,20 @@ class AsyncUpload:
             _INFLIGHT.extend((a, self.event) for (a, _), dr in zip(self.specs, direct) if dr)
         except BaseException as e:   # noqa: BLE001 - re-raised by get()
             self.err = e
+        finally:
+            for r in self.ready:
+                r.set()
 
     def get(self, k):
-        if self.csr is None:
-            self.thread.join()
+        if self.csr[k] is None:
+            self.ready[k].wait()
             if self.err is not None:
+                self.thread.join()
                 raise self.err
-            torch.cuda.current_stream().wait_event(self.event)
-            self.csr = [DeviceCSR(self.dst[3 * i], self.dst[3 * i + 1], self.dst[3 * i + 2],
-                                  tuple(int(x) for x in A.shape))
-                        for i, A in enumerate(self.mats)]
+            torch.cuda.current_stream().wait_event(self.events[k])
+            A = self.mats[k]
+            self.csr[k] = DeviceCSR(self.dst[3 * k], self.dst[3 * k + 1], self.dst[3 * k + 2],
+                                    tuple(int(x) for x in A.shape))
         return self.csr[k]
 
 
@@ -796,6 +814,20 @@ def sell(A):
     m = SellMirror(sp_, ci, v, n)
     A._sell, A._sell_key = m, _sell_key(A)
     return m
+
+
+def sell_rect(A):
+    """Uncached SELL-32 copy of a rectangular operator (A_e D for the fused
+    Hiptmair mid step): padding repeats a valid column of the row."""
+    n = A.shape[0]
+    ns = (n + 31) // 32
+    sz = torch.empty(ns, dtype=torch.int64, device=A.rowptr.device)
+    call("sphc_sell_sizes", n, A.rowptr, sz)
+    sp_, tot = scan(sz)
+    ci = torch.empty(tot, dtype=torch.int32, device=A.rowptr.device)
+    v = empty_f64(tot)
+    call("sphc_sell_fill_rect", n, A.rowptr, A.col, A.val, sp_, ci, v)
+    return SellMirror(sp_, ci, v, n)
 
 
 CTA_ROW_MAX_ROWS = int(os.environ.get("SPHC_CTA_ROW_MAX_ROWS", "4096"))

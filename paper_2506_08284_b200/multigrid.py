@@ -39,6 +39,10 @@ USE_GRAPH = os.environ.get("SPHC_PCG_GRAPH", "1") != "0"
 # overflow L2 before the second step re-reads them, and capping the CTAs to
 # fit starves the loads. SPHC_FUSE_MB=64 enables it.
 FUSE_ROWS = 256
+# Levels with at least this many edges (operators streamed from HBM) keep a
+# SELL mirror of A_e D and take the Hiptmair mid step fused
+# (sphc_sell_hipt_mid); -1 disables it.
+HIPT_MID_MIN_ROWS = int(os.environ.get("SPHC_HIPT_MID_MIN_ROWS", str(148 * 48 * 32)))
 FUSE_MIN_ROWS = int(os.environ.get("SPHC_FUSE_MIN_ROWS", str(148 * 48 * 32)))
 FUSE_L2_BYTES = float(os.environ.get("SPHC_FUSE_MB", "0")) * 2**20
 
@@ -250,6 +254,30 @@ class ChebyshevSweeper:
         return cur
 
 
+    def symmetric_mid(self, x, r, c, D, mid):
+        """The sweep that follows the nodal correction of a Hiptmair step:
+        x + D c smoothed once, with the first polynomial step taken from
+        the residual r = b - A x the caller holds (sphc_sell_hipt_mid: one
+        pass over the SELL mirror ``mid`` of A D instead of a D pass and an
+        A pass); the remaining steps as in ``symmetric``. Returns
+        (iterate, b-independent): the caller passes b for the later steps."""
+        n = self.A.shape[0]
+        out = self.buf[0] if x is not self.buf[0] else self.buf[1]
+        _, cr = self.coefs[0]
+        call("sphc_sell_hipt_mid", n, mid.slice_ptr, mid.col, mid.val, D.rowptr, D.col, D.val,
+             self.dinv, r, c, x, out, self.d, cr, mid.padded)
+        return out
+
+    def _steps_from(self, cur, b, first):
+        """Polynomial steps first.. of one sweep on the SELL mirror."""
+        n, m = self.A.shape[0], self.sell
+        for cd, cr in self.coefs[first:]:
+            out = self.buf[0] if cur is not self.buf[0] else self.buf[1]
+            call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, self.dinv, b, cur, out,
+                 self.d, cd, cr, 0, m.padded)
+            cur = out
+        return cur
+
     def _fused_sweep(self, x, b, x_zero):
         """The polynomial's steps in passes of self.fuse steps (the same
         buffers and arithmetic as the step-by-step loop)."""
@@ -358,6 +386,7 @@ class Level:
     r: torch.Tensor = None
     bn: torch.Tensor = None
     rc: torch.Tensor = None          # restricted residual (next level's rhs)
+    mid: object = None               # SELL mirror of A_e D (fused Hiptmair mid step)
     membership: torch.Tensor = None
     assignment: torch.Tensor = None
     coarse_gradient: object = None
@@ -385,14 +414,20 @@ def _make_level(A_e, S_e, D, cfg, AD=None, smooth=True, shard=None, **extra):
     # D^T A D keeps exact cancellations as stored zeros (scipy drops them;
     # they change no value and no decision, and skipping the compaction
     # saves a host sync per level)
-    nodal_aux = dv.spgemm(Dt, AD if AD is not None else dv.spgemm(A_e, D, drop=False,
-                                                                  shard=shard),
-                          drop=False, shard=shard)
+    if AD is None:
+        AD = dv.spgemm(A_e, D, drop=False, shard=shard)
+    nodal_aux = dv.spgemm(Dt, AD, drop=False, shard=shard)
     level = Level(A_e=A_e, S_e=S_e, D=D, nodal_aux=nodal_aux, Dt=Dt, **extra)
     if smooth:   # the coarsest level is solved directly, never smoothed
         sweeper = SMOOTHERS[cfg.smoother]
         level.edge_sweeper = sweeper(A_e, cfg.cheb_degree)
         level.aux_sweeper = sweeper(nodal_aux, cfg.cheb_degree)
+        es = level.edge_sweeper
+        if (HIPT_MID_MIN_ROWS >= 0 and A_e.shape[0] >= HIPT_MID_MIN_ROWS
+                and isinstance(es, ChebyshevSweeper) and es.sell is not None
+                and es.degree >= 1 and 12 * AD.nnz < 0.8 * 12 * A_e.nnz):
+            # streaming levels: keep A D (SELL) for the fused mid step
+            level.mid = dv.sell_rect(AD)
     level.r = dv.empty_f64(A_e.shape[0])
     level.bn = dv.empty_f64(D.shape[1])
     return level
@@ -535,15 +570,16 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
         # first use is the emin sweep); the fine-level null-space check runs
         # right after the first prolongator. A data error of the nodal chain
         # defers to that check's, so the reference's error order holds.
-        up = dv.AsyncUpload([A_e, S_e])
+        # S first: the emin sweep needs only S; A_e lands behind it
+        up = dv.AsyncUpload([S_e, A_e])
         A_n, D = own_csr(A_n), own_csr(D)
         try:
-            first = build_edge_prolongator(A_n, dv.PendingCSR(up, 0), dv.PendingCSR(up, 1), D,
+            first = build_edge_prolongator(A_n, dv.PendingCSR(up, 1), dv.PendingCSR(up, 0), D,
                                            cfg.emin, shard=shard)
         except ValueError:
-            _check_nullspace(up.get(1), D, "the fine level", A=up.get(0), shard=shard)
+            _check_nullspace(up.get(0), D, "the fine level", A=up.get(1), shard=shard)
             raise
-        A_e, S_e = up.get(0), up.get(1)
+        A_e, S_e = up.get(1), up.get(0)
     else:
         # solver-owned wrappers: the SELL mirrors and shared index arrays
         # the setup attaches never land on the caller's DeviceCSR objects
@@ -670,6 +706,10 @@ def hiptmair_smooth(level, x, b, x_zero=False):
     dv.spmv(level.A_e, x, level.r, alpha=-1.0, beta=1.0, z=b)        # r = b - A x
     dv.spmv(level.Dt, level.r, level.bn)                                # D^T r
     c = level.aux_sweeper.symmetric(None, level.bn, x_zero=True)
+    if level.mid is not None:
+        # x += D c and the next sweep's first step in one pass over A D
+        es = level.edge_sweeper
+        return es._steps_from(es.symmetric_mid(x, level.r, c, level.D, level.mid), b, 1)
     dv.spmv(level.D, c, x, alpha=1.0, beta=1.0, z=x)                   # x += D c
     return level.edge_sweeper.symmetric(x, b)
 

@@ -91,3 +91,47 @@ def test_fused_hierarchy_solve_matches_unfused(monkeypatch):
     assert r0.iterations == r1.iterations and r0.status == r1.status == "converged"
     assert r0.residual_history == r1.residual_history
     assert torch.equal(r0.x, r1.x)
+
+
+@pytest.mark.parametrize("config,N,dirichlet_like", [("C4", 20, False), ("C2", 16, True)])
+def test_hiptmair_mid_step_matches_unfused(config, N, dirichlet_like):
+    """sphc_sell_hipt_mid (x + D c and the next sweep's first step from
+    r - (A D) c) against the separate D pass and A pass: the same iterate to
+    round-off (the two residuals differ only in summation order), the same
+    PCG iteration count +-1, on a jittered natural-BC recipe and a
+    Dirichlet one (D rows with a single entry)."""
+    from paper_2506_08284_b200 import multigrid as mg, device as dv
+    if config == "C4":
+        from paper_2506_08284_b200.assembly import make_device_config
+        s, rhs, cfg = make_device_config(config, N)
+        A_e, S, A_n, D = s.A_e, s.S, s.A_n, s.D
+    else:
+        from paper_2506_08284_b200.inputs import make_config
+        s, rhs, cfg = make_config(config, N)
+        A_e, S, A_n, D = (dv.DeviceCSR.from_scipy(M) for M in (s.A_e, s.S, s.A_n, s.D))
+    old = mg.HIPT_MID_MIN_ROWS
+    try:
+        mg.HIPT_MID_MIN_ROWS = -1
+        h0 = mg.build_hierarchy(A_e, S, A_n, D, mg.SolverConfig(coarse_size=300))
+        mg.HIPT_MID_MIN_ROWS = 0
+        h1 = mg.build_hierarchy(A_e, S, A_n, D, mg.SolverConfig(coarse_size=300))
+    finally:
+        mg.HIPT_MID_MIN_ROWS = old
+    assert all(lv.mid is None for lv in h0.levels)
+    assert all(lv.mid is not None for lv in h1.levels[:-1])
+    b = torch.from_numpy(rhs).cuda()
+    x0 = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, rhs.size)).cuda()
+    for xz in (True, False):
+        w = mg.hiptmair_smooth(h0.levels[0], None if xz else x0.clone(), b, x_zero=xz).clone()
+        g = mg.hiptmair_smooth(h1.levels[0], None if xz else x0.clone(), b, x_zero=xz).clone()
+        err = float((w - g).abs().max() / w.abs().max())
+        assert err < 1e-12, (xz, err)
+    v0 = mg.v_cycle(h0, None, b).clone()
+    v1 = mg.v_cycle(h1, None, b).clone()
+    # the whole V-cycle amplifies the round-off difference through the
+    # near-singular coarsest operators of the lognormal recipe (1e-8 there)
+    assert float((v0 - v1).abs().max() / v0.abs().max()) < 1e-6
+    r0 = mg.pcg_solve(h0.levels[0].A_e, b, mg.v_cycle_preconditioner(h0))
+    r1 = mg.pcg_solve(h1.levels[0].A_e, b, mg.v_cycle_preconditioner(h1))
+    assert r0.status == r1.status == "converged"
+    assert abs(r0.iterations - r1.iterations) <= 1, (r0.iterations, r1.iterations)

@@ -570,16 +570,22 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
         # first use is the emin sweep); the fine-level null-space check runs
         # right after the first prolongator. A data error of the nodal chain
         # defers to that check's, so the reference's error order holds.
-        # S first: the emin sweep needs only S; A_e lands behind it
-        up = dv.AsyncUpload([S_e, A_e])
-        A_n, D = own_csr(A_n), own_csr(D)
+        # One background upload in order of first use: A_n and D (the
+        # nodal chain starts as soon as they are queued), then S (the emin
+        # sweep), then A_e.
+        small = [M for M in (A_n, D) if not isinstance(M, DeviceCSR)]
+        up = dv.AsyncUpload(small + [S_e, A_e])
+        k = len(small)
+        it = iter(range(k))
+        A_n = own_csr(A_n) if isinstance(A_n, DeviceCSR) else up.get(next(it))
+        D = own_csr(D) if isinstance(D, DeviceCSR) else up.get(next(it))
         try:
-            first = build_edge_prolongator(A_n, dv.PendingCSR(up, 1), dv.PendingCSR(up, 0), D,
-                                           cfg.emin, shard=shard)
+            first = build_edge_prolongator(A_n, dv.PendingCSR(up, k + 1),
+                                           dv.PendingCSR(up, k), D, cfg.emin, shard=shard)
         except ValueError:
-            _check_nullspace(up.get(0), D, "the fine level", A=up.get(1), shard=shard)
+            _check_nullspace(up.get(k), D, "the fine level", A=up.get(k + 1), shard=shard)
             raise
-        A_e, S_e = up.get(1), up.get(0)
+        A_e, S_e = up.get(k + 1), up.get(k)
     else:
         # solver-owned wrappers: the SELL mirrors and shared index arrays
         # the setup attaches never land on the caller's DeviceCSR objects

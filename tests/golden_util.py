@@ -110,3 +110,20 @@ def check_values(M, arrays, key, fro=None):
 
 def pattern_sha(M):
     return sha(M.indptr.astype(np.int64), M.indices.astype(np.int64))
+
+
+def embed_in_pattern(M, P):
+    """M (pattern a subset of canonical CSR P's) on P's pattern with explicit
+    zeros at the entries M lacks; returns (embedded CSR, number of entries
+    added). Raises if M holds an entry outside P."""
+    M = sp.csr_matrix(M)
+    P = sp.csr_matrix(P)
+    n = np.int64(P.shape[1])
+    kp = np.repeat(np.arange(P.shape[0], dtype=np.int64), np.diff(P.indptr)) * n + P.indices
+    km = np.repeat(np.arange(M.shape[0], dtype=np.int64), np.diff(M.indptr)) * n + M.indices
+    pos = np.searchsorted(kp, km)
+    if pos.size and (pos.max() >= kp.size or not np.array_equal(kp[pos], km)):
+        raise AssertionError("pattern is not a subset")
+    data = np.zeros(P.nnz)
+    data[pos] = M.data
+    return sp.csr_matrix((data, P.indices, P.indptr), shape=P.shape), int(P.nnz - M.nnz)

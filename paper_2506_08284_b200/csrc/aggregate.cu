@@ -46,11 +46,13 @@ __device__ __forceinline__ void agg_st_release64(i64* p, i64 v) {
 // decided without a root decides "root". Deciding as early as the data
 // allows keeps the dependency depth at the wavefront depth (~2N on an N^3
 // mesh) instead of a chain through every lower node.
-#define AGG_LCAP 1024
+#define AGG_LCAP 256   // distinct lower distance-2 nodes held per warp
+#define AGG_HCAP 512   // open-addressing slots of the de-duplication set
 __global__ void __launch_bounds__(AGG_WARPS * 32)
     k_agg_roots(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci, int* state,
                 int* ticket) {
   __shared__ int lst[AGG_WARPS][AGG_LCAP];
+  __shared__ int hset[AGG_WARPS][AGG_HCAP];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   volatile int* vs = state;
   while (true) {
@@ -59,7 +61,14 @@ __global__ void __launch_bounds__(AGG_WARPS * 32)
     t = __shfl_sync(FULL_MASK, t, 0);
     if (t >= n) return;
     i64 i = t;
-    // lower distance-2 nodes (duplicates allowed); lanes over j in N[i]
+    // distinct lower distance-2 nodes; lanes over j in N[i]. A 27-point
+    // stencil lists each distance-2 node up to 8 times: a shared-memory
+    // hash set keeps first occurrences only (the wait below is order
+    // independent; a sort + unique pass here cost ~4x the rest of the kernel)
+    int* L = lst[w];
+    int* H = hset[w];
+    for (int a = lane; a < AGG_HCAP; a += 32) H[a] = -1;
+    __syncwarp();
     int cnt = 0;
     bool over = false;
     i64 js = rp[i], je = rp[i + 1];
@@ -73,11 +82,29 @@ __global__ void __launch_bounds__(AGG_WARPS * 32)
       for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL_MASK, mx, o));
       for (int u = 0; u < mx; u++) {
         int k = u < len ? ci[k0 + u] : 0x7fffffff;
-        bool low = k < i;
-        unsigned bal = __ballot_sync(FULL_MASK, low);
+        bool fresh = false;
+        if (k < i) {
+          unsigned h = ((unsigned)k * 2654435761u) >> 23;     // 9 bits: AGG_HCAP slots
+          int probe = 0;
+          for (; probe < AGG_HCAP; probe++) {
+            int cur = ((volatile int*)H)[h];
+            if (cur == k) break;
+            if (cur == -1) {
+              int old = atomicCAS(&H[h], -1, k);
+              if (old == -1) {
+                fresh = true;
+                break;
+              }
+              if (old == k) break;
+            }
+            h = (h + 1) & (AGG_HCAP - 1);
+          }
+          if (probe == AGG_HCAP) over = true;
+        }
+        unsigned bal = __ballot_sync(FULL_MASK, fresh);
         int o = cnt + __popc(bal & ((1u << lane) - 1));
-        if (low) {
-          if (o < AGG_LCAP) lst[w][o] = k;
+        if (fresh) {
+          if (o < AGG_LCAP) L[o] = k;
           else over = true;
         }
         cnt += __popc(bal);
@@ -87,38 +114,6 @@ __global__ void __launch_bounds__(AGG_WARPS * 32)
     __syncwarp();
     bool covered = false;
     if (!over) {
-      // distinct nodes only (a 27-point stencil lists each distance-2 node up
-      // to 8 times): sort, then keep first occurrences
-      int* L = lst[w];
-      int m = 1;
-      while (m < cnt) m <<= 1;
-      for (int a = cnt + lane; a < m; a += 32) L[a] = 0x7fffffff;
-      __syncwarp();
-      for (int size = 2; size <= m; size <<= 1)
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          for (int t2 = lane; t2 < (m >> 1); t2 += 32) {
-            int lo = ((t2 & ~(stride - 1)) << 1) | (t2 & (stride - 1)), hi = lo + stride;
-            bool up = (lo & size) == 0;
-            int a = L[lo], b = L[hi];
-            if ((a > b) == up) {
-              L[lo] = b;
-              L[hi] = a;
-            }
-          }
-          __syncwarp();
-        }
-      int u = 0;
-      for (int a0 = 0; a0 < cnt; a0 += 32) {
-        int a = a0 + lane;
-        int key = a < cnt ? L[a] : 0x7fffffff;
-        bool first = a < cnt && (a == 0 || L[a - 1] != key);
-        unsigned bal = __ballot_sync(FULL_MASK, first);
-        __syncwarp();
-        if (first) L[u + __popc(bal & ((1u << lane) - 1))] = key;
-        u += __popc(bal);
-        __syncwarp();
-      }
-      cnt = u;
       // wait: drop decided non-roots each rescan, stop at the first root
       while (true) {
         bool root = false;

@@ -202,81 +202,123 @@ extern "C" int sphc_maxabs(int64_t n, const double* x, double* out, void* stream
 // elements i = 16 q + l; chains combine as (l, l+2) within each 4-lane ymm,
 // then ymm0+ymm1, ymm2+ymm3, their sum, and a horizontal add; the n % 16 tail
 // is added unfused in index order.
-#define HSW_TILE 4096     // elements per shared-memory tile (x and y)
-#define HSW_THREADS 1024
+#define HSW_TILE 1024     // elements per shared-memory tile (x and y each)
+#define HSW_STAGES 4      // tiles in flight (64 KB of bulk copies hide HBM latency)
 
-// One CTA. Warps 1..31 stream the next tile of x and y into shared memory
-// (double buffered) while lanes 0..15 of warp 0 run the sixteen sequential
-// FMA chains over the current tile, so the chains, not HBM latency, set the
-// pace.
-__global__ void __launch_bounds__(HSW_THREADS)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+// One warp. Lane 0 keeps HSW_STAGES bulk copies (cp.async.bulk, the TMA's
+// 1-D path) of the next x / y tiles in flight, each completing on its
+// stage's mbarrier; lanes 0..15 run the sixteen sequential FMA chains over
+// the landed tile. The chains -- 1 dependent DFMA per 16 elements -- set the
+// pace, not the loads, and the kernel holds one warp and 64 KB of one SM, so
+// the setup's other kernels run beside it (nodal_amg.RhoEstimate).
+// Requires 16-byte aligned x, y (any torch allocation); else the caller takes
+// the plain-load variant.
+template <bool BULK>
+__global__ void __launch_bounds__(32)
     k_hsw_dot(i64 n, const double* __restrict__ x, const double* __restrict__ y, double* out) {
-  extern __shared__ double hsm[];  // [2][2][HSW_TILE]
-  int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ __align__(128) unsigned char hsw_raw[];
+  double* tiles = (double*)hsw_raw;                           // [STAGES][2][TILE]
+  unsigned long long* bars = (unsigned long long*)(tiles + (size_t)HSW_STAGES * 2 * HSW_TILE);
+  int lane = threadIdx.x;
   i64 n1 = n & ~(i64)15;
   i64 ntiles = (n1 + HSW_TILE - 1) / HSW_TILE;
   double acc = 0.0;
-  auto load = [&](i64 t, int buf, int t0, int nt) {
-    double* bx = hsm + (size_t)buf * 2 * HSW_TILE;
+  auto issue = [&](i64 t) {       // lane 0 (BULK) or the whole warp (!BULK)
+    int st = (int)(t % HSW_STAGES);
+    double* bx = tiles + (size_t)st * 2 * HSW_TILE;
     double* by = bx + HSW_TILE;
     i64 base = t * HSW_TILE;
-    for (int k = t0; k < HSW_TILE; k += nt) {
-      i64 i = base + k;
-      if (i < n1) {
-        bx[k] = x[i];
-        by[k] = y[i];
+    int m = (int)min((i64)HSW_TILE, n1 - base);
+    if (BULK) {
+      unsigned bytes = (unsigned)m * 8u, bar = smem_u32(&bars[st]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"(2u * bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(smem_u32(bx)), "l"(x + base), "r"(bytes), "r"(bar) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(smem_u32(by)), "l"(y + base), "r"(bytes), "r"(bar) : "memory");
+    } else {
+      for (int k = lane; k < m; k += 32) {
+        bx[k] = x[base + k];
+        by[k] = y[base + k];
       }
     }
   };
-  if (ntiles) load(0, 0, tid, HSW_THREADS);
-  __syncthreads();
+  if (BULK) {
+    if (lane == 0) {
+      for (int st = 0; st < HSW_STAGES; st++)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[st])));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    if (lane == 0)
+      for (i64 t = 0; t < ntiles && t < HSW_STAGES; t++) issue(t);
+  }
   for (i64 t = 0; t < ntiles; t++) {
-    if (warp != 0) {
-      if (t + 1 < ntiles) load(t + 1, (int)((t + 1) & 1), tid - 32, HSW_THREADS - 32);
-    } else if (lane < 16) {
-      const double* bx = hsm + (size_t)(t & 1) * 2 * HSW_TILE;
+    int st = (int)(t % HSW_STAGES);
+    if (BULK) {
+      unsigned bar = smem_u32(&bars[st]), parity = (unsigned)((t / HSW_STAGES) & 1), done = 0;
+      while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+            "selp.u32 %0, 1, 0, p; }"
+            : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    } else {
+      issue(t);
+      __syncwarp();
+    }
+    if (lane < 16) {
+      const double* bx = tiles + (size_t)st * 2 * HSW_TILE;
       const double* by = bx + HSW_TILE;
-      i64 cnt = n1 - t * HSW_TILE;
-      int m = cnt < HSW_TILE ? (int)cnt : HSW_TILE;
+      int m = (int)min((i64)HSW_TILE, n1 - t * HSW_TILE);
 #pragma unroll 8
       for (int k = lane; k < m; k += 16) acc = __fma_rn(bx[k], by[k], acc);
     }
-    __syncthreads();
+    __syncwarp();     // every chain is done with this stage before it is refilled
+    if (BULK && lane == 0 && t + HSW_STAGES < ntiles) issue(t + HSW_STAGES);
   }
-  if (warp == 0) {
-    double a[16];
+  double a[16];
 #pragma unroll
-    for (int l = 0; l < 16; l++) a[l] = __shfl_sync(FULL_MASK, acc, l);
-    if (lane == 0) {
-      double dot = 0.0;
-      if (n1) {
-        double h0[4], h1[4];
+  for (int l = 0; l < 16; l++) a[l] = __shfl_sync(FULL_MASK, acc, l);
+  if (lane == 0) {
+    double dot = 0.0;
+    if (n1) {
+      double h0[4], h1[4];
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-          h0[q] = __dadd_rn(a[4 * q + 0], a[4 * q + 2]);
-          h1[q] = __dadd_rn(a[4 * q + 1], a[4 * q + 3]);
-        }
-        double u0 = __dadd_rn(__dadd_rn(h0[0], h0[1]), __dadd_rn(h0[2], h0[3]));
-        double u1 = __dadd_rn(__dadd_rn(h1[0], h1[1]), __dadd_rn(h1[2], h1[3]));
-        dot = __dadd_rn(u0, u1);
+      for (int q = 0; q < 4; q++) {
+        h0[q] = __dadd_rn(a[4 * q + 0], a[4 * q + 2]);
+        h1[q] = __dadd_rn(a[4 * q + 1], a[4 * q + 3]);
       }
-      for (i64 i = n1; i < n; i++) dot = __dadd_rn(dot, __dmul_rn(y[i], x[i]));
-      *out = dot;
+      double u0 = __dadd_rn(__dadd_rn(h0[0], h0[1]), __dadd_rn(h0[2], h0[3]));
+      double u1 = __dadd_rn(__dadd_rn(h1[0], h1[1]), __dadd_rn(h1[2], h1[3]));
+      dot = __dadd_rn(u0, u1);
     }
+    for (i64 i = n1; i < n; i++) dot = __dadd_rn(dot, __dmul_rn(y[i], x[i]));
+    *out = dot;
   }
 }
 
 extern "C" int sphc_hsw_dot(int64_t n, const double* x, const double* y, double* out,
                             void* stream) {
   cudaStream_t s = as_stream(stream);
-  size_t sm = 4 * HSW_TILE * sizeof(double);
+  size_t sm = (size_t)HSW_STAGES * 2 * HSW_TILE * sizeof(double) + HSW_STAGES * 8;
   static bool attr = false;
   if (!attr) {
-    SPHC_CUDA(cudaFuncSetAttribute(k_hsw_dot, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SPHC_CUDA(cudaFuncSetAttribute(k_hsw_dot<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)sm));
+    SPHC_CUDA(cudaFuncSetAttribute(k_hsw_dot<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr = true;
   }
-  k_hsw_dot<<<1, HSW_THREADS, sm, s>>>(n, x, y, out);
+  bool aligned = (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
+  if (aligned) k_hsw_dot<true><<<1, 32, sm, s>>>(n, x, y, out);
+  else k_hsw_dot<false><<<1, 32, sm, s>>>(n, x, y, out);
   SPHC_LAUNCH_CHECK();
   return 0;
 }

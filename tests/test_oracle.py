@@ -253,8 +253,22 @@ def _check_device_config(name):
         assert pattern_sha(lv.P_e) == L["P_e_pattern"]
         check_values(lv.P_e, arrays, f"L{li}_Pe", L["P_e_fro"])
         assert np.allclose(lv.emin.energy_history, L["emin_energy"], rtol=1e-10, atol=0)
-    res = O.solve(h, rhs)
-    assert abs(res.iterations - meta["cheb"]["iterations"]) <= 1
+    ref = meta["cheb"]
+    if ref["status"] == "converged":
+        res = O.solve(h, rhs)
+        assert abs(res.iterations - ref["iterations"]) <= 1
+    else:
+        # the reference's own solve hits maxit here (near-singular coarsest
+        # operator under its LU solve, C5 recipe): the oracle must follow the
+        # same residual history over the first iterations (the 1e-10
+        # differences of the coarse operators grow through that solve: 3e-6
+        # after one iteration, 2e-4 after four, percents after nine)
+        k = 4
+        res = O.solve(h, rhs, maxit=k)
+        assert res.status == "maxit" and res.iterations == k
+        want = np.array(ref["residual_history"][:k + 1])
+        got = np.array(res.residual_history[:k + 1])
+        assert np.allclose(got, want, rtol=1e-3, atol=0), (got / want - 1)
 
 
 def test_oracle_device_config_c4s():

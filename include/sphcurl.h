@@ -175,6 +175,23 @@ int sphc_spgemm_fill_pair(int64_t n, const int64_t *arp, const int32_t *aci, con
                           int32_t *cci, double *cv1, double *cv2, int64_t max_cols,
                           int64_t *status, void *stream);
 
+/* Thin products (rows with few products and <= 32 distinct output columns:
+ * A_e D, S_e D, D^T (A D) -- csr_matmat call sites multigrid.py:103,111): one
+ * thread per output row with a private hash table in shared memory, products
+ * in scipy's order (bitwise csr_matmat). sphc_spgemm_count_thin counts every
+ * row (rows beyond 32 columns through the warp kernel; any_over: 1-int device
+ * scratch). sphc_spgemm_fill_thin fills every row: av2 / bv2 / cv2 non-NULL =
+ * the pair product on one pattern; `ordered` picks the warp kernels' ordered
+ * sums for the rows beyond 32 columns; max_cols as in sphc_spgemm_fill. */
+int sphc_spgemm_count_thin(int64_t n, const int64_t *arp, const int32_t *aci,
+                           const int64_t *brp, const int32_t *bci, int64_t *counts,
+                           int32_t *any_over, int64_t *status, void *stream);
+int sphc_spgemm_fill_thin(int64_t n, const int64_t *arp, const int32_t *aci, const double *av1,
+                          const double *av2, const int64_t *brp, const int32_t *bci,
+                          const double *bv1, const double *bv2, const int64_t *crp,
+                          int32_t *cci, double *cv1, double *cv2, int ordered,
+                          int64_t max_cols, int64_t *status, void *stream);
+
 /* Long-row variants (one CTA of 8 warps per output row) for products whose A
  * rows are long: the Galerkin R (A P) with R = P_e^T (150-2000 entries per
  * row, multigrid.py:150-151). Same outputs and capacity rule (<= 256 columns

@@ -402,9 +402,9 @@ template <bool ORDERED, bool PAIR>
 static int fill_launch(i64 n, const i64* arp, const int* aci, const double* av,
                        const double* av2, const i64* brp, const int* bci, const double* bv,
                        const double* bv2, const i64* crp, int* cci, double* cv, double* cv2,
-                       i64* status, cudaStream_t s, i64 max_cols) {
+                       i64* status, cudaStream_t s, i64 max_cols, int skip0 = 0) {
   int rc = fill_launch_c<ORDERED, PAIR, SpgSmall>(n, arp, aci, av, av2, brp, bci, bv, bv2, crp,
-                                                  cci, cv, cv2, status, s, 0);
+                                                  cci, cv, cv2, status, s, skip0);
   if (rc || (max_cols >= 0 && max_cols <= SpgSmall::CCAP)) return rc;
   return fill_launch_c<ORDERED, PAIR, SpgBig>(n, arp, aci, av, av2, brp, bci, bv, bv2, crp, cci,
                                               cv, cv2, status, s, SpgSmall::CCAP);
@@ -432,6 +432,210 @@ extern "C" int sphc_spgemm_fill_pair(int64_t n, const int64_t* arp, const int32_
   if (n <= 0) return 0;
   return fill_launch<false, true>(n, arp, aci, av1, av2, brp, bci, bv1, bv2, crp, cci, cv1,
                                   cv2, status, as_stream(stream), max_cols);
+}
+
+// ---------------------------------------------------------------------------
+// Thin rows: one THREAD per output row, for products whose rows have few
+// products and <= THIN_CAP distinct columns (A_e D, S_e D: 66 products and
+// ~18 columns per row; D^T (A D): ~108 and ~27). A warp per row left most
+// lanes idle on these and spent ~2,600 warp instructions per row on batch
+// bookkeeping; here a thread walks its row's products in scipy's order
+// (A entries ascending, each B row ascending, separate multiply and add --
+// bitwise csr_matmat, so ORDERED for free) into a private THIN_CAP-slot hash
+// table that lives in shared memory, transposed ([slot][thread]) so a warp's
+// accesses are conflict free whatever the slots. Rows with more distinct
+// columns are counted -1 and left to the warp kernels (the fill skips them
+// by their count).
+#define THIN_CAP 32
+#define THIN_TPB 128
+
+__device__ __forceinline__ unsigned thin_h(int col) {
+  return ((unsigned)col * 2654435761u) >> 27;    // 5 bits: THIN_CAP slots
+}
+
+// slot of col in the thread's table (inserting it), -1 if the table is full
+__device__ __forceinline__ int thin_slot(int (*keys)[THIN_TPB], int tid, int col, int& used) {
+  unsigned h = thin_h(col);
+  for (int p = 0; p < THIN_CAP; p++) {
+    int cur = keys[h][tid];
+    if (cur == col) return (int)h;
+    if (cur < 0) {
+      keys[h][tid] = col;
+      used++;
+      return (int)h;
+    }
+    h = (h + 1) & (THIN_CAP - 1);
+  }
+  return -1;
+}
+
+// only_missing: count only the rows another pass left at -1 (never here:
+// the thin pass runs first); counts[row] = -1 for rows beyond THIN_CAP.
+__global__ void __launch_bounds__(THIN_TPB)
+    k_spgemm_thin_count(i64 n, const i64* __restrict__ arp, const int* __restrict__ aci,
+                        const i64* __restrict__ brp, const int* __restrict__ bci,
+                        i64* __restrict__ counts, int* any_over) {
+  __shared__ int keys[THIN_CAP][THIN_TPB];
+  int tid = threadIdx.x;
+  for (i64 row = (i64)blockIdx.x * THIN_TPB + tid; row < n; row += (i64)gridDim.x * THIN_TPB) {
+#pragma unroll
+    for (int q = 0; q < THIN_CAP; q++) keys[q][tid] = -1;
+    int used = 0;
+    bool ok = true;
+    i64 ae = arp[row + 1];
+    for (i64 j = arp[row]; j < ae && ok; j++) {
+      int k = aci[j];
+      i64 be = brp[k + 1];
+      for (i64 q = brp[k]; q < be; q++)
+        if (thin_slot(keys, tid, bci[q], used) < 0) {
+          ok = false;
+          break;
+        }
+    }
+    counts[row] = ok ? used : -1;
+    if (!ok) *any_over = 1;
+  }
+}
+
+template <bool PAIR>
+__global__ void __launch_bounds__(THIN_TPB)
+    k_spgemm_thin_fill(i64 n, const i64* __restrict__ arp, const int* __restrict__ aci,
+                       const double* __restrict__ av, const double* __restrict__ av2,
+                       const i64* __restrict__ brp, const int* __restrict__ bci,
+                       const double* __restrict__ bv, const double* __restrict__ bv2,
+                       const i64* __restrict__ crp, int* __restrict__ cci,
+                       double* __restrict__ cv, double* __restrict__ cv2) {
+  extern __shared__ unsigned char thin_smem[];
+  int (*keys)[THIN_TPB] = (int (*)[THIN_TPB])thin_smem;
+  double (*acc)[THIN_TPB] = (double (*)[THIN_TPB])(thin_smem + sizeof(int) * THIN_CAP * THIN_TPB);
+  double (*acc2)[THIN_TPB] = PAIR ? acc + THIN_CAP : nullptr;
+  int tid = threadIdx.x;
+  for (i64 row = (i64)blockIdx.x * THIN_TPB + tid; row < n; row += (i64)gridDim.x * THIN_TPB) {
+    int nu = (int)(crp[row + 1] - crp[row]);
+    if (nu > THIN_CAP) continue;            // a warp-kernel row (> THIN_CAP columns)
+#pragma unroll
+    for (int q = 0; q < THIN_CAP; q++) keys[q][tid] = -1;
+    int used = 0;
+    i64 ae = arp[row + 1];
+    for (i64 j = arp[row]; j < ae; j++) {
+      int k = aci[j];
+      double a = av[j], a2 = PAIR ? av2[j] : 0.0;
+      i64 be = brp[k + 1];
+      for (i64 q = brp[k]; q < be; q++) {
+        int before = used;
+        int sl = thin_slot(keys, tid, bci[q], used);
+        double p1 = __dmul_rn(a, bv[q]);
+        double p2 = PAIR ? __dmul_rn(a2, bv2[q]) : 0.0;
+        if (used != before) {               // first term of this column: 0 + p
+          acc[sl][tid] = __dadd_rn(0.0, p1);
+          if (PAIR) acc2[sl][tid] = __dadd_rn(0.0, p2);
+        } else {
+          acc[sl][tid] = __dadd_rn(acc[sl][tid], p1);
+          if (PAIR) acc2[sl][tid] = __dadd_rn(acc2[sl][tid], p2);
+        }
+      }
+    }
+    // ascending columns: repeated minimum over the table
+    i64 o = crp[row];
+    int last = -1;
+    for (int t = 0; t < nu; t++) {
+      int best = 0x7fffffff, bs = 0;
+#pragma unroll
+      for (int q = 0; q < THIN_CAP; q++) {
+        int kq = keys[q][tid];
+        if (kq > last && kq < best) {
+          best = kq;
+          bs = q;
+        }
+      }
+      cci[o + t] = best;
+      cv[o + t] = acc[bs][tid];
+      if (PAIR) cv2[o + t] = acc2[bs][tid];
+      last = best;
+    }
+  }
+}
+
+// the warp kernel on the rows the thin pass left at -1 (none, usually)
+__global__ void __launch_bounds__(SPG_WARPS * 32)
+    k_spgemm_count_missing(i64 n, const i64* __restrict__ arp, const int* __restrict__ aci,
+                           const i64* __restrict__ brp, const int* __restrict__ bci,
+                           i64* __restrict__ counts, const int* any_over, i64* status) {
+  if (!*any_over) return;
+  __shared__ SpgCount sc[SPG_WARPS];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  SpgCount& S = sc[w];
+  for (i64 row = (i64)blockIdx.x * SPG_WARPS + w; row < n; row += (i64)gridDim.x * SPG_WARPS) {
+    if (counts[row] >= 0) continue;
+    int prods = spg_row_products(row, arp, aci, brp, lane);
+    int ts = pow2_at_least(2 * prods, 32);
+    if (ts > SPG_HCAP) ts = SPG_HCAP;
+    bool ok = spg_symbolic<SPG_STG, SPG_CCAP>(row, arp, aci, brp, bci, S.keys, ts, &S.ucount,
+                                              S.B, lane);
+    if (lane == 0) {
+      counts[row] = ok ? S.ucount : -1;
+      if (!ok) report(status, SPHC_ST_SPGEMM_CAPACITY, row);
+    }
+    __syncwarp();
+  }
+}
+
+extern "C" int sphc_spgemm_count_thin(int64_t n, const int64_t* arp, const int32_t* aci,
+                                      const int64_t* brp, const int32_t* bci, int64_t* counts,
+                                      int32_t* any_over, int64_t* status, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  SPHC_CUDA(cudaMemsetAsync(any_over, 0, sizeof(int32_t), s));
+  k_spgemm_thin_count<<<grid_for(n, THIN_TPB, SPHC_NUM_SMS * 16), THIN_TPB, 0, s>>>(
+      n, arp, aci, brp, bci, counts, any_over);
+  SPHC_LAUNCH_CHECK();
+  k_spgemm_count_missing<<<grid_for(n, SPG_WARPS, SPHC_NUM_SMS * 32), SPG_WARPS * 32, 0, s>>>(
+      n, arp, aci, brp, bci, counts, any_over, status);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+template <bool PAIR>
+static int thin_fill_launch(i64 n, const i64* arp, const int* aci, const double* av,
+                            const double* av2, const i64* brp, const int* bci, const double* bv,
+                            const double* bv2, const i64* crp, int* cci, double* cv, double* cv2,
+                            cudaStream_t s) {
+  size_t sm = (size_t)THIN_CAP * THIN_TPB * (sizeof(int) + (PAIR ? 2 : 1) * sizeof(double));
+  static bool attr = false;
+  if (!attr) {
+    SPHC_CUDA(cudaFuncSetAttribute(k_spgemm_thin_fill<PAIR>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr = true;
+  }
+  k_spgemm_thin_fill<PAIR><<<grid_for(n, THIN_TPB, SPHC_NUM_SMS * 16), THIN_TPB, sm, s>>>(
+      n, arp, aci, av, av2, brp, bci, bv, bv2, crp, cci, cv, cv2);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+// Thin rows by the thread-per-row kernel, the rest (max_cols > THIN_CAP; a
+// negative max_cols = unknown) by the warp kernels, which skip the thin rows.
+extern "C" int sphc_spgemm_fill_thin(int64_t n, const int64_t* arp, const int32_t* aci,
+                                     const double* av1, const double* av2, const int64_t* brp,
+                                     const int32_t* bci, const double* bv1, const double* bv2,
+                                     const int64_t* crp, int32_t* cci, double* cv1,
+                                     double* cv2, int ordered, int64_t max_cols,
+                                     int64_t* status, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  int rc = av2 ? thin_fill_launch<true>(n, arp, aci, av1, av2, brp, bci, bv1, bv2, crp, cci, cv1,
+                                        cv2, s)
+               : thin_fill_launch<false>(n, arp, aci, av1, nullptr, brp, bci, bv1, nullptr, crp,
+                                         cci, cv1, nullptr, s);
+  if (rc || (max_cols >= 0 && max_cols <= THIN_CAP)) return rc;
+  if (av2)
+    return fill_launch<false, true>(n, arp, aci, av1, av2, brp, bci, bv1, bv2, crp, cci, cv1,
+                                    cv2, status, s, max_cols, THIN_CAP);
+  if (ordered)
+    return fill_launch<true, false>(n, arp, aci, av1, nullptr, brp, bci, bv1, nullptr, crp, cci,
+                                    cv1, nullptr, status, s, max_cols, THIN_CAP);
+  return fill_launch<false, false>(n, arp, aci, av1, nullptr, brp, bci, bv1, nullptr, crp, cci,
+                                   cv1, nullptr, status, s, max_cols, THIN_CAP);
 }
 
 // ---------------------------------------------------------------------------

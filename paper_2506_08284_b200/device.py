@@ -603,6 +603,29 @@ def _long_rows(A):
     return A.shape[0] > 0 and A.nnz >= LONG_ROW * A.shape[0]
 
 
+THIN_PRODUCTS = float(os.environ.get("SPHC_THIN_PRODUCTS", "160"))
+
+
+def _thin_rows(A, B):
+    """Products with few multiplications per output row (A_e D, S_e D,
+    D^T (A D): mean row products nnz(A)/rows(A) x nnz(B)/rows(B) below
+    THIN_PRODUCTS) go to the thread-per-row kernels (sphc_spgemm_*_thin);
+    no host sync: sizes are known."""
+    if A.shape[0] == 0 or B.shape[0] == 0 or THIN_PRODUCTS <= 0:
+        return False
+    return (A.nnz / A.shape[0]) * (B.nnz / B.shape[0]) <= THIN_PRODUCTS
+
+
+_ANY_OVER = {}
+
+
+def _any_over(dev):
+    t = _ANY_OVER.get(dev)
+    if t is None:
+        t = _ANY_OVER[dev] = torch.zeros(1, dtype=torch.int32, device=dev)
+    return t
+
+
 def _rows(A, lo):
     """Row-pointer view starting at row lo (absolute positions into A's
     column / value arrays, so a kernel launched on it computes rows lo..)."""
@@ -692,9 +715,14 @@ def spgemm(A, B, drop=True, ordered=False, shard=None):
     cnt = torch.empty(n, dtype=torch.int64, device=A.rowptr.device)
     blocks = shard.blocks(n) if shard is not None else [(0, 0, n)]
     long_rows = _long_rows(A) and not ordered
+    thin = not long_rows and _thin_rows(A, B)
     for _, lo, hi in blocks:
-        call("sphc_spgemm_count_long" if long_rows else "sphc_spgemm_count", hi - lo,
-             _rows(A, lo), A.col, B.rowptr, B.col, cnt[lo:], st.t)
+        if thin:
+            call("sphc_spgemm_count_thin", hi - lo, _rows(A, lo), A.col, B.rowptr, B.col,
+                 cnt[lo:], _any_over(cnt.device), st.t)
+        else:
+            call("sphc_spgemm_count_long" if long_rows else "sphc_spgemm_count", hi - lo,
+                 _rows(A, lo), A.col, B.rowptr, B.col, cnt[lo:], st.t)
     if shard is not None:
         shard.gather_ranges(cnt, shard.bounds(n))
         shard.min_(st.t)
@@ -702,7 +730,10 @@ def spgemm(A, B, drop=True, ordered=False, shard=None):
     ci = torch.empty(nnz, dtype=torch.int32, device=A.rowptr.device)
     v = empty_f64(nnz)
     for _, lo, hi in blocks:
-        if long_rows:
+        if thin:
+            call("sphc_spgemm_fill_thin", hi - lo, _rows(A, lo), A.col, A.val, None, B.rowptr,
+                 B.col, B.val, None, rp[lo:], ci, v, None, int(ordered), mcols, st.t)
+        elif long_rows:
             call("sphc_spgemm_fill_long", hi - lo, _rows(A, lo), A.col, A.val, None, B.rowptr,
                  B.col, B.val, None, rp[lo:], ci, v, None)
         else:
@@ -742,9 +773,14 @@ def spgemm_pair(A1, A2, B1, B2, drop=True, shard=None):
     cnt = torch.empty(n, dtype=torch.int64, device=A1.rowptr.device)
     blocks = shard.blocks(n) if shard is not None else [(0, 0, n)]
     long_rows = _long_rows(A1)
+    thin = not long_rows and _thin_rows(A1, B1)
     for _, lo, hi in blocks:
-        call("sphc_spgemm_count_long" if long_rows else "sphc_spgemm_count", hi - lo,
-             _rows(A1, lo), A1.col, B1.rowptr, B1.col, cnt[lo:], st.t)
+        if thin:
+            call("sphc_spgemm_count_thin", hi - lo, _rows(A1, lo), A1.col, B1.rowptr, B1.col,
+                 cnt[lo:], _any_over(cnt.device), st.t)
+        else:
+            call("sphc_spgemm_count_long" if long_rows else "sphc_spgemm_count", hi - lo,
+                 _rows(A1, lo), A1.col, B1.rowptr, B1.col, cnt[lo:], st.t)
     if shard is not None:
         shard.gather_ranges(cnt, shard.bounds(n))
         shard.min_(st.t)
@@ -752,7 +788,10 @@ def spgemm_pair(A1, A2, B1, B2, drop=True, shard=None):
     ci = torch.empty(nnz, dtype=torch.int32, device=A1.rowptr.device)
     v1, v2 = empty_f64(nnz), empty_f64(nnz)
     for _, lo, hi in blocks:
-        if long_rows:
+        if thin:
+            call("sphc_spgemm_fill_thin", hi - lo, _rows(A1, lo), A1.col, A1.val, A2.val,
+                 B1.rowptr, B1.col, B1.val, B2.val, rp[lo:], ci, v1, v2, 0, mcols, st.t)
+        elif long_rows:
             call("sphc_spgemm_fill_long", hi - lo, _rows(A1, lo), A1.col, A1.val, A2.val,
                  B1.rowptr, B1.col, B1.val, B2.val, rp[lo:], ci, v1, v2)
         else:

@@ -14,9 +14,11 @@ host build of the same rows (oracle/host_assembly.py).
 
 value = edge DOFs/s of setup + solve with the inputs resident in HBM; e2e = the
 same through the public API with host (scipy / numpy) inputs and the solution
-copied back, host<->device copies inside the timed region. Multi-GPU (torchrun):
-every rank solves its own replica (weak scaling, no data-path collective --
-DESIGN.md "Multi-GPU"); timing is the max over ranks.
+copied back, host<->device copies inside the timed region. Multi-GPU (torchrun,
+--gpus N): ONE problem, row-block sharded setup + row-block partitioned solve
+(strong scaling; neighbour halo exchanges and all-reduced PCG scalars over
+NCCL -- DESIGN.md "Multi-GPU"); --replicas runs N independent replicas instead
+(weak scaling, no data-path collective). Timing is the max over ranks.
 
 --impl reference times the reference algorithm's CPU implementation (the
 oracle port in oracle/, Gauss-Seidel smoother as in the reference) on rank 0,

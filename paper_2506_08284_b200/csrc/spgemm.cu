@@ -982,6 +982,10 @@ __global__ void __launch_bounds__(SPG_GT)
     atomicAdd(&ucount, mine);
     __syncthreads();
     int nu = ucount;
+    // every thread holds nu before thread 0 reuses the counter below (a
+    // late reader saw 0 or a partial collect count: its sort loops then ran
+    // a different number of barriers -- an intermittent hang)
+    __syncthreads();
     if (!FILL) {
       if (threadIdx.x == 0) counts[row] = nu;
       __syncthreads();

@@ -99,34 +99,69 @@ extern "C" int sphc_pattern_union_fill(int64_t n, const int64_t* arp, const int3
 // w_i = sum over j DESCENDING of fl(fl(dinv_i a_ij) x_j), sequential from 0
 // (DESC false: in storage order, scipy csr_matvec on any row order; dinv
 // null: the stored values as they are)
+// One thread per row keeps the sequential sum; the 32 rows of a warp are one
+// contiguous CSR segment, staged in shared memory with coalesced loads first
+// (a thread walking its own row straight from global memory reads 32 lines
+// per step: 0.58 TB/s on the 57M-entry A_n of 128^3, ~10x under HBM speed, in
+// the middle of the power method's serial chain). Segments beyond PMV_WCAP
+// entries (irregular coarse rows) are read directly.
+#define PMV_WCAP 1024
+#define PMV_WARPS 4
 template <bool DESC>
-__global__ void k_nodal_powmv(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
-                              const double* __restrict__ v, const double* __restrict__ dinv,
-                              const double* __restrict__ x, double* __restrict__ y) {
-  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (i64)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    i64 b = rp[i], e = rp[i + 1];
-    if (dinv) {
-      double inv = dinv[i];
-      for (i64 t = 0; t < e - b; t++) {
-        i64 j = DESC ? e - 1 - t : b + t;
-        s = __dadd_rn(s, __dmul_rn(__dmul_rn(inv, v[j]), x[ci[j]]));
-      }
-    } else {
-      for (i64 t = 0; t < e - b; t++) {
-        i64 j = DESC ? e - 1 - t : b + t;
-        s = __dadd_rn(s, __dmul_rn(v[j], x[ci[j]]));
+__global__ void __launch_bounds__(PMV_WARPS * 32)
+    k_nodal_powmv(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
+                  const double* __restrict__ v, const double* __restrict__ dinv,
+                  const double* __restrict__ x, double* __restrict__ y) {
+  __shared__ int sc[PMV_WARPS][PMV_WCAP];
+  __shared__ double sv[PMV_WARPS][PMV_WCAP];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (i64 row0 = ((i64)blockIdx.x * PMV_WARPS + w) * 32; row0 < n;
+       row0 += (i64)gridDim.x * PMV_WARPS * 32) {
+    i64 i = row0 + lane;
+    bool act = i < n;
+    i64 b = act ? rp[i] : 0, e = act ? rp[i + 1] : 0;
+    i64 s0 = __shfl_sync(FULL_MASK, b, 0);
+    i64 last = row0 + 32 < n ? row0 + 32 : n;
+    i64 s1 = rp[last];
+    int tot = (int)min(s1 - s0, (i64)PMV_WCAP + 1);
+    bool staged = tot <= PMV_WCAP;
+    if (staged) {
+      for (int t = lane; t < tot; t += 32) {
+        sc[w][t] = ci[s0 + t];
+        sv[w][t] = v[s0 + t];
       }
     }
-    y[i] = s;
+    __syncwarp();
+    if (act) {
+      double s = 0.0;
+      int len = (int)(e - b);
+      double inv = dinv ? dinv[i] : 0.0;
+      if (staged) {
+        const int* c = sc[w] + (b - s0);
+        const double* a = sv[w] + (b - s0);
+        for (int t = 0; t < len; t++) {
+          int j = DESC ? len - 1 - t : t;
+          double aj = dinv ? __dmul_rn(inv, a[j]) : a[j];
+          s = __dadd_rn(s, __dmul_rn(aj, x[c[j]]));
+        }
+      } else {
+        for (int t = 0; t < len; t++) {
+          i64 j = DESC ? e - 1 - t : b + t;
+          double aj = dinv ? __dmul_rn(inv, v[j]) : v[j];
+          s = __dadd_rn(s, __dmul_rn(aj, x[ci[j]]));
+        }
+      }
+      y[i] = s;
+    }
+    __syncwarp();
   }
 }
 
 extern "C" int sphc_nodal_powmv(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
                                 const double* dinv, const double* x, double* y, void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_nodal_powmv<true><<<grid_for(n, 128), 128, 0, s>>>(n, rp, ci, v, dinv, x, y);
+  k_nodal_powmv<true><<<grid_for(n, PMV_WARPS * 32), PMV_WARPS * 32, 0, s>>>(n, rp, ci, v, dinv,
+                                                                           x, y);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -135,7 +170,8 @@ extern "C" int sphc_spmv_stored_order(int64_t n, const int64_t* rp, const int32_
                                       const double* v, const double* x, double* y,
                                       void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_nodal_powmv<false><<<grid_for(n, 128), 128, 0, s>>>(n, rp, ci, v, nullptr, x, y);
+  k_nodal_powmv<false><<<grid_for(n, PMV_WARPS * 32), PMV_WARPS * 32, 0, s>>>(n, rp, ci, v,
+                                                                            nullptr, x, y);
   SPHC_LAUNCH_CHECK();
   return 0;
 }

@@ -205,46 +205,53 @@ def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
             ends.append((min(a, b), max(a, b)))
             I.append(len(ends) - 1)
         final[i] = I
+    # appended ids per repaired row (ascending); the rows' full patterns are
+    # their original rows plus these
+    extras = {i: [e for e in I if e >= n0] for i, I in final.items()}
     new_edges = list(range(n0, len(ends)))
+    state = None
     if new_edges:
-        # post pass (emin_setup.py:311-333)
-        aff = set()
+        # post pass (emin_setup.py:311-333), vectorised: a row sees appended
+        # edge e iff its J holds both ends, i.e. iff it lies in both R_dp
+        # columns -- the (row, edge) pairs come straight from the column
+        # intersections, sorted by row then edge
+        rr, ee = [], []
         for e in new_edges:
             a, b = ends[e]
             ka = column(a)[0]
-            aff.update(ka[_isect_sorted(ka, column(b)[0])[0]].tolist())
-        aff = sorted(aff)
-        rows_T = dict(zip(aff, _rows(T, aff)))
-        rows_I = dict(zip(aff, _rows(pattern, aff)))
-        emptyish = (flag_h & 2).astype(bool)
-        by_node = {}                             # endpoint -> appended edges
-        for e in new_edges:
-            for n in ends[e]:
-                by_node.setdefault(n, []).append(e)
+            rows_e = ka[_isect_sorted(ka, column(b)[0])[0]]
+            rr.append(rows_e)
+            ee.append(np.full(rows_e.size, e, dtype=np.int64))
+        rr, ee = np.concatenate(rr), np.concatenate(ee)
+        order = np.lexsort((ee, rr))
+        rr, ee = rr[order], ee[order]
+        aff, start, cnt = np.unique(rr, return_index=True, return_counts=True)
+        # original pattern lengths of the affected rows (one gather)
+        aff_d = torch.from_numpy(aff).to(dev)
+        len0 = (pattern.rowptr[aff_d + 1] - pattern.rowptr[aff_d]).cpu().numpy()
+        emptyish = (flag_h[aff] & 2).astype(bool)
+        repaired = np.isin(aff, need_rows)
+        # rows the main loop left empty stay empty; every other row that was
+        # not repaired grows by all the edges it sees
+        grown = ~repaired & ~(emptyish & (len0 == 0))
         post = []
-        for i in aff:
-            J, I0 = rows_T[i][0], rows_I[i][0]
-            prev = final.get(i)
-            if prev is None and emptyish[i] and I0.size == 0:
-                continue                         # a row the main loop left empty
-            Jl = J.tolist()
-            Jset = set(Jl)
-            add = sorted({e for n in Jl for e in by_node.get(n, ())
-                          if ends[e][0] in Jset and ends[e][1] in Jset})
-            I1 = sorted(set(I0.tolist()) | set(add))
-            if len(I1) == len(prev if prev is not None else I0):
-                continue
-            # grown rows: the reference re-checks them in ascending order and
-            # repairs the reducible ones. The check runs on the device (the
-            # refill pass flags them, emin_setup.setup_constraints); only the
-            # flagged rows come back here (finish_post_pass), in the same
-            # order, so the appended edge ids are the reference's.
-            final[i] = I1
+        for x in np.flatnonzero(grown):
+            i = int(aff[x])
+            extras[i] = ee[start[x]:start[x] + cnt[x]].tolist()
             post.append(i)
-        state = _PostState(ends, final, n0, {i: rows_T[i][0] for i in post}, repair)
-    else:
-        state = None
-    cg2, xrp, xeid = _extras(cg, ends, final, n0, n_e, dev)
+        for x in np.flatnonzero(repaired):       # few: the main loop's rows
+            i = int(aff[x])
+            merged = sorted(set(extras[i]) | set(ee[start[x]:start[x] + cnt[x]].tolist()))
+            if len(merged) > len(extras[i]):
+                extras[i] = merged
+                post.append(i)
+        # grown rows: the reference re-checks them in ascending order and
+        # repairs the reducible ones. The check runs on the device (the
+        # refill pass flags them, emin_setup.setup_constraints); only the
+        # flagged rows come back here (finish_post_pass), in the same
+        # order, so the appended edge ids are the reference's.
+        state = _PostState(ends, extras, n0, set(post), repair, T, pattern)
+    cg2, xrp, xeid = _extras(cg, ends, extras, n0, n_e, dev)
     return cg2, xrp, xeid, len(ends) - n0, state
 
 
@@ -252,35 +259,38 @@ class _PostState:
     """What finish_post_pass needs to repair the post-pass rows the device
     found reducible."""
 
-    def __init__(self, ends, final, n0, J, repair):
-        self.ends, self.final, self.n0, self.J, self.repair = ends, final, n0, J, repair
+    def __init__(self, ends, extras, n0, post, repair, T, pattern):
+        self.ends, self.extras, self.n0, self.post = ends, extras, n0, post
+        self.repair, self.T, self.pattern = repair, T, pattern
 
 
 def finish_post_pass(state, rows, cg0, n_e):
     """Repair the post-pass rows the device flagged reducible, ascending
     (emin_setup.py:311-333: further edges stay local to the row). Returns the
     augmented coarse gradient and per-row extras like make_irreducible_pass."""
-    for i in sorted(int(r) for r in rows):
-        if i not in state.J:
+    rows = sorted(int(r) for r in rows)
+    for i in rows:
+        if i not in state.post:
             raise RuntimeError(f"fine edge {i}: reducible after the make_irreducible pass "
                                "(internal error)")
-        state.final[i] = state.repair(i, list(state.final[i]), state.J[i])
+    Js = _rows(state.T, rows)
+    I0s = _rows(state.pattern, rows)
+    for i, (J, _), (I0, _) in zip(rows, Js, I0s):
+        I = state.repair(i, I0.tolist() + list(state.extras[i]), J)
+        state.extras[i] = [e for e in I if e >= state.n0]
     dev = cg0.ep_a.device
-    cg2, xrp, xeid = _extras(cg0, state.ends, state.final, state.n0, n_e, dev)
+    cg2, xrp, xeid = _extras(cg0, state.ends, state.extras, state.n0, n_e, dev)
     return cg2, xrp, xeid, len(state.ends) - state.n0
 
 
-def _extras(cg, ends, final, n0, n_e, dev):
+def _extras(cg, ends, extras, n0, n_e, dev):
     """Per-row extras (appended ids of each repaired row, ascending) and
     the coarse gradient with the appended edges."""
+    rows = sorted(i for i, ex in extras.items() if ex)
     counts = np.zeros(n_e, dtype=np.int64)
-    items = []
-    import bisect
-    for i in sorted(final):
-        fi = final[i]                   # ascending: original ids, then appended
-        ex = fi[bisect.bisect_left(fi, n0):]
-        counts[i] = len(ex)
-        items.extend(ex)
+    if rows:
+        counts[np.asarray(rows, dtype=np.int64)] = [len(extras[i]) for i in rows]
+    items = [e for i in rows for e in extras[i]]
     xrp_h = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
     xrp = torch.from_numpy(xrp_h).to(dev)
     xeid = torch.from_numpy(np.asarray(items, dtype=np.int32)).to(dev)

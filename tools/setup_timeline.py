@@ -32,6 +32,17 @@ for a, d, st, n in k:
     busy += max(0.0, a + d - max(a, cur)); cur = max(cur, a + d)
 print(f"setup GPU span {(tend - t0) / 1e3:.1f} ms, busy (union) {busy / 1e3:.1f} ms, "
       f"sum of kernel times {sum(d for _, d, _, _ in k) / 1e3:.1f} ms")
+# idle gaps (GPU waiting for the host) with the kernels around them
+gaps, cur, prev = [], t0, None
+for a, d, st, n in k:
+    if a > cur:
+        gaps.append((a - cur, prev, n, cur - t0))
+    if a + d > cur:
+        cur, prev = a + d, n
+gaps.sort(reverse=True)
+print(f"{len(gaps)} gaps, total {sum(g[0] for g in gaps) / 1e3:.1f} ms; largest:")
+for g, p_, n_, at in gaps[:int(os.environ.get("TOPGAPS", "12"))]:
+    print(f"   {g / 1e3:6.2f} ms at {at / 1e3:7.1f}: {str(p_)[:38]} -> {n_[:38]}")
 mn = float(os.environ.get("MIN_MS", "0.4")) * 1e3
 for a, d, st, n in k:
     if d >= mn:

@@ -118,3 +118,51 @@ def test_aggregation_high_degree_nodes():
     memb, n_agg = O.aggregate(O.strength_pattern(G))
     assert agg.n_agg == n_agg
     assert np.array_equal(agg.membership.cpu().numpy(), memb)
+
+
+def test_thin_spgemm_is_bitwise_scipy():
+    """The thread-per-row kernels (sphc_spgemm_*_thin: products with few
+    multiplications per row, <= 32 distinct columns) walk their products in
+    scipy's csr_matmat order, so even the unordered entry points are bitwise
+    scipy; rows beyond 32 columns fall to the warp kernels (TOL there), rows
+    with no entries and empty B rows included. Pair product likewise."""
+    from paper_2506_08284_b200 import device as dv
+    # a gradient-like B (<= 2 entries per row, some rows empty)
+    rng = np.random.default_rng(11)
+    n, m = 5000, 1800
+    A = _rand(n, 4000, 9, 2)
+    A.data[A.indptr[17]:A.indptr[18]] = 0.0      # an empty A row
+    A.eliminate_zeros()
+    bi, bj, bv = [], [], []
+    for r in range(4000):
+        k = rng.integers(0, 3)
+        c = rng.choice(m, size=k, replace=False)
+        bi += [r] * k
+        bj += list(c)
+        bv += list(rng.choice([-1.0, 1.0], size=k))
+    B = sp.csr_matrix((bv, (bi, bj)), shape=(4000, m))
+    B.sort_indices()
+    assert dv._thin_rows(dv.DeviceCSR.from_scipy(A), dv.DeviceCSR.from_scipy(B))
+    ref = (A @ B).tocsr()
+    ref.sort_indices()
+    dA, dB = dv.DeviceCSR.from_scipy(A), dv.DeviceCSR.from_scipy(B)
+    C = dv.spgemm(dA, dB, drop=False).to_scipy()
+    assert csr_hash(C) == csr_hash(ref)
+    A2 = A.copy()
+    A2.data = A2.data * 0.25 - 3.0
+    C1, C2 = dv.spgemm_pair(dA, dv.DeviceCSR.from_scipy(A2), dB, dB, drop=False)
+    ref2 = (A2 @ B).tocsr()
+    ref2.sort_indices()
+    assert csr_hash(C1.to_scipy()) == csr_hash(ref) and csr_hash(C2.to_scipy()) == csr_hash(ref2)
+    # mixed: a few A rows reach > 32 distinct columns -> warp kernels for those
+    Ab = _rand(3000, 4000, 9, 5, dense_rows=(3, 1500, 2999), dense_len=60)
+    dAb = dv.DeviceCSR.from_scipy(Ab)
+    assert dv._thin_rows(dAb, dB)
+    refb = (Ab @ B).tocsr()
+    refb.sort_indices()
+    assert np.diff(refb.indptr).max() > 32
+    Cb = dv.spgemm(dAb, dB, drop=False).to_scipy()
+    assert np.array_equal(Cb.indptr, refb.indptr) and np.array_equal(Cb.indices, refb.indices)
+    assert rel_max_diff(Cb, refb) <= 1e-14
+    Co = dv.spgemm(dAb, dB, drop=False, ordered=True).to_scipy()
+    assert csr_hash(Co) == csr_hash(refb)

@@ -620,9 +620,12 @@ _ANY_OVER = {}
 
 
 def _any_over(dev):
-    t = _ANY_OVER.get(dev)
+    """One-int device scratch of the thin count pass, per (device, stream):
+    virtual-rank threads drive their own streams."""
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    t = _ANY_OVER.get(key)
     if t is None:
-        t = _ANY_OVER[dev] = torch.zeros(1, dtype=torch.int32, device=dev)
+        t = _ANY_OVER[key] = torch.zeros(1, dtype=torch.int32, device=dev)
     return t
 
 

@@ -397,7 +397,9 @@ class AsyncUpload:
             direct = [own and a.dtype == np.dtype(d) and pinned_in_place(a)
                       for (a, d), own in zip(self.specs, self.owned)]
             from concurrent.futures import ThreadPoolExecutor
-            with ThreadPoolExecutor(self.nthreads) as ex, torch.cuda.stream(self.stream):
+            # small systems: one copy thread (a pool costs more than it saves)
+            nthreads = self.nthreads if self.nbytes >= (64 << 20) else 1
+            with ThreadPoolExecutor(nthreads) as ex, torch.cuda.stream(self.stream):
                 futs = []
                 for idx, ((a, d), o, dr) in enumerate(zip(self.specs, self.offs, direct)):
                     isz = np.dtype(d).itemsize

@@ -67,6 +67,17 @@ def test_hsw_dot_bitwise():
         xt = torch.from_numpy(x).cuda()
         call("sphc_hsw_dot", n, xt, xt, out)
         assert out.item() == hsw_dot(x, x), n
+    # two different vectors; tile boundaries of the TMA pipeline (1024-element
+    # tiles, 4 stages); a source that is only 8-byte aligned takes the
+    # plain-load variant of the kernel
+    for n in (1023, 1024, 1040, 4096, 4097 + 16, 5 * 1024 + 7, 300_001):
+        x = rng.standard_normal(n + 1)
+        y = rng.standard_normal(n + 1) * np.exp(rng.standard_normal(n + 1))
+        xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        call("sphc_hsw_dot", n, xt, yt, out)
+        assert out.item() == hsw_dot(x[:n], y[:n]), n
+        call("sphc_hsw_dot", n, xt[1:], yt[1:], out)          # misaligned by 8 bytes
+        assert out.item() == hsw_dot(x[1:n + 1], y[1:n + 1]), n
 
 
 @pytest.mark.parametrize("lanes", [1, 2, 4, 8, 16, 32])

@@ -334,11 +334,12 @@ def ctypes_void(p):
 
 class AsyncUpload:
     """Host -> device upload of scipy CSR matrices in the background: a
-    helper thread casts / copies the arrays into one pinned staging buffer
-    with a small pool of threads (numpy releases the GIL) and queues the DMAs
-    on a side stream; ``get(k)`` makes the caller's stream wait on the copy
-    event (no host sync). The caller keeps launching device work meanwhile
-    (build_hierarchy runs the nodal chain while A_e and S arrive)."""
+    helper thread casts / copies the arrays chunk by chunk into a ring of
+    pinned staging slots with a small pool of threads (numpy releases the
+    GIL) and queues each chunk's DMA on a side stream; ``get(k)`` makes the
+    caller's stream wait on matrix k's copy event (no host sync). The caller
+    keeps launching device work meanwhile (build_hierarchy runs the nodal
+    chain while S and A_e arrive)."""
 
     def __init__(self, mats, nthreads=8):
         dev = device()
@@ -376,57 +377,81 @@ class AsyncUpload:
         self.csr = [None] * nm
 
     CHUNK = 1 << 25          # staging granularity (bytes)
+    SLOTS = 16               # ring of pinned chunks (512 MB, whatever the inputs' size)
 
     def _run(self):
         try:
             torch.cuda.set_device(self.dev)
-            prev = _STAGE.get("event")
-            if prev is not None:
-                prev.synchronize()             # the buffer's previous DMAs are done
-            buf = _STAGE.get("buf")
-            if buf is None or buf.numel() < self.nbytes:
-                buf = torch.empty(max(self.nbytes, 1 << 24), dtype=torch.uint8,
-                                  pin_memory=True)
-                _STAGE["buf"] = buf
-            hv = buf.numpy()
+            ring = _STAGE.get("ring")
+            if ring is None:
+                ring = _STAGE["ring"] = torch.empty(self.SLOTS * self.CHUNK, dtype=torch.uint8,
+                                                    pin_memory=True)
+                _STAGE["slot_events"] = [None] * self.SLOTS
+            slot_ev = _STAGE["slot_events"]
+            hv = ring.numpy()
             # arrays already in the device dtype DMA straight from the
             # caller's page-locked memory (opt-in); the rest are cast into
-            # staging chunk by chunk, and each chunk's DMA is queued as soon
-            # as its host copy is done, so the copies of later chunks (and
-            # of S) overlap the transfers of earlier ones (and of A_e)
+            # the ring chunk by chunk by a small pool of threads, and each
+            # chunk's DMA is queued as soon as its host copy is done, so the
+            # copies of later chunks (and of A_e) overlap the transfers of
+            # earlier ones (and of S). A slot is reused once its DMA is done.
             direct = [own and a.dtype == np.dtype(d) and pinned_in_place(a)
                       for (a, d), own in zip(self.specs, self.owned)]
+            chunks = []              # (array index, first element, elements, last of array)
+            for idx, ((a, d), dr) in enumerate(zip(self.specs, direct)):
+                if dr or not a.size:
+                    chunks.append((idx, 0, 0, True))
+                    continue
+                per = max(1, self.CHUNK // np.dtype(d).itemsize)
+                for k in range(0, a.size, per):
+                    n = min(per, a.size - k)
+                    chunks.append((idx, k, n, k + n == a.size))
             from concurrent.futures import ThreadPoolExecutor
             # small systems: one copy thread (a pool costs more than it saves)
             nthreads = self.nthreads if self.nbytes >= (64 << 20) else 1
+            depth = min(self.SLOTS, 2 * nthreads)
+
+            def stage(c, slot):
+                idx, k, n, _ = chunks[c]
+                a, d = self.specs[idx]
+                dstv = hv[slot * self.CHUNK:slot * self.CHUNK + n * np.dtype(d).itemsize].view(d)
+                np.copyto(dstv, a[k:k + n], casting="unsafe")
+
             with ThreadPoolExecutor(nthreads) as ex, torch.cuda.stream(self.stream):
-                futs = []
-                for idx, ((a, d), o, dr) in enumerate(zip(self.specs, self.offs, direct)):
-                    isz = np.dtype(d).itemsize
-                    if dr or not a.size:
-                        futs.append((None, idx, 0, 0, True))
-                        continue
-                    dstv = hv[o:o + a.size * isz].view(d)
-                    per = max(1, self.CHUNK // isz)
-                    for k in range(0, a.size, per):
-                        n = min(per, a.size - k)
-                        f = ex.submit(np.copyto, dstv[k:k + n], a[k:k + n], casting="unsafe")
-                        futs.append((f, idx, k * isz, n * isz, k + n == a.size))
-                for f, idx, rel, nb, last in futs:
+                futs = {}
+                submitted = issued = 0
+                nslot = 0                      # staged chunks so far (slot = nslot % SLOTS)
+                slot_of = {}
+                while issued < len(chunks):
+                    while submitted < len(chunks) and submitted - issued < depth:
+                        if chunks[submitted][2]:
+                            slot = nslot % self.SLOTS
+                            nslot += 1
+                            if slot_ev[slot] is not None:
+                                slot_ev[slot].synchronize()      # its last DMA is done
+                            slot_of[submitted] = slot
+                            futs[submitted] = ex.submit(stage, submitted, slot)
+                        submitted += 1
+                    idx, k, n, last = chunks[issued]
                     a, d = self.specs[idx]
-                    if f is None:
-                        if a.size:
-                            call("sphc_copy_h2d", self.dst[idx], a, a.nbytes)
-                    else:
-                        f.result()
-                        o = self.offs[idx] + rel
-                        self.dst[idx].view(torch.uint8)[rel:rel + nb].copy_(
-                            buf[o:o + nb], non_blocking=True)
-                    if last and idx % 3 == 2:          # a matrix's last array is queued
+                    if n:
+                        futs.pop(issued).result()
+                        slot = slot_of.pop(issued)
+                        isz = np.dtype(d).itemsize
+                        self.dst[idx].view(torch.uint8)[k * isz:(k + n) * isz].copy_(
+                            ring[slot * self.CHUNK:slot * self.CHUNK + n * isz],
+                            non_blocking=True)
+                        ev = slot_ev[slot]
+                        if ev is None:
+                            ev = slot_ev[slot] = torch.cuda.Event()
+                        ev.record(self.stream)
+                    elif a.size:               # direct (page-locked caller array)
+                        call("sphc_copy_h2d", self.dst[idx], a, a.nbytes)
+                    if last and idx % 3 == 2:  # a matrix's last array is queued
                         m = idx // 3
                         self.events[m].record(self.stream)
                         self.ready[m].set()
-            _STAGE["event"] = self.event
+                    issued += 1
             # direct sources stay referenced (self.mats) until get() has
             # made the compute stream wait on the copies; keep them alive
             # past that too, until the copies are done

@@ -178,6 +178,43 @@ def _retire_inflight():
         _INFLIGHT.pop(0)
 
 
+_COPY_POOL = []
+
+
+def parallel_copyto(dst, src, nthreads=8):
+    """np.copyto(dst, src, casting="unsafe") split over a few threads for
+    large arrays (numpy releases the GIL; a fresh destination's page faults
+    spread over the threads too)."""
+    n = dst.size
+    if n * dst.itemsize < (8 << 20):
+        np.copyto(dst, src, casting="unsafe")
+        return
+    if not _COPY_POOL:
+        from concurrent.futures import ThreadPoolExecutor
+        _COPY_POOL.append(ThreadPoolExecutor(nthreads))
+    step = -(-n // nthreads)
+    list(_COPY_POOL[0].map(lambda k: np.copyto(dst[k:k + step], src[k:k + step],
+                                               casting="unsafe"), range(0, n, step)))
+
+
+def to_host(t):
+    """Device tensor -> new numpy array through a pinned staging buffer (one
+    DMA at pinned-memory bandwidth, then a threaded copy out); waits for the
+    current stream."""
+    t = t.contiguous()
+    nbytes = t.numel() * t.element_size()
+    if nbytes < (1 << 20):
+        return t.cpu().numpy()
+    buf = _PINNED.get("d2h")
+    if buf is None or buf.numel() < nbytes:
+        buf = _PINNED["d2h"] = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    buf[:nbytes].copy_(t.view(-1).view(torch.uint8), non_blocking=True)
+    call("sphc_stream_sync")
+    out = np.empty(t.numel(), dtype=_NP[t.dtype])
+    parallel_copyto(out, buf[:nbytes].numpy().view(_NP[t.dtype]))
+    return out.reshape(tuple(t.shape))
+
+
 def upload(a, dtype, dev=None, owned=True):
     """Host array -> new device tensor through a reused pinned staging buffer
     (one cast on the host, one DMA at pinned-memory bandwidth).
@@ -212,7 +249,7 @@ def upload(a, dtype, dev=None, owned=True):
         buf = torch.empty(max(nbytes, 1 << 24), dtype=torch.uint8, pin_memory=True)
         _PINNED["buf"] = buf
     host = buf[:nbytes].numpy().view(dtype)
-    np.copyto(host, a, casting="unsafe")
+    parallel_copyto(host, a.reshape(-1))
     t.view(torch.uint8).copy_(buf[:nbytes], non_blocking=True)
     if ev is None:
         ev = _PINNED["event"] = torch.cuda.Event()

@@ -953,7 +953,7 @@ def pcg_solve(A, b, precond, rtol=1e-8, maxit=500):
     nb = math.sqrt(bb)
 
     def out(v):
-        return v.cpu().numpy() if host else v.clone()
+        return dv.to_host(v) if host else v.clone()
 
     if nb == 0.0:
         return PcgResult(out(x), 0, [0.0], [0.0], "converged", 0.0)

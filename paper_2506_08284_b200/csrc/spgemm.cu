@@ -516,12 +516,31 @@ __global__ void __launch_bounds__(THIN_TPB)
 #pragma unroll
     for (int q = 0; q < THIN_CAP; q++) keys[q][tid] = -1;
     int used = 0;
-    i64 ae = arp[row + 1];
-    for (i64 j = arp[row]; j < ae; j++) {
-      int k = aci[j];
-      double a = av[j], a2 = PAIR ? av2[j] : 0.0;
-      i64 be = brp[k + 1];
-      for (i64 q = brp[k]; q < be; q++) {
+    i64 aj = arp[row], ae = arp[row + 1];
+    // the next A entry and its B-row bounds are loaded while the current B
+    // row is accumulated (the chain A col -> B bounds -> B entries is
+    // otherwise exposed once per A entry: only ~8 warps per SM run here)
+    int kn = 0;
+    double an = 0.0, an2 = 0.0;
+    i64 bsn = 0, ben = 0;
+    if (aj < ae) {
+      kn = aci[aj];
+      an = av[aj];
+      if (PAIR) an2 = av2[aj];
+      bsn = brp[kn];
+      ben = brp[kn + 1];
+    }
+    for (i64 j = aj; j < ae; j++) {
+      double a = an, a2 = an2;
+      i64 bs = bsn, be = ben;
+      if (j + 1 < ae) {
+        kn = aci[j + 1];
+        an = av[j + 1];
+        if (PAIR) an2 = av2[j + 1];
+        bsn = brp[kn];
+        ben = brp[kn + 1];
+      }
+      for (i64 q = bs; q < be; q++) {
         int before = used;
         int sl = thin_slot(keys, tid, bci[q], used);
         double p1 = __dmul_rn(a, bv[q]);

@@ -438,6 +438,8 @@ def _check_nullspace(S, D, where, A=None, shard=None):
     as S) the product A D is formed in the same pass and returned for the
     level's D^T A D."""
     AD = None
+    if A is not None:
+        A, S = _work_pair(A, S)
     if A is not None and dv.same_pattern(A, S):
         AD, SD = dv.spgemm_pair(A, S, D, D, drop=False, shard=shard)
         # (stored zeros of A D only feed D^T A D; see _make_level)
@@ -651,14 +653,46 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
     return Hierarchy(levels=levels, coarse_factorization=inv, operator_complexity=oc)
 
 
+def _work_pair(A, S):
+    """The undropped, shared-pattern versions of a Galerkin pair (see
+    _galerkin_edge), else the matrices themselves."""
+    wa, ws = getattr(A, "_work", None), getattr(S, "_work", None)
+    if wa is not None and ws is not None and wa.rowptr is ws.rowptr and wa.col is ws.col:
+        return wa, ws
+    return A, S
+
+
 def _galerkin_edge(A_e, S_e, P_e, R_e, shard=None):
-    """compress(P^T (A P)) for A_e and S_e (multigrid.py:150-151)."""
-    if dv.same_pattern(A_e, S_e):
+    """compress(P^T (A P)) for A_e and S_e (multigrid.py:150-151).
+
+    The two products share one pattern and one pass. ``compress`` then drops
+    each product's exact zeros, and a handful of round-off-sized entries of
+    P^T (S P) do cancel exactly (2 of 25.9M at 128^3), which would split the
+    patterns and send every later product of the pair through two separate
+    passes. The returned (compressed) matrices therefore carry their
+    undropped shared-pattern versions as ``_work``: the next level's pair
+    products and null-space check run on those (stored zeros add nothing to
+    any sum and cancel again in the products' own compress), and release
+    them."""
+    Aw, Sw = _work_pair(A_e, S_e)
+    if dv.same_pattern(Aw, Sw):
         # one pass for both: P^T (A_e P) and P^T (S_e P) share patterns
-        AP, SP = dv.spgemm_pair(A_e, S_e, P_e, P_e, drop=False, shard=shard)
-        return dv.spgemm_pair(R_e, R_e, AP, SP, shard=shard)
-    return (dv.spgemm(R_e, dv.spgemm(A_e, P_e, shard=shard), shard=shard),
-            dv.spgemm(R_e, dv.spgemm(S_e, P_e, shard=shard), shard=shard))
+        AP, SP = dv.spgemm_pair(Aw, Sw, P_e, P_e, drop=False, shard=shard)
+        C1w, C2w = dv.spgemm_pair(R_e, R_e, AP, SP, drop=False, shard=shard)
+        C1, C2 = dv.drop_zeros_many(C1w, C2w)
+        if C1 is not C1w or C2 is not C2w:
+            if C1 is C1w:          # keep the visible matrix free of the attribute cycle
+                C1 = DeviceCSR(C1w.rowptr, C1w.col, C1w.val, C1w.shape)
+            if C2 is C2w:
+                C2 = DeviceCSR(C2w.rowptr, C2w.col, C2w.val, C2w.shape)
+            C1._work, C2._work = C1w, C2w
+    else:
+        C1 = dv.spgemm(R_e, dv.spgemm(A_e, P_e, shard=shard), shard=shard)
+        C2 = dv.spgemm(R_e, dv.spgemm(S_e, P_e, shard=shard), shard=shard)
+    for M in (A_e, S_e):           # the inputs' work copies are spent
+        if getattr(M, "_work", None) is not None:
+            M._work = None
+    return C1, C2
 
 
 @checked

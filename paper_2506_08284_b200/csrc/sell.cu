@@ -258,6 +258,150 @@ extern "C" int sphc_sell_cheb_step(int64_t n, const int64_t* slice_ptr, const in
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Delta-coded columns for the streamed operators. A row's sorted columns are
+// stored as 16-bit differences to the previous one (the first column of every
+// row in a 32-bit array; padding repeats the last column: delta 0, value 0),
+// so a pass moves 10 instead of 12 bytes per stored entry -- the V-cycle's
+// A_e passes run at the HBM roofline, so fewer bytes is the only lever left.
+// Same entries, same order, same fma chain: bitwise the 32-bit kernels.
+// Eligible when every difference fits 16 bits (sphc_sell_fill16 reports it):
+// true for the 128^3 mesh numbering (largest jump ~3 N^2 = 49.9k).
+__global__ void k_sell_fill16(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
+                              const i64* __restrict__ sp, unsigned short* __restrict__ d16,
+                              int* __restrict__ c0, int* too_big, int rect) {
+  bool big = false;
+  for (i64 row = (i64)blockIdx.x * blockDim.x + threadIdx.x; row < ((n + 31) & ~(i64)31);
+       row += (i64)gridDim.x * blockDim.x) {
+    i64 s = row / SELL_C;
+    int r = (int)(row % SELL_C);
+    int w = (int)((sp[s + 1] - sp[s]) / SELL_C);
+    i64 base = sp[s] + r;
+    int len = 0;
+    i64 j0 = 0;
+    if (row < n) {
+      j0 = rp[row];
+      len = (int)(rp[row + 1] - j0);
+    }
+    int prev = len ? ci[j0] : ((row < n && !rect) ? (int)row : 0);
+    if (row < n) c0[row] = prev;
+    for (int j = 0; j < w; j++) {
+      int c = j < len ? ci[j0 + j] : prev;
+      int d = c - prev;
+      big |= d < 0 || d > 65535;
+      d16[base + (i64)j * SELL_C] = (unsigned short)d;
+      prev = c;
+    }
+  }
+  if (big) *too_big = 1;
+}
+
+extern "C" int sphc_sell_fill16(int64_t n, const int64_t* rp, const int32_t* ci,
+                                const int64_t* slice_ptr, uint16_t* d16, int32_t* c0,
+                                int32_t* too_big, int rect, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  SPHC_CUDA(cudaMemsetAsync(too_big, 0, sizeof(int32_t), s));
+  k_sell_fill16<<<grid_for(n, 256), 256, 0, s>>>(n, rp, ci, slice_ptr, d16, c0, too_big, rect);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+// one thread's row: the column runs along with the 16-bit differences
+__device__ __forceinline__ double sell_row16(i64 base, int w, int c,
+                                             const unsigned short* __restrict__ d16,
+                                             const double* __restrict__ sv,
+                                             const double* __restrict__ x) {
+  constexpr int U = 4;
+  double acc = 0.0;
+  for (int j0 = 0; j0 < w; j0 += U) {
+    unsigned short d[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      int j = j0 + u;
+      d[u] = 0;
+      v[u] = 0.0;
+      if (j < w) {
+        i64 o = base + (i64)j * SELL_C;
+        v[u] = __ldcs(sv + o);
+        d[u] = __ldcs(d16 + o);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (j0 + u < w) {
+        c += d[u];
+        acc = fma(v[u], __ldg(x + c), acc);
+      }
+  }
+  return acc;
+}
+
+// y = alpha A x + beta z (streamed operators, one warp per slice)
+__global__ void __launch_bounds__(SELL_PER_BLOCK, 8)
+    k_sell_spmv16(i64 n, const i64* __restrict__ sp, const unsigned short* __restrict__ d16,
+                  const int* __restrict__ c0, const double* __restrict__ sv,
+                  const double* __restrict__ x, double alpha, double beta, const double* z,
+                  double* y) {
+  pdl_begin();
+  i64 row = (i64)blockIdx.x * SELL_PER_BLOCK + threadIdx.x;
+  if (row >= n) return;
+  i64 s = row >> 5;
+  i64 b0 = sp[s];
+  int w = (int)((sp[s + 1] - b0) / SELL_C);
+  double acc = sell_row16(b0 + (threadIdx.x & 31), w, c0[row], d16, sv, x);
+  double r = alpha * acc;
+  if (z) r = fma(beta, z[row], r);
+  y[row] = r;
+}
+
+// d <- cd d + cr dinv (b - A x_in); x_out = x_in + d
+__global__ void __launch_bounds__(SELL_PER_BLOCK, 8)
+    k_sell_cheb16(i64 n, const i64* __restrict__ sp, const unsigned short* __restrict__ d16,
+                  const int* __restrict__ c0, const double* __restrict__ sv,
+                  const double* __restrict__ dinv, const double* __restrict__ b,
+                  const double* __restrict__ x_in, double* __restrict__ x_out,
+                  double* __restrict__ d, double cd, double cr) {
+  pdl_begin();
+  i64 row = (i64)blockIdx.x * SELL_PER_BLOCK + threadIdx.x;
+  if (row >= n) return;
+  i64 s = row >> 5;
+  i64 b0 = sp[s];
+  int w = (int)((sp[s + 1] - b0) / SELL_C);
+  double ax = sell_row16(b0 + (threadIdx.x & 31), w, c0[row], d16, sv, x_in);
+  double r = b[row] - ax;
+  double dn = cr * dinv[row] * r;
+  if (cd != 0.0) dn = fma(cd, d[row], dn);
+  d[row] = dn;
+  x_out[row] = x_in[row] + dn;
+}
+
+extern "C" int sphc_sell_spmv16(int64_t n, const int64_t* slice_ptr, const uint16_t* d16,
+                                const int32_t* c0, const double* sv, const double* x,
+                                double alpha, double beta, const double* z, double* y,
+                                void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  unsigned g = (unsigned)((n + SELL_PER_BLOCK - 1) / SELL_PER_BLOCK);
+  launch_pdl(k_sell_spmv16, g, SELL_PER_BLOCK, 0, s, n, slice_ptr, d16, c0, sv, x, alpha, beta, z,
+             y);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int sphc_sell_cheb_step16(int64_t n, const int64_t* slice_ptr, const uint16_t* d16,
+                                     const int32_t* c0, const double* sv, const double* dinv,
+                                     const double* b, const double* x_in, double* x_out,
+                                     double* d, double cd, double cr, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  unsigned g = (unsigned)((n + SELL_PER_BLOCK - 1) / SELL_PER_BLOCK);
+  launch_pdl(k_sell_cheb16, g, SELL_PER_BLOCK, 0, s, n, slice_ptr, d16, c0, sv, dinv, b, x_in,
+             x_out, d, cd, cr);
+  SPHC_LAUNCH_CHECK();
+  return 0;
+}
+
 // Hiptmair mid step (multigrid.py:164-173, between the nodal correction and
 // the second edge sweep): x1 = x + D c, then the first Chebyshev step of the
 // next edge sweep taken from the residual r = b - A x the caller already
@@ -284,6 +428,44 @@ __global__ void __launch_bounds__(SELL_PER_BLOCK, (STREAM && K == 1) ? 8 : 5)
   double dn = cr * dinv[row] * (r[row] - adc);
   d[row] = dn;
   x_out[row] = (x_in[row] + u) + dn;
+}
+
+// the same step on delta-coded columns of A D (one warp per slice)
+__global__ void __launch_bounds__(SELL_PER_BLOCK, 8)
+    k_sell_hipt_mid16(i64 n, const i64* __restrict__ sp, const unsigned short* __restrict__ d16,
+                      const int* __restrict__ c0, const double* __restrict__ sv,
+                      const i64* __restrict__ drp, const int* __restrict__ dci,
+                      const double* __restrict__ dvv, const double* __restrict__ dinv,
+                      const double* __restrict__ r, const double* __restrict__ c,
+                      const double* __restrict__ x_in, double* __restrict__ x_out,
+                      double* __restrict__ d, double cr) {
+  pdl_begin();
+  i64 row = (i64)blockIdx.x * SELL_PER_BLOCK + threadIdx.x;
+  if (row >= n) return;
+  i64 s = row >> 5;
+  i64 b0 = sp[s];
+  int w = (int)((sp[s + 1] - b0) / SELL_C);
+  double adc = sell_row16(b0 + (threadIdx.x & 31), w, c0[row], d16, sv, c);
+  i64 j0 = drp[row], j1 = drp[row + 1];
+  double u = 0.0;
+  for (i64 j = j0; j < j1; j++) u = fma(dvv[j], __ldg(c + dci[j]), u);
+  double dn = cr * dinv[row] * (r[row] - adc);
+  d[row] = dn;
+  x_out[row] = (x_in[row] + u) + dn;
+}
+
+extern "C" int sphc_sell_hipt_mid16(int64_t n, const int64_t* slice_ptr, const uint16_t* d16,
+                                    const int32_t* c0, const double* sv, const int64_t* drp,
+                                    const int32_t* dci, const double* dv, const double* dinv,
+                                    const double* r, const double* c, const double* x_in,
+                                    double* x_out, double* d, double cr, void* stream) {
+  if (n <= 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  unsigned g = (unsigned)((n + SELL_PER_BLOCK - 1) / SELL_PER_BLOCK);
+  launch_pdl(k_sell_hipt_mid16, g, SELL_PER_BLOCK, 0, s, n, slice_ptr, d16, c0, sv, drp, dci, dv,
+             dinv, r, c, x_in, x_out, d, cr);
+  SPHC_LAUNCH_CHECK();
+  return 0;
 }
 
 extern "C" int sphc_sell_hipt_mid(int64_t n, const int64_t* slice_ptr, const int32_t* sci,

@@ -884,10 +884,14 @@ class SellMirror:
     col: torch.Tensor         # int32 [padded entries]
     val: torch.Tensor         # float64 [padded entries]
     n: int
+    # streamed operators: 16-bit column differences + first column per row
+    # (sphc_sell_fill16), None when not built / not representable
+    d16: torch.Tensor = None
+    c0: torch.Tensor = None
 
     @property
     def padded(self):
-        return int(self.col.numel())
+        return int(self.val.numel())
 
 
 def _sell_key(A):
@@ -918,6 +922,15 @@ def sell(A):
     v = empty_f64(tot)
     call("sphc_sell_fill", n, A.rowptr, A.col, A.val, sp_, ci, v)
     m = SellMirror(sp_, ci, v, n)
+    if SELL16 and tot * 12 > SELL16_MIN_BYTES and ns >= 148 * 48:
+        # operators streamed from HBM by one warp per slice: delta-coded
+        # columns (10 instead of 12 bytes per entry), if they fit 16 bits
+        d16 = torch.empty(tot, dtype=torch.int16, device=A.rowptr.device)
+        c0 = torch.empty(n, dtype=torch.int32, device=A.rowptr.device)
+        big = torch.empty(1, dtype=torch.int32, device=A.rowptr.device)
+        call("sphc_sell_fill16", n, A.rowptr, A.col, sp_, d16, c0, big, 0)
+        if int(readback(big)[0][0]) == 0:
+            m.d16, m.c0 = d16, c0
     A._sell, A._sell_key = m, _sell_key(A)
     return m
 
@@ -933,7 +946,20 @@ def sell_rect(A):
     ci = torch.empty(tot, dtype=torch.int32, device=A.rowptr.device)
     v = empty_f64(tot)
     call("sphc_sell_fill_rect", n, A.rowptr, A.col, A.val, sp_, ci, v)
-    return SellMirror(sp_, ci, v, n)
+    m = SellMirror(sp_, ci, v, n)
+    if SELL16 and tot * 12 > SELL16_MIN_BYTES and ns >= 148 * 48:
+        d16 = torch.empty(tot, dtype=torch.int16, device=A.rowptr.device)
+        c0 = torch.empty(n, dtype=torch.int32, device=A.rowptr.device)
+        big = torch.empty(1, dtype=torch.int32, device=A.rowptr.device)
+        call("sphc_sell_fill16", n, A.rowptr, A.col, sp_, d16, c0, big, 1)
+        if int(readback(big)[0][0]) == 0:
+            m.d16, m.c0 = d16, c0
+            m.col = None          # only the delta-coded kernel reads this mirror
+    return m
+
+
+SELL16 = os.environ.get("SPHC_SELL16", "1") != "0"
+SELL16_MIN_BYTES = 48 << 20          # the kernels' streaming threshold (csrc/sell.cu)
 
 
 CTA_ROW_MAX_ROWS = int(os.environ.get("SPHC_CTA_ROW_MAX_ROWS", "4096"))
@@ -944,7 +970,11 @@ def spmv(A, x, y, alpha=1.0, beta=0.0, z=None, lanes=None):
     """y = alpha A x + beta z (on A's SELL mirror when it has a current one)."""
     m = sell_mirror(A)
     if m is not None:
-        call("sphc_sell_spmv", m.n, m.slice_ptr, m.col, m.val, x, alpha, beta, z, y, m.padded)
+        if m.d16 is not None:
+            call("sphc_sell_spmv16", m.n, m.slice_ptr, m.d16, m.c0, m.val, x, alpha, beta, z, y)
+        else:
+            call("sphc_sell_spmv", m.n, m.slice_ptr, m.col, m.val, x, alpha, beta, z, y,
+                 m.padded)
         return y
     if lanes is None:
         lanes = A.lanes()

@@ -243,7 +243,10 @@ class ChebyshevSweeper:
                 out = self.buf[0] if cur is not self.buf[0] else self.buf[1]
                 z = x_zero and step == 0
                 m = self.sell
-                if m is not None:
+                if m is not None and m.d16 is not None and not z:
+                    call("sphc_sell_cheb_step16", n, m.slice_ptr, m.d16, m.c0, m.val, self.dinv,
+                         b, cur, out, self.d, cd, cr)
+                elif m is not None:
                     call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, self.dinv, b,
                          None if z else cur, out, self.d, cd, cr, int(z), m.padded)
                 else:
@@ -264,8 +267,12 @@ class ChebyshevSweeper:
         n = self.A.shape[0]
         out = self.buf[0] if x is not self.buf[0] else self.buf[1]
         _, cr = self.coefs[0]
-        call("sphc_sell_hipt_mid", n, mid.slice_ptr, mid.col, mid.val, D.rowptr, D.col, D.val,
-             self.dinv, r, c, x, out, self.d, cr, mid.padded)
+        if mid.d16 is not None:
+            call("sphc_sell_hipt_mid16", n, mid.slice_ptr, mid.d16, mid.c0, mid.val, D.rowptr,
+                 D.col, D.val, self.dinv, r, c, x, out, self.d, cr)
+        else:
+            call("sphc_sell_hipt_mid", n, mid.slice_ptr, mid.col, mid.val, D.rowptr, D.col,
+                 D.val, self.dinv, r, c, x, out, self.d, cr, mid.padded)
         return out
 
     def _steps_from(self, cur, b, first):
@@ -273,8 +280,12 @@ class ChebyshevSweeper:
         n, m = self.A.shape[0], self.sell
         for cd, cr in self.coefs[first:]:
             out = self.buf[0] if cur is not self.buf[0] else self.buf[1]
-            call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, self.dinv, b, cur, out,
-                 self.d, cd, cr, 0, m.padded)
+            if m.d16 is not None:
+                call("sphc_sell_cheb_step16", n, m.slice_ptr, m.d16, m.c0, m.val, self.dinv, b,
+                     cur, out, self.d, cd, cr)
+            else:
+                call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, self.dinv, b, cur,
+                     out, self.d, cd, cr, 0, m.padded)
             cur = out
         return cur
 

@@ -135,3 +135,73 @@ def test_hiptmair_mid_step_matches_unfused(config, N, dirichlet_like):
     r1 = mg.pcg_solve(h1.levels[0].A_e, b, mg.v_cycle_preconditioner(h1))
     assert r0.status == r1.status == "converged"
     assert abs(r0.iterations - r1.iterations) <= 1, (r0.iterations, r1.iterations)
+
+
+def test_delta_coded_sell_kernels_are_bitwise():
+    """sphc_sell_spmv16 / sphc_sell_cheb_step16 (16-bit column differences)
+    against the 32-bit SELL kernels on a streamed operator (A_e of a 48^3
+    jittered mesh): same entries, order and fma chain, so bitwise equal; a
+    matrix with a column jump beyond 16 bits is reported as not
+    representable and keeps its 32-bit columns."""
+    from paper_2506_08284_b200 import device as dv
+    from paper_2506_08284_b200._lib import call
+    from paper_2506_08284_b200.assembly import assemble_hex
+    N = 48
+    rng = np.random.default_rng(3)
+    s = assemble_hex(N, 1e-2, False, rng.uniform(-0.2 / N, 0.2 / N, ((N - 1) ** 3, 3)))
+    A = dv.own_csr(s.A_e)
+    n = A.shape[0]
+    old = dv.SELL16_MIN_BYTES
+    try:
+        dv.SELL16_MIN_BYTES = 0
+        m = dv.sell(A)
+    finally:
+        dv.SELL16_MIN_BYTES = old
+    assert m.d16 is not None and m.c0 is not None
+    x = torch.from_numpy(rng.uniform(-1, 1, n)).cuda()
+    b = torch.from_numpy(rng.uniform(-1, 1, n)).cuda()
+    dinv = dv.reciprocal(dv.diagonal(A))
+    y0, y1 = torch.empty_like(x), torch.empty_like(x)
+    call("sphc_sell_spmv", n, m.slice_ptr, m.col, m.val, x, -1.0, 1.0, b, y0, m.padded)
+    call("sphc_sell_spmv16", n, m.slice_ptr, m.d16, m.c0, m.val, x, -1.0, 1.0, b, y1)
+    assert torch.equal(y0, y1)
+    d0 = torch.from_numpy(rng.uniform(-1, 1, n)).cuda()
+    d1 = d0.clone()
+    o0, o1 = torch.empty_like(x), torch.empty_like(x)
+    call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, dinv, b, x, o0, d0, 0.3, 0.7, 0,
+         m.padded)
+    call("sphc_sell_cheb_step16", n, m.slice_ptr, m.d16, m.c0, m.val, dinv, b, x, o1, d1, 0.3,
+         0.7)
+    assert torch.equal(o0, o1) and torch.equal(d0, d1)
+    # the fused Hiptmair mid step on delta-coded columns of A D
+    D = dv.own_csr(s.D)
+    AD = dv.spgemm(A, D, drop=False)
+    old16 = dv.SELL16
+    try:
+        dv.SELL16 = False
+        m32 = dv.sell_rect(AD)
+        dv.SELL16, dv.SELL16_MIN_BYTES = True, 0
+        m16 = dv.sell_rect(AD)
+    finally:
+        dv.SELL16, dv.SELL16_MIN_BYTES = old16, old
+    assert m32.d16 is None and m16.d16 is not None
+    c = torch.from_numpy(rng.uniform(-1, 1, D.shape[1])).cuda()
+    r = torch.from_numpy(rng.uniform(-1, 1, n)).cuda()
+    o0, o1 = torch.empty_like(x), torch.empty_like(x)
+    e0, e1 = torch.empty_like(x), torch.empty_like(x)
+    call("sphc_sell_hipt_mid", n, m32.slice_ptr, m32.col, m32.val, D.rowptr, D.col, D.val, dinv,
+         r, c, x, o0, e0, 0.7, m32.padded)
+    call("sphc_sell_hipt_mid16", n, m16.slice_ptr, m16.d16, m16.c0, m16.val, D.rowptr, D.col,
+         D.val, dinv, r, c, x, o1, e1, 0.7)
+    assert torch.equal(o0, o1) and torch.equal(e0, e1)
+    # a far-apart pair of columns in one row: not representable
+    import scipy.sparse as sp
+    B = sp.identity(300_000, format="lil")
+    B[5, 299_999] = 2.0
+    dB = dv.DeviceCSR.from_scipy(B.tocsr())
+    try:
+        dv.SELL16_MIN_BYTES = 0
+        mb = dv.sell(dB)
+    finally:
+        dv.SELL16_MIN_BYTES = old
+    assert mb.d16 is None

@@ -306,12 +306,18 @@ extern "C" int sphc_sell_fill16(int64_t n, const int64_t* rp, const int32_t* ci,
   return 0;
 }
 
+// entries per load group: 6 keeps ~50% more bytes in flight than the 32-bit
+// kernels' 4 at the same 32 registers (C4: 0.4065 -> 0.3865 ms per pass; 8
+// measures the same; packing two differences per word measured slower)
+#ifndef SELL16_U
+#define SELL16_U 6
+#endif
 // one thread's row: the column runs along with the 16-bit differences
 __device__ __forceinline__ double sell_row16(i64 base, int w, int c,
                                              const unsigned short* __restrict__ d16,
                                              const double* __restrict__ sv,
                                              const double* __restrict__ x) {
-  constexpr int U = 4;
+  constexpr int U = SELL16_U;
   double acc = 0.0;
   for (int j0 = 0; j0 < w; j0 += U) {
     unsigned short d[U];

@@ -216,12 +216,12 @@ def cheb_kernel_bytes(A):
     return 12 * A.nnz + 8 * (n + 1) + 8 * 6 * n
 
 
-def cheb_kernel_bytes_coded(A):
+def cheb_kernel_bytes_coded(A, nbase=1):
     """The same step on delta-coded columns (csrc/sell.cu k_sell_cheb16): 8 B
     of value + 2 B of column difference per entry, 4 B of first column per
     row, the slice pointers, the same six vector passes."""
     n = A.shape[0]
-    return 10 * A.nnz + 4 * n + 8 * (n // 32 + 2) + 8 * 6 * n
+    return 10 * A.nnz + 4 * nbase * n + 8 * (n // 32 + 2) + 8 * 6 * n
 
 
 def vcycle_bytes_moved(h, degree=3):
@@ -536,7 +536,7 @@ def run_ours(args):
         def kstep():
             if coded:
                 _lib.call("sphc_sell_cheb_step16", n_e, m0.slice_ptr, m0.d16, m0.c0, m0.val,
-                          sw.dinv, b, x0, sw.buf[0], sw.d, cd, cr)
+                          sw.dinv, b, x0, sw.buf[0], sw.d, cd, cr, m0.nbase)
             else:
                 _lib.call("sphc_sell_cheb_step", n_e, m0.slice_ptr, m0.col, m0.val, sw.dinv, b,
                           x0, sw.buf[0], sw.d, cd, cr, 0, m0.padded)
@@ -563,7 +563,7 @@ def run_ours(args):
     # hardware utilisation is judged on the bytes of the format the kernel
     # reads (delta-coded columns: 10 B per entry); the survey's 12 B formula
     # is reported beside it
-    kbytes_fmt = (cheb_kernel_bytes_coded(A0) if (not gs_mode and coded) else kbytes)
+    kbytes_fmt = (cheb_kernel_bytes_coded(A0, m0.nbase) if (not gs_mode and coded) else kbytes)
     vmoved = vcycle_bytes_moved(h, scfg.cheb_degree) if not gs_mode else vbytes
     # the main roofline is already at scale (> L2) for C3-C5
     at_scale = (None if args.no_scale_roofline or args.config in DEVICE_INPUTS

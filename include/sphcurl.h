@@ -238,28 +238,31 @@ int sphc_sell_fill(int64_t n, const int64_t *rp, const int32_t *ci, const double
                    const int64_t *slice_ptr, int32_t *sci, double *sv, void *stream);
 /* Delta-coded columns of a SELL mirror for the streamed operators: d16 holds
  * each stored entry's column as a 16-bit difference to the previous entry of
- * its row (SELL positions; padding: 0), c0 the first column of every row;
- * *too_big is set when a difference does not fit (the caller then keeps the
- * 32-bit columns). sphc_sell_spmv16 / sphc_sell_cheb_step16: the same
- * arithmetic as sphc_sell_spmv / sphc_sell_cheb_step (bitwise) on 10 instead
- * of 12 bytes per stored entry; one warp per slice (operators of at least
- * 148 * 48 slices). */
+ * its row (SELL positions; padding: 0), c0 the row's 32-bit bases: nbase = 1,
+ * the first column; nbase = 4, up to three more, a difference code 0xFFFF
+ * meaning "this entry's column is the row's next base" (a jump beyond 16
+ * bits: the next mesh plane at 256^3). *too_big is set when a row needs more
+ * (the caller then keeps the 32-bit columns). rect = 1: an empty row's
+ * column is 0, not the row index (A D). sphc_sell_spmv16 /
+ * sphc_sell_cheb_step16 / sphc_sell_hipt_mid16: the same arithmetic as
+ * sphc_sell_spmv / sphc_sell_cheb_step / sphc_sell_hipt_mid (bitwise) on 10
+ * instead of 12 bytes per stored entry; one warp per slice (operators of at
+ * least 148 * 48 slices). */
 int sphc_sell_fill16(int64_t n, const int64_t *rp, const int32_t *ci, const int64_t *slice_ptr,
-                     uint16_t *d16, int32_t *c0, int32_t *too_big, int rect, void *stream);
-/* sphc_sell_hipt_mid on delta-coded columns of A D (rect = 1 in the fill: an
- * empty row's column is 0, not the row index). */
+                     uint16_t *d16, int32_t *c0, int32_t *too_big, int rect, int nbase,
+                     void *stream);
 int sphc_sell_hipt_mid16(int64_t n, const int64_t *slice_ptr, const uint16_t *d16,
                          const int32_t *c0, const double *sv, const int64_t *drp,
                          const int32_t *dci, const double *dv, const double *dinv,
                          const double *r, const double *c, const double *x_in, double *x_out,
-                         double *d, double cr, void *stream);
+                         double *d, double cr, int nbase, void *stream);
 int sphc_sell_spmv16(int64_t n, const int64_t *slice_ptr, const uint16_t *d16, const int32_t *c0,
                      const double *sv, const double *x, double alpha, double beta,
-                     const double *z, double *y, void *stream);
+                     const double *z, double *y, int nbase, void *stream);
 int sphc_sell_cheb_step16(int64_t n, const int64_t *slice_ptr, const uint16_t *d16,
                           const int32_t *c0, const double *sv, const double *dinv,
                           const double *b, const double *x_in, double *x_out, double *d,
-                          double cd, double cr, void *stream);
+                          double cd, double cr, int nbase, void *stream);
 /* SELL fill for a rectangular operator (A_e D): padding entries repeat the
  * row's first column (0 for an empty row) instead of the row index. */
 int sphc_sell_fill_rect(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,

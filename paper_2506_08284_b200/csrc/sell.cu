@@ -267,9 +267,12 @@ extern "C" int sphc_sell_cheb_step(int64_t n, const int64_t* slice_ptr, const in
 // Same entries, same order, same fma chain: bitwise the 32-bit kernels.
 // Eligible when every difference fits 16 bits (sphc_sell_fill16 reports it):
 // true for the 128^3 mesh numbering (largest jump ~3 N^2 = 49.9k).
+#define SELL16_ESC 0xFFFF   // difference code: restart from the row's next base
+#define SELL16_NBASE 4      // bases per row of the escaped variant
+
 __global__ void k_sell_fill16(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
                               const i64* __restrict__ sp, unsigned short* __restrict__ d16,
-                              int* __restrict__ c0, int* too_big, int rect) {
+                              int* __restrict__ c0, int* too_big, int rect, int nbase) {
   bool big = false;
   for (i64 row = (i64)blockIdx.x * blockDim.x + threadIdx.x; row < ((n + 31) & ~(i64)31);
        row += (i64)gridDim.x * blockDim.x) {
@@ -284,11 +287,25 @@ __global__ void k_sell_fill16(i64 n, const i64* __restrict__ rp, const int* __re
       len = (int)(rp[row + 1] - j0);
     }
     int prev = len ? ci[j0] : ((row < n && !rect) ? (int)row : 0);
-    if (row < n) c0[row] = prev;
+    int g = 0;
+    if (row < n) {
+      c0[row * nbase] = prev;
+      for (int q = 1; q < nbase; q++) c0[row * nbase + q] = prev;
+    }
     for (int j = 0; j < w; j++) {
       int c = j < len ? ci[j0 + j] : prev;
       int d = c - prev;
-      big |= d < 0 || d > 65535;
+      if (d < 0 || d >= SELL16_ESC) {
+        // a jump beyond 16 bits (the next mesh plane at 256^3): restart from
+        // the row's next 32-bit base, if it has one left
+        if (g + 1 < nbase && row < n) {
+          c0[row * nbase + (++g)] = c;
+          d = SELL16_ESC;
+        } else {
+          big = true;
+          d = 0;
+        }
+      }
       d16[base + (i64)j * SELL_C] = (unsigned short)d;
       prev = c;
     }
@@ -298,10 +315,12 @@ __global__ void k_sell_fill16(i64 n, const i64* __restrict__ rp, const int* __re
 
 extern "C" int sphc_sell_fill16(int64_t n, const int64_t* rp, const int32_t* ci,
                                 const int64_t* slice_ptr, uint16_t* d16, int32_t* c0,
-                                int32_t* too_big, int rect, void* stream) {
+                                int32_t* too_big, int rect, int nbase, void* stream) {
   cudaStream_t s = as_stream(stream);
+  if (nbase != 1 && nbase != SELL16_NBASE) return SPHC_ERR_ARG;
   SPHC_CUDA(cudaMemsetAsync(too_big, 0, sizeof(int32_t), s));
-  k_sell_fill16<<<grid_for(n, 256), 256, 0, s>>>(n, rp, ci, slice_ptr, d16, c0, too_big, rect);
+  k_sell_fill16<<<grid_for(n, 256), 256, 0, s>>>(n, rp, ci, slice_ptr, d16, c0, too_big, rect,
+                                                 nbase);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -313,12 +332,20 @@ extern "C" int sphc_sell_fill16(int64_t n, const int64_t* rp, const int32_t* ci,
 #define SELL16_U 6
 #endif
 // one thread's row: the column runs along with the 16-bit differences
-__device__ __forceinline__ double sell_row16(i64 base, int w, int c,
+template <int NB>
+__device__ __forceinline__ double sell_row16(i64 base, int w, const int* __restrict__ bases,
                                              const unsigned short* __restrict__ d16,
                                              const double* __restrict__ sv,
                                              const double* __restrict__ x) {
   constexpr int U = SELL16_U;
   double acc = 0.0;
+  int c = bases[0];
+  int nb[NB > 1 ? NB - 1 : 1];
+  if (NB > 1) {
+#pragma unroll
+    for (int q = 1; q < NB; q++) nb[q - 1] = bases[q];
+  }
+  int g = 0;
   for (int j0 = 0; j0 < w; j0 += U) {
     unsigned short d[U];
     double v[U];
@@ -336,7 +363,13 @@ __device__ __forceinline__ double sell_row16(i64 base, int w, int c,
 #pragma unroll
     for (int u = 0; u < U; u++)
       if (j0 + u < w) {
-        c += d[u];
+        if (NB > 1 && d[u] == SELL16_ESC) {
+          // (NB - 1 = 3 further bases: a select chain, no local memory)
+          c = g == 0 ? nb[0] : (g == 1 ? nb[NB > 2 ? 1 : 0] : nb[NB > 3 ? 2 : 0]);
+          g++;
+        } else {
+          c += d[u];
+        }
         acc = fma(v[u], __ldg(x + c), acc);
       }
   }
@@ -344,7 +377,8 @@ __device__ __forceinline__ double sell_row16(i64 base, int w, int c,
 }
 
 // y = alpha A x + beta z (streamed operators, one warp per slice)
-__global__ void __launch_bounds__(SELL_PER_BLOCK, 8)
+template <int NB>
+__global__ void __launch_bounds__(SELL_PER_BLOCK, NB > 1 ? 6 : 8)
     k_sell_spmv16(i64 n, const i64* __restrict__ sp, const unsigned short* __restrict__ d16,
                   const int* __restrict__ c0, const double* __restrict__ sv,
                   const double* __restrict__ x, double alpha, double beta, const double* z,
@@ -355,14 +389,15 @@ __global__ void __launch_bounds__(SELL_PER_BLOCK, 8)
   i64 s = row >> 5;
   i64 b0 = sp[s];
   int w = (int)((sp[s + 1] - b0) / SELL_C);
-  double acc = sell_row16(b0 + (threadIdx.x & 31), w, c0[row], d16, sv, x);
+  double acc = sell_row16<NB>(b0 + (threadIdx.x & 31), w, c0 + row * NB, d16, sv, x);
   double r = alpha * acc;
   if (z) r = fma(beta, z[row], r);
   y[row] = r;
 }
 
 // d <- cd d + cr dinv (b - A x_in); x_out = x_in + d
-__global__ void __launch_bounds__(SELL_PER_BLOCK, 8)
+template <int NB>
+__global__ void __launch_bounds__(SELL_PER_BLOCK, NB > 1 ? 6 : 8)
     k_sell_cheb16(i64 n, const i64* __restrict__ sp, const unsigned short* __restrict__ d16,
                   const int* __restrict__ c0, const double* __restrict__ sv,
                   const double* __restrict__ dinv, const double* __restrict__ b,
@@ -374,7 +409,7 @@ __global__ void __launch_bounds__(SELL_PER_BLOCK, 8)
   i64 s = row >> 5;
   i64 b0 = sp[s];
   int w = (int)((sp[s + 1] - b0) / SELL_C);
-  double ax = sell_row16(b0 + (threadIdx.x & 31), w, c0[row], d16, sv, x_in);
+  double ax = sell_row16<NB>(b0 + (threadIdx.x & 31), w, c0 + row * NB, d16, sv, x_in);
   double r = b[row] - ax;
   double dn = cr * dinv[row] * r;
   if (cd != 0.0) dn = fma(cd, d[row], dn);
@@ -385,12 +420,16 @@ __global__ void __launch_bounds__(SELL_PER_BLOCK, 8)
 extern "C" int sphc_sell_spmv16(int64_t n, const int64_t* slice_ptr, const uint16_t* d16,
                                 const int32_t* c0, const double* sv, const double* x,
                                 double alpha, double beta, const double* z, double* y,
-                                void* stream) {
+                                int nbase, void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
   unsigned g = (unsigned)((n + SELL_PER_BLOCK - 1) / SELL_PER_BLOCK);
-  launch_pdl(k_sell_spmv16, g, SELL_PER_BLOCK, 0, s, n, slice_ptr, d16, c0, sv, x, alpha, beta, z,
-             y);
+  if (nbase == 1)
+    launch_pdl(k_sell_spmv16<1>, g, SELL_PER_BLOCK, 0, s, n, slice_ptr, d16, c0, sv, x, alpha,
+               beta, z, y);
+  else
+    launch_pdl(k_sell_spmv16<SELL16_NBASE>, g, SELL_PER_BLOCK, 0, s, n, slice_ptr, d16, c0, sv,
+               x, alpha, beta, z, y);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -398,12 +437,17 @@ extern "C" int sphc_sell_spmv16(int64_t n, const int64_t* slice_ptr, const uint1
 extern "C" int sphc_sell_cheb_step16(int64_t n, const int64_t* slice_ptr, const uint16_t* d16,
                                      const int32_t* c0, const double* sv, const double* dinv,
                                      const double* b, const double* x_in, double* x_out,
-                                     double* d, double cd, double cr, void* stream) {
+                                     double* d, double cd, double cr, int nbase,
+                                     void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
   unsigned g = (unsigned)((n + SELL_PER_BLOCK - 1) / SELL_PER_BLOCK);
-  launch_pdl(k_sell_cheb16, g, SELL_PER_BLOCK, 0, s, n, slice_ptr, d16, c0, sv, dinv, b, x_in,
-             x_out, d, cd, cr);
+  if (nbase == 1)
+    launch_pdl(k_sell_cheb16<1>, g, SELL_PER_BLOCK, 0, s, n, slice_ptr, d16, c0, sv, dinv, b,
+               x_in, x_out, d, cd, cr);
+  else
+    launch_pdl(k_sell_cheb16<SELL16_NBASE>, g, SELL_PER_BLOCK, 0, s, n, slice_ptr, d16, c0, sv,
+               dinv, b, x_in, x_out, d, cd, cr);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -437,7 +481,8 @@ __global__ void __launch_bounds__(SELL_PER_BLOCK, (STREAM && K == 1) ? 8 : 5)
 }
 
 // the same step on delta-coded columns of A D (one warp per slice)
-__global__ void __launch_bounds__(SELL_PER_BLOCK, 8)
+template <int NB>
+__global__ void __launch_bounds__(SELL_PER_BLOCK, NB > 1 ? 6 : 8)
     k_sell_hipt_mid16(i64 n, const i64* __restrict__ sp, const unsigned short* __restrict__ d16,
                       const int* __restrict__ c0, const double* __restrict__ sv,
                       const i64* __restrict__ drp, const int* __restrict__ dci,
@@ -451,7 +496,7 @@ __global__ void __launch_bounds__(SELL_PER_BLOCK, 8)
   i64 s = row >> 5;
   i64 b0 = sp[s];
   int w = (int)((sp[s + 1] - b0) / SELL_C);
-  double adc = sell_row16(b0 + (threadIdx.x & 31), w, c0[row], d16, sv, c);
+  double adc = sell_row16<NB>(b0 + (threadIdx.x & 31), w, c0 + row * NB, d16, sv, c);
   i64 j0 = drp[row], j1 = drp[row + 1];
   double u = 0.0;
   for (i64 j = j0; j < j1; j++) u = fma(dvv[j], __ldg(c + dci[j]), u);
@@ -464,12 +509,17 @@ extern "C" int sphc_sell_hipt_mid16(int64_t n, const int64_t* slice_ptr, const u
                                     const int32_t* c0, const double* sv, const int64_t* drp,
                                     const int32_t* dci, const double* dv, const double* dinv,
                                     const double* r, const double* c, const double* x_in,
-                                    double* x_out, double* d, double cr, void* stream) {
+                                    double* x_out, double* d, double cr, int nbase,
+                                    void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = as_stream(stream);
   unsigned g = (unsigned)((n + SELL_PER_BLOCK - 1) / SELL_PER_BLOCK);
-  launch_pdl(k_sell_hipt_mid16, g, SELL_PER_BLOCK, 0, s, n, slice_ptr, d16, c0, sv, drp, dci, dv,
-             dinv, r, c, x_in, x_out, d, cr);
+  if (nbase == 1)
+    launch_pdl(k_sell_hipt_mid16<1>, g, SELL_PER_BLOCK, 0, s, n, slice_ptr, d16, c0, sv, drp, dci,
+               dv, dinv, r, c, x_in, x_out, d, cr);
+  else
+    launch_pdl(k_sell_hipt_mid16<SELL16_NBASE>, g, SELL_PER_BLOCK, 0, s, n, slice_ptr, d16, c0, sv,
+               drp, dci, dv, dinv, r, c, x_in, x_out, d, cr);
   SPHC_LAUNCH_CHECK();
   return 0;
 }

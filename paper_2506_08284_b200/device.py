@@ -887,7 +887,8 @@ class SellMirror:
     # streamed operators: 16-bit column differences + first column per row
     # (sphc_sell_fill16), None when not built / not representable
     d16: torch.Tensor = None
-    c0: torch.Tensor = None
+    c0: torch.Tensor = None   # int32 [n * nbase]: the rows' 32-bit bases
+    nbase: int = 1
 
     @property
     def padded(self):
@@ -925,14 +926,25 @@ def sell(A):
     if SELL16 and tot * 12 > SELL16_MIN_BYTES and ns >= 148 * 48:
         # operators streamed from HBM by one warp per slice: delta-coded
         # columns (10 instead of 12 bytes per entry), if they fit 16 bits
-        d16 = torch.empty(tot, dtype=torch.int16, device=A.rowptr.device)
-        c0 = torch.empty(n, dtype=torch.int32, device=A.rowptr.device)
-        big = torch.empty(1, dtype=torch.int32, device=A.rowptr.device)
-        call("sphc_sell_fill16", n, A.rowptr, A.col, sp_, d16, c0, big, 0)
-        if int(readback(big)[0][0]) == 0:
-            m.d16, m.c0 = d16, c0
+        _delta_code(m, A, sp_, tot, 0)
     A._sell, A._sell_key = m, _sell_key(A)
     return m
+
+
+def _delta_code(m, A, sp_, tot, rect):
+    """Attach delta-coded columns to mirror ``m`` if A's rows can be coded:
+    with one 32-bit base per row, else with four (escapes for the jumps
+    beyond 16 bits: the plane-to-plane jumps of a 256^3 numbering)."""
+    n, dev = A.shape[0], A.rowptr.device
+    d16 = torch.empty(tot, dtype=torch.int16, device=dev)
+    big = torch.empty(1, dtype=torch.int32, device=dev)
+    for nbase in (1, 4):
+        c0 = torch.empty(n * nbase, dtype=torch.int32, device=dev)
+        call("sphc_sell_fill16", n, A.rowptr, A.col, sp_, d16, c0, big, rect, nbase)
+        if int(readback(big)[0][0]) == 0:
+            m.d16, m.c0, m.nbase = d16, c0, nbase
+            return True
+    return False
 
 
 def sell_rect(A):
@@ -948,12 +960,7 @@ def sell_rect(A):
     call("sphc_sell_fill_rect", n, A.rowptr, A.col, A.val, sp_, ci, v)
     m = SellMirror(sp_, ci, v, n)
     if SELL16 and tot * 12 > SELL16_MIN_BYTES and ns >= 148 * 48:
-        d16 = torch.empty(tot, dtype=torch.int16, device=A.rowptr.device)
-        c0 = torch.empty(n, dtype=torch.int32, device=A.rowptr.device)
-        big = torch.empty(1, dtype=torch.int32, device=A.rowptr.device)
-        call("sphc_sell_fill16", n, A.rowptr, A.col, sp_, d16, c0, big, 1)
-        if int(readback(big)[0][0]) == 0:
-            m.d16, m.c0 = d16, c0
+        if _delta_code(m, A, sp_, tot, 1):
             m.col = None          # only the delta-coded kernel reads this mirror
     return m
 
@@ -971,7 +978,8 @@ def spmv(A, x, y, alpha=1.0, beta=0.0, z=None, lanes=None):
     m = sell_mirror(A)
     if m is not None:
         if m.d16 is not None:
-            call("sphc_sell_spmv16", m.n, m.slice_ptr, m.d16, m.c0, m.val, x, alpha, beta, z, y)
+            call("sphc_sell_spmv16", m.n, m.slice_ptr, m.d16, m.c0, m.val, x, alpha, beta, z, y,
+                 m.nbase)
         else:
             call("sphc_sell_spmv", m.n, m.slice_ptr, m.col, m.val, x, alpha, beta, z, y,
                  m.padded)

@@ -245,7 +245,7 @@ class ChebyshevSweeper:
                 m = self.sell
                 if m is not None and m.d16 is not None and not z:
                     call("sphc_sell_cheb_step16", n, m.slice_ptr, m.d16, m.c0, m.val, self.dinv,
-                         b, cur, out, self.d, cd, cr)
+                         b, cur, out, self.d, cd, cr, m.nbase)
                 elif m is not None:
                     call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, self.dinv, b,
                          None if z else cur, out, self.d, cd, cr, int(z), m.padded)
@@ -269,7 +269,7 @@ class ChebyshevSweeper:
         _, cr = self.coefs[0]
         if mid.d16 is not None:
             call("sphc_sell_hipt_mid16", n, mid.slice_ptr, mid.d16, mid.c0, mid.val, D.rowptr,
-                 D.col, D.val, self.dinv, r, c, x, out, self.d, cr)
+                 D.col, D.val, self.dinv, r, c, x, out, self.d, cr, mid.nbase)
         else:
             call("sphc_sell_hipt_mid", n, mid.slice_ptr, mid.col, mid.val, D.rowptr, D.col,
                  D.val, self.dinv, r, c, x, out, self.d, cr, mid.padded)
@@ -282,7 +282,7 @@ class ChebyshevSweeper:
             out = self.buf[0] if cur is not self.buf[0] else self.buf[1]
             if m.d16 is not None:
                 call("sphc_sell_cheb_step16", n, m.slice_ptr, m.d16, m.c0, m.val, self.dinv, b,
-                     cur, out, self.d, cd, cr)
+                     cur, out, self.d, cd, cr, m.nbase)
             else:
                 call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, self.dinv, b, cur,
                      out, self.d, cd, cr, 0, m.padded)

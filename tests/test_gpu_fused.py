@@ -163,7 +163,7 @@ def test_delta_coded_sell_kernels_are_bitwise():
     dinv = dv.reciprocal(dv.diagonal(A))
     y0, y1 = torch.empty_like(x), torch.empty_like(x)
     call("sphc_sell_spmv", n, m.slice_ptr, m.col, m.val, x, -1.0, 1.0, b, y0, m.padded)
-    call("sphc_sell_spmv16", n, m.slice_ptr, m.d16, m.c0, m.val, x, -1.0, 1.0, b, y1)
+    call("sphc_sell_spmv16", n, m.slice_ptr, m.d16, m.c0, m.val, x, -1.0, 1.0, b, y1, m.nbase)
     assert torch.equal(y0, y1)
     d0 = torch.from_numpy(rng.uniform(-1, 1, n)).cuda()
     d1 = d0.clone()
@@ -171,7 +171,7 @@ def test_delta_coded_sell_kernels_are_bitwise():
     call("sphc_sell_cheb_step", n, m.slice_ptr, m.col, m.val, dinv, b, x, o0, d0, 0.3, 0.7, 0,
          m.padded)
     call("sphc_sell_cheb_step16", n, m.slice_ptr, m.d16, m.c0, m.val, dinv, b, x, o1, d1, 0.3,
-         0.7)
+         0.7, m.nbase)
     assert torch.equal(o0, o1) and torch.equal(d0, d1)
     # the fused Hiptmair mid step on delta-coded columns of A D
     D = dv.own_csr(s.D)
@@ -192,16 +192,46 @@ def test_delta_coded_sell_kernels_are_bitwise():
     call("sphc_sell_hipt_mid", n, m32.slice_ptr, m32.col, m32.val, D.rowptr, D.col, D.val, dinv,
          r, c, x, o0, e0, 0.7, m32.padded)
     call("sphc_sell_hipt_mid16", n, m16.slice_ptr, m16.d16, m16.c0, m16.val, D.rowptr, D.col,
-         D.val, dinv, r, c, x, o1, e1, 0.7)
+         D.val, dinv, r, c, x, o1, e1, 0.7, m16.nbase)
     assert torch.equal(o0, o1) and torch.equal(e0, e1)
-    # a far-apart pair of columns in one row: not representable
+    assert m.nbase == 1 and m16.nbase == 1
+    # jumps beyond 16 bits: up to three per row restart from the row's next
+    # 32-bit base (the plane jumps of a 256^3 numbering); more are not
+    # representable and the mirror keeps its 32-bit columns
     import scipy.sparse as sp
-    B = sp.identity(300_000, format="lil")
-    B[5, 299_999] = 2.0
-    dB = dv.DeviceCSR.from_scipy(B.tocsr())
+    nb = 300_000
+    rows = np.repeat(np.arange(nb), 5)
+    off = np.tile(np.array([0, 3, 70_000, 140_001, 210_500]), nb)
+    cols = rows + off
+    keep = cols < nb                       # no wrap-around: at most 3 far jumps per row
+    rows, cols = rows[keep], cols[keep]
+    Bs = sp.csr_matrix((rng.uniform(-1, 1, rows.size), (rows, cols)), shape=(nb, nb))
+    Bs.sum_duplicates()
+    Bs.sort_indices()
+    dB = dv.DeviceCSR.from_scipy(Bs)
     try:
         dv.SELL16_MIN_BYTES = 0
         mb = dv.sell(dB)
     finally:
         dv.SELL16_MIN_BYTES = old
-    assert mb.d16 is None
+    assert mb.d16 is not None and mb.nbase == 4
+    xb = torch.from_numpy(rng.uniform(-1, 1, nb)).cuda()
+    y0, y1 = torch.empty_like(xb), torch.empty_like(xb)
+    call("sphc_sell_spmv", nb, mb.slice_ptr, mb.col, mb.val, xb, 1.0, 0.0, None, y0, mb.padded)
+    call("sphc_sell_spmv16", nb, mb.slice_ptr, mb.d16, mb.c0, mb.val, xb, 1.0, 0.0, None, y1,
+         mb.nbase)
+    assert torch.equal(y0, y1)
+    assert np.allclose(y1.cpu().numpy(), Bs @ xb.cpu().numpy(), rtol=1e-12, atol=1e-12)
+    off6 = np.tile(np.array([0, 66_000, 132_001, 198_002, 264_003, 299_000]), nb)
+    rows6 = np.repeat(np.arange(nb), 6)
+    cols6 = rows6 + off6
+    k6 = cols6 < nb                        # row 0 keeps all six: four far jumps
+    B6 = sp.csr_matrix((np.ones(int(k6.sum())), (rows6[k6], cols6[k6])), shape=(nb, nb))
+    B6.sum_duplicates()
+    B6.sort_indices()
+    try:
+        dv.SELL16_MIN_BYTES = 0
+        m6 = dv.sell(dv.DeviceCSR.from_scipy(B6))
+    finally:
+        dv.SELL16_MIN_BYTES = old
+    assert m6.d16 is None

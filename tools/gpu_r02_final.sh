@@ -2,7 +2,7 @@
 # Round-2 closing measurements (delta-coded SELL kernels in): bench lines, the
 # C4 launch list and setup timeline, ncu --set full of the three 16-bit
 # kernels. Text only in gpurun_out/.
-tag=${1:-r02e}
+tag=${1:-r02f}
 mkdir -p gpurun_out
 run() { name=$1; shift; timeout 900 "$@" > gpurun_out/${tag}_$name.json 2> gpurun_out/${tag}_$name.err; echo "$name rc=$? $(grep '^{' gpurun_out/${tag}_$name.json | tail -1 | head -c 120)"; }
 run bench_c4 python bench.py --steps 5 --warmup 3

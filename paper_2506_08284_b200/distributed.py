@@ -362,6 +362,13 @@ class CudaOps:
 
     def cheb(self, A, dinv, b, x_ext, x_out, d, cd, cr, x_zero):
         m = self.dv.sell(A)      # SELL-32 mirror of the local rows (cached on A)
+        if m.d16 is not None and not x_zero:
+            # delta-coded columns (a lower neighbour's halo columns come first
+            # in a row and sit above the owned ones: those rows restart from
+            # a further 32-bit base, csrc/sell.cu)
+            self.call("sphc_sell_cheb_step16", A.shape[0], m.slice_ptr, m.d16, m.c0, m.val,
+                      dinv, b, x_ext, x_out, d, cd, cr, m.nbase)
+            return
         self.call("sphc_sell_cheb_step", A.shape[0], m.slice_ptr, m.col, m.val, dinv, b,
                   None if x_zero else x_ext, x_out, d, cd, cr, int(x_zero), m.padded)
 

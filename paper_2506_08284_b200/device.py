@@ -326,6 +326,8 @@ def as_device_csr(A):
 
 
 _STAGE = {}
+import threading as _threading  # noqa: E402
+_STAGE_LOCK = _threading.Lock()
 _REG = {}      # (address, bytes) -> weakref of the page-locked host array
 
 
@@ -417,6 +419,11 @@ class AsyncUpload:
     SLOTS = 16               # ring of pinned chunks (512 MB, whatever the inputs' size)
 
     def _run(self):
+        # one upload at a time owns the staging ring
+        with _STAGE_LOCK:
+            self._run_locked()
+
+    def _run_locked(self):
         try:
             torch.cuda.set_device(self.dev)
             ring = _STAGE.get("ring")

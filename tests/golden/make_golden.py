@@ -346,16 +346,47 @@ def _write_case(name, meta, arrays):
     np.savez_compressed(os.path.join(HERE, f"hier_{name}.npz"), **arrays)
 
 
-def run_device_case(name, config, N, coarse_size, limit, with_gs, cheb_maxit=500):
+# Other element families of the reference (meshing.py:15 SUPPORTED: quad, tri,
+# hex, tet): the unmodified reference on its own meshes and assembly. The hot
+# path only sees (A_e, S, A_n, D), so the INPUTS are stored with the golden
+# (the repo's generators are hex only) and the tests upload them as they are.
+MESH = {
+    # name: (dim, kind, nodal shape, dirichlet, sigma, coarse_size, rhs seed)
+    "T9n": (3, "tet", 9, False, 1.0, 100, 11),
+    "T8d": (3, "tet", 8, True, 1e-2, 100, 12),
+    "Q41d": (2, "quad", 41, True, 1.0, 500, 13),
+    "R33n": (2, "tri", 33, False, 1e-2, 100, 14),
+}
+
+
+def run_mesh_case(name, dim, kind, shape, dirichlet, sigma, coarse_size, seed):
+    m = build_structured_mesh(dim, kind, shape, dirichlet)
+    sysm = discretize(m, sigma)
+    rhs = np.random.default_rng(seed).uniform(-1.0, 1.0, sysm.A_e.shape[0])
+    inputs = (sp.csr_matrix(sysm.A_e), sp.csr_matrix(sysm.S), sp.csr_matrix(sysm.A_n),
+              sp.csr_matrix(sysm.D), rhs,
+              {"dirichlet": dirichlet, "dim": dim, "kind": kind, "shape": shape,
+               "sigma": sigma, "seed": seed})
+    return run_device_case(name, f"{kind}{dim}d", shape, coarse_size, None, True,
+                           inputs=inputs)
+
+
+def run_device_case(name, config, N, coarse_size, limit, with_gs, cheb_maxit=500,
+                    inputs=None):
     from types import SimpleNamespace
     from hcurlamg import nodal_amg as na, coarse_gradient as cgm
-    from oracle.host_assembly import config_host
-    A_e, S, A_n, D, rhs, cfg = config_host(config, N)
+    if inputs is None:
+        from oracle.host_assembly import config_host
+        A_e, S, A_n, D, rhs, cfg = config_host(config, N)
+    else:
+        A_e, S, A_n, D, rhs, cfg = inputs
     s = SimpleNamespace(A_e=A_e, S=S, A_n=A_n, D=D)
     meta = {"config": config, "N": N, "dirichlet": bool(cfg["dirichlet"]),
             "coarse_size": coarse_size, "limit": limit,
             "inputs": {k: csr_hash(getattr(s, k)) for k in ("A_e", "S", "A_n", "D")},
             "rhs": sha(rhs), "levels": []}
+    if inputs is not None:
+        meta["mesh"] = cfg
     t0 = time.perf_counter()
     h = mg.build_hierarchy(A_e, S, A_n, D, mg.SolverConfig(coarse_size=coarse_size))
     meta["t_setup_ref"] = time.perf_counter() - t0
@@ -365,6 +396,14 @@ def run_device_case(name, config, N, coarse_size, limit, with_gs, cheb_maxit=500
                  "n_edges": [lv.A_e.shape[0] for lv in h.levels],
                  "nnz_A_e": [int(lv.A_e.nnz) for lv in h.levels]})
     arrays = {}
+    if inputs is not None:
+        for k in ("A_e", "S", "A_n", "D"):
+            M = sp.csr_matrix(getattr(s, k))
+            arrays[f"in_{k}_indptr"] = M.indptr.astype(np.int64)
+            arrays[f"in_{k}_indices"] = M.indices.astype(np.int32)
+            arrays[f"in_{k}_data"] = M.data.astype(np.float64)
+            arrays[f"in_{k}_shape"] = np.array(M.shape, dtype=np.int64)
+        arrays["in_rhs"] = rhs
     for li, lv in enumerate(h.levels):
         L = {"n_edges": lv.A_e.shape[0], "n_nodes": lv.D.shape[1],
              "A_e": csr_hash(lv.A_e), "S_e": csr_hash(lv.S_e), "D": csr_hash(lv.D),
@@ -495,6 +534,14 @@ def main(which):
         with open(os.path.join(HERE, "inputs.json"), "w") as f:
             json.dump(inputs_table(), f, indent=1, sort_keys=True)
         print("inputs.json written")
+    for name, spec in MESH.items():
+        if which and name not in which:
+            continue
+        meta, arrays = run_mesh_case(name, *spec)
+        _write_case(name, meta, arrays)
+        print(name, "levels", meta["n_edges"], "gs", meta["gs"]["iterations"],
+              meta["gs"]["status"], "cheb", meta["cheb"]["iterations"], meta["cheb"]["status"],
+              flush=True)
     for name, spec in BIG.items():
         if name not in which:           # only on request (minutes to hours)
             continue
@@ -515,4 +562,5 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(set(sys.argv[1:]) or set(["inputs", "errors", "repair", "pcg_status"] + list(CASES) + list(RELAX)))
+    main(set(sys.argv[1:]) or set(["inputs", "errors", "repair", "pcg_status"] + list(CASES) + list(RELAX)
+                                  + list(MESH)))

@@ -127,3 +127,17 @@ def embed_in_pattern(M, P):
     data = np.zeros(P.nnz)
     data[pos] = M.data
     return sp.csr_matrix((data, P.indices, P.indptr), shape=P.shape), int(P.nnz - M.nnz)
+
+
+MESH = ["T9n", "T8d", "Q41d", "R33n"]
+
+
+def stored_inputs(arrays):
+    """(A_e, S, A_n, D, rhs) of a golden that carries its own inputs (the
+    reference's tet / quad / tri meshes: the repo's generators are hex only)."""
+    out = []
+    for k in ("A_e", "S", "A_n", "D"):
+        out.append(sp.csr_matrix((arrays[f"in_{k}_data"], arrays[f"in_{k}_indices"],
+                                  arrays[f"in_{k}_indptr"]),
+                                 shape=tuple(int(x) for x in arrays[f"in_{k}_shape"])))
+    return (*out, arrays["in_rhs"])

@@ -6,6 +6,9 @@ Goldens ``hier_C4s`` (C4 recipe at 16^3), ``hier_C3`` (64^3, sigma jump),
 the smallest size where ``make_irreducible`` fires: 154 coarse edges appended
 on level 2) were made by running the reference on the host build of the
 device assembly (oracle/host_assembly.py, tests/golden/make_golden.py BIG).
+Goldens ``hier_T9n`` / ``hier_T8d`` (tet meshes), ``hier_Q41d`` (2-D quads)
+and ``hier_R33n`` (2-D triangles) are the reference on its own other element
+families (meshing.py:15), inputs stored with the golden.
 Each test assembles the same config on the B200, proves the inputs identical
 (sha256 of A_e, S, A_n, D and of the RHS), builds the hierarchy through the
 public API and checks:
@@ -38,8 +41,8 @@ import os
 import numpy as np
 import pytest
 
-from golden_util import (GOLDEN, check_values, csr_hash, embed_in_pattern, load_case,
-                         pattern_sha, sha)
+from golden_util import (GOLDEN, MESH, check_values, csr_hash, embed_in_pattern, load_case,
+                         pattern_sha, sha, stored_inputs)
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -61,12 +64,20 @@ def _case(name):
     return load_case(name)
 
 
-@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("name", CASES + MESH)
 def test_device_config_vs_reference(name):
-    from paper_2506_08284_b200 import multigrid as mg
+    from types import SimpleNamespace
+    from paper_2506_08284_b200 import multigrid as mg, device as dv
     from paper_2506_08284_b200.assembly import make_device_config
     meta, arrays = _case(name)
-    s, rhs, cfg = make_device_config(meta["config"], meta["N"])
+    if "mesh" in meta:
+        # the reference's own tet / quad / tri system (meshing.py:15), stored
+        # with the golden: the path only sees (A_e, S, A_n, D)
+        A_e, S, A_n, D, rhs = stored_inputs(arrays)
+        s = SimpleNamespace(A_e=dv.DeviceCSR.from_scipy(A_e), S=dv.DeviceCSR.from_scipy(S),
+                            A_n=dv.DeviceCSR.from_scipy(A_n), D=dv.DeviceCSR.from_scipy(D))
+    else:
+        s, rhs, cfg = make_device_config(meta["config"], meta["N"])
     # identical inputs: the device assembly is the reference run's input
     for k, M in (("A_e", s.A_e), ("S", s.S), ("A_n", s.A_n), ("D", s.D)):
         assert csr_hash(M.to_scipy()) == meta["inputs"][k], k

@@ -229,7 +229,11 @@ def _check_device_config(name):
     from golden_util import check_values, pattern_sha
     from oracle.host_assembly import config_host
     meta, arrays = load_case(name)
-    A_e, S, A_n, D, rhs, _ = config_host(meta["config"], meta["N"])
+    if "mesh" in meta:      # the reference's own tet / quad / tri system, stored
+        from golden_util import stored_inputs
+        A_e, S, A_n, D, rhs = stored_inputs(arrays)
+    else:
+        A_e, S, A_n, D, rhs, _ = config_host(meta["config"], meta["N"])
     for k, M in (("A_e", A_e), ("S", S), ("A_n", A_n), ("D", D)):
         assert csr_hash(M) == meta["inputs"][k], k
     assert sha(rhs) == meta["rhs"]
@@ -273,6 +277,13 @@ def _check_device_config(name):
 
 def test_oracle_device_config_c4s():
     _check_device_config("C4s")
+
+
+@pytest.mark.parametrize("name", ["T9n", "T8d", "Q41d", "R33n"])
+def test_oracle_other_element_families(name):
+    """The reference's tet (3-D) and quad / tri (2-D) meshes
+    (meshing.py:15): the path only sees (A_e, S, A_n, D)."""
+    _check_device_config(name)
 
 
 @pytest.mark.slow

@@ -43,6 +43,10 @@ FUSE_ROWS = 256
 # SELL mirror of A_e D and take the Hiptmair mid step fused
 # (sphc_sell_hipt_mid); -1 disables it.
 HIPT_MID_MIN_ROWS = int(os.environ.get("SPHC_HIPT_MID_MIN_ROWS", str(148 * 48 * 32)))
+# coarsest operators up to this size take the eigendecomposition (pseudo-
+# inverse) when their Cholesky factorisation breaks down; larger ones the
+# shifted factorisation first
+COARSE_EIGH_MAX = int(os.environ.get("SPHC_COARSE_EIGH_MAX", "2048"))
 FUSE_MIN_ROWS = int(os.environ.get("SPHC_FUSE_MIN_ROWS", str(148 * 48 * 32)))
 FUSE_L2_BYTES = float(os.environ.get("SPHC_FUSE_MB", "0")) * 2**20
 
@@ -513,13 +517,22 @@ def _coarse_inverse_start(Ad, solver="cholesky"):
     As = sc[:, None] * A * sc[None, :]
     As = 0.5 * (As + As.T)
     L, info = torch.linalg.cholesky_ex(As)
+    # A factorisation that "succeeds" on a round-off pivot (an exactly
+    # singular operator: min pivot^2 6e-19 on the 2-D quad case Q41s) is a
+    # breakdown too: its inverse carries a 1e16 null-space mode and a
+    # negative eigenvalue, and PCG stalls. Healthy coarsest operators sit
+    # orders above the threshold (C3: 4.6e-12 against n eps = 3e-14).
+    dl = torch.diagonal(L)
+    n_ = As.shape[0]
+    tiny = (dl.min() ** 2 < n_ * torch.finfo(torch.float64).eps * dl.max() ** 2)
+    info = info.reshape(1).to(torch.int64) + tiny.reshape(1).to(torch.int64)
     # L^-T L^-1 from one triangular solve against I and a GEMM (0.37 ms
     # at n = 364 against 0.56 ms for cholesky_inverse's blocked potrs)
     Li = torch.linalg.solve_triangular(L, torch.eye(L.shape[0], dtype=L.dtype,
                                                     device=L.device), upper=False)
     inv = Li.T @ Li
     inv = sc[:, None] * inv * sc[None, :]
-    return 0.5 * (inv + inv.T), info.reshape(1).to(torch.int64), (As, sc)
+    return 0.5 * (inv + inv.T), info, (As, sc)
 
 
 def _coarse_inverse_finish(inv, info, state):
@@ -534,14 +547,22 @@ def _coarse_inverse_finish(inv, info, state):
     # blows up are the null vectors of P (P A_c^-1 P^T never sees them),
     # and it perturbs the rest less than truncating them would.
     n = As.shape[0]
-    shift = n * torch.finfo(torch.float64).eps * As.abs().sum(1).max()
-    L, info = torch.linalg.cholesky_ex(As + shift * torch.eye(n, dtype=As.dtype,
-                                                              device=As.device))
-    if int(info) == 0:
-        Li = torch.linalg.solve_triangular(L, torch.eye(n, dtype=L.dtype, device=L.device),
-                                           upper=False)
-        inv = Li.T @ Li
-    else:
+    info = 1
+    if n > COARSE_EIGH_MAX:
+        shift = n * torch.finfo(torch.float64).eps * As.abs().sum(1).max()
+        L, info = torch.linalg.cholesky_ex(As + shift * torch.eye(n, dtype=As.dtype,
+                                                                  device=As.device))
+        if int(info) == 0:
+            Li = torch.linalg.solve_triangular(L, torch.eye(n, dtype=L.dtype,
+                                                            device=L.device), upper=False)
+            inv = Li.T @ Li
+    if int(info) != 0:
+        # the pseudo-inverse: eigenvalues <= n eps lambda_max are the null
+        # space of the prolongator (P A_c^+ P^T never sees them). Exact to
+        # round-off on the range, where the shifted explicit inverse (entries
+        # ~1 / shift) is only good to ~1e-3 -- enough for a preconditioner, so
+        # it is kept for the big coarsest operators, whose eigendecomposition
+        # costs ~1 s (C5's 9,165 edges)
         lam, V = torch.linalg.eigh(As)
         tiny = lam.abs().max() * As.shape[0] * torch.finfo(torch.float64).eps
         w = torch.where(lam > tiny, 1.0 / lam, torch.zeros_like(lam))

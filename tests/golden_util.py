@@ -130,6 +130,9 @@ def embed_in_pattern(M, P):
 
 
 MESH = ["T9n", "T8d", "Q41d", "R33n"]
+# a numerically singular coarsest operator (device parity only: the oracle's
+# LU meets an exact zero pivot there, the reference's a round-off one)
+MESH_SINGULAR = ["Q41s"]
 
 
 def stored_inputs(arrays):

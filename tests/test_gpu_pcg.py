@@ -151,3 +151,44 @@ def test_coarse_lu_matches_scipy_lu_solve():
         mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D,
                            mg.SolverConfig(coarse_size=200, coarse_solver="cholesky"))))
     assert r.status == rc.status == "converged" and abs(r.iterations - rc.iterations) <= 1
+
+
+def test_coarse_inverse_breakdown_fallbacks():
+    """The coarsest solve's fallbacks (multigrid._coarse_inverse_finish): a
+    numerically singular SPD operator (the Galerkin operator of a
+    rank-deficient prolongator) breaks the Cholesky factorisation (or leaves
+    a round-off pivot) -> pseudo-inverse by eigendecomposition (small
+    operators) or shifted factorisation (large ones: an explicit inverse with
+    entries ~1 / shift, good to ~1e-3 on the range); a slightly indefinite
+    one breaks the shifted factorisation too -> eigendecomposition. Every
+    inverse must be symmetric positive semidefinite and solve A x = b for b
+    in the range of A."""
+    from paper_2506_08284_b200 import multigrid as mg
+    rng = np.random.default_rng(7)
+    n, r = 60, 52
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.concatenate([rng.uniform(1.0, 100.0, r), np.zeros(n - r)])
+    A = (Q * lam) @ Q.T                             # rank 52 of 60: exactly semidefinite
+    A = 0.5 * (A + A.T)
+    for kind, Ad, tol, eigh_max in (("pseudo-inverse", A, 1e-9, 2048),
+                                    ("shifted", A, 1e-2, 0),
+                                    ("eigen after shifted", A - 1e-7 * np.abs(A).max()
+                                     * np.eye(n), 1e-5, 0)):
+        At = torch.from_numpy(Ad).cuda()
+        inv, info, state = mg._coarse_inverse_start(At)
+        assert int(info) != 0, kind                # a breakdown or a round-off pivot
+        old = mg.COARSE_EIGH_MAX
+        try:
+            mg.COARSE_EIGH_MAX = eigh_max
+            inv = mg._coarse_inverse_finish(inv, int(info), state)
+        finally:
+            mg.COARSE_EIGH_MAX = old
+        assert torch.isfinite(inv).all(), kind
+        assert float((inv - inv.T).abs().max()) == 0.0
+        lo = float(torch.linalg.eigvalsh(inv)[0])
+        assert lo > -1e-9 * float(inv.abs().max()), (kind, lo)     # positive semidefinite
+        y = rng.standard_normal(n)
+        b = A @ y                                  # in the range
+        x = (inv @ torch.from_numpy(b).cuda()).cpu().numpy()
+        res = np.linalg.norm(A @ x - b) / np.linalg.norm(b)
+        assert res < tol, (kind, res)

@@ -41,7 +41,7 @@ import os
 import numpy as np
 import pytest
 
-from golden_util import (GOLDEN, MESH, check_values, csr_hash, embed_in_pattern, load_case,
+from golden_util import (GOLDEN, MESH, MESH_SINGULAR, check_values, csr_hash, embed_in_pattern, load_case,
                          pattern_sha, sha, stored_inputs)
 
 torch = pytest.importorskip("torch")
@@ -64,7 +64,7 @@ def _case(name):
     return load_case(name)
 
 
-@pytest.mark.parametrize("name", CASES + MESH)
+@pytest.mark.parametrize("name", CASES + MESH + MESH_SINGULAR)
 def test_device_config_vs_reference(name):
     from types import SimpleNamespace
     from paper_2506_08284_b200 import multigrid as mg, device as dv

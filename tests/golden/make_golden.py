@@ -364,6 +364,31 @@ MESH = {
 }
 
 
+# Non-default knobs of the path (EminConfig: omega, iterations, n_passes,
+# drop_tol -- edge_prolongator.py:28-44; SolverConfig.max_levels --
+# multigrid.py:23-30) on small hex meshes, inputs stored like MESH.
+VARIANTS = {
+    # name: (nodal shape, dirichlet, sigma, coarse_size, seed, emin kwargs, max_levels)
+    "V9a": (9, False, 1e-2, 100, 21, dict(iterations=3, omega=0.7), 10),
+    "V9b": (9, True, 1.0, 100, 22, dict(drop_tol=0.05), 10),
+    "V9e": (9, False, 1.0, 100, 25, dict(n_passes=1), 10),
+    "V11c": (11, False, 1.0, 100, 23, dict(n_passes=3, iterations=0), 10),
+    "V9d": (9, True, 1e-4, 50, 24, dict(iterations=2, omega=1.2), 2),
+}
+
+
+def run_variant_case(name, shape, dirichlet, sigma, coarse_size, seed, emin, max_levels):
+    m = build_structured_mesh(3, "hex", shape, dirichlet)
+    sysm = discretize(m, sigma)
+    rhs = np.random.default_rng(seed).uniform(-1.0, 1.0, sysm.A_e.shape[0])
+    inputs = (sp.csr_matrix(sysm.A_e), sp.csr_matrix(sysm.S), sp.csr_matrix(sysm.A_n),
+              sp.csr_matrix(sysm.D), rhs,
+              {"dirichlet": dirichlet, "dim": 3, "kind": "hex", "shape": shape,
+               "sigma": sigma, "seed": seed})
+    return run_device_case(name, "hex3d", shape, coarse_size, None, True, inputs=inputs,
+                           emin=emin, max_levels=max_levels)
+
+
 def run_mesh_case(name, dim, kind, shape, dirichlet, sigma, coarse_size, seed):
     m = build_structured_mesh(dim, kind, shape, dirichlet)
     sysm = discretize(m, sigma)
@@ -377,9 +402,12 @@ def run_mesh_case(name, dim, kind, shape, dirichlet, sigma, coarse_size, seed):
 
 
 def run_device_case(name, config, N, coarse_size, limit, with_gs, cheb_maxit=500,
-                    inputs=None):
+                    inputs=None, emin=None, max_levels=10):
     from types import SimpleNamespace
     from hcurlamg import nodal_amg as na, coarse_gradient as cgm
+    from hcurlamg.edge_prolongator import EminConfig
+    emin = dict(emin or {})
+    ecfg = EminConfig(**emin)
     if inputs is None:
         from oracle.host_assembly import config_host
         A_e, S, A_n, D, rhs, cfg = config_host(config, N)
@@ -392,8 +420,11 @@ def run_device_case(name, config, N, coarse_size, limit, with_gs, cheb_maxit=500
             "rhs": sha(rhs), "levels": []}
     if inputs is not None:
         meta["mesh"] = cfg
+    meta["emin"] = emin
+    meta["max_levels"] = max_levels
     t0 = time.perf_counter()
-    h = mg.build_hierarchy(A_e, S, A_n, D, mg.SolverConfig(coarse_size=coarse_size))
+    h = mg.build_hierarchy(A_e, S, A_n, D, mg.SolverConfig(coarse_size=coarse_size,
+                                                           max_levels=max_levels, emin=ecfg))
     meta["t_setup_ref"] = time.perf_counter() - t0
     print(name, "setup", meta["t_setup_ref"], "levels", [lv.A_e.shape[0] for lv in h.levels],
           flush=True)
@@ -421,6 +452,13 @@ def run_device_case(name, config, N, coarse_size, limit, with_gs, cheb_maxit=500
         if li > 0:
             _store_values(arrays, f"L{li}_A_e", lv.A_e, limit)
             _store_values(arrays, f"L{li}_S_e", lv.S_e, limit)
+            if limit is None:
+                # small cases: the patterns themselves, for the rule "equal up to
+                # round-off-sized entries" when an exact cancellation differs
+                for key, M in (("A_e", lv.A_e), ("S_e", lv.S_e)):
+                    M = sp.csr_matrix(M)
+                    arrays[f"L{li}_{key}_indptr"] = M.indptr.astype(np.int64)
+                    arrays[f"L{li}_{key}_indices"] = M.indices.astype(np.int32)
             L["A_e_fro"] = float(np.linalg.norm(lv.A_e.data))
             L["S_e_fro"] = float(np.linalg.norm(lv.S_e.data))
         if lv.P_e is not None:
@@ -446,10 +484,10 @@ def run_device_case(name, config, N, coarse_size, limit, with_gs, cheb_maxit=500
 
     for li, lv in enumerate(h.levels[:-1]):
         An = _an(h, li, s)
-        agg = na.aggregate(na.strength_graph(An, 0.0))
+        agg = na.aggregate(na.strength_graph(An, ecfg.drop_tol))
         nod = na.smooth_and_normalize(An, na.tentative_prolongator(agg))
         assert (nod.P != lv.P_n).nnz == 0
-        Pc = cgm.gen_piecewise_const(nod.P, 2)
+        Pc = cgm.gen_piecewise_const(nod.P, ecfg.n_passes)
         assign = Pc.indices[Pc.indptr[:-1]].astype(np.int64)
         cg = cgm.augment_dirichlet_edges(cgm.build_coarse_gradient(lv.D, Pc), lv.D, Pc)
         pairs = np.array([e for e in cg.edge_endpoints if len(e) == 2],
@@ -547,6 +585,14 @@ def main(which):
         print(name, "levels", meta["n_edges"], "gs", meta["gs"]["iterations"],
               meta["gs"]["status"], "cheb", meta["cheb"]["iterations"], meta["cheb"]["status"],
               flush=True)
+    for name, spec in VARIANTS.items():
+        if which and name not in which:
+            continue
+        meta, arrays = run_variant_case(name, *spec)
+        _write_case(name, meta, arrays)
+        print(name, "levels", meta["n_edges"], "gs", meta["gs"]["iterations"],
+              meta["gs"]["status"], "cheb", meta["cheb"]["iterations"], meta["cheb"]["status"],
+              flush=True)
     for name, spec in BIG.items():
         if name not in which:           # only on request (minutes to hours)
             continue
@@ -568,4 +614,4 @@ def main(which):
 
 if __name__ == "__main__":
     main(set(sys.argv[1:]) or set(["inputs", "errors", "repair", "pcg_status"] + list(CASES) + list(RELAX)
-                                  + list(MESH)))
+                                  + list(MESH) + list(VARIANTS)))

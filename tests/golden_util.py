@@ -144,3 +144,36 @@ def stored_inputs(arrays):
                                   arrays[f"in_{k}_indptr"]),
                                  shape=tuple(int(x) for x in arrays[f"in_{k}_shape"])))
     return (*out, arrays["in_rhs"])
+
+
+# non-default EminConfig / SolverConfig knobs (make_golden.py VARIANTS)
+VARIANTS = ["V9a", "V9b", "V9e", "V11c", "V9d"]
+
+
+def check_coarse_operator(M, L, arrays, li, key, A_struct=None):
+    """A coarse A_e / S_e against its golden: pattern by sha256 and values to
+    TOL. Both sides drop the EXACT zeros of P^T (X P) (compress,
+    multigrid.py:150-151), and which round-off-sized entries cancel exactly
+    depends on the summation order, so on a pattern mismatch the operator
+    must equal the reference up to entries of magnitude <= 1e-12 max: checked
+    on the stored pattern (small goldens) or, when the reference kept the
+    whole structural pattern ``A_struct`` (large ones), on that pattern with
+    zeros restored."""
+    M = sp.csr_matrix(M)
+    pre = f"L{li}_{key}"
+    if pattern_sha(M) == L[f"{key}_pattern"]:
+        check_values(M, arrays, pre, L[f"{key}_fro"])
+        return
+    if pre + "_indptr" in arrays:
+        assert int(arrays[pre + "_stride"]) == 1
+        ref = sp.csr_matrix((arrays[pre + "_vals"], arrays[pre + "_indices"],
+                             arrays[pre + "_indptr"]), shape=M.shape)
+        cnt, mag = roundoff_pattern_diff(M, ref)
+        assert cnt <= max(8, ref.nnz // 100) and mag <= 1e-12, (li, key, cnt, mag)
+        assert rel_max_diff(M, ref) <= 1e-10, (li, key)
+        return
+    assert A_struct is not None and L[f"{key}_nnz"] == A_struct.nnz, (li, key)
+    E, missing = embed_in_pattern(M, A_struct)
+    assert 0 < missing <= max(8, E.nnz // 1_000_000), (li, key, missing)
+    assert pattern_sha(E) == L[f"{key}_pattern"], (li, key)
+    check_values(E, arrays, pre, L[f"{key}_fro"])

@@ -6,6 +6,8 @@ Goldens ``hier_C4s`` (C4 recipe at 16^3), ``hier_C3`` (64^3, sigma jump),
 the smallest size where ``make_irreducible`` fires: 154 coarse edges appended
 on level 2) were made by running the reference on the host build of the
 device assembly (oracle/host_assembly.py, tests/golden/make_golden.py BIG).
+Goldens ``hier_V*`` run non-default EminConfig / SolverConfig knobs (omega,
+iterations, n_passes, drop_tol, max_levels) on small hex meshes.
 Goldens ``hier_T9n`` / ``hier_T8d`` (tet meshes), ``hier_Q41d`` (2-D quads)
 and ``hier_R33n`` (2-D triangles) are the reference on its own other element
 families (meshing.py:15), inputs stored with the golden.
@@ -41,7 +43,7 @@ import os
 import numpy as np
 import pytest
 
-from golden_util import (GOLDEN, MESH, MESH_SINGULAR, check_values, csr_hash, embed_in_pattern, load_case,
+from golden_util import (GOLDEN, MESH, MESH_SINGULAR, VARIANTS, check_coarse_operator, check_values, csr_hash, embed_in_pattern, load_case,
                          pattern_sha, sha, stored_inputs)
 
 torch = pytest.importorskip("torch")
@@ -64,7 +66,7 @@ def _case(name):
     return load_case(name)
 
 
-@pytest.mark.parametrize("name", CASES + MESH + MESH_SINGULAR)
+@pytest.mark.parametrize("name", CASES + MESH + MESH_SINGULAR + VARIANTS)
 def test_device_config_vs_reference(name):
     from types import SimpleNamespace
     from paper_2506_08284_b200 import multigrid as mg, device as dv
@@ -83,34 +85,23 @@ def test_device_config_vs_reference(name):
         assert csr_hash(M.to_scipy()) == meta["inputs"][k], k
     assert sha(rhs) == meta["rhs"]
 
-    h = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D,
-                           mg.SolverConfig(coarse_size=meta["coarse_size"]))
+    from paper_2506_08284_b200.edge_prolongator import EminConfig
+    scfg = mg.SolverConfig(coarse_size=meta["coarse_size"],
+                           max_levels=meta.get("max_levels", 10),
+                           emin=EminConfig(**meta.get("emin", {})))
+    h = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, scfg)
     assert [lv.A_e.shape[0] for lv in h.levels] == meta["n_edges"]
     assert [lv.A_e.nnz for lv in h.levels] == meta["nnz_A_e"]
     assert abs(h.operator_complexity - meta["operator_complexity"]) < 1e-14
     for li, (lv, L) in enumerate(zip(h.levels, meta["levels"])):
         assert csr_hash(lv.D.to_scipy()) == L["D"], li
         if li > 0:
+            # STRUCT + TOL; an exact cancellation that differs by summation
+            # order (two entries of 25.9M at 128^3) is accepted as round-off
+            # (golden_util.check_coarse_operator)
             As = lv.A_e.to_scipy()
-            assert pattern_sha(As) == L["A_e_pattern"], (li, "A_e")
-            check_values(As, arrays, f"L{li}_A_e", L["A_e_fro"])
-            Ss = lv.S_e.to_scipy()
-            if pattern_sha(Ss) != L["S_e_pattern"]:
-                # Both sides drop the EXACT zeros of P^T (S P) (compress,
-                # multigrid.py:151), and which round-off-sized entries cancel
-                # exactly depends on the summation order: at 128^3 two
-                # entries of 25.9M do on the device and none in the
-                # reference. The reference kept the whole structural pattern
-                # here (its nnz(S_e) == nnz(A_e), whose pattern is proven
-                # equal above), so the device S_e must be that pattern minus
-                # a handful of entries that are round-off in the reference:
-                # on the reference's pattern (zeros restored) every stored
-                # value still agrees to TOL.
-                assert L["S_e_nnz"] == L["A_e_nnz"], li
-                Ss, missing = embed_in_pattern(Ss, As)
-                assert 0 < missing <= max(8, Ss.nnz // 1_000_000), (li, missing)
-                assert pattern_sha(Ss) == L["S_e_pattern"], (li, "S_e")
-            check_values(Ss, arrays, f"L{li}_S_e", L["S_e_fro"])
+            check_coarse_operator(As, L, arrays, li, "A_e")
+            check_coarse_operator(lv.S_e.to_scipy(), L, arrays, li, "S_e", A_struct=As)
         if lv.P_e is None:
             continue
         assert sha(lv.membership.cpu().numpy().astype(np.int64)) == L["membership"], li

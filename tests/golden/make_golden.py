@@ -269,6 +269,15 @@ def error_cases():
         out["N8d_cs100"] = None
     except ValueError as e:
         out["N8d_cs100"] = str(e)
+    # Algorithm 1's safeguard failing (coarse_gradient.py:90-96): a strength
+    # threshold that leaves a coarse node with no donor row
+    from hcurlamg.edge_prolongator import EminConfig
+    try:
+        mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D,
+                           mg.SolverConfig(coarse_size=100, emin=EminConfig(drop_tol=0.25)))
+        out["N8d_droptol025"] = None
+    except ValueError as e:
+        out["N8d_droptol025"] = str(e)
     return out
 
 

@@ -514,6 +514,24 @@ def test_error_case_matches_reference():
     assert str(e.value).split(":")[0] == msg.split(":")[0]
 
 
+def test_piecewise_const_safeguard_error_matches_reference():
+    """Algorithm 1's safeguard failing inside build_hierarchy (a strength
+    threshold that leaves a coarse node without a donor row,
+    coarse_gradient.py:90-96): the reference's ValueError, same column."""
+    import json
+    import os
+    from golden_util import GOLDEN
+    from paper_2506_08284_b200 import multigrid as mg
+    from paper_2506_08284_b200.edge_prolongator import EminConfig
+    with open(os.path.join(GOLDEN, "errors.json")) as f:
+        msg = json.load(f)["N8d_droptol025"]
+    s = _system(8, 1.0, True)
+    with pytest.raises(ValueError) as e:
+        mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D,
+                           mg.SolverConfig(coarse_size=100, emin=EminConfig(drop_tol=0.25)))
+    assert str(e.value) == msg
+
+
 def test_partitioned_solve_single_rank_nccl():
     """distributed.py on the GPU with CudaOps and an NCCL group of one rank:
     the partitioned V-cycle / PCG equals the single-GPU solve."""

@@ -276,6 +276,17 @@ def _check_device_config(name):
         assert np.allclose(got, want, rtol=1e-3, atol=0), (got / want - 1)
 
 
+def test_oracle_piecewise_const_safeguard_error():
+    import json
+    from golden_util import GOLDEN
+    with open(os.path.join(GOLDEN, "errors.json")) as f:
+        msg = json.load(f)["N8d_droptol025"]
+    s = discretize_hex(8, 1.0, True)
+    with pytest.raises(ValueError) as e:
+        O.build_hierarchy(s.A_e, s.S, s.A_n, s.D, coarse_size=100, drop_tol=0.25)
+    assert str(e.value) == msg
+
+
 def test_oracle_device_config_c4s():
     _check_device_config("C4s")
 

@@ -58,8 +58,13 @@ extern "C" {
 #define SPHC_ST_AGG_CAPACITY 16    /* aggregation row longer than the device kernel's buffer */
 #define SPHC_ST_PC_NO_FIXPOINT 17  /* Algorithm 1 claiming pass did not converge (internal) */
 
+/* emin constraint blocks: the on-chip default class (4 rows per CTA) and the
+ * wide class its overflow rows are re-run through (one row per CTA); beyond
+ * the wide class -> SPHC_ST_EMIN_CAPACITY */
 #define SPHC_EMIN_JMAX 16
 #define SPHC_EMIN_IMAX 128
+#define SPHC_EMIN_JWIDE 32 /* one lane per coarse node                          */
+#define SPHC_EMIN_IWIDE 592 /* 496 node pairs + 32 single-node edges + appended */
 #define SPHC_DIMS_I 129 /* subproblem_dims histogram is [SPHC_DIMS_I][SPHC_DIMS_J] */
 #define SPHC_DIMS_J 17
 
@@ -211,7 +216,7 @@ int sphc_spgemm_fill_long(int64_t n, const int64_t *arp, const int32_t *aci, con
  * joined greedily by the largest |R_dp[:, a] . R_dp[:, b]| over bridging
  * pairs (columns of R_dp = T^T in ttrp/ttci/ttv, summed in ascending fine
  * edge, unfused; ties: smallest (a, b)). ncnt[r] = number of joins, their
- * (a, b) in pairs[2 * (15 r + j)]; -1 single-node graph, -2 |J| > 16. */
+ * (a, b) in pairs[2 * (31 r + j)]; -1 single-node graph, -2 |J| > 32. */
 int sphc_emin_repair(int64_t nrows, const int64_t *rows, const int64_t *trp, const int32_t *tci,
                      const int64_t *prp, const int32_t *pci, const int32_t *ep_a,
                      const int32_t *ep_b, const int64_t *ttrp, const int32_t *ttci,
@@ -506,16 +511,23 @@ int sphc_build_coarse_gradient(int64_t n_agg, int64_t n_int, const int64_t *adj_
 
 /* Per fine edge (emin_setup.py:62-336, Appendix C): node set J (= T row),
  * coarse-edge set I (= prolongator pattern N row), |I|,|J|, the
- * subproblem_dims histogram [65][17] (rows with |I| > 0) and
+ * subproblem_dims histogram [SPHC_DIMS_I][SPHC_DIMS_J] (rows with |I| > 0
+ * inside the table; the caller adds the wider rows from icount / jcount) and
  * rmax2[0] = max |D_h P_n| over all rows (emin_setup.py:289),
- * rmax2[1] = the same over rows whose I is empty (emin_setup.py:292-295). */
+ * rmax2[1] = the same over rows whose I is empty (emin_setup.py:292-295).
+ * Capacity classes: rows with |J| > jcap or |I| > icap (<= 0 or above the
+ * default class = SPHC_EMIN_JMAX / SPHC_EMIN_IMAX; tests lower them) are
+ * counted in *over (caller zeroes it before the count pass) and handled by a
+ * second launch of the wide class, which returns at once while *over == 0.
+ * sphc_emin_fill and sphc_emin_step take the same jcap, icap and over. */
 int sphc_emin_count(int64_t n_e, const int64_t *drp, const int32_t *dci, const double *dv,
                     const int64_t *prp, const int32_t *pci, const double *pv,
                     const int64_t *adj_rp, const int32_t *adj_col, int64_t n_int,
                     const int32_t *single_id, const int64_t *xrp, const int32_t *xeid,
                     const int32_t *ep_a, const int32_t *ep_b, int64_t *icount,
                     int64_t *jcount, double *rmax2, int64_t *dims, uint8_t *rowflag,
-                    double *rowmax, int64_t *status, void *stream);
+                    double *rowmax, int32_t jcap, int32_t icap, int64_t *over,
+                    int64_t *status, void *stream);
 /* Row extras: coarse edges appended by the host make_irreducible pass
  * (emin_setup.py:183-217,311-333) as a CSR over fine edges (xrp, xeid; NULL
  * xrp = none); ep_a/ep_b = endpoints of every coarse edge. The count pass only
@@ -532,7 +544,8 @@ int sphc_emin_fill(int64_t n_e, const int64_t *drp, const int32_t *dci, const do
                    const int32_t *single_id, const int64_t *xrp, const int32_t *xeid,
                    const int32_t *ep_a, const int32_t *ep_b, const int64_t *trp,
                    int32_t *tci, double *tv, const int64_t *erp, int32_t *eci, double *ev,
-                   uint8_t *rowflag, int64_t *status, void *stream);
+                   uint8_t *rowflag, int32_t jcap, int32_t icap, int64_t *over,
+                   int64_t *status, void *stream);
 
 /* One projected damped-Jacobi sweep (edge_prolongator.py:170-176) fused with
  * the masked product S P on the fixed pattern, the energy of the INPUT values
@@ -548,7 +561,8 @@ int sphc_emin_step(int64_t row0, int64_t row1, const int64_t *srp, const int32_t
                    const double *tv, const int64_t *erp, const int32_t *eci,
                    const double *p_in, double *p_out, const int32_t *ep_a,
                    const int32_t *ep_b, double omega, int update, double *e_row,
-                   double *res_max, int64_t *status, void *stream);
+                   double *res_max, int32_t jcap, int32_t icap, const int64_t *over,
+                   int64_t *status, void *stream);
 
 /* SpGEMM rows beyond the on-chip kernels' capacity (the count kernels
  * mark them with count -1: > 256 distinct columns, a B row longer than a

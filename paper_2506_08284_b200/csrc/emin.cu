@@ -14,34 +14,46 @@
 #include "common.cuh"
 
 #define EM_WARPS 4
-#define EM_HCAP 256  // open-addressing slots per warp (|I| <= 128)
 #define JM SPHC_EMIN_JMAX
 #define IM SPHC_EMIN_IMAX
 
-struct EminRow {
-  int J[JM];
-  double r[JM];
-  int Icol[IM];
-  signed char pa[IM];  // position of tail node in J, -1 for single-node edges
-  signed char pb[IM];  // position of head (or the single) node in J
-  double L[JM * (JM + 1) / 2];  // packed lower Cholesky factor, row p at p(p+1)/2
-  double y[JM];
-  double g[IM];
-  double p[IM];
-  int sc[2][JM];       // staged P_n rows of the two endpoints (em_build_J)
-  double sv[2][JM];
-  unsigned adj[JM];    // interior-edge adjacency bitmasks over J (em_factor)
-  int hkey[EM_HCAP];   // coarse column -> position in Icol (masked S P lookups)
-  unsigned char hpos[EM_HCAP];
-  unsigned incm;       // J nodes incident to some edge of I
-  int nJ, nI, k, err, fc;
+// Per-warp working set of one constraint block. Two capacity classes: the
+// on-chip default (|J| <= 16, |I| <= 128, 4 warps per CTA) that every mesh
+// family of the reference fits, and a wide one (|J| <= 32 = one lane per
+// coarse node, |I| <= 592, which |J| <= 32 bounds: 496 interior pairs + 32
+// single-node edges + the appended ones; 1 warp per CTA) that the rows the
+// default class cannot hold are re-run through. Same arithmetic, same order.
+template <int JMAX_, int IMAX_, int HCAP_, typename HPOS>
+struct EminRowT {
+  static constexpr int JMAX = JMAX_, IMAX = IMAX_, HCAP = HCAP_;
+  int J[JMAX_];
+  double r[JMAX_];
+  int Icol[IMAX_];
+  signed char pa[IMAX_];  // position of tail node in J, -1 for single-node edges
+  signed char pb[IMAX_];  // position of head (or the single) node in J
+  double L[JMAX_ * (JMAX_ + 1) / 2];  // packed lower Cholesky factor, row p at p(p+1)/2
+  double y[JMAX_];
+  double g[IMAX_];
+  double p[IMAX_];
+  int sc[2][JMAX_];       // staged P_n rows of the two endpoints (em_build_J)
+  double sv[2][JMAX_];
+  unsigned adj[JMAX_];    // interior-edge adjacency bitmasks over J (em_factor)
+  int hkey[HCAP_];        // coarse column -> position in Icol (masked S P lookups)
+  HPOS hpos[HCAP_];
+  unsigned incm;          // J nodes incident to some edge of I
+  int nJ, nI, k, err, fc; // err: 1 = reported error, 2 = beyond this class's capacity
 };
+typedef EminRowT<JM, IM, 256, unsigned char> EminRow;
+typedef EminRowT<SPHC_EMIN_JWIDE, SPHC_EMIN_IWIDE, 2048, unsigned short> EminRowWide;
+
+__device__ __forceinline__ unsigned low_mask(int n) { return n >= 32 ? 0xffffffffu : (1u << n) - 1u; }
 
 // all lanes: the P_n rows of the (<=2) free endpoints are staged in shared
 // memory with one coalesced load each, then lane 0 merges them into J, r
 // (scipy csr_matmat order). Serial global loads here used to dominate the
 // pass: every merge step waited on an L2 round trip.
-__device__ void em_build_J(EminRow& R, i64 i, const i64* __restrict__ drp,
+template <class Row>
+__device__ void em_build_J(Row& R, i64 i, const i64* __restrict__ drp,
                            const int* __restrict__ dci, const double* __restrict__ dv,
                            const i64* __restrict__ prp, const int* __restrict__ pci,
                            const double* __restrict__ pv, i64* status, int lane) {
@@ -69,21 +81,32 @@ __device__ void em_build_J(EminRow& R, i64 i, const i64* __restrict__ drp,
     b0 = prp[hb];
     nb = (int)(prp[hb + 1] - b0);
   }
-  if (na > JM || nb > JM) {   // the merged row would exceed JM as well
+  constexpr int JC = Row::JMAX;
+  if (na > JC || nb > JC) {   // the merged row would exceed the class as well
     if (lane == 0) {
-      report(status, SPHC_ST_EMIN_CAPACITY, i);
-      R.err = 1;
+      R.err = 2;
       R.nJ = 0;
     }
     __syncwarp();
     return;
   }
-  if (lane < na) {
-    R.sc[0][lane] = pci[a0 + lane];
-    R.sv[0][lane] = pv[a0 + lane];
-  } else if (lane >= 16 && lane - 16 < nb) {
-    R.sc[1][lane - 16] = pci[b0 + lane - 16];
-    R.sv[1][lane - 16] = pv[b0 + lane - 16];
+  if (JC <= 16) {             // both rows in one round of loads
+    if (lane < na) {
+      R.sc[0][lane] = pci[a0 + lane];
+      R.sv[0][lane] = pv[a0 + lane];
+    } else if (lane >= 16 && lane - 16 < nb) {
+      R.sc[1][lane - 16] = pci[b0 + lane - 16];
+      R.sv[1][lane - 16] = pv[b0 + lane - 16];
+    }
+  } else {
+    if (lane < na) {
+      R.sc[0][lane] = pci[a0 + lane];
+      R.sv[0][lane] = pv[a0 + lane];
+    }
+    if (lane < nb) {
+      R.sc[1][lane] = pci[b0 + lane];
+      R.sv[1][lane] = pv[b0 + lane];
+    }
   }
   __syncwarp();
   if (lane == 0) {
@@ -97,9 +120,8 @@ __device__ void em_build_J(EminRow& R, i64 i, const i64* __restrict__ drp,
       double acc = 0.0;
       if (ca == c) acc = __dadd_rn(acc, __dmul_rn(sa, R.sv[0][ia++]));
       if (cb == c) acc = __dadd_rn(acc, __dmul_rn(sb, R.sv[1][ib++]));
-      if (n >= JM) {
-        report(status, SPHC_ST_EMIN_CAPACITY, i);
-        R.err = 1;
+      if (n >= JC) {
+        R.err = 2;
         n = 0;
         break;
       }
@@ -118,11 +140,13 @@ __device__ void em_build_J(EminRow& R, i64 i, const i64* __restrict__ drp,
 
 // all lanes: I = interior coarse edges among J pairs (lexicographic = ascending
 // ids) followed by single-node edges of J nodes (ascending ids).
-__device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
+template <class Row>
+__device__ void em_build_I(Row& R, i64 i, const i64* __restrict__ adj_rp,
                            const int* __restrict__ adj_col, const int* __restrict__ single_id,
                            const i64* __restrict__ xrp, const int* __restrict__ xeid,
                            const int* __restrict__ ep_a, const int* __restrict__ ep_b,
                            i64* status, int lane) {
+  constexpr int IC = Row::IMAX;
   int nJ = R.nJ;
   int npairs = nJ * (nJ - 1) / 2;
   int nI = 0;
@@ -149,7 +173,7 @@ __device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
     unsigned bal = __ballot_sync(FULL_MASK, e >= 0);
     if (e >= 0) {
       int o = nI + __popc(bal & ((1u << lane) - 1));
-      if (o < IM) {
+      if (o < IC) {
         R.Icol[o] = e;
         R.pa[o] = (signed char)pa;
         R.pb[o] = (signed char)pb;
@@ -163,7 +187,7 @@ __device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
     unsigned bal = __ballot_sync(FULL_MASK, sid >= 0);
     if (sid >= 0) {
       int o = nI + __popc(bal & ((1u << lane) - 1));
-      if (o < IM) {
+      if (o < IC) {
         R.Icol[o] = sid;
         R.pa[o] = -1;
         R.pb[o] = (signed char)p;
@@ -178,7 +202,7 @@ __device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
     for (i64 t = x0 + lane; t < x1; t += 32) {
       int o = nI + (int)(t - x0);
       int e = xeid[t];
-      if (o < IM) {
+      if (o < IC) {
         R.Icol[o] = e;
         R.pa[o] = (signed char)lower_bound_i32(R.J, nJ, ep_a[e]);
         R.pb[o] = (signed char)lower_bound_i32(R.J, nJ, ep_b[e]);
@@ -186,13 +210,10 @@ __device__ void em_build_I(EminRow& R, i64 i, const i64* __restrict__ adj_rp,
     }
     nI += (int)(x1 - x0);
   }
-  over = nI > IM;
+  over = nI > IC;
   if (lane == 0) {
     R.nI = over ? 0 : nI;
-    if (over) {
-      report(status, SPHC_ST_EMIN_CAPACITY, i);
-      R.err = 1;
-    }
+    if (over) R.err = 2;
   }
   __syncwarp();
 }
@@ -205,13 +226,14 @@ __device__ __forceinline__ int tri(int p, int m) { return p * (p + 1) / 2 + m; }
 // pivot spread over the lanes. Every factor entry is computed with the
 // serial loop's operation order, so the factor is bitwise the serial one.
 // Returns (warp-uniform) 0 ok, 1 reducible, 2 rank failure (reported).
-__device__ int em_factor(EminRow& R, i64 i, i64* status, int lane) {
+template <class Row>
+__device__ int em_factor(Row& R, i64 i, i64* status, int lane) {
   int nJ = R.nJ, nI = R.nI;
   // irreducibility (emin_setup.py check_irreducible): every J node incident
   // to an edge of I and J connected by the interior edges. Lanes take the
   // edges and build adjacency bitmasks; reachability from node 0 is a
   // warp-wide OR per BFS level (<= |J| <= 16 levels).
-  if (lane < JM) R.adj[lane] = 0u;
+  if (lane < Row::JMAX) R.adj[lane] = 0u;
   if (lane == 0) R.incm = 0u;
   __syncwarp();
   bool dir = false;
@@ -228,7 +250,7 @@ __device__ int em_factor(EminRow& R, i64 i, i64* status, int lane) {
   }
   bool dirich = __any_sync(FULL_MASK, dir);
   __syncwarp();
-  unsigned full = (1u << nJ) - 1u;
+  unsigned full = low_mask(nJ);
   unsigned myadj = lane < nJ ? R.adj[lane] : 0u;
   unsigned reach = nJ ? 1u : 0u;
   for (;;) {
@@ -287,7 +309,8 @@ __device__ int em_factor(EminRow& R, i64 i, i64* status, int lane) {
 }
 
 // lane 0: y <- M^-1 y (k entries) with the Cholesky factor
-__device__ void em_solve(const EminRow& R, double* y) {
+template <class Row>
+__device__ void em_solve(const Row& R, double* y) {
   int k = R.k;
   const double* L = R.L;
   for (int j = 0; j < k; j++) {
@@ -303,8 +326,13 @@ __device__ void em_solve(const EminRow& R, double* y) {
   }
 }
 
-template <bool FILL>
-__global__ void __launch_bounds__(EM_WARPS * 32)
+// One pass over the fine edges. WIDE = false: every row, the default class;
+// rows beyond (jcap, icap) -- the class's capacity unless a test lowers it --
+// are marked (count: icount = -1 and *over += 1) and left to the wide pass.
+// WIDE = true: launched right behind on the same stream, returns at once
+// unless *over != 0, then handles exactly the marked rows.
+template <bool FILL, bool WIDE, class Row, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
     k_emin_setup(i64 n_e, const i64* __restrict__ drp, const int* __restrict__ dci,
                  const double* __restrict__ dv, const i64* __restrict__ prp,
                  const int* __restrict__ pci, const double* __restrict__ pv,
@@ -315,20 +343,41 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
                  i64* dims, unsigned char* rowflag, double* rowmax,
                  const i64* __restrict__ trp, int* __restrict__ tci,
                  double* __restrict__ tv, const i64* __restrict__ erp, int* __restrict__ eci,
-                 double* __restrict__ ev, i64* status) {
-  __shared__ EminRow rows[EM_WARPS];
+                 double* __restrict__ ev, int jcap, int icap, i64* over, i64* status) {
+  if (WIDE && *(volatile i64*)over == 0) return;
+  __shared__ Row rows[WARPS];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  EminRow& R = rows[w];
-  for (i64 i = (i64)blockIdx.x * EM_WARPS + w; i < n_e; i += (i64)gridDim.x * EM_WARPS) {
-    em_build_J(R, i, drp, dci, dv, prp, pci, pv, status, lane);
-    if (R.err) {
-      if (!FILL && lane == 0) { icount[i] = 0; jcount[i] = 0; }
-      __syncwarp();
+  Row& R = rows[w];
+  for (i64 i = (i64)blockIdx.x * WARPS + w; i < n_e; i += (i64)gridDim.x * WARPS) {
+    if (FILL) {
+      // the count pass sized the rows: the row's class follows from its sizes
+      bool wide = trp[i + 1] - trp[i] > jcap || erp[i + 1] - erp[i] > icap;
+      if (wide != WIDE) continue;
+    } else if (WIDE && icount[i] != -1) {
       continue;
     }
-    em_build_I(R, i, adj_rp, adj_col, single_id, xrp, xeid, ep_a, ep_b, status, lane);
+    em_build_J(R, i, drp, dci, dv, prp, pci, pv, status, lane);
+    if (!R.err && !WIDE && R.nJ > jcap) {
+      __syncwarp();
+      if (lane == 0) R.err = 2;
+      __syncwarp();
+    }
+    if (!R.err) em_build_I(R, i, adj_rp, adj_col, single_id, xrp, xeid, ep_a, ep_b, status, lane);
+    if (!R.err && !WIDE && R.nI > icap) {
+      __syncwarp();
+      if (lane == 0) R.err = 2;
+      __syncwarp();
+    }
     if (R.err) {
-      if (!FILL && lane == 0) { icount[i] = 0; jcount[i] = R.nJ; }
+      if (lane == 0) {
+        bool defer = R.err == 2 && !WIDE && !FILL;
+        if (R.err == 2 && !defer) report(status, SPHC_ST_EMIN_CAPACITY, i);
+        if (!FILL) {
+          icount[i] = defer ? -1 : 0;
+          jcount[i] = defer ? -1 : 0;
+          if (defer) atomicAdd((unsigned long long*)over, 1ull);
+        }
+      }
       __syncwarp();
       continue;
     }
@@ -339,7 +388,8 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
         for (int q = 0; q < nJ; q++) rm = fmax(rm, fabs(R.r[q]));
         atomic_max_nonneg(&rmax2[0], rm);
         if (nI == 0) atomic_max_nonneg(&rmax2[1], rm);
-        else atomicAdd((unsigned long long*)&dims[nI * SPHC_DIMS_J + nJ], 1ull);
+        else if (nI < SPHC_DIMS_I && nJ < SPHC_DIMS_J)
+          atomicAdd((unsigned long long*)&dims[nI * SPHC_DIMS_J + nJ], 1ull);
         icount[i] = nI;
         jcount[i] = nJ;
         if (rowflag) rowflag[i] = nI == 0 ? 2 : 0;
@@ -402,19 +452,29 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
   }
 }
 
+static inline int em_cap(int cap, int top) { return cap <= 0 || cap > top ? top : cap; }
+
 extern "C" int sphc_emin_count(int64_t n_e, const int64_t* drp, const int32_t* dci,
                                const double* dv, const int64_t* prp, const int32_t* pci,
                                const double* pv, const int64_t* adj_rp, const int32_t* adj_col,
                                int64_t n_int, const int32_t* single_id, const int64_t* xrp,
                                const int32_t* xeid, const int32_t* ep_a, const int32_t* ep_b,
                                int64_t* icount, int64_t* jcount, double* rmax2, int64_t* dims,
-                               uint8_t* rowflag, double* rowmax, int64_t* status,
-                               void* stream) {
+                               uint8_t* rowflag, double* rowmax, int32_t jcap, int32_t icap,
+                               int64_t* over, int64_t* status, void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_emin_setup<false><<<grid_for(n_e, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
+  jcap = em_cap(jcap, JM);
+  icap = em_cap(icap, IM);
+  k_emin_setup<false, false, EminRow, EM_WARPS>
+      <<<grid_for(n_e, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
+          n_e, drp, dci, dv, prp, pci, pv, adj_rp, adj_col, single_id, xrp, xeid, ep_a, ep_b,
+          icount, jcount, rmax2, dims, rowflag, rowmax, nullptr, nullptr, nullptr, nullptr,
+          nullptr, nullptr, jcap, icap, over, status);
+  SPHC_LAUNCH_CHECK();
+  k_emin_setup<false, true, EminRowWide, 1><<<grid_for(n_e, 1, SPHC_NUM_SMS * 32), 32, 0, s>>>(
       n_e, drp, dci, dv, prp, pci, pv, adj_rp, adj_col, single_id, xrp, xeid, ep_a, ep_b,
       icount, jcount, rmax2, dims, rowflag, rowmax, nullptr, nullptr, nullptr, nullptr,
-      nullptr, nullptr, status);
+      nullptr, nullptr, jcap, icap, over, status);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -425,33 +485,44 @@ extern "C" int sphc_emin_fill(int64_t n_e, const int64_t* drp, const int32_t* dc
                               int64_t n_int, const int32_t* single_id, const int64_t* xrp,
                               const int32_t* xeid, const int32_t* ep_a, const int32_t* ep_b,
                               const int64_t* trp, int32_t* tci, double* tv, const int64_t* erp,
-                              int32_t* eci, double* ev, uint8_t* rowflag, int64_t* status,
-                              void* stream) {
+                              int32_t* eci, double* ev, uint8_t* rowflag, int32_t jcap,
+                              int32_t icap, int64_t* over, int64_t* status, void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_emin_setup<true><<<grid_for(n_e, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
+  jcap = em_cap(jcap, JM);
+  icap = em_cap(icap, IM);
+  k_emin_setup<true, false, EminRow, EM_WARPS>
+      <<<grid_for(n_e, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
+          n_e, drp, dci, dv, prp, pci, pv, adj_rp, adj_col, single_id, xrp, xeid, ep_a, ep_b,
+          nullptr, nullptr, nullptr, nullptr, rowflag, nullptr, trp, tci, tv, erp, eci, ev,
+          jcap, icap, over, status);
+  SPHC_LAUNCH_CHECK();
+  k_emin_setup<true, true, EminRowWide, 1><<<grid_for(n_e, 1, SPHC_NUM_SMS * 32), 32, 0, s>>>(
       n_e, drp, dci, dv, prp, pci, pv, adj_rp, adj_col, single_id, xrp, xeid, ep_a, ep_b,
-      nullptr, nullptr, nullptr, nullptr, rowflag, nullptr, trp, tci, tv, erp, eci, ev,
-      status);
+      nullptr, nullptr, nullptr, nullptr, rowflag, nullptr, trp, tci, tv, erp, eci, ev, jcap,
+      icap, over, status);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
 
+template <class Row>
 __device__ __forceinline__ unsigned em_h(int col) {
-  return ((unsigned)col * 2654435761u) & (EM_HCAP - 1);
+  return ((unsigned)col * 2654435761u) & (Row::HCAP - 1);
 }
 
 // position of coarse column col in the row's I, -1 if absent
-__device__ __forceinline__ int em_lookup(const EminRow& R, int col) {
-  unsigned h = em_h(col);
+template <class Row>
+__device__ __forceinline__ int em_lookup(const Row& R, int col) {
+  unsigned h = em_h<Row>(col);
   for (;;) {
     int k = R.hkey[h];
     if (k == col) return R.hpos[h];
     if (k < 0) return -1;
-    h = (h + 1) & (EM_HCAP - 1);
+    h = (h + 1) & (Row::HCAP - 1);
   }
 }
 
-__global__ void __launch_bounds__(EM_WARPS * 32)
+template <bool WIDE, class Row, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
     k_emin_step(i64 row0, i64 row1, const i64* __restrict__ srp, const int* __restrict__ sci,
                 const double* __restrict__ sv, const double* __restrict__ dinv,
                 const i64* __restrict__ trp, const int* __restrict__ tci,
@@ -459,15 +530,17 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
                 const int* __restrict__ eci, const double* __restrict__ p_in,
                 double* __restrict__ p_out, const int* __restrict__ ep_a,
                 const int* __restrict__ ep_b, double omega, int update,
-                double* __restrict__ e_row, double* res_max, i64* status) {
-  __shared__ EminRow rows[EM_WARPS];
+                double* __restrict__ e_row, double* res_max, int jcap, int icap,
+                const i64* over, i64* status) {
+  if (WIDE && *(volatile const i64*)over == 0) return;
+  __shared__ Row rows[WARPS];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  EminRow& R = rows[w];
-  for (i64 i = row0 + (i64)blockIdx.x * EM_WARPS + w; i < row1;
-       i += (i64)gridDim.x * EM_WARPS) {
+  Row& R = rows[w];
+  for (i64 i = row0 + (i64)blockIdx.x * WARPS + w; i < row1; i += (i64)gridDim.x * WARPS) {
     i64 t0 = trp[i], e0 = erp[i];
     int nJ = (int)(trp[i + 1] - t0), nI = (int)(erp[i + 1] - e0);
-    if (nI == 0 || nJ > JM || nI > IM) {
+    if ((nJ > jcap || nI > icap) != WIDE) continue;      // the other class's row
+    if (nI == 0 || nJ > Row::JMAX || nI > Row::IMAX) {
       if (lane == 0) e_row[i] = 0.0;
       continue;
     }
@@ -476,7 +549,7 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
       R.r[q] = tv[t0 + q];
     }
     __syncwarp();
-    for (int t = lane; t < EM_HCAP; t += 32) R.hkey[t] = -1;
+    for (int t = lane; t < Row::HCAP; t += 32) R.hkey[t] = -1;
     __syncwarp();
     for (int e = lane; e < nI; e += 32) {
       int col = eci[e0 + e];
@@ -486,9 +559,9 @@ __global__ void __launch_bounds__(EM_WARPS * 32)
       int a = ep_a[col], b = ep_b[col];
       R.pb[e] = (signed char)lower_bound_i32(R.J, nJ, b);
       R.pa[e] = (signed char)(a < 0 ? -1 : lower_bound_i32(R.J, nJ, a));
-      unsigned h = em_h(col);     // columns of a row are distinct
-      while (atomicCAS(&R.hkey[h], -1, col) != -1) h = (h + 1) & (EM_HCAP - 1);
-      R.hpos[h] = (unsigned char)e;
+      unsigned h = em_h<Row>(col);     // columns of a row are distinct
+      while (atomicCAS(&R.hkey[h], -1, col) != -1) h = (h + 1) & (Row::HCAP - 1);
+      R.hpos[h] = e;
     }
     if (lane == 0) {
       R.nJ = nJ;
@@ -617,12 +690,20 @@ extern "C" int sphc_emin_step(int64_t row0, int64_t row1, const int64_t* srp, co
                               const int32_t* tci, const double* tv, const int64_t* erp,
                               const int32_t* eci, const double* p_in, double* p_out,
                               const int32_t* ep_a, const int32_t* ep_b, double omega, int update,
-                              double* e_row, double* res_max, int64_t* status, void* stream) {
+                              double* e_row, double* res_max, int32_t jcap, int32_t icap,
+                              const int64_t* over, int64_t* status, void* stream) {
   cudaStream_t s = as_stream(stream);
   if (row1 <= row0) return 0;
-  k_emin_step<<<grid_for(row1 - row0, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
-      row0, row1, srp, sci, sv, dinv, trp, tci, tv, erp, eci, p_in, p_out, ep_a, ep_b, omega, update,
-      e_row, res_max, status);
+  jcap = em_cap(jcap, JM);
+  icap = em_cap(icap, IM);
+  k_emin_step<false, EminRow, EM_WARPS>
+      <<<grid_for(row1 - row0, EM_WARPS, SPHC_NUM_SMS * 32), EM_WARPS * 32, 0, s>>>(
+          row0, row1, srp, sci, sv, dinv, trp, tci, tv, erp, eci, p_in, p_out, ep_a, ep_b, omega,
+          update, e_row, res_max, jcap, icap, over, status);
+  SPHC_LAUNCH_CHECK();
+  k_emin_step<true, EminRowWide, 1><<<grid_for(row1 - row0, 1, SPHC_NUM_SMS * 32), 32, 0, s>>>(
+      row0, row1, srp, sci, sv, dinv, trp, tci, tv, erp, eci, p_in, p_out, ep_a, ep_b, omega,
+      update, e_row, res_max, jcap, icap, over, status);
   SPHC_LAUNCH_CHECK();
   return 0;
 }
@@ -643,7 +724,7 @@ extern "C" int sphc_emin_step(int64_t row0, int64_t row1, const int64_t* srp, co
 // ascending row order. Output: ncnt[r] edges in pairs[r * 15 + j] (a, b);
 // ncnt[r] = -1: single-node graph (the reference's ValueError), -2: the row
 // exceeds the kernel's |J| <= 16.
-#define RP_MAXNEW (JM - 1)
+#define RP_MAXNEW (SPHC_EMIN_JWIDE - 1)
 
 __global__ void __launch_bounds__(128)
     k_emin_repair(i64 nrows, const i64* __restrict__ rows, const i64* __restrict__ trp,
@@ -660,7 +741,7 @@ __global__ void __launch_bounds__(128)
     i64 i = rows[r];
     i64 t0 = trp[i];
     int nJ = (int)(trp[i + 1] - t0);
-    if (nJ > JM) {
+    if (nJ > SPHC_EMIN_JWIDE) {
       if (lane == 0) ncnt[r] = -2;
       continue;
     }
@@ -686,7 +767,7 @@ __global__ void __launch_bounds__(128)
       // component label = lowest node index reachable (BFS by bitmask OR)
       unsigned reach = 1u << lane;
       if (lane >= nJ) reach = 0u;
-      for (int it = 0; it < JM; it++) {
+      for (int it = 0; it < SPHC_EMIN_JWIDE; it++) {
         unsigned nr = reach;
         for (int q = 0; q < nJ; q++) {
           unsigned aq = __shfl_sync(FULL_MASK, adj, q);

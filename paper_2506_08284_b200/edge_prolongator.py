@@ -84,6 +84,8 @@ def emin_sweeps(S, setup, omega, iterations, shard=None):
     res = torch.zeros(1, dtype=torch.float64, device=e_row.device)
     esum = dv.empty_f64(iterations + 1)
     vals = Pp.val
+    jcap, icap = es.DEFAULT_CLASS_CAPS
+    over = setup.over if setup.over is not None else dv.zeros_i64(1)
     blocks = shard.blocks(n_e) if shard is not None else [(0, 0, n_e)]
     if shard is not None and shard.collective:
         from .sharding import host_offsets
@@ -105,7 +107,7 @@ def emin_sweeps(S, setup, omega, iterations, shard=None):
             for _, lo, hi in blocks:
                 call("sphc_emin_step", lo, hi, S.rowptr, S.col, S.val, dinv, T.rowptr, T.col,
                      T.val, Pp.rowptr, Pp.col, vals, out, cg.ep_a, cg.ep_b, float(omega), 1,
-                     e_row, res, st.t)
+                     e_row, res, jcap, icap, over, st.t)
             gather(out)
             dv.vsum(e_row, esum[it:it + 1])
             vals = out
@@ -114,7 +116,7 @@ def emin_sweeps(S, setup, omega, iterations, shard=None):
     for _, lo, hi in blocks:
         call("sphc_emin_step", lo, hi, S.rowptr, S.col, S.val, None, T.rowptr, T.col, T.val,
              Pp.rowptr, Pp.col, vals, None, cg.ep_a, cg.ep_b, float(omega), 0, e_row, res,
-             st.t)
+             jcap, icap, over, st.t)
     gather(None)
     dv.vsum(e_row, esum[iterations:iterations + 1])
     if shard is not None:
@@ -198,9 +200,11 @@ def emin_step(S, values, setup, structure, omega):
     e_row = dv.empty_f64(n_e)
     res = torch.zeros(1, dtype=torch.float64, device=e_row.device)
     out = torch.empty_like(values)
+    jcap, icap = es.DEFAULT_CLASS_CAPS
+    over = setup.over if setup.over is not None else dv.zeros_i64(1)
     call("sphc_emin_step", 0, n_e, S.rowptr, S.col, S.val, jacobi_diag_inverse(S), T.rowptr,
          T.col, T.val, structure.rowptr, structure.col, values, out, cg.ep_a, cg.ep_b,
-         float(omega), 1, e_row, res, st.t)
+         float(omega), 1, e_row, res, jcap, icap, over, st.t)
     st.defer(es._checker(S))
     return out
 

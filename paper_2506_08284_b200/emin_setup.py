@@ -30,6 +30,7 @@ class EminSetup:
     subproblem_dims: Counter
     rdp_scale: float
     n_augmented: int = 0
+    over: torch.Tensor = None   # device count of rows in the wide capacity class
 
     @property
     def R_dp(self):
@@ -50,7 +51,7 @@ def _checker(D):
                              "pattern (isolated edge or pattern bug)")
         if "EMIN_CAPACITY" in rows:
             raise RuntimeError(f"fine edge {rows['EMIN_CAPACITY']}: constraint block exceeds "
-                               f"the device kernel capacity (|J| <= 16, |I| <= 128)")
+                               f"the device kernels' wide class (|J| <= 32, |I| <= 592)")
         if "REDUCIBLE" in rows:
             # only reachable if a block is still reducible after the repair pass
             raise RuntimeError(
@@ -60,6 +61,14 @@ def _checker(D):
             raise ValueError(f"fine edge {rows['RANK_LOW']}: numerical rank below the "
                              "expected rank (topology bug)")
     return check
+
+
+# Capacity of the default (on-chip, 4 rows per CTA) class of the emin kernels:
+# rows with |J| or |I| above it are re-run through the wide class (|J| <= 32).
+# (0, 0) = the compiled capacity (16, 128); tests lower it to drive ordinary
+# rows through the wide kernels.
+DEFAULT_CLASS_CAPS = (0, 0)
+_TABLE = (129, 17)      # SPHC_DIMS_I, SPHC_DIMS_J
 
 
 def _raise(st, D):
@@ -80,11 +89,13 @@ def _count(D, P, cg, xrp, xeid, flags, shard=None):
     dims = torch.zeros(129 * 17, dtype=torch.int64, device=dev)
     rowflag = torch.zeros(n_e, dtype=torch.uint8, device=dev) if flags else None
     rowmax = torch.empty(n_e, dtype=torch.float64, device=dev) if flags else None
+    over = dv.zeros_i64(1)
+    jcap, icap = DEFAULT_CLASS_CAPS
     for _, lo, hi in (shard.blocks(n_e) if shard else [(0, 0, n_e)]):
         call("sphc_emin_count", hi - lo, D.rowptr[lo:], D.col, D.val, P.rowptr, P.col, P.val,
              cg.adj.rowptr, cg.adj.col, cg.n_interior, cg.single_id, _view(xrp, lo), xeid,
              cg.ep_a, cg.ep_b, icount[lo:], jcount[lo:], rmax2, dims, _view(rowflag, lo),
-             _view(rowmax, lo), st.t)
+             _view(rowmax, lo), jcap, icap, over, st.t)
     if shard is not None:
         b = shard.bounds(n_e)
         for t in (icount, jcount, rowflag, rowmax):
@@ -92,11 +103,12 @@ def _count(D, P, cg, xrp, xeid, flags, shard=None):
                 shard.gather_ranges(t, b)
         shard.max_(rmax2)
         shard.sum_(dims)
+        shard.sum_(over)
         shard.min_(st.t)
-    return st, icount, jcount, rmax2, dims, rowflag, rowmax
+    return st, icount, jcount, rmax2, dims, rowflag, rowmax, over
 
 
-def _fill(D, P, cg, icount, jcount, xrp, xeid, st, rowflag=None, shard=None):
+def _fill(D, P, cg, icount, jcount, xrp, xeid, st, over, rowflag=None, shard=None):
     n_e = D.shape[0]
     dev = D.rowptr.device
     (trp, tnnz), (erp, ennz) = dv.scan_many(jcount, icount)
@@ -104,10 +116,12 @@ def _fill(D, P, cg, icount, jcount, xrp, xeid, st, rowflag=None, shard=None):
     tv = torch.empty(tnnz, dtype=torch.float64, device=dev)
     eci = torch.empty(ennz, dtype=torch.int32, device=dev)
     ev = torch.empty(ennz, dtype=torch.float64, device=dev)
+    jcap, icap = DEFAULT_CLASS_CAPS
     for _, lo, hi in (shard.blocks(n_e) if shard else [(0, 0, n_e)]):
         call("sphc_emin_fill", hi - lo, D.rowptr[lo:], D.col, D.val, P.rowptr, P.col, P.val,
              cg.adj.rowptr, cg.adj.col, cg.n_interior, cg.single_id, _view(xrp, lo), xeid,
-             cg.ep_a, cg.ep_b, trp[lo:], tci, tv, erp[lo:], eci, ev, _view(rowflag, lo), st.t)
+             cg.ep_a, cg.ep_b, trp[lo:], tci, tv, erp[lo:], eci, ev, _view(rowflag, lo),
+             jcap, icap, over, st.t)
     if shard is not None:
         b = shard.bounds(n_e)
         if shard.collective:
@@ -139,13 +153,13 @@ def setup_constraints(D_h, P_n, cg, shard=None):
     n_e = D.shape[0]
     check = _checker(D)
     with phase("emin.count"):
-        st, icount, jcount, rmax2, dims, rowflag, rowmax = _count(D, P, cg, None, None, True,
-                                                                  shard)
+        st, icount, jcount, rmax2, dims, rowflag, rowmax, over = _count(D, P, cg, None, None,
+                                                                        True, shard)
     # the count pass's checks ride on the fill pass's scan readback
     st.defer(check)
     # the fill pass factors every block and flags the reducible ones
     with phase("emin.fill"):
-        T, pattern = _fill(D, P, cg, icount, jcount, None, None, st, rowflag, shard)
+        T, pattern = _fill(D, P, cg, icount, jcount, None, None, st, over, rowflag, shard)
     flags = rowflag
     # reducible rows, and empty-pattern rows whose commutator row exceeds
     # 1e-12 rdp_scale (rdp_scale = max(1, max|R_dp|)); decided on the device
@@ -153,7 +167,7 @@ def setup_constraints(D_h, P_n, cg, shard=None):
     need = (flags & 1).bool() | ((rmax2[1:2] > 1e-12 * scale)
                                  & (flags & 2).bool() & (rowmax > 1e-12 * scale))
     st.defer(check)
-    rm, any_need, h = dv.readback(rmax2, need.any(), dims)
+    rm, any_need, h, ov = dv.readback(rmax2, need.any(), dims, over)
     rdp_scale = max(1.0, float(rm[0]))
     n_aug = 0
     if bool(any_need[0]):
@@ -166,29 +180,35 @@ def setup_constraints(D_h, P_n, cg, shard=None):
             # the refill flags the post-pass rows that are still reducible
             # (instead of raising); the host repairs just those, then refills
             track = post is not None
-            st, icount, jcount, rmax2, dims, rowflag, _ = _count(D, P, cg, xrp, xeid, track,
-                                                                 shard)
+            st, icount, jcount, rmax2, dims, rowflag, _, over = _count(D, P, cg, xrp, xeid,
+                                                                       track, shard)
             st.defer(check)
-            T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st,
+            T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st, over,
                                rowflag=rowflag, shard=shard)
             st.defer(check)
             if track:
                 red = torch.nonzero(rowflag & 1).flatten()    # (syncs: sized output)
-                h = dv.readback(dims)[0]
+                h, ov = dv.readback(dims, over)
                 if red.numel():
                     with phase("emin.repair"):
                         cg, xrp, xeid, n_aug = repair.finish_post_pass(
                             post, red.cpu().numpy(), cg0, n_e)
-                    st, icount, jcount, rmax2, dims, _, _ = _count(D, P, cg, xrp, xeid, False,
-                                                                   shard)
+                    st, icount, jcount, rmax2, dims, _, _, over = _count(D, P, cg, xrp, xeid,
+                                                                         False, shard)
                     st.defer(check)
-                    T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st, shard=shard)
+                    T, pattern = _fill(D, P, cg, icount, jcount, xrp, xeid, st, over,
+                                       shard=shard)
                     st.defer(check)
-                    h = dv.readback(dims)[0]
+                    h, ov = dv.readback(dims, over)
             else:
-                h = dv.readback(dims)[0]
-    h = h.reshape(129, 17)
+                h, ov = dv.readback(dims, over)
+    h = h.reshape(*_TABLE)
     nz = np.argwhere(h)
     counter = Counter({(int(i), int(j)): int(h[i, j]) for i, j in nz})
+    if int(ov[0]):
+        # wide-class rows beyond the device histogram's table (rare: sized gather)
+        big = torch.nonzero((icount >= _TABLE[0]) | (jcount >= _TABLE[1])).flatten()
+        ij = torch.stack((icount[big], jcount[big]), 1).cpu().numpy()
+        counter.update((int(i), int(j)) for i, j in ij if i > 0)
     return EminSetup(T=T, pattern=pattern, cg=cg, subproblem_dims=counter,
-                     rdp_scale=rdp_scale, n_augmented=n_aug)
+                     rdp_scale=rdp_scale, n_augmented=n_aug, over=over)

@@ -185,12 +185,12 @@ def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
     nr = len(need_rows)
     rows_d = torch.from_numpy(need_rows.astype(np.int64)).to(dev)
     ncnt = torch.empty(nr, dtype=torch.int32, device=dev)
-    pairs = torch.empty(nr * 15 * 2, dtype=torch.int32, device=dev)
+    pairs = torch.empty(nr * 31 * 2, dtype=torch.int32, device=dev)
     st = dv.Status()
     dv.call("sphc_emin_repair", nr, rows_d, T.rowptr, T.col, pattern.rowptr, pattern.col,
             cg.ep_a, cg.ep_b, Tt.rowptr, Tt.col, Tt.val, ncnt, pairs, st.t)
     cnt_h, pairs_h = dv.readback(ncnt, pairs)
-    pairs_h = pairs_h.reshape(nr, 15, 2)
+    pairs_h = pairs_h.reshape(nr, 31, 2)
     for r, i in enumerate(need_rows.tolist()):
         c = int(cnt_h[r])
         if c == -1:
@@ -198,7 +198,7 @@ def make_irreducible_pass(need, flags, rowmax, rdp_scale, T, pattern, cg):
                              "constraint graph")
         if c < 0:
             raise RuntimeError(f"fine edge {i}: constraint block exceeds the device "
-                               "make_irreducible kernel (|J| <= 16)")
+                               "make_irreducible kernel (|J| <= 32)")
         I = data_I[i][0].tolist()
         for j in range(c):
             a, b = int(pairs_h[r, j, 0]), int(pairs_h[r, j, 1])

@@ -8,7 +8,12 @@ MatrixMarket systems, mmio.py, have no structural bound).
   ordered product;
 * a whole hierarchy driven through that path (every row of more than 8
   output columns) equals the on-chip one;
-* aggregation of nodes with > 256 aggregated neighbours.
+* aggregation of nodes with > 256 aggregated neighbours;
+* emin constraint blocks beyond the default class (|J| > 16 or |I| > 128)
+  re-run through the wide class (one lane per coarse node, |J| <= 32): a
+  whole hierarchy and the make_irreducible flow driven through it are bitwise
+  the default ones, genuinely wide blocks match the oracle, and blocks
+  beyond the wide class raise.
 """
 
 import numpy as np
@@ -166,3 +171,107 @@ def test_thin_spgemm_is_bitwise_scipy():
     assert rel_max_diff(Cb, refb) <= 1e-14
     Co = dv.spgemm(dAb, dB, drop=False, ordered=True).to_scipy()
     assert csr_hash(Co) == csr_hash(refb)
+
+
+def _same_csr(A, B):
+    return (torch.equal(A.rowptr, B.rowptr) and torch.equal(A.col, B.col)
+            and torch.equal(A.val, B.val))
+
+
+@pytest.mark.parametrize("N,sigma,dirichlet,coarse", [(10, 1.0, False, 100), (12, 1e-2, True, 200)])
+def test_hierarchy_through_wide_emin_class(N, sigma, dirichlet, coarse):
+    """Every constraint block with |J| > 6 or |I| > 12 driven through the wide
+    capacity class of the emin kernels (count, fill, sweeps): the hierarchy is
+    bit for bit the default one (same arithmetic in the same order)."""
+    from paper_2506_08284_b200 import emin_setup as es
+    from paper_2506_08284_b200 import multigrid as mg
+    from paper_2506_08284_b200.inputs import discretize_hex
+    s = discretize_hex(N, sigma, dirichlet)
+    cfg = mg.SolverConfig(coarse_size=coarse)
+    h0 = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, cfg)
+    old = es.DEFAULT_CLASS_CAPS
+    es.DEFAULT_CLASS_CAPS = (6, 12)
+    try:
+        h1 = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D, cfg)
+    finally:
+        es.DEFAULT_CLASS_CAPS = old
+    assert h0.n_levels == h1.n_levels
+    for a, b in zip(h0.levels, h1.levels):
+        assert _same_csr(a.A_e, b.A_e) and _same_csr(a.S_e, b.S_e)
+        if a.P_e is None:
+            continue
+        assert _same_csr(a.P_e, b.P_e)
+        assert a.subproblem_dims == b.subproblem_dims
+        assert a.emin_energy == b.emin_energy
+        assert a.commutator_residual == b.commutator_residual
+        assert max(k[1] for k in a.subproblem_dims) > 6      # the wide class did run
+
+
+def test_make_irreducible_through_wide_emin_class():
+    """The repair flow (flagged rows, appended coarse edges, refill) with the
+    blocks in the wide class: same result as the default class, which
+    test_gpu_parity.py pins to the reference's make_irreducible."""
+    import json
+    import os
+    from golden_util import GOLDEN
+    from paper_2506_08284_b200 import coarse_gradient as cg_mod
+    from paper_2506_08284_b200 import emin_setup as es
+    from paper_2506_08284_b200 import nodal_amg as na
+    from paper_2506_08284_b200.inputs import discretize_hex
+    with open(os.path.join(GOLDEN, "repair_N10d.json")) as f:
+        meta = json.load(f)
+    arr = dict(np.load(os.path.join(GOLDEN, "repair_N10d.npz")))
+    s = discretize_hex(10, 1.0, True)
+    agg = na.aggregate(na.strength_graph(s.A_n, 0.0))
+    nod = na.smooth_and_normalize(s.A_n, agg)
+
+    def run():
+        cg = cg_mod.coarse_gradient_from_edges(arr["pairs"], arr["singles"], meta["n_nodes"])
+        return es.setup_constraints(s.D, nod.P, cg)
+    s0 = run()
+    old = es.DEFAULT_CLASS_CAPS
+    es.DEFAULT_CLASS_CAPS = (5, 10)
+    try:
+        s1 = run()
+    finally:
+        es.DEFAULT_CLASS_CAPS = old
+    assert s0.n_augmented == s1.n_augmented == meta["n_augmented"] > 0
+    assert [list(e) for e in s1.cg.augmented_edges] == meta["augmented"]
+    assert _same_csr(s0.pattern, s1.pattern) and _same_csr(s0.T, s1.T)
+    assert s0.subproblem_dims == s1.subproblem_dims
+
+
+def test_wide_constraint_blocks_vs_oracle():
+    """Blocks that really exceed the default class: the C4 recipe at 10^3 with
+    drop_tol = 0.08 shrinks the aggregates until 1387 fine edges see 17-28
+    coarse nodes (|I| up to 118). First level against the oracle (which has no
+    capacity): STRUCT, subproblem dims, TOL 1e-10; then the whole hierarchy
+    builds and PCG converges. drop_tol = 0.09 gives |J| = 34: beyond the wide
+    class too, which must raise, not truncate."""
+    from oracle import hcurl_oracle as O
+    from paper_2506_08284_b200 import edge_prolongator as ep
+    from paper_2506_08284_b200 import multigrid as mg
+    from paper_2506_08284_b200.assembly import make_device_config
+    s, rhs, cfg = make_device_config("C4", 10)
+    A_e, S, A_n, D = (M.to_scipy() for M in (s.A_e, s.S, s.A_n, s.D))
+    prol, cgd, nod = ep.build_edge_prolongator(s.A_n, s.A_e, s.S, s.D,
+                                               ep.EminConfig(drop_tol=0.08))
+    memb, nagg = O.aggregate(O.strength_pattern(A_n, 0.08))
+    Po, _, _ = O.smoothed_prolongator(A_n, memb, nagg)
+    ce = O.coarse_edges(D, O.piecewise_const(Po, 2), nagg)
+    em = O.emin_prolongator(D, Po, ce, S)
+    assert max(k[1] for k in em.subproblem_dims) > 16
+    assert dict(prol.subproblem_dims) == dict(em.subproblem_dims)
+    P = prol.P_e.to_scipy()
+    assert np.array_equal(P.indptr, em.P_e.indptr)
+    assert np.array_equal(P.indices, em.P_e.indices)
+    assert rel_max_diff(P, em.P_e) <= 1e-10
+    assert np.allclose(prol.energy_history, em.energy_history, rtol=1e-10, atol=0)
+    assert prol.commutator_residual <= 1e-12
+    assert prol.n_augmented == em.n_augmented
+    h = mg.build_hierarchy(s.A_e, s.S, s.A_n, s.D,
+                           mg.SolverConfig(coarse_size=200, emin=ep.EminConfig(drop_tol=0.08)))
+    r = mg.pcg_solve(h.levels[0].A_e, rhs, mg.v_cycle_preconditioner(h))
+    assert r.status == "converged"
+    with pytest.raises(RuntimeError, match="wide class"):
+        ep.build_edge_prolongator(s.A_n, s.A_e, s.S, s.D, ep.EminConfig(drop_tol=0.09))

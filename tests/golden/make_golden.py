@@ -281,6 +281,18 @@ def error_cases():
     return out
 
 
+def error_input_cases():
+    """Every case of tests/error_inputs.py on the unmodified reference."""
+    from types import SimpleNamespace
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    import error_inputs
+    from hcurlamg import nodal_amg as na, coarse_gradient as cgm, emin_setup as es
+    from hcurlamg import edge_prolongator as epm
+    m = SimpleNamespace(na=na, cgm=cgm, es=es, epm=epm, mg=mg)
+    s = discretize(build_structured_mesh(3, "hex", 5, False), 1.0)
+    return {name: error_inputs.run(m, s, name) for name in error_inputs.CASES}
+
+
 def repair_case():
     """make_irreducible exercised through the reference's own setup_constraints:
     level-0 inputs of N=10 Dirichlet with every 17th interior coarse edge
@@ -571,6 +583,9 @@ def main(which):
             json.dump(meta, f, indent=1)
         np.savez_compressed(os.path.join(HERE, "pcg_status.npz"), **arrays)
         print("pcg status cases", {k: (v["status"], v["iterations"]) for k, v in meta.items()})
+    if "error_inputs" in which:
+        with open(os.path.join(HERE, "error_inputs.json"), "w") as f:
+            json.dump(error_input_cases(), f, indent=1)
     if "errors" in which:
         with open(os.path.join(HERE, "errors.json"), "w") as f:
             json.dump(error_cases(), f, indent=1)
@@ -622,5 +637,5 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(set(sys.argv[1:]) or set(["inputs", "errors", "repair", "pcg_status"] + list(CASES) + list(RELAX)
+    main(set(sys.argv[1:]) or set(["inputs", "errors", "error_inputs", "repair", "pcg_status"] + list(CASES) + list(RELAX)
                                   + list(MESH) + list(VARIANTS)))

@@ -293,6 +293,18 @@ def error_input_cases():
     return {name: error_inputs.run(m, s, name) for name in error_inputs.CASES}
 
 
+def edge_case_results():
+    """Every case of tests/edge_cases.py on the unmodified reference."""
+    from types import SimpleNamespace
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    import edge_cases
+    m = SimpleNamespace(
+        mg=mg, config=lambda **kw: mg.SolverConfig(**kw),
+        system=lambda N, sigma, dirichlet: discretize(
+            build_structured_mesh(3, "hex", N + 1, dirichlet), sigma))
+    return {name: edge_cases.run(m, name) for name in edge_cases.CASES}
+
+
 def repair_case():
     """make_irreducible exercised through the reference's own setup_constraints:
     level-0 inputs of N=10 Dirichlet with every 17th interior coarse edge
@@ -583,6 +595,9 @@ def main(which):
             json.dump(meta, f, indent=1)
         np.savez_compressed(os.path.join(HERE, "pcg_status.npz"), **arrays)
         print("pcg status cases", {k: (v["status"], v["iterations"]) for k, v in meta.items()})
+    if "edge_cases" in which:
+        with open(os.path.join(HERE, "edge_cases.json"), "w") as f:
+            json.dump(edge_case_results(), f, indent=1)
     if "error_inputs" in which:
         with open(os.path.join(HERE, "error_inputs.json"), "w") as f:
             json.dump(error_input_cases(), f, indent=1)
@@ -637,5 +652,5 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(set(sys.argv[1:]) or set(["inputs", "errors", "error_inputs", "repair", "pcg_status"] + list(CASES) + list(RELAX)
+    main(set(sys.argv[1:]) or set(["inputs", "errors", "error_inputs", "edge_cases", "repair", "pcg_status"] + list(CASES) + list(RELAX)
                                   + list(MESH) + list(VARIANTS)))

@@ -71,8 +71,12 @@ def jacobi_diag_inverse(S):
 
 
 @checked
-def emin_sweeps(S, setup, omega, iterations, shard=None):
+def emin_sweeps(S, setup, omega, iterations, shard=None, final_energy=True):
     """Projected damped-Jacobi sweeps; returns (values, energies, residual).
+    ``final_energy=False`` (build_hierarchy): the energy of the last iterate,
+    trace(P^T S P), is left to the caller, who forms P^T S P anyway -- that
+    saves the masked S P pass that only measures it (the last sweep already
+    reports the commutator residual of its output).
     With ``shard`` every rank sweeps its block of fine edges and the value
     ranges are all-gathered after each sweep (the next sweep's masked S P
     reads neighbouring rows)."""
@@ -111,24 +115,26 @@ def emin_sweeps(S, setup, omega, iterations, shard=None):
             gather(out)
             dv.vsum(e_row, esum[it:it + 1])
             vals = out
-    # energy of the final iterate and its commutator residual
-    res.zero_()
-    for _, lo, hi in blocks:
-        call("sphc_emin_step", lo, hi, S.rowptr, S.col, S.val, None, T.rowptr, T.col, T.val,
-             Pp.rowptr, Pp.col, vals, None, cg.ep_a, cg.ep_b, float(omega), 0, e_row, res,
-             jcap, icap, over, st.t)
-    gather(None)
-    dv.vsum(e_row, esum[iterations:iterations + 1])
+    last = final_energy or not iterations
+    if last:
+        # energy of the final iterate and its commutator residual
+        res.zero_()
+        for _, lo, hi in blocks:
+            call("sphc_emin_step", lo, hi, S.rowptr, S.col, S.val, None, T.rowptr, T.col,
+                 T.val, Pp.rowptr, Pp.col, vals, None, cg.ep_a, cg.ep_b, float(omega), 0,
+                 e_row, res, jcap, icap, over, st.t)
+        gather(None)
+        dv.vsum(e_row, esum[iterations:iterations + 1])
     if shard is not None:
         shard.min_(st.t)
     st.defer(es._checker(S))
     eh, rh = dv.readback(esum, res)
-    energies = [float(x) for x in eh] if iterations else []
+    energies = [float(x) for x in eh[:iterations + (1 if last else 0)]] if iterations else []
     return vals, energies, float(rh[0])
 
 
 @checked
-def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None, shard=None):
+def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None, shard=None, final_energy=True):
     """Edge prolongator and coarse gradient for one level
     (edge_prolongator.py:184-228). Returns
     (EdgeProlongator, CoarseGradient, NodalProlongator). ``shard`` (a
@@ -138,7 +144,10 @@ def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None, shard=None):
     cfg.mode == "rsamg" (edge_prolongator.py:200-213): the nodal transfer is
     the tentative prolongator itself (omega = rho = 0) and no emin sweeps
     run, so P_e is the feasible initial guess (entries +-1, 0 and the
-    least-norm fractions of Dirichlet rows; many empty rows)."""
+    least-norm fractions of Dirichlet rows; many empty rows).
+
+    ``final_energy=False``: energy_history lacks its last entry, the energy of
+    the returned P_e, which equals trace(P_e^T S P_e) (see emin_sweeps)."""
     cfg = cfg or EminConfig()
     rsamg = cfg.mode == "rsamg"
     with phase("setup.strength"):
@@ -160,7 +169,7 @@ def build_edge_prolongator(A_n, A_e, S, D_h, cfg=None, shard=None):
         cg = setup.cg                      # with any edges make_irreducible appended
     with phase("setup.emin_sweeps"):
         vals, energy, res = emin_sweeps(S, setup, cfg.omega, 0 if rsamg else cfg.iterations,
-                                        shard=shard)
+                                        shard=shard, final_energy=final_energy)
     P = setup.pattern
     P_e = DeviceCSR(P.rowptr, P.col, vals, P.shape)
     prol = EdgeProlongator(P_e=P_e, energy_history=energy, commutator_residual=res,

@@ -615,7 +615,8 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
         D = own_csr(D) if isinstance(D, DeviceCSR) else up.get(next(it))
         try:
             first = build_edge_prolongator(A_n, dv.PendingCSR(up, k + 1),
-                                           dv.PendingCSR(up, k), D, cfg.emin, shard=shard)
+                                           dv.PendingCSR(up, k), D, cfg.emin, shard=shard,
+                                           final_energy=False)
         except ValueError:
             _check_nullspace(up.get(k), D, "the fine level", A=up.get(k + 1), shard=shard)
             raise
@@ -626,12 +627,13 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
         A_e, S_e = own_csr(A_e), own_csr(S_e)
         A_n, D = own_csr(A_n), own_csr(D)
     AD = _check_nullspace(S_e, D, "the fine level", A=A_e, shard=shard)
-    levels = []
+    levels, traces = [], []
     while A_e.shape[0] > cfg.coarse_size and len(levels) < cfg.max_levels - 1:
         if first is not None:
             (prol, cg, nod), first = first, None
         else:
-            prol, cg, nod = build_edge_prolongator(A_n, A_e, S_e, D, cfg.emin, shard=shard)
+            prol, cg, nod = build_edge_prolongator(A_n, A_e, S_e, D, cfg.emin, shard=shard,
+                                                   final_energy=False)
         P_e, P_n = prol.P_e, nod.P
         n_coarse = cg.n_edges
         if n_coarse == 0:
@@ -655,6 +657,13 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
         levels.append(lv)
         with phase("level.galerkin_edge"):
             A_e, S_e = _galerkin_edge(A_e, S_e, P_e, lv.R_e, shard)
+            if prol.energy_history:
+                # the energy of the final iterate (edge_prolongator.py:154-156,
+                # trace(P^T S P)) is the trace of the coarse curl-curl
+                # operator just formed; read back with the sweepers' scalars
+                tr = dv.zeros_f64(1)
+                dv.vsum(dv.diagonal(S_e), tr)
+                traces.append((lv, tr))
         with phase("level.galerkin_nodal"):
             A_n = dv.spgemm(dv.transpose(P_n), dv.spgemm(A_n, P_n, ordered=True, shard=shard),
                             ordered=True, shard=shard)
@@ -680,7 +689,9 @@ def build_hierarchy(A_e, S_e, A_n, D, cfg=None, shard=None):
     last.r = dv.empty_f64(A_e.shape[0])
     nnz0 = levels[0].A_e.nnz
     oc = sum(lv.A_e.nnz for lv in levels) / nnz0
-    (info_h,) = finalize_sweepers(info)
+    info_h, *tr_h = finalize_sweepers(info, *(t for _, t in traces))
+    for (lv, _), t in zip(traces, tr_h):
+        lv.emin_energy = list(lv.emin_energy) + [float(t[0])]
     inv = _coarse_inverse_finish(inv, info_h[0], inv_state)
     return Hierarchy(levels=levels, coarse_factorization=inv, operator_complexity=oc)
 

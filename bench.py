@@ -801,6 +801,7 @@ def workload_config(config, cfg, n_e, coarse_size):
 # itself ~3 h), far beyond a bench run, so each step runs the
 # same recipe at 32^3
 REF_SAMPLE_N = {"C3": 32, "C4": 32, "C5": 32}
+REF_BUDGET_S = 150
 
 
 def run_reference(args):
@@ -808,7 +809,7 @@ def run_reference(args):
     Gauss-Seidel smoother; the reference package itself cannot travel to
     the GPU box) on one pinned core, rank 0 only. Each step is one full
     setup + solve of a bounded sample of the workload: the same recipe at
-    REF_SAMPLE_N (capped at --ref-steps steps)."""
+    REF_SAMPLE_N; --steps of them, or as many as fit REF_BUDGET_S."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return None
@@ -817,15 +818,19 @@ def run_reference(args):
     sysm, rhs, cfg = host_problem(args.config, nsamp or args.N)
     n_e = sysm.A_e.shape[0]
     cs = args.coarse_size or cfg.get("coarse_size", 1000)
-    wu = min(args.warmup, 1)
+    wu = args.warmup
+    s1, r1, _ = host_problem("C1")
     for _ in range(wu):        # warm-up on a small instance (imports, page-in)
-        s1, r1, _ = host_problem("C1")
         _oracle_step(s1, r1, 1000, "gs")
-    k = max(1, min(args.steps, args.ref_steps))
-    times, res = [], None
-    for _ in range(k):
+    # K timed steps, as many as fit REF_BUDGET_S of CPU time (or --ref-steps)
+    kmax = args.steps if args.ref_steps is None else min(args.steps, args.ref_steps)
+    times, res, t0 = [], None, time.perf_counter()
+    while len(times) < max(1, kmax):
         t, res, ts, tv = _oracle_step(sysm, rhs, cs, "gs")
         times.append((t, ts, tv))
+        if args.ref_steps is None and time.perf_counter() - t0 + t > REF_BUDGET_S:
+            break
+    k = len(times)
     tm = sum(x[0] for x in times) / k
     v = n_e / tm
     hi = host_info()
@@ -843,8 +848,9 @@ def run_reference(args):
             "cpu_baseline": {"value": v, "unit": "edge DOFs/s",
                              "cores": hi["affinity_cores"] or 1, "kind": "port",
                              "sample": f"{args.config} recipe at {cfg['N']}^3 ({n_e} edges): "
-                                       f"full setup + Gauss-Seidel PCG x{k} (capped at "
-                                       f"--ref-steps {args.ref_steps}), one core",
+                                       f"full setup + Gauss-Seidel PCG, {k} of the "
+                                       f"{args.steps} requested steps (CPU budget "
+                                       f"{REF_BUDGET_S} s), one core",
                              "host": hi},
             "e2e": {"value": v, "unit": "edge DOFs/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -864,7 +870,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--smoother", default="chebyshev", choices=["chebyshev", "gauss_seidel"])
-    ap.add_argument("--ref-steps", type=int, default=1)
+    ap.add_argument("--ref-steps", type=int, default=None,
+                    help="cap on the reference arm's timed steps (default: as many of "
+                         "--steps as fit its CPU time budget)")
     ap.add_argument("--ref-N", type=int, default=None,
                     help="reference-arm sample size (default REF_SAMPLE_N; 0: full size)")
     ap.add_argument("--cpu-sample", action="store_true", help=argparse.SUPPRESS)

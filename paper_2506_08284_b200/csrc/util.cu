@@ -415,8 +415,10 @@ __device__ void bitonic(int* k, double* v, int n, int tid, int nthr) {
   }
 }
 
+// *any_long is set when some row is left to the block kernel, which returns
+// at once otherwise (it would scan every row pointer for nothing)
 __global__ void k_sort_rows_warp(i64 n, const i64* __restrict__ rp, int* ci, double* v,
-                                 i64* status) {
+                                 int* any_long, i64* status) {
   __shared__ int sk[SORT_WARPS][WARP_SORT_CAP];
   __shared__ double sv[SORT_WARPS][WARP_SORT_CAP];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -424,7 +426,11 @@ __global__ void k_sort_rows_warp(i64 n, const i64* __restrict__ rp, int* ci, dou
   for (i64 row = row0; row < n; row += (i64)gridDim.x * SORT_WARPS) {
     i64 s = rp[row];
     int len = (int)(rp[row + 1] - s);
-    if (len <= 1 || len > WARP_SORT_CAP) continue;
+    if (len > WARP_SORT_CAP) {
+      if (lane == 0 && !*(volatile int*)any_long) *any_long = 1;
+      continue;
+    }
+    if (len <= 1) continue;
     // already sorted rows are left untouched
     bool sorted = true;
     for (int t = lane; t + 1 < len; t += 32) sorted &= ci[s + t] <= ci[s + t + 1];
@@ -444,7 +450,8 @@ __global__ void k_sort_rows_warp(i64 n, const i64* __restrict__ rp, int* ci, dou
 }
 
 __global__ void k_sort_rows_block(i64 n, const i64* __restrict__ rp, int* ci, double* v,
-                                  i64* status) {
+                                  const int* any_long, i64* status) {
+  if (!*(volatile const int*)any_long) return;
   extern __shared__ unsigned char smem[];
   double* sv = (double*)smem;
   int* sk = (int*)(sv + BLOCK_SORT_CAP);
@@ -472,8 +479,11 @@ __global__ void k_sort_rows_block(i64 n, const i64* __restrict__ rp, int* ci, do
 
 static int sort_rows(i64 n, const i64* rp, int* ci, double* v, i64* status, cudaStream_t s) {
   if (n <= 0) return 0;
-  k_sort_rows_warp<<<grid_for(n, SORT_WARPS, 148 * 32), SORT_WARPS * 32, 0, s>>>(n, rp, ci, v,
-                                                                                 status);
+  int* any_long = nullptr;
+  if (scratch(&any_long, 1, s)) return SPHC_ERR_CUDA;
+  SPHC_CUDA(cudaMemsetAsync(any_long, 0, sizeof(int), s));
+  k_sort_rows_warp<<<grid_for(n, SORT_WARPS, 148 * 32), SORT_WARPS * 32, 0, s>>>(
+      n, rp, ci, v, any_long, status);
   SPHC_LAUNCH_CHECK();
   size_t sm = BLOCK_SORT_CAP * (sizeof(double) + sizeof(int));
   static bool attr = false;
@@ -481,9 +491,9 @@ static int sort_rows(i64 n, const i64* rp, int* ci, double* v, i64* status, cuda
     cudaFuncSetAttribute(k_sort_rows_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
-  k_sort_rows_block<<<grid_for(n, 1, 148 * 4), 512, sm, s>>>(n, rp, ci, v, status);
+  k_sort_rows_block<<<grid_for(n, 1, 148 * 4), 512, sm, s>>>(n, rp, ci, v, any_long, status);
   SPHC_LAUNCH_CHECK();
-  return 0;
+  return scratch_free(any_long, s);
 }
 
 extern "C" int sphc_csr_sort_rows(int64_t n, const int64_t* rp, int32_t* ci, double* v,

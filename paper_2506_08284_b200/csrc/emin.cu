@@ -232,7 +232,7 @@ __device__ int em_factor(Row& R, i64 i, i64* status, int lane) {
   // irreducibility (emin_setup.py check_irreducible): every J node incident
   // to an edge of I and J connected by the interior edges. Lanes take the
   // edges and build adjacency bitmasks; reachability from node 0 is a
-  // warp-wide OR per BFS level (<= |J| <= 16 levels).
+  // warp-wide OR per BFS level (<= |J| levels).
   if (lane < Row::JMAX) R.adj[lane] = 0u;
   if (lane == 0) R.incm = 0u;
   __syncwarp();
@@ -711,7 +711,7 @@ extern "C" int sphc_emin_step(int64_t row0, int64_t row1, const int64_t* srp, co
 // ---------------------------------------------------------------------------
 // make_irreducible's main loop (emin_setup.py:183-217, 283-301) for the rows
 // the count/fill passes flagged: one warp per row. The row's constraint
-// graph (coarse nodes J <= 16 from T, its original pattern edges I) is
+// graph (coarse nodes J <= 32 from T, its original pattern edges I) is
 // connected greedily: among node pairs in different components, join the
 // one with the largest |(D_h P_n)[:, a] . (D_h P_n)[:, b]| (ties and zeros:
 // lexicographically smallest (a, b)), until every node is incident to an
@@ -721,9 +721,9 @@ extern "C" int sphc_emin_step(int64_t row0, int64_t row1, const int64_t* srp, co
 // the decisions are the reference's. Main-loop repairs do not see each
 // other's new edges (the reference extracts every row from the original
 // pattern), so rows are independent; the caller numbers the new edges in
-// ascending row order. Output: ncnt[r] edges in pairs[r * 15 + j] (a, b);
+// ascending row order. Output: ncnt[r] edges in pairs[r * 31 + j] (a, b);
 // ncnt[r] = -1: single-node graph (the reference's ValueError), -2: the row
-// exceeds the kernel's |J| <= 16.
+// exceeds the kernel's |J| <= 32.
 #define RP_MAXNEW (SPHC_EMIN_JWIDE - 1)
 
 __global__ void __launch_bounds__(128)
@@ -749,7 +749,7 @@ __global__ void __launch_bounds__(128)
     // adjacency bitmasks over J from the original pattern edges
     unsigned adj = 0u, inc = 0u;
     i64 p0 = prp[i], p1 = prp[i + 1];
-    for (i64 e = p0; e < p1; e++) {        // warp-uniform loop, <= 128 edges
+    for (i64 e = p0; e < p1; e++) {        // warp-uniform loop over the row's edges
       int col = pci[e];
       int a = ep_a[col], b = ep_b[col];
       unsigned ba = __ballot_sync(FULL_MASK, lane < nJ && myJ == b);
